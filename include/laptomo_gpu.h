@@ -1,0 +1,246 @@
+/*
+ * laptomo_gpu.h — C ABI of the B200-native shifted-FGMRES / Laplace-THT hot path.
+ *
+ * Drop-in boundary for the reference's solver API (/root/reference/proj/include/laptomo).
+ * Every entry point below names the reference interface it replaces (file:line).
+ * Plain pointers and sizes only: complex numbers are interleaved (re, im) doubles,
+ * layout-compatible with std::complex<double>, Eigen::VectorXcd data and CUDA double2.
+ *
+ * Conventions
+ *  - Every call returns an lt_status; on failure lt_last_error() (thread-local) holds a
+ *    message.  The reference's exceptions map to codes:
+ *      std::invalid_argument  -> LT_ERR_INVALID_ARGUMENT
+ *      FactorizationError     -> LT_ERR_PRECONDITIONER
+ *      ConvergenceError       -> LT_ERR_NOT_CONVERGED  (indices via lt_last_unconverged)
+ *  - One lt_ctx = one device + one CUDA stream.  Calls are synchronous at return.
+ *    A handle is not thread-safe; distinct handles may be used concurrently.
+ *  - `mem` arguments say where caller buffers live: LT_MEM_HOST or LT_MEM_DEVICE.
+ *  - Multi-RHS buffers are RHS-major: rhs b occupies [b*n, (b+1)*n).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute call fails
+ *    with LT_ERR_CUDA.
+ */
+#ifndef LAPTOMO_GPU_H
+#define LAPTOMO_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  double re, im;
+} lt_complex;
+
+typedef enum {
+  LT_OK = 0,
+  LT_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument                      */
+  LT_ERR_PRECONDITIONER = 2,   /* FactorizationError (errors.hpp:14-17)       */
+  LT_ERR_NOT_CONVERGED = 3,    /* ConvergenceError (errors.hpp:20-25)         */
+  LT_ERR_CUDA = 4,
+  LT_ERR_OOM = 5,
+  LT_ERR_INTERNAL = 6
+} lt_status;
+
+enum { LT_MEM_HOST = 0, LT_MEM_DEVICE = 1 };
+
+/* KrylovVariant (shifted_solver.hpp:21) */
+enum { LT_VARIANT_FOM = 0, LT_VARIANT_GMRES = 1 };
+/* SolverKind (forward.hpp:16) */
+enum { LT_SOLVER_SINGLE = 0, LT_SOLVER_FLEXIBLE = 1, LT_SOLVER_DIRECT = 2 };
+/* Discretisations: FD_CELL = cell-centred finite volume (BASELINE configs). */
+enum { LT_GRID_FD_CELL = 0 };
+
+typedef struct lt_ctx_s* lt_ctx;
+typedef struct lt_pencil_s* lt_pencil;
+
+/* ---- library / context ------------------------------------------------------------- */
+const char* lt_version(void);
+const char* lt_last_error(void);
+/* Unconverged shift indices of the last LT_ERR_NOT_CONVERGED (ConvergenceError::unconverged_shifts). */
+int lt_last_unconverged(int* indices, int capacity);
+
+lt_status lt_ctx_create(int device, lt_ctx* out);
+lt_status lt_ctx_destroy(lt_ctx ctx);
+lt_status lt_ctx_synchronize(lt_ctx ctx);
+/* The cudaStream_t all work of this context is issued on. */
+void* lt_ctx_stream(lt_ctx ctx);
+
+/* Per-kernel-class device timing (CUDA events on the context stream) for roofline reporting. */
+lt_status lt_ctx_set_profiling(lt_ctx ctx, int enabled);
+lt_status lt_ctx_reset_profile(lt_ctx ctx);
+/* Returns the number of kernel classes; fills up to `capacity` entries. name_buf holds
+ * capacity*64 chars (NUL-terminated names). */
+int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, int64_t* launches,
+                   double* algorithmic_bytes);
+/* Total kernel launches issued by this context since creation / last reset. */
+int64_t lt_ctx_launch_count(lt_ctx ctx);
+
+/* ---- talbot (talbot.hpp:23-63; host arithmetic, no device work) ---------------------- */
+typedef struct {
+  double sigma0, mu0, nu, alpha; /* TalbotParams (talbot.hpp:23-28) */
+} lt_talbot_params;
+
+void lt_talbot_default_params(lt_talbot_params* out);
+/* build_contour (talbot.cpp:49-80): n_quad/2 entries per output (any output may be NULL). */
+lt_status lt_talbot_build(int n_quad, double time, const lt_talbot_params* params, double* thetas,
+                          lt_complex* nodes, lt_complex* dnodes, lt_complex* weights);
+/* qhat_step (talbot.cpp:96-101). */
+lt_status lt_qhat_step(double q0, lt_complex z, lt_complex* out);
+/* select_preconditioner_shifts (shifted_solver.cpp:85-104): taus[2], pattern[5]. */
+lt_status lt_select_preconditioner_shifts(const lt_complex* shifts, int n_shifts, lt_complex* taus,
+                                          int* n_taus, int* pattern, int* pattern_len);
+
+/* ---- pencil (ShiftedPencil, shifted_solver.hpp:88-104; assemble, assembly.hpp:37-39) -- */
+typedef struct {
+  int kind;     /* LT_GRID_FD_CELL */
+  int dim;      /* 2 or 3 */
+  int shape[3]; /* cells along x, y, z (z ignored for dim 2); cell a = (k*ny + j)*nx + i */
+  double h;     /* uniform spacing */
+} lt_grid;
+
+/* Assembles (K, M) on the device from per-cell log fields (host or device arrays of n
+ * doubles) and builds the preconditioner hierarchy.  Replaces assemble() +
+ * ShiftedPencil(K, M) (assembly.cpp:69-113, shifted_solver.cpp:106-107). */
+lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* log_kappa,
+                                const double* log_storativity, int mem, lt_pencil* out);
+lt_status lt_pencil_destroy(lt_pencil p);
+int64_t lt_pencil_rows(lt_pencil p);
+int lt_pencil_levels(lt_pencil p);
+
+/* (K + z M) x, (K + conj(z) M) x, M x for n_rhs RHS (shifted_solver.cpp:109-118). */
+lt_status lt_pencil_apply(lt_pencil p, lt_complex z, const lt_complex* x, lt_complex* y,
+                          int n_rhs, int mem);
+lt_status lt_pencil_apply_adjoint(lt_pencil p, lt_complex z, const lt_complex* x, lt_complex* y,
+                                  int n_rhs, int mem);
+lt_status lt_pencil_apply_mass(lt_pencil p, const lt_complex* x, lt_complex* y, int n_rhs,
+                               int mem);
+
+/* The factorisation-cache analogue (ShiftedPencil::factorization, cpp:120-128): prepares
+ * the exact shift-and-invert preconditioner for each tau (cached by exact value). */
+lt_status lt_pencil_prepare(lt_pencil p, const lt_complex* taus, int n_taus);
+int lt_pencil_factorization_count(lt_pencil p);
+/* Inner-solve accuracy of the shift-and-invert preconditioner (relative residual). */
+lt_status lt_pencil_set_inner_tolerance(lt_pencil p, double rel_tol, int max_iterations);
+/* u = (K + tau M)^{-1} v  (SparseComplexFactorization::solve, factorization.hpp:23) and
+ * u = (K + tau M)^{-H} v (solve_adjoint, factorization.hpp:25). */
+lt_status lt_pencil_solve(lt_pencil p, lt_complex tau, const lt_complex* v, lt_complex* u,
+                          int n_rhs, int mem);
+lt_status lt_pencil_solve_adjoint(lt_pencil p, lt_complex tau, const lt_complex* v,
+                                  lt_complex* u, int n_rhs, int mem);
+
+/* Multilinear cell-centre weights of a point (FD analogue of point_source, mesh.cpp:91-125). */
+lt_status lt_pencil_point_weights(lt_pencil p, const double* point, int64_t* indices,
+                                  double* weights, int* count);
+
+/* ---- shifted solver (shifted_solver.hpp:44-132) ------------------------------------- */
+typedef struct {
+  int variant;        /* LT_VARIANT_GMRES (default) | LT_VARIANT_FOM */
+  double tol;         /* 1e-10 */
+  int maxit;          /* 0 -> min(n, 10 n_shifts) */
+  int keep_basis;     /* 0 */
+  int record_history; /* 1 */
+} lt_solve_options;
+
+void lt_solve_default_options(lt_solve_options* out);
+
+typedef struct {
+  int converged;
+  int iteration;        /* Arnoldi step at which the shift froze (1-based) */
+  double estimate;      /* relative */
+  double true_residual; /* relative, checked at freeze */
+} lt_shift_status;
+
+/* solve_shifted_flexible / solve_shifted_single (shifted_solver.cpp:291-322) for n_rhs
+ * right-hand sides in lockstep, all with the same shifts and schedule.
+ *   b         n * n_rhs
+ *   x_out     n * n_shifts * n_rhs (RHS-major, then shift), may be NULL
+ *   status    n_rhs * n_shifts, iterations n_rhs (both host, may be NULL)
+ *   history   n_rhs * n_shifts * maxit estimates (host, NaN-padded), may be NULL
+ * Never fails on non-convergence (like run_flexible): check status. */
+lt_status lt_solve_shifted(lt_pencil p, const lt_complex* b, int n_rhs, const lt_complex* shifts,
+                           int n_shifts, const lt_complex* taus, int n_taus, const int* pattern,
+                           int pattern_len, const lt_solve_options* options, int mem,
+                           lt_complex* x_out, lt_shift_status* status, int* iterations,
+                           double* history);
+
+/* FlexibleBasisState (shifted_solver.hpp:63-74) of the last lt_solve_shifted with
+ * keep_basis = 1, for rhs index `rhs`.  Sizes: V n*(m+1), U n*m, Hbar (m+1)*m column-major,
+ * taus m.  Pass NULL buffers to query m (steps_out) first. */
+lt_status lt_last_basis(lt_pencil p, int rhs, int* steps_out, double* beta_out, lt_complex* V,
+                        lt_complex* U, lt_complex* Hbar, lt_complex* taus);
+
+/* solve_shifted_direct (shifted_solver.cpp:324-332): one exact shift-and-invert per shift. */
+lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs,
+                                  const lt_complex* shifts, int n_shifts, int mem,
+                                  lt_complex* x_out);
+
+/* ---- drivers (forward.hpp:52-61, jacobian.hpp:79-101) -------------------------------- */
+typedef struct {
+  int kind;    /* LT_SOLVER_* (SolverConfig, forward.hpp:18-23) */
+  int variant; /* LT_VARIANT_* */
+  double tol;
+  int maxit;
+} lt_solver_config;
+
+void lt_solver_default_config(lt_solver_config* out);
+
+typedef struct {
+  int iterations;
+  int all_converged;
+} lt_time_diag;
+
+/* solve_forward (forward.cpp:75-118) for n_src independent problems that share times,
+ * n_quad, contour and solver (each its own source vector and rate), batched in lockstep.
+ *   sources        n * n_src weight vectors (free dofs)
+ *   initial_head   n * n_src or NULL (phi0 = 0)
+ *   heads_out      n * n_times * n_src (per source: column t of HeadSolution.heads), or NULL
+ *   receivers      n_rec receiver points (dim doubles each) -> drawdown_out
+ *                  n_src * n_rec * n_times ((s*n_rec + r)*n_times + t), either may be NULL
+ *   shift_residuals n_src * n_times * n_half (verified relative residual per shift), or NULL
+ * pooled != 0 selects solve_forward_batch (forward.cpp:126-198).
+ * Throws-equivalent: LT_ERR_NOT_CONVERGED when shifts fail to converge. */
+lt_status lt_forward(lt_pencil p, const double* sources, const double* rates, int n_src,
+                     const double* initial_head, const double* times, int n_times, int n_quad,
+                     const lt_talbot_params* contour, const lt_solver_config* solver, int pooled,
+                     int mem, double* heads_out, const double* receivers, int n_rec,
+                     double* drawdown_out, lt_time_diag* diag_out, double* shift_residuals);
+
+/* ThtExperiment (jacobian.hpp:22-42) with point coordinates (dim doubles per point). */
+typedef struct {
+  const double* sources;   /* n_src * dim */
+  const double* rates;     /* n_src */
+  int n_src;
+  const double* receivers; /* n_rec * dim */
+  int n_rec;
+  const double* times;     /* n_times */
+  int n_times;
+  int n_quad;
+  lt_talbot_params contour;
+  lt_solver_config solver;
+  int include_storativity;
+  int storativity_z_factor;
+} lt_experiment;
+
+void lt_experiment_defaults(lt_experiment* out);
+
+/* One time slice of ThtForwardModel::jacobian (jacobian.cpp:189-247) on the pencil's
+ * fields: rows (s*n_rec + r) of the slice, row-major, n_param = n (kappa block) or 2n
+ * (storativity block appended).  jac_out is n_src*n_rec*n_param doubles (host or device
+ * per `mem`), predictions_out n_src*n_rec (host).  Either may be NULL. */
+lt_status lt_jacobian_slice(lt_pencil p, const lt_experiment* exp, int time_index, int mem,
+                            double* jac_out, double* predictions_out);
+
+/* Full ThtForwardModel::jacobian: J n_meas x n_param row-major in the reference's row
+ * order (s*n_rec + r)*n_times + t (jacobian.hpp:37-41), predictions n_meas.  Host only. */
+lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out,
+                      double* predictions_out);
+
+/* ThtForwardModel::predict (jacobian.cpp:158-187): n_meas predictions. */
+lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAPTOMO_GPU_H */

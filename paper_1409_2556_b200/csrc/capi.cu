@@ -1,0 +1,495 @@
+// extern "C" boundary (include/laptomo_gpu.h): argument checks, exception -> status mapping,
+// host/device staging of caller buffers.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "drivers.hpp"
+#include "lt_internal.hpp"
+#include "talbot_host.hpp"
+
+namespace lt {
+lt_ctx ctx_create(int device);
+void ctx_destroy(lt_ctx ctx);
+}  // namespace lt
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+lt_status guard(F&& f) {
+  try {
+    f();
+    return LT_OK;
+  } catch (const lt::Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return LT_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LT_ERR_INTERNAL;
+  }
+}
+
+using cd = std::complex<double>;
+
+void set_device(lt_ctx ctx) { LT_CUDA(cudaSetDevice(ctx->device)); }
+
+// Stage an n_vals complex buffer onto the device (no copy when already device memory).
+struct Staged {
+  lt::DeviceBuffer buf;
+  double2* ptr = nullptr;
+};
+
+Staged stage_in(const lt_complex* x, size_t count, int mem, cudaStream_t st) {
+  Staged s;
+  if (mem == LT_MEM_DEVICE) {
+    s.ptr = reinterpret_cast<double2*>(const_cast<lt_complex*>(x));
+  } else {
+    s.buf.allocate(sizeof(double2) * count, st);
+    s.ptr = s.buf.as<double2>();
+    LT_CUDA(cudaMemcpyAsync(s.ptr, x, sizeof(double2) * count, cudaMemcpyHostToDevice, st));
+  }
+  return s;
+}
+
+Staged stage_out(lt_complex* y, size_t count, int mem, cudaStream_t st) {
+  Staged s;
+  if (mem == LT_MEM_DEVICE) {
+    s.ptr = reinterpret_cast<double2*>(y);
+  } else {
+    s.buf.allocate(sizeof(double2) * count, st);
+    s.ptr = s.buf.as<double2>();
+  }
+  return s;
+}
+
+void finish_out(lt_complex* y, const Staged& s, size_t count, int mem, cudaStream_t st) {
+  if (mem != LT_MEM_DEVICE)
+    LT_CUDA(cudaMemcpyAsync(y, s.ptr, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+void check_pencil(lt_pencil p) { LT_REQUIRE(p != nullptr, "null pencil"); }
+
+void apply_common(lt_pencil p, double2 z, const lt_complex* x, lt_complex* y, int n_rhs, int mem, bool mass) {
+  check_pencil(p);
+  LT_REQUIRE(n_rhs >= 0, "n_rhs must be nonnegative");
+  if (n_rhs == 0) return;
+  set_device(p->ctx);
+  cudaStream_t st = p->ctx->stream;
+  const size_t count = (size_t)p->n * n_rhs;
+  Staged xin = stage_in(x, count, mem, st);
+  Staged yout = stage_out(y, count, mem, st);
+  std::vector<double2> taus(n_rhs, z);
+  lt::DeviceBuffer dt(sizeof(double2) * n_rhs, st);
+  LT_CUDA(cudaMemcpyAsync(dt.get(), taus.data(), sizeof(double2) * n_rhs, cudaMemcpyHostToDevice, st));
+  lt::apply_batch(p, 0, dt.as<double2>(), xin.ptr, p->n, yout.ptr, p->n, n_rhs, mass, mass ? "apply_mass" : "apply");
+  finish_out(y, yout, count, mem, st);
+}
+
+void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
+  check_pencil(p);
+  LT_REQUIRE(n_rhs >= 0, "n_rhs must be nonnegative");
+  if (n_rhs == 0) return;
+  set_device(p->ctx);
+  cudaStream_t st = p->ctx->stream;
+  const size_t count = (size_t)p->n * n_rhs;
+  Staged vin = stage_in(v, count, mem, st);
+  Staged uout = stage_out(u, count, mem, st);
+  std::vector<double2> taus(n_rhs, tau);
+  lt::inner_solve(p, n_rhs, taus.data(), vin.ptr, p->n, uout.ptr, p->n);
+  finish_out(u, uout, count, mem, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lt_version(void) { return "laptomo-b200 0.1 (sm_100a, FP64)"; }
+const char* lt_last_error(void) { return g_err.c_str(); }
+
+int lt_last_unconverged(int* indices, int capacity) {
+  const auto& v = lt::g_last_unconverged;
+  for (int i = 0; i < (int)v.size() && i < capacity; ++i) indices[i] = v[i];
+  return (int)v.size();
+}
+
+lt_status lt_ctx_create(int device, lt_ctx* out) {
+  return guard([&] {
+    LT_REQUIRE(out != nullptr, "lt_ctx_create: null output");
+    *out = lt::ctx_create(device);
+  });
+}
+
+lt_status lt_ctx_destroy(lt_ctx ctx) {
+  return guard([&] { lt::ctx_destroy(ctx); });
+}
+
+lt_status lt_ctx_synchronize(lt_ctx ctx) {
+  return guard([&] {
+    LT_REQUIRE(ctx, "null context");
+    LT_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+void* lt_ctx_stream(lt_ctx ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+lt_status lt_ctx_set_profiling(lt_ctx ctx, int enabled) {
+  return guard([&] {
+    LT_REQUIRE(ctx, "null context");
+    ctx->resolve_profile();
+    ctx->profiling = enabled != 0;
+  });
+}
+
+lt_status lt_ctx_reset_profile(lt_ctx ctx) {
+  return guard([&] {
+    LT_REQUIRE(ctx, "null context");
+    ctx->resolve_profile();
+    ctx->profile.clear();
+    ctx->launches = 0;
+  });
+}
+
+int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, int64_t* launches,
+                   double* algorithmic_bytes) {
+  if (!ctx) return -1;
+  try {
+    ctx->resolve_profile();
+  } catch (const lt::Error& e) {
+    g_err = e.what();
+    return -1;
+  }
+  int i = 0;
+  for (const auto& kv : ctx->profile) {
+    if (i < capacity) {
+      if (name_buf) {
+        std::strncpy(name_buf + 64 * i, kv.first.c_str(), 63);
+        name_buf[64 * i + 63] = 0;
+      }
+      if (total_ms) total_ms[i] = kv.second.ms;
+      if (launches) launches[i] = kv.second.launches;
+      if (algorithmic_bytes) algorithmic_bytes[i] = kv.second.bytes;
+    }
+    ++i;
+  }
+  return i;
+}
+
+int64_t lt_ctx_launch_count(lt_ctx ctx) { return ctx ? ctx->launches : -1; }
+
+void lt_talbot_default_params(lt_talbot_params* out) {
+  if (out) *out = lt_talbot_params{-0.6122, 0.5017, 0.2645 / 0.5017, 0.6407};
+}
+
+lt_status lt_talbot_build(int n_quad, double time, const lt_talbot_params* params, double* thetas,
+                          lt_complex* nodes, lt_complex* dnodes, lt_complex* weights) {
+  return guard([&] {
+    LT_REQUIRE(n_quad >= 4 && n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
+    LT_REQUIRE(time > 0.0, "build_contour: time must be positive");
+    lt_talbot_params p;
+    if (params) p = *params; else lt_talbot_default_params(&p);
+    std::vector<double> th;
+    std::vector<cd> z, dz, w;
+    lt::talbot_build(n_quad, time, p, &th, &z, &dz, &w);
+    for (size_t k = 0; k < z.size(); ++k) {
+      if (thetas) thetas[k] = th[k];
+      if (nodes) nodes[k] = lt_complex{z[k].real(), z[k].imag()};
+      if (dnodes) dnodes[k] = lt_complex{dz[k].real(), dz[k].imag()};
+      if (weights) weights[k] = lt_complex{w[k].real(), w[k].imag()};
+    }
+  });
+}
+
+lt_status lt_qhat_step(double q0, lt_complex z, lt_complex* out) {
+  return guard([&] {
+    LT_REQUIRE(!(z.re == 0.0 && z.im == 0.0), "qhat_step: z must be nonzero");
+    const cd v = q0 / cd(z.re, z.im);
+    *out = lt_complex{v.real(), v.imag()};
+  });
+}
+
+lt_status lt_select_preconditioner_shifts(const lt_complex* shifts, int n_shifts, lt_complex* taus, int* n_taus,
+                                          int* pattern, int* pattern_len) {
+  return guard([&] {
+    LT_REQUIRE(n_shifts > 0, "select_preconditioner_shifts: empty shift list");
+    std::vector<cd> s(n_shifts);
+    for (int k = 0; k < n_shifts; ++k) s[k] = cd(shifts[k].re, shifts[k].im);
+    lt::Schedule sch = lt::select_schedule(s);
+    *n_taus = (int)sch.taus.size();
+    for (size_t i = 0; i < sch.taus.size(); ++i) taus[i] = lt_complex{sch.taus[i].real(), sch.taus[i].imag()};
+    *pattern_len = (int)sch.pattern.size();
+    for (size_t i = 0; i < sch.pattern.size(); ++i) pattern[i] = sch.pattern[i];
+  });
+}
+
+lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* log_kappa, const double* log_storativity,
+                                int mem, lt_pencil* out) {
+  return guard([&] {
+    LT_REQUIRE(ctx && grid && out, "lt_pencil_create_grid: null argument");
+    LT_REQUIRE(grid->kind == LT_GRID_FD_CELL, "lt_pencil_create_grid: unsupported grid kind");
+    LT_REQUIRE(grid->dim == 2 || grid->dim == 3, "lt_pencil_create_grid: dim must be 2 or 3");
+    for (int d = 0; d < grid->dim; ++d) LT_REQUIRE(grid->shape[d] >= 1, "lt_pencil_create_grid: empty grid");
+    LT_REQUIRE(grid->h > 0.0, "lt_pencil_create_grid: spacing must be positive");
+    LT_REQUIRE(log_kappa && log_storativity, "assemble: one kappa and one storativity value per element");
+    set_device(ctx);
+    auto* p = new lt_pencil_s();
+    p->ctx = ctx;
+    p->grid = *grid;
+    if (grid->dim == 2) p->grid.shape[2] = 1;
+    p->dim = grid->dim;
+    try {
+      lt::pencil_build(p, log_kappa, log_storativity, mem);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+lt_status lt_pencil_destroy(lt_pencil p) {
+  return guard([&] {
+    if (!p) return;
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    delete p;
+    cudaStreamSynchronize(nullptr);
+  });
+}
+
+int64_t lt_pencil_rows(lt_pencil p) { return p ? p->n : -1; }
+int lt_pencil_levels(lt_pencil p) { return p ? (int)p->levels.size() : -1; }
+
+lt_status lt_pencil_apply(lt_pencil p, lt_complex z, const lt_complex* x, lt_complex* y, int n_rhs, int mem) {
+  return guard([&] { apply_common(p, make_double2(z.re, z.im), x, y, n_rhs, mem, false); });
+}
+
+lt_status lt_pencil_apply_adjoint(lt_pencil p, lt_complex z, const lt_complex* x, lt_complex* y, int n_rhs, int mem) {
+  // K and M are real symmetric: (K + z M)^H = K + conj(z) M (shifted_solver.cpp:112-116)
+  return guard([&] { apply_common(p, make_double2(z.re, -z.im), x, y, n_rhs, mem, false); });
+}
+
+lt_status lt_pencil_apply_mass(lt_pencil p, const lt_complex* x, lt_complex* y, int n_rhs, int mem) {
+  return guard([&] { apply_common(p, make_double2(0, 0), x, y, n_rhs, mem, true); });
+}
+
+lt_status lt_pencil_prepare(lt_pencil p, const lt_complex* taus, int n_taus) {
+  return guard([&] {
+    check_pencil(p);
+    set_device(p->ctx);
+    for (int i = 0; i < n_taus; ++i) p->factor(make_double2(taus[i].re, taus[i].im));
+  });
+}
+
+int lt_pencil_factorization_count(lt_pencil p) { return p ? (int)p->factors.size() : -1; }
+
+lt_status lt_pencil_set_inner_tolerance(lt_pencil p, double rel_tol, int max_iterations) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(rel_tol > 0.0 && max_iterations > 0, "inner tolerance and iteration cap must be positive");
+    p->inner_tol = rel_tol;
+    p->inner_maxit = max_iterations;
+  });
+}
+
+lt_status lt_pencil_solve(lt_pencil p, lt_complex tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
+  return guard([&] { solve_common(p, make_double2(tau.re, tau.im), v, u, n_rhs, mem); });
+}
+
+lt_status lt_pencil_solve_adjoint(lt_pencil p, lt_complex tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
+  return guard([&] { solve_common(p, make_double2(tau.re, -tau.im), v, u, n_rhs, mem); });
+}
+
+lt_status lt_pencil_point_weights(lt_pencil p, const double* point, int64_t* indices, double* weights, int* count) {
+  return guard([&] {
+    check_pencil(p);
+    lt::point_weights(p, point, indices, weights, count);
+  });
+}
+
+void lt_solve_default_options(lt_solve_options* out) {
+  if (out) *out = lt_solve_options{LT_VARIANT_GMRES, 1e-10, 0, 0, 1};
+}
+
+lt_status lt_solve_shifted(lt_pencil p, const lt_complex* b, int n_rhs, const lt_complex* shifts, int n_shifts,
+                           const lt_complex* taus, int n_taus, const int* pattern, int pattern_len,
+                           const lt_solve_options* options, int mem, lt_complex* x_out, lt_shift_status* status,
+                           int* iterations, double* history) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(n_taus > 0 && pattern_len > 0 && taus && pattern,
+               "solve_shifted_flexible: empty preconditioner schedule");
+    for (int i = 0; i < pattern_len; ++i)
+      LT_REQUIRE(pattern[i] >= 0 && pattern[i] < n_taus, "solve_shifted_flexible: pattern index out of range");
+    LT_REQUIRE(n_rhs >= 1 && n_shifts >= 0, "lt_solve_shifted: bad sizes");
+    set_device(p->ctx);
+    cudaStream_t st = p->ctx->stream;
+    lt_solve_options opt;
+    if (options) opt = *options; else lt_solve_default_options(&opt);
+    const int64_t n = p->n;
+    Staged bin = stage_in(b, (size_t)n * n_rhs, mem, st);
+    lt::OuterProblem prob;
+    prob.B = n_rhs;
+    prob.n_shifts = n_shifts;
+    prob.b = bin.ptr;
+    prob.variant = opt.variant;
+    prob.tol = opt.tol;
+    prob.maxit = opt.maxit;
+    prob.record_history = history != nullptr && opt.record_history;
+    prob.keep_basis = opt.keep_basis != 0;
+    const int me = opt.maxit > 0 ? (int)std::min<int64_t>(n, opt.maxit) : (int)std::min<int64_t>(n, 10 * (int64_t)n_shifts);
+    prob.shifts.resize((size_t)n_rhs * n_shifts);
+    prob.tau_table.assign(n_rhs, std::vector<double2>(std::max(me, 1)));
+    for (int r = 0; r < n_rhs; ++r) {
+      for (int k = 0; k < n_shifts; ++k) prob.shifts[(size_t)r * n_shifts + k] = make_double2(shifts[k].re, shifts[k].im);
+      for (int j = 0; j < me; ++j) {
+        const lt_complex t = taus[pattern[j % pattern_len]];
+        prob.tau_table[r][j] = make_double2(t.re, t.im);
+      }
+    }
+    lt::OuterResult res;
+    lt::outer_solve(p, prob, res);
+    if (x_out && n_shifts > 0) {
+      const size_t count = (size_t)n * n_shifts * n_rhs;
+      Staged xo = stage_out(x_out, count, mem, st);
+      lt::expand_solutions(p, res, nullptr, xo.ptr);
+      finish_out(x_out, xo, count, mem, st);
+    }
+    if (status)
+      for (size_t t = 0; t < res.status.size(); ++t) status[t] = res.status[t];
+    if (iterations)
+      for (int r = 0; r < n_rhs; ++r) iterations[r] = res.iterations[r];
+    if (history && prob.record_history) {
+      for (int r = 0; r < n_rhs; ++r)
+        for (int k = 0; k < n_shifts; ++k)
+          for (int j = 0; j < me; ++j)
+            history[((size_t)r * n_shifts + k) * me + j] = res.history[((size_t)r * n_shifts + k) * res.maxit + j];
+    }
+  });
+}
+
+lt_status lt_last_basis(lt_pencil p, int rhs, int* steps_out, double* beta_out, lt_complex* V, lt_complex* U,
+                        lt_complex* Hbar, lt_complex* taus) {
+  return guard([&] {
+    check_pencil(p);
+    const auto& kb = p->kept;
+    LT_REQUIRE(rhs >= 0 && rhs < kb.n_rhs, "lt_last_basis: no kept basis for this rhs (keep_basis = 1?)");
+    const int m = kb.steps[rhs];
+    if (steps_out) *steps_out = m;
+    if (beta_out) *beta_out = kb.beta[rhs];
+    if (V) std::memcpy(V, kb.V[rhs].data(), sizeof(double2) * kb.V[rhs].size());
+    if (U) std::memcpy(U, kb.U[rhs].data(), sizeof(double2) * kb.U[rhs].size());
+    if (Hbar) std::memcpy(Hbar, kb.H[rhs].data(), sizeof(double2) * kb.H[rhs].size());
+    if (taus) std::memcpy(taus, kb.taus[rhs].data(), sizeof(double2) * kb.taus[rhs].size());
+  });
+}
+
+lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs, const lt_complex* shifts, int n_shifts,
+                                  int mem, lt_complex* x_out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(n_rhs >= 1 && n_shifts >= 0 && x_out, "lt_solve_shifted_direct: bad arguments");
+    set_device(p->ctx);
+    cudaStream_t st = p->ctx->stream;
+    const int64_t n = p->n;
+    Staged bin = stage_in(b, (size_t)n * n_rhs, mem, st);
+    const size_t count = (size_t)n * n_shifts * n_rhs;
+    Staged xo = stage_out(x_out, count, mem, st);
+    for (int k = 0; k < n_shifts; ++k) {
+      std::vector<double2> t(n_rhs, make_double2(shifts[k].re, shifts[k].im));
+      lt::inner_solve(p, n_rhs, t.data(), bin.ptr, n, xo.ptr + (size_t)k * n, (int64_t)n * n_shifts);
+    }
+    finish_out(x_out, xo, count, mem, st);
+  });
+}
+
+void lt_solver_default_config(lt_solver_config* out) {
+  if (out) *out = lt_solver_config{LT_SOLVER_FLEXIBLE, LT_VARIANT_GMRES, 1e-10, 0};
+}
+
+lt_status lt_forward(lt_pencil p, const double* sources, const double* rates, int n_src, const double* initial_head,
+                     const double* times, int n_times, int n_quad, const lt_talbot_params* contour,
+                     const lt_solver_config* solver, int pooled, int mem, double* heads_out, const double* receivers,
+                     int n_rec, double* drawdown_out, lt_time_diag* diag_out, double* shift_residuals) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(sources && rates && times, "solve_forward: missing operators");
+    set_device(p->ctx);
+    lt_talbot_params tp;
+    if (contour) tp = *contour; else lt_talbot_default_params(&tp);
+    lt_solver_config cfg;
+    if (solver) cfg = *solver; else lt_solver_default_config(&cfg);
+    lt::forward(p, sources, rates, n_src, initial_head, times, n_times, n_quad, tp, cfg, pooled != 0, mem, heads_out,
+                receivers, n_rec, drawdown_out, diag_out, shift_residuals);
+  });
+}
+
+void lt_experiment_defaults(lt_experiment* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof(*out));
+  out->n_quad = 20;
+  lt_talbot_default_params(&out->contour);
+  lt_solver_default_config(&out->solver);
+  out->include_storativity = 0;
+  out->storativity_z_factor = 1;
+}
+
+lt_status lt_jacobian_slice(lt_pencil p, const lt_experiment* exp, int time_index, int mem, double* jac_out,
+                            double* predictions_out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(exp, "null experiment");
+    set_device(p->ctx);
+    lt::jacobian_slice(p, *exp, time_index, mem, jac_out, predictions_out);
+  });
+}
+
+lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out, double* predictions_out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(exp, "null experiment");
+    set_device(p->ctx);
+    const int64_t n_param = exp->include_storativity ? 2 * p->n : p->n;
+    const int pairs = exp->n_src * exp->n_rec;
+    std::vector<double> slice(jac_out ? (size_t)pairs * n_param : 0), pred(pairs);
+    for (int t = 0; t < exp->n_times; ++t) {
+      lt::jacobian_slice(p, *exp, t, LT_MEM_HOST, jac_out ? slice.data() : nullptr, pred.data());
+      for (int q = 0; q < pairs; ++q) {
+        const size_t row = (size_t)q * exp->n_times + t;  // (s*n_rec + r)*n_times + t
+        if (jac_out) std::memcpy(jac_out + row * n_param, slice.data() + (size_t)q * n_param, sizeof(double) * n_param);
+        if (predictions_out) predictions_out[row] = pred[q];
+      }
+    }
+  });
+}
+
+lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(exp && predictions_out, "null argument");
+    LT_REQUIRE(exp->n_src >= 1 && exp->n_rec >= 1 && exp->n_times >= 1, "ThtForwardModel: experiment must be nonempty");
+    set_device(p->ctx);
+    const int64_t n = p->n;
+    std::vector<double> src((size_t)n * exp->n_src, 0.0);
+    for (int s = 0; s < exp->n_src; ++s) {
+      int64_t idx[8];
+      double w[8];
+      int cnt = 0;
+      lt::point_weights(p, exp->sources + (size_t)s * p->dim, idx, w, &cnt);
+      for (int q = 0; q < cnt; ++q) src[(size_t)s * n + idx[q]] += w[q];
+    }
+    lt::forward(p, src.data(), exp->rates, exp->n_src, nullptr, exp->times, exp->n_times, exp->n_quad, exp->contour,
+                exp->solver, false, LT_MEM_HOST, nullptr, exp->receivers, exp->n_rec, predictions_out, nullptr, nullptr);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// Context: device, stream, launch accounting and per-kernel-class CUDA-event timing.
+#include <algorithm>
+#include <cstring>
+
+#include "lt_internal.hpp"
+
+cudaEvent_t lt_ctx_s::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  LT_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+void lt_ctx_s::resolve_profile() {
+  if (pending.empty()) return;
+  LT_CUDA(cudaEventSynchronize(pending.back().stop));
+  for (auto& pe : pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pe.start, pe.stop);
+    auto& e = profile[pe.name];
+    e.ms += ms;
+    e.launches += 1;
+    e.bytes += pe.bytes;
+    event_pool.push_back(pe.start);
+    event_pool.push_back(pe.stop);
+  }
+  pending.clear();
+}
+
+namespace lt {
+lt_ctx ctx_create(int device) {
+  int count = 0;
+  LT_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) throw Error(LT_ERR_INVALID_ARGUMENT, "lt_ctx_create: bad device index");
+  LT_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  LT_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) throw Error(LT_ERR_CUDA, "lt_ctx_create: this library is built for sm_100a (B200)");
+  auto* ctx = new lt_ctx_s();
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  LT_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  // Keep freed stream-ordered memory in the pool (repeated solves reuse it).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  return ctx;
+}
+
+void ctx_destroy(lt_ctx ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& pe : ctx->pending) {
+    cudaEventDestroy(pe.start);
+    cudaEventDestroy(pe.stop);
+  }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+}  // namespace lt

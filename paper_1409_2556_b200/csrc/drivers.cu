@@ -1,0 +1,662 @@
+// Physics drivers on the device: per-time contour forward solves (solve_forward /
+// solve_forward_batch, forward.cpp:75-198), quadrature recombination in basis form
+// (phi(t) = 2 Re U c, c_j = sum_k w_k qhat_k y_kj; talbot.cpp:82-94 + forward.cpp:104-115),
+// adjoint solves (jacobian.cpp:47-55) and the adjoint-state Jacobian assembly
+// (sensitivity_row_conductivity / _storativity, jacobian.cpp:57-125, FD form of SURVEY
+// App. A) for all source/receiver pairs of a time slice.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "drivers.hpp"
+#include "lt_internal.hpp"
+#include "stencil.cuh"
+#include "talbot_host.hpp"
+
+namespace lt {
+
+thread_local std::vector<int> g_last_unconverged;
+
+namespace {
+
+constexpr int kT = 256;
+using cd = std::complex<double>;
+
+inline double2 d2(cd c) { return make_double2(c.real(), c.imag()); }
+
+// heads[dst[b] + a] += 2 Re sum_j c[b][j] U_j[b][a]   (dst[b] < 0: item skipped)
+__global__ void __launch_bounds__(kT) recombine_kernel(int64_t n, int B, int mc, const double2* const* __restrict__ Ucols,
+                                                       const double2* __restrict__ c, const int64_t* __restrict__ dst,
+                                                       double* __restrict__ heads) {
+  const int b = blockIdx.x % B;
+  const int64_t a = (int64_t)(blockIdx.x / B) * blockDim.x + threadIdx.x;
+  if (a >= n || dst[b] < 0) return;
+  double s = 0.0;
+  for (int j = 0; j < mc; ++j) {
+    const double2 cj = c[b * mc + j];
+    const double2 u = Ucols[j][b * n + a];
+    s += cj.x * u.x - cj.y * u.y;
+  }
+  heads[dst[b] + a] += 2.0 * s;
+}
+
+// drawdown[b][r] = sum_q w_q heads[b][idx_q]
+__global__ void gather_points(int64_t n, int B, int n_pts, const double* __restrict__ heads, const int64_t* __restrict__ idx,
+                              const double* __restrict__ w, const int* __restrict__ cnt, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B * n_pts) return;
+  const int b = t / n_pts, r = t % n_pts;
+  double s = 0.0;
+  for (int q = 0; q < cnt[r]; ++q) s += w[r * 8 + q] * heads[b * n + idx[r * 8 + q]];
+  out[t] = s;
+}
+
+// predictions[s][r] = 2 Re sum_k w_k sum_q wq phi_{s,k}[idx_q]
+__global__ void predict_kernel(int64_t n, int n_src, int n_rec, int ns, const double2* __restrict__ fields,
+                               const double2* __restrict__ w, const int64_t* __restrict__ idx, const double* __restrict__ wt,
+                               const int* __restrict__ cnt, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_src * n_rec) return;
+  const int s = t / n_rec, r = t % n_rec;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = 0; k < ns; ++k) {
+    const double2* f = fields + ((int64_t)s * ns + k) * n;
+    double2 v = make_double2(0.0, 0.0);
+    for (int q = 0; q < cnt[r]; ++q) v = cadd(v, cscale(f[idx[r * 8 + q]], wt[r * 8 + q]));
+    acc = cadd(acc, cmul(w[k], v));
+  }
+  out[t] = 2.0 * acc.x;
+}
+
+// ---- Jacobian assembly -----------------------------------------------------------------
+// J_k[(s,r), a] = 2 Re sum_k w_k sum_{f in faces(a)} dT_f/dln k_a (phi_a - phi_b)(psi_a - psi_b)
+// J_S[(s,r), a] = 2 Re sum_k w_k z_k^p S_a h^d phi_a psi_a
+// A CTA owns TC consecutive cells and a range of (source-block x receiver-block) register
+// tiles; per (shift, face) stage the weighted face differences of all sources (P) and
+// receivers (Q) at its cells are staged in shared memory and every thread accumulates
+// its SB x RB tile of Re(P Q) for one cell.
+constexpr int SB = 4;
+constexpr int RB = 8;
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double* __restrict__ kappa,
+                                                      const double* __restrict__ stor, double hd, double face_scale,
+                                                      const double2* __restrict__ fields, int n_src, int n_rec, int ns,
+                                                      const double2* __restrict__ w, const double2* __restrict__ wz,
+                                                      int TC, int subs_per_cta, int nsub_r, int nsub_total,
+                                                      double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj) {
+  extern __shared__ double2 smem[];
+  const int n_items = n_src + n_rec;
+  double2* P = smem;                    // [n_src][TC]
+  double2* Q = smem + (size_t)n_src * TC;  // [n_rec][TC]
+  double* dT = reinterpret_cast<double*>(Q + (size_t)n_rec * TC);  // [TC]
+  const int64_t n = L.n;
+  const int64_t a0 = (int64_t)blockIdx.x * TC;
+  const int tid = threadIdx.x;
+  const int c = tid % TC;
+  const int sub = blockIdx.y * subs_per_cta + tid / TC;
+  const bool owner = (tid / TC) < subs_per_cta && sub < nsub_total && a0 + c < n;
+  const int s0 = owner ? (sub / nsub_r) * SB : 0;
+  const int r0 = owner ? (sub % nsub_r) * RB : 0;
+  double accK[SB][RB], accS[SB][RB];
+#pragma unroll
+  for (int i = 0; i < SB; ++i)
+#pragma unroll
+    for (int j = 0; j < RB; ++j) { accK[i][j] = 0.0; accS[i][j] = 0.0; }
+
+  const int nfaces = 2 * DIM;
+  for (int k = 0; k < ns; ++k) {
+    const double2 wk = w[k], wzk = wz[k];
+    for (int f = 0; f <= nfaces; ++f) {
+      // per-cell face weight dT_f/dln k_a (or S_a h^d for the storativity stage) and the
+      // neighbour offset (0 when the face is a Dirichlet boundary face)
+      if (tid < TC) {
+        const int64_t a = a0 + tid;
+        double wt = 0.0;
+        if (a < n) {
+          if (f == nfaces) {
+            wt = stor[a] * hd;
+          } else {
+            int i, j, kk;
+            decode<DIM>(L, a, i, j, kk);
+            const int d = f >> 1, hi = f & 1;
+            const int coord = d == 0 ? i : (d == 1 ? j : kk);
+            const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
+            const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : (int64_t)L.nx * L.ny);
+            const double ka = kappa[a];
+            const bool boundary = hi ? coord == ext - 1 : coord == 0;
+            if (boundary) {
+              wt = 2.0 * ka * face_scale;
+            } else {
+              const double kb = kappa[hi ? a + stride : a - stride];
+              const double T = 2.0 * ka * kb / (ka + kb) * face_scale;
+              wt = T * kb / (ka + kb);
+            }
+          }
+        }
+        dT[tid] = wt;
+      }
+      __syncthreads();
+      // stage P (sources, weighted) and Q (receivers)
+      for (int e = tid; e < n_items * TC; e += blockDim.x) {
+        const int it = e / TC, cc = e % TC;
+        const int64_t a = a0 + cc;
+        double2 v = make_double2(0.0, 0.0);
+        if (a < n) {
+          const double2* fld = fields + ((int64_t)it * ns + k) * n;
+          const double2 fa = fld[a];
+          if (f == nfaces) {
+            v = fa;
+          } else {
+            int i, j, kk;
+            decode<DIM>(L, a, i, j, kk);
+            const int d = f >> 1, hi = f & 1;
+            const int coord = d == 0 ? i : (d == 1 ? j : kk);
+            const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
+            const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : (int64_t)L.nx * L.ny);
+            const bool boundary = hi ? coord == ext - 1 : coord == 0;
+            v = boundary ? fa : csub(fa, fld[hi ? a + stride : a - stride]);
+          }
+        }
+        if (it < n_src) {
+          P[(size_t)it * TC + cc] = cscale(cmul(f == nfaces ? wzk : wk, v), dT[cc]);
+        } else {
+          Q[(size_t)(it - n_src) * TC + cc] = v;
+        }
+      }
+      __syncthreads();
+      if (owner) {
+        double2 pv[SB];
+#pragma unroll
+        for (int i = 0; i < SB; ++i) pv[i] = (s0 + i < n_src) ? P[(size_t)(s0 + i) * TC + c] : make_double2(0.0, 0.0);
+        if (f == nfaces) {
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            const double2 qv = (r0 + j < n_rec) ? Q[(size_t)(r0 + j) * TC + c] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < SB; ++i) accS[i][j] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accS[i][j]));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            const double2 qv = (r0 + j < n_rec) ? Q[(size_t)(r0 + j) * TC + c] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < SB; ++i) accK[i][j] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accK[i][j]));
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (!owner) return;
+  const int64_t a = a0 + c;
+#pragma unroll
+  for (int i = 0; i < SB; ++i) {
+    if (s0 + i >= n_src) continue;
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      if (r0 + j >= n_rec) continue;
+      const int64_t row = (int64_t)(s0 + i) * n_rec + (r0 + j);
+      Jk[row * ldj + a] = 2.0 * accK[i][j];
+      if (Js) Js[row * ldj + a] = 2.0 * accS[i][j];
+    }
+  }
+}
+
+struct PointSet {
+  std::vector<int64_t> idx;  // n_pts * 8
+  std::vector<double> w;
+  std::vector<int> cnt;
+};
+
+PointSet make_points(lt_pencil p, const double* pts, int n_pts) {
+  PointSet ps;
+  ps.idx.assign((size_t)n_pts * 8, 0);
+  ps.w.assign((size_t)n_pts * 8, 0.0);
+  ps.cnt.assign(n_pts, 0);
+  for (int r = 0; r < n_pts; ++r)
+    point_weights(p, pts + (size_t)r * p->dim, ps.idx.data() + r * 8, ps.w.data() + r * 8, &ps.cnt[r]);
+  return ps;
+}
+
+std::vector<double> dense_weights(lt_pencil p, const PointSet& ps, int r, double scale) {
+  std::vector<double> v(p->n, 0.0);
+  for (int q = 0; q < ps.cnt[r]; ++q) v[ps.idx[r * 8 + q]] += scale * ps.w[r * 8 + q];
+  return v;
+}
+
+void throw_unconverged(const OuterResult& res, const char* what) {
+  for (int b = 0; b < res.B; ++b) {
+    std::vector<int> bad;
+    for (int k = 0; k < res.n_shifts; ++k)
+      if (!res.status[(size_t)b * res.n_shifts + k].converged) bad.push_back(k);
+    if (!bad.empty()) {
+      g_last_unconverged = bad;
+      throw Error(LT_ERR_NOT_CONVERGED, std::string(what) + ": " + std::to_string(bad.size()) + " of " +
+                                            std::to_string(res.n_shifts) + " shifts unconverged after " +
+                                            std::to_string(res.iterations[b]) + " iterations");
+    }
+  }
+}
+
+// Shifts and schedule of one family (solve_family, forward.cpp:40-71).
+void fill_schedule(OuterProblem& prob, int b, const std::vector<cd>& shifts, int kind, int maxit_eff) {
+  Schedule sch = select_schedule(shifts);
+  if (kind == LT_SOLVER_SINGLE) {
+    sch.taus = {sch.taus[0]};
+    sch.pattern = {0};
+  }
+  prob.tau_table[b].resize(maxit_eff);
+  for (int j = 0; j < maxit_eff; ++j) prob.tau_table[b][j] = d2(sch.tau_at(j));
+  for (size_t k = 0; k < shifts.size(); ++k) prob.shifts[(size_t)b * shifts.size() + k] = d2(shifts[k]);
+}
+
+int effective_maxit(int64_t n, int maxit, int ns) {
+  return maxit > 0 ? (int)std::min<int64_t>(n, maxit) : (int)std::min<int64_t>(n, 10 * (int64_t)ns);
+}
+
+// Direct mode (solve_shifted_direct): one exact shift-and-invert solve per shift, stored as a
+// basis whose coefficient vectors select column k.
+void direct_solve(lt_pencil p, int B, const double2* b_dev, const std::vector<cd>& shifts_all, int ns,
+                  OuterResult& res) {
+  cudaStream_t st = p->ctx->stream;
+  const int64_t n = p->n;
+  res.B = B;
+  res.n_shifts = ns;
+  res.maxit = ns;
+  res.cap = ns;
+  res.iterations.assign(B, 0);
+  res.status.assign((size_t)B * ns, lt_shift_status{1, 0, 0.0, 0.0});
+  res.m_used.assign((size_t)B * ns, 0);
+  res.U.clear();
+  std::vector<double2> Y((size_t)B * ns * ns, make_double2(0, 0));
+  for (int k = 0; k < ns; ++k) {
+    res.U.emplace_back(sizeof(double2) * (size_t)B * n, st);
+    std::vector<double2> taus(B);
+    for (int b = 0; b < B; ++b) taus[b] = d2(shifts_all[(size_t)b * ns + k]);
+    inner_solve(p, B, taus.data(), b_dev, n, res.U.back().as<double2>(), n);
+    for (int b = 0; b < B; ++b) {
+      Y[((size_t)b * ns + k) * ns + k] = make_double2(1.0, 0.0);
+      res.m_used[(size_t)b * ns + k] = k + 1;
+    }
+  }
+  res.Y.allocate(sizeof(double2) * Y.size(), st);
+  LT_CUDA(cudaMemcpyAsync(res.Y.get(), Y.data(), sizeof(double2) * Y.size(), cudaMemcpyHostToDevice, st));
+}
+
+// Run one batch of families (same n_shifts) with the configured solver.
+void solve_families(lt_pencil p, const lt_solver_config& cfg, int B, const double2* b_dev,
+                    const std::vector<std::vector<cd>>& shifts, OuterResult& res) {
+  const int ns = (int)shifts[0].size();
+  if (cfg.kind == LT_SOLVER_DIRECT) {
+    std::vector<cd> all;
+    for (auto& s : shifts) all.insert(all.end(), s.begin(), s.end());
+    direct_solve(p, B, b_dev, all, ns, res);
+    return;
+  }
+  OuterProblem prob;
+  prob.B = B;
+  prob.n_shifts = ns;
+  prob.b = b_dev;
+  prob.variant = cfg.variant;
+  prob.tol = cfg.tol;
+  prob.maxit = cfg.maxit;
+  prob.record_history = false;
+  const int me = effective_maxit(p->n, cfg.maxit, ns);
+  prob.shifts.resize((size_t)B * ns);
+  prob.tau_table.resize(B);
+  for (int b = 0; b < B; ++b) fill_schedule(prob, b, shifts[b], cfg.kind, me);
+  outer_solve(p, prob, res);
+}
+
+// c[b][j] = sum_k coef[b][k] y[b][k][j]  (j < m_used[b][k])
+std::vector<double2> basis_coefficients(const OuterResult& res, const std::vector<cd>& coef, int& mc,
+                                        int k_begin, int k_end, cudaStream_t st) {
+  const int B = res.B, ns = res.n_shifts;
+  std::vector<double2> Y((size_t)B * ns * res.maxit);
+  LT_CUDA(cudaMemcpyAsync(Y.data(), res.Y.get(), sizeof(double2) * Y.size(), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  mc = (int)res.U.size();
+  std::vector<double2> c((size_t)B * std::max(mc, 1), make_double2(0, 0));
+  for (int b = 0; b < B; ++b)
+    for (int k = k_begin; k < k_end; ++k) {
+      const cd ck = coef[(size_t)b * ns + k];
+      const int mu = res.m_used[(size_t)b * ns + k];
+      for (int j = 0; j < mu; ++j) {
+        const double2 y = Y[((size_t)b * ns + k) * res.maxit + j];
+        const cd v = ck * cd(y.x, y.y);
+        c[(size_t)b * mc + j].x += v.real();
+        c[(size_t)b * mc + j].y += v.imag();
+      }
+    }
+  return c;
+}
+
+void recombine(lt_pencil p, const OuterResult& res, const std::vector<double2>& c, int mc,
+               const std::vector<int64_t>& dst, double* heads_dev) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = p->n;
+  const int B = res.B;
+  std::vector<const double2*> cols(std::max(mc, 1), nullptr);
+  for (int j = 0; j < mc; ++j) cols[j] = res.U[j].as<double2>();
+  DeviceBuffer dcols(sizeof(void*) * cols.size(), st), dc(sizeof(double2) * c.size(), st),
+      ddst(sizeof(int64_t) * dst.size(), st);
+  LT_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(void*) * cols.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dc.get(), c.data(), sizeof(double2) * c.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(ddst.get(), dst.data(), sizeof(int64_t) * dst.size(), cudaMemcpyHostToDevice, st));
+  launch(ctx, "recombine", (double)n * B * (16.0 * mc + 16.0), [&] {
+    recombine_kernel<<<blocks_for(n, kT) * B, kT, 0, st>>>(n, B, mc, dcols.as<const double2*>(), dc.as<double2>(),
+                                                            ddst.as<int64_t>(), heads_dev);
+  });
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+void forward(lt_pencil p, const double* sources, const double* rates, int n_src, const double* initial_head,
+             const double* times, int n_times, int n_quad, const lt_talbot_params& contour, const lt_solver_config& cfg,
+             bool pooled, int mem, double* heads_out, const double* receivers, int n_rec, double* drawdown_out,
+             lt_time_diag* diag_out, double* shift_residuals) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = p->n;
+  LT_REQUIRE(n_src >= 1, "solve_forward: no source");
+  LT_REQUIRE(n_times >= 1, "solve_forward: no target times");
+  double previous = 0.0;
+  for (int t = 0; t < n_times; ++t) {
+    LT_REQUIRE(times[t] > 0.0, "solve_forward: times must be positive");
+    LT_REQUIRE(times[t] >= previous, "solve_forward: times must be ascending");
+    previous = times[t];
+  }
+  LT_REQUIRE(n_quad >= 4 && n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
+  const int nh = n_quad / 2;
+  std::vector<std::vector<cd>> nodes(n_times), weights(n_times);
+  for (int t = 0; t < n_times; ++t) talbot_build(n_quad, times[t], contour, nullptr, &nodes[t], nullptr, &weights[t]);
+
+  // host copies of the source vectors (and initial heads) for the families
+  auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  DeviceBuffer src_dev(sizeof(double) * (size_t)n * n_src, st);
+  LT_CUDA(cudaMemcpyAsync(src_dev.get(), sources, sizeof(double) * n * n_src, kind, st));
+  std::vector<double> src_h((size_t)n * n_src);
+  LT_CUDA(cudaMemcpyAsync(src_h.data(), src_dev.get(), sizeof(double) * n * n_src, cudaMemcpyDeviceToHost, st));
+  std::vector<double> ih_h;
+  std::vector<int> with_initial(n_src, 0);
+  if (initial_head) {
+    ih_h.resize((size_t)n * n_src);
+    LT_CUDA(cudaMemcpyAsync(ih_h.data(), initial_head, sizeof(double) * n * n_src,
+                            mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+  for (int s = 0; s < n_src && initial_head; ++s) {
+    double mx = 0.0;
+    for (int64_t a = 0; a < n; ++a) mx = std::max(mx, std::fabs(ih_h[(size_t)s * n + a]));
+    with_initial[s] = mx > 0.0;
+  }
+
+  // Families: (source, time) items with the rate transform, and (source, time) items with
+  // rhs M phi0 when the initial head is nonzero.  Pooled mode: one item per source with the
+  // pooled shifts of every time.
+  struct Fam { int s; int t; bool initial; };
+  std::vector<Fam> fams;
+  for (int s = 0; s < n_src; ++s) {
+    if (pooled) {
+      if (rates[s] != 0.0) fams.push_back({s, -1, false});
+      if (with_initial[s]) fams.push_back({s, -1, true});
+    } else {
+      for (int t = 0; t < n_times; ++t) {
+        if (rates[s] != 0.0) fams.push_back({s, t, false});
+        if (with_initial[s]) fams.push_back({s, t, true});
+      }
+    }
+  }
+  const int F = (int)fams.size();
+  const int ns = pooled ? nh * n_times : nh;
+  DeviceBuffer heads_dev(sizeof(double) * (size_t)n * n_times * n_src, st);
+  LT_CUDA(cudaMemsetAsync(heads_dev.get(), 0, heads_dev.bytes(), st));
+  std::vector<lt_time_diag> diags(n_times, lt_time_diag{0, 1});
+  if (shift_residuals)
+    for (size_t q = 0; q < (size_t)n_src * n_times * nh; ++q) shift_residuals[q] = NAN;
+
+  // item chunks bounded by memory: ~ (2 maxit-columns) vectors per item
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double per_item = (double)n * sizeof(double2) * 14.0;
+  const int chunk = std::max(1, (int)std::min<double>(F, 0.6 * (double)free_b / per_item));
+
+  for (int f0 = 0; f0 < F; f0 += chunk) {
+    const int B = std::min(chunk, F - f0);
+    // right-hand sides
+    std::vector<double2> rhs_h((size_t)B * n);
+    DeviceBuffer rhs(sizeof(double2) * (size_t)B * n, st);
+    std::vector<std::vector<cd>> shifts(B);
+    for (int q = 0; q < B; ++q) {
+      const Fam& fm = fams[f0 + q];
+      if (!fm.initial) {
+        for (int64_t a = 0; a < n; ++a) rhs_h[(size_t)q * n + a] = make_double2(src_h[(size_t)fm.s * n + a], 0.0);
+      }
+      if (pooled) {
+        for (int t = 0; t < n_times; ++t) shifts[q].insert(shifts[q].end(), nodes[t].begin(), nodes[t].end());
+      } else {
+        shifts[q] = nodes[fm.t];
+      }
+    }
+    LT_CUDA(cudaMemcpyAsync(rhs.get(), rhs_h.data(), sizeof(double2) * rhs_h.size(), cudaMemcpyHostToDevice, st));
+    for (int q = 0; q < B; ++q) {
+      const Fam& fm = fams[f0 + q];
+      if (fm.initial) {
+        // rhs = M phi0 (apply_mass)
+        std::vector<double2> ih((size_t)n);
+        for (int64_t a = 0; a < n; ++a) ih[a] = make_double2(ih_h[(size_t)fm.s * n + a], 0.0);
+        DeviceBuffer tmp(sizeof(double2) * n, st);
+        LT_CUDA(cudaMemcpyAsync(tmp.get(), ih.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+        apply_batch(p, 0, nullptr, tmp.as<double2>(), n, rhs.as<double2>() + (size_t)q * n, n, 1, true, "apply_mass");
+        LT_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+    OuterResult res;
+    solve_families(p, cfg, B, rhs.as<double2>(), shifts, res);
+    // diagnostics and convergence (forward.cpp:57-69)
+    for (int q = 0; q < B; ++q) {
+      const Fam& fm = fams[f0 + q];
+      for (int t = 0; t < n_times; ++t) {
+        if (!pooled && fm.t != t) continue;
+        diags[t].iterations = std::max(diags[t].iterations, res.iterations[q]);
+        for (int k = 0; k < ns; ++k) {
+          const auto& stt = res.status[(size_t)q * ns + k];
+          if (!stt.converged) diags[t].all_converged = 0;
+        }
+      }
+      if (shift_residuals && !fm.initial) {
+        for (int k = 0; k < ns; ++k) {
+          const int t = pooled ? k / nh : fm.t;
+          const int kk = pooled ? k % nh : k;
+          shift_residuals[((size_t)fm.s * n_times + t) * nh + kk] = res.status[(size_t)q * ns + k].true_residual;
+        }
+      }
+    }
+    throw_unconverged(res, pooled ? "batch solve" : "shifted solve");
+    // recombination per time into heads[s][t]
+    for (int t = 0; t < n_times; ++t) {
+      std::vector<cd> coef((size_t)B * ns, cd(0.0, 0.0));
+      bool any = false;
+      for (int q = 0; q < B; ++q) {
+        const Fam& fm = fams[f0 + q];
+        if (!pooled && fm.t != t) continue;
+        any = true;
+        for (int k = 0; k < nh; ++k) {
+          const int kk = pooled ? t * nh + k : k;
+          const cd z = nodes[t][k];
+          const cd qh = fm.initial ? cd(1.0, 0.0) : rates[fm.s] / z;  // qhat_step
+          coef[(size_t)q * ns + kk] = weights[t][k] * qh;
+        }
+      }
+      if (!any) continue;
+      int mc = 0;
+      std::vector<double2> c = basis_coefficients(res, coef, mc, 0, ns, st);
+      // two passes so the rate and initial-head families of one (s, t) never race
+      for (int pass = 0; pass < 2; ++pass) {
+        std::vector<int64_t> dst(B, -1);
+        bool anyp = false;
+        for (int q = 0; q < B; ++q) {
+          const Fam& fm = fams[f0 + q];
+          if ((!pooled && fm.t != t) || (int)fm.initial != pass) continue;
+          dst[q] = ((int64_t)fm.s * n_times + t) * n;
+          anyp = true;
+        }
+        if (anyp) recombine(p, res, c, mc, dst, heads_dev.as<double>());
+      }
+      LT_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  if (heads_out) {
+    auto k2 = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    LT_CUDA(cudaMemcpyAsync(heads_out, heads_dev.get(), sizeof(double) * (size_t)n * n_times * n_src, k2, st));
+  }
+  if (receivers && n_rec > 0 && drawdown_out) {
+    PointSet ps = make_points(p, receivers, n_rec);
+    DeviceBuffer didx(sizeof(int64_t) * ps.idx.size(), st), dw(sizeof(double) * ps.w.size(), st),
+        dcnt(sizeof(int) * ps.cnt.size(), st), dout(sizeof(double) * (size_t)n_src * n_times * n_rec, st);
+    LT_CUDA(cudaMemcpyAsync(didx.get(), ps.idx.data(), sizeof(int64_t) * ps.idx.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dw.get(), ps.w.data(), sizeof(double) * ps.w.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dcnt.get(), ps.cnt.data(), sizeof(int) * ps.cnt.size(), cudaMemcpyHostToDevice, st));
+    const int Bh = n_src * n_times;
+    launch(ctx, "gather_points", 0.0, [&] {
+      gather_points<<<blocks_for((int64_t)Bh * n_rec, 128), 128, 0, st>>>(n, Bh, n_rec, heads_dev.as<double>(),
+                                                                          didx.as<int64_t>(), dw.as<double>(), dcnt.as<int>(),
+                                                                          dout.as<double>());
+    });
+    std::vector<double> g((size_t)Bh * n_rec);
+    LT_CUDA(cudaMemcpyAsync(g.data(), dout.get(), sizeof(double) * g.size(), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    // reorder (s, t, r) -> (s, r, t)  (ThtExperiment::measurement_index, jacobian.hpp:37-41)
+    for (int s = 0; s < n_src; ++s)
+      for (int t = 0; t < n_times; ++t)
+        for (int r = 0; r < n_rec; ++r)
+          drawdown_out[((size_t)s * n_rec + r) * n_times + t] = g[((size_t)s * n_times + t) * n_rec + r];
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+  if (diag_out)
+    for (int t = 0; t < n_times; ++t) diag_out[t] = diags[t];
+}
+
+void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double* jac_out, double* pred_out) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = p->n;
+  const int n_src = ex.n_src, n_rec = ex.n_rec;
+  LT_REQUIRE(n_src >= 1 && n_rec >= 1 && ex.n_times >= 1, "ThtForwardModel: experiment must be nonempty");
+  LT_REQUIRE(t >= 0 && t < ex.n_times, "jacobian_slice: time index out of range");
+  LT_REQUIRE(ex.n_quad >= 4 && ex.n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
+  LT_REQUIRE(ex.times[t] > 0.0, "build_contour: time must be positive");
+  const int ns = ex.n_quad / 2;
+  std::vector<cd> nodes, weights;
+  talbot_build(ex.n_quad, ex.times[t], ex.contour, nullptr, &nodes, nullptr, &weights);
+
+  PointSet src = make_points(p, ex.sources, n_src);
+  PointSet rec = make_points(p, ex.receivers, n_rec);
+  const int B = n_src + n_rec;
+  // rhs: sources b_s, receivers -e_r  (jacobian.cpp:216, 227, solve_adjoint_fields cpp:49)
+  std::vector<double2> rhs_h((size_t)B * n, make_double2(0.0, 0.0));
+  for (int s = 0; s < n_src; ++s)
+    for (int q = 0; q < src.cnt[s]; ++q) rhs_h[(size_t)s * n + src.idx[s * 8 + q]].x += src.w[s * 8 + q];
+  for (int r = 0; r < n_rec; ++r)
+    for (int q = 0; q < rec.cnt[r]; ++q) rhs_h[(size_t)(n_src + r) * n + rec.idx[r * 8 + q]].x -= rec.w[r * 8 + q];
+  DeviceBuffer rhs(sizeof(double2) * rhs_h.size(), st);
+  LT_CUDA(cudaMemcpyAsync(rhs.get(), rhs_h.data(), sizeof(double2) * rhs_h.size(), cudaMemcpyHostToDevice, st));
+  std::vector<std::vector<cd>> shifts(B, nodes);
+  OuterResult res;
+  solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
+  // forward failures first (jacobian.cpp:214-218), then adjoint
+  {
+    OuterResult* r = &res;
+    for (int b = 0; b < B; ++b) {
+      std::vector<int> bad;
+      for (int k = 0; k < ns; ++k)
+        if (!r->status[(size_t)b * ns + k].converged) bad.push_back(k);
+      if (!bad.empty()) {
+        g_last_unconverged = bad;
+        throw Error(LT_ERR_NOT_CONVERGED, std::string(b < n_src ? "forward solve" : "adjoint solve") + ": " +
+                                              std::to_string(bad.size()) + " of " + std::to_string(ns) +
+                                              " shifts unconverged after " + std::to_string(r->iterations[b]) + " iterations");
+      }
+    }
+  }
+  // fields: phi_{s,k} = qhat_k U_s y_{s,k}; psi_{r,k} = U_r y_{r,k}
+  std::vector<double2> scale((size_t)B * ns, make_double2(1.0, 0.0));
+  for (int s = 0; s < n_src; ++s)
+    for (int k = 0; k < ns; ++k) scale[(size_t)s * ns + k] = d2(ex.rates[s] / nodes[k]);
+  DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
+  LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
+  DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n, st);
+  expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>());
+  res.U.clear();  // free the bases before the slice
+
+  std::vector<double2> w(ns), wz(ns);
+  for (int k = 0; k < ns; ++k) {
+    w[k] = d2(weights[k]);
+    wz[k] = d2(ex.storativity_z_factor ? weights[k] * nodes[k] : weights[k]);
+  }
+  DeviceBuffer dw(sizeof(double2) * 2 * ns, st);
+  LT_CUDA(cudaMemcpyAsync(dw.get(), w.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dw.as<double2>() + ns, wz.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
+
+  if (jac_out) {
+    const int64_t n_param = ex.include_storativity ? 2 * n : n;
+    double* J = jac_out;
+    DeviceBuffer jtmp;
+    if (mem != LT_MEM_DEVICE) {
+      jtmp.allocate(sizeof(double) * (size_t)n_src * n_rec * n_param, st);
+      J = jtmp.as<double>();
+    }
+    const int nsub_s = (n_src + SB - 1) / SB, nsub_r = (n_rec + RB - 1) / RB;
+    const int nsub_total = nsub_s * nsub_r;
+    const int subs_per_cta = std::min(nsub_total, kT);
+    const int TC = std::max(1, kT / subs_per_cta);
+    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)((nsub_total + subs_per_cta - 1) / subs_per_cta));
+    const size_t smem = sizeof(double2) * (size_t)B * TC + sizeof(double) * TC;
+    LevelView L = p->view(0);
+    const double h = p->grid.h;
+    const double face_scale = p->dim == 3 ? h : 1.0;
+    const double hd = p->dim == 3 ? h * h * h : h * h;
+    const double flops = 2.0 * 2.0 * (double)n * n_src * n_rec * ns * (2 * p->dim + 1);
+    (void)flops;
+    const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
+    if (smem > 48 * 1024) {
+      auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
+      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    launch(ctx, "jacobian", bytes, [&] {
+      if (p->dim == 3)
+        jacobian_kernel<3><<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
+                                                   fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(),
+                                                   dw.as<double2>() + ns, TC, subs_per_cta, nsub_r, nsub_total, J,
+                                                   ex.include_storativity ? J + n : nullptr, n_param);
+      else
+        jacobian_kernel<2><<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
+                                                   fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(),
+                                                   dw.as<double2>() + ns, TC, subs_per_cta, nsub_r, nsub_total, J,
+                                                   ex.include_storativity ? J + n : nullptr, n_param);
+    });
+    if (mem != LT_MEM_DEVICE)
+      LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
+  }
+  if (pred_out) {
+    DeviceBuffer didx(sizeof(int64_t) * rec.idx.size(), st), dwt(sizeof(double) * rec.w.size(), st),
+        dcnt(sizeof(int) * rec.cnt.size(), st), dout(sizeof(double) * (size_t)n_src * n_rec, st);
+    LT_CUDA(cudaMemcpyAsync(didx.get(), rec.idx.data(), sizeof(int64_t) * rec.idx.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dwt.get(), rec.w.data(), sizeof(double) * rec.w.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dcnt.get(), rec.cnt.data(), sizeof(int) * rec.cnt.size(), cudaMemcpyHostToDevice, st));
+    launch(ctx, "predict", 0.0, [&] {
+      predict_kernel<<<blocks_for((int64_t)n_src * n_rec, 128), 128, 0, st>>>(n, n_src, n_rec, ns, fields.as<double2>(),
+                                                                             dw.as<double2>(), didx.as<int64_t>(),
+                                                                             dwt.as<double>(), dcnt.as<int>(), dout.as<double>());
+    });
+    LT_CUDA(cudaMemcpyAsync(pred_out, dout.get(), sizeof(double) * (size_t)n_src * n_rec, cudaMemcpyDeviceToHost, st));
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace lt

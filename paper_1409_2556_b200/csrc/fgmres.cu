@@ -1,0 +1,838 @@
+// Flexible shifted FOM/GMRES (FGMRES-Sh, Algorithm 1) on the device, batched over B
+// right-hand sides in lockstep.  Restates run_flexible (shifted_solver.cpp:132-287):
+//   v0 = b/beta;  per iteration j:  u_j = (K + tau_j M)^{-1} v_j  (inner.cu);  s = M u_j;
+//   Gram-Schmidt of s against V_{j+1} with one conditional re-orthogonalisation when the
+//   norm drops below 1/sqrt(2) of its value (cpp:196-210; classical GS passes, which equal
+//   the reference's MGS in exact arithmetic and read each basis vector once);
+//   h_{j+1,j} = ||s||, breakdown at <= 1e-14 ||s0||;  per unconverged shift the small
+//   problem on Hbar(z; T) = [I; 0] + Hbar (z I - T) (cpp:26-65: GMRES least squares via
+//   Givens QR, FOM via Hessenberg partial-pivot LU), estimate/beta <= verify_at triggers
+//   the true-residual check ||b - (K + zM) U y|| / beta (fused stencil kernel) and a
+//   freeze, otherwise verify_at = estimate/2 (cpp:235-249).
+// Solutions stay in basis form (U, y); expand_solutions materialises x = U y on demand.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "lt_internal.hpp"
+#include "stencil.cuh"
+
+namespace lt {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr double kBreakdownTol = 1e-14;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffff, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum_c(double2 v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffff, v.x, o);
+    v.y += __shfl_down_sync(0xffffffff, v.y, o);
+  }
+  return v;
+}
+// block reduction into thread 0 using caller-provided shared scratch of 32 entries
+__device__ __forceinline__ double2 block_sum_c(double2 v, double2* sh) {
+  v = warp_sum_c(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : make_double2(0.0, 0.0);
+    v = warp_sum_c(v);
+  }
+  return v;
+}
+__device__ __forceinline__ double block_sum_d(double v, double* sh) {
+  v = warp_sum_d(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+    v = warp_sum_d(v);
+  }
+  return v;
+}
+
+struct State {
+  int B, ns, maxit, cap;
+  int64_t n;
+  int nblk;
+  double tol;
+  int variant;
+  int record_history;
+  const int* active;     // B: item still iterating
+  const double* beta;    // B
+  const double2* shifts; // B*ns
+  const double2* taus;   // B*maxit (tau applied at iteration j)
+  double2* H;            // B*maxit*(maxit+1): H[(b*maxit + j)*(maxit+1) + i] = h_{i,j}
+  int* conv;             // B*ns
+  int* iter;
+  double* est;
+  double* true_res;
+  double* verify_at;
+  int* flag;             // B*ns: verify requested this iteration
+  int* m_used;           // B*ns
+  double2* Y;            // B*ns*maxit
+  double* history;       // B*ns*maxit or null
+  double2* scratch;      // B*ns*(cap+1)*cap
+  double* norm0;         // B: ||s|| before orthogonalisation
+  double* norm1;         // B: ||s|| after the first pass
+  int* reorth;           // B
+  int* breakdown;        // B
+  double* hnext;         // B
+  int* n_unconv;         // B
+};
+
+// s = M u (written into V_{j+1}), partial conj(V_i) . s for i <= j and ||s||^2
+template <int DIM>
+__global__ void __launch_bounds__(kT) mass_multidot(LevelView L, State S, int j, const double2* __restrict__ u,
+                                                    double2* __restrict__ s_out, const double2* const* __restrict__ Vcols,
+                                                    double2* __restrict__ part) {
+  __shared__ double2 sh[32];
+  const int b = blockIdx.x % S.B;
+  const int64_t cb = blockIdx.x / S.B;
+  if (!S.active[b]) return;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = a < L.n;
+  double2 s = make_double2(0.0, 0.0);
+  if (in) {
+    s = cscale(u[b * L.n + a], __ldg(L.M + a));
+    s_out[b * L.n + a] = s;
+  }
+  double2* pb = part + (int64_t)b * (j + 2) * S.nblk;
+  for (int i = 0; i <= j; ++i) {
+    double2 v = in ? Vcols[i][b * L.n + a] : make_double2(0.0, 0.0);
+    double2 d = block_sum_c(cmulc(v, s), sh);
+    if (threadIdx.x == 0) pb[(int64_t)i * S.nblk + cb] = d;
+  }
+  double2 nn = block_sum_c(make_double2(cabs2(s), 0.0), sh);
+  if (threadIdx.x == 0) pb[(int64_t)(j + 1) * S.nblk + cb] = nn;
+}
+
+// partial conj(V_i) . s for i <= j (re-orthogonalisation pass, items with reorth set)
+__global__ void __launch_bounds__(kT) multidot(State S, int j, const double2* __restrict__ s_in,
+                                               const double2* const* __restrict__ Vcols, double2* __restrict__ part) {
+  __shared__ double2 sh[32];
+  const int b = blockIdx.x % S.B;
+  const int64_t cb = blockIdx.x / S.B;
+  if (!S.active[b] || !S.reorth[b]) return;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = a < S.n;
+  const double2 s = in ? s_in[b * S.n + a] : make_double2(0.0, 0.0);
+  double2* pb = part + (int64_t)b * (j + 2) * S.nblk;
+  for (int i = 0; i <= j; ++i) {
+    double2 v = in ? Vcols[i][b * S.n + a] : make_double2(0.0, 0.0);
+    double2 d = block_sum_c(cmulc(v, s), sh);
+    if (threadIdx.x == 0) pb[(int64_t)i * S.nblk + cb] = d;
+  }
+}
+
+// sum the partials: coefficients into hcoef[b*(j+1) + i] (pass 0: set; pass 1: add into H),
+// norm into norm0 (pass 0)
+__global__ void __launch_bounds__(kT) reduce_dots(State S, int j, const double2* __restrict__ part, int pass,
+                                                  double2* __restrict__ hcoef) {
+  __shared__ double2 sh[32];
+  const int b = blockIdx.x / (j + 2);
+  const int i = blockIdx.x % (j + 2);
+  if (!S.active[b]) return;
+  if (pass == 1 && (!S.reorth[b] || i == j + 1)) return;
+  const double2* pb = part + ((int64_t)b * (j + 2) + i) * S.nblk;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = threadIdx.x; k < S.nblk; k += blockDim.x) s = cadd(s, pb[k]);
+  s = block_sum_c(s, sh);
+  if (threadIdx.x != 0) return;
+  if (i == j + 1) {
+    S.norm0[b] = sqrt(s.x);
+    return;
+  }
+  hcoef[b * (j + 1) + i] = s;
+  double2* Hc = S.H + ((int64_t)b * S.maxit + j) * (S.maxit + 1);
+  if (pass == 0) Hc[i] = s;
+  else Hc[i] = cadd(Hc[i], s);
+}
+
+// s -= sum_i c_i V_i ; partial ||s||^2 (pass 1 only for reorth items)
+__global__ void __launch_bounds__(kT) gs_update(State S, int j, int pass, double2* __restrict__ s_io,
+                                                const double2* const* __restrict__ Vcols,
+                                                const double2* __restrict__ hcoef, double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x % S.B;
+  const int64_t cb = blockIdx.x / S.B;
+  if (!S.active[b]) return;
+  if (pass == 1 && !S.reorth[b]) return;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  double nn = 0.0;
+  if (a < S.n) {
+    double2 s = s_io[b * S.n + a];
+    for (int i = 0; i <= j; ++i) s = csub(s, cmul(hcoef[b * (j + 1) + i], Vcols[i][b * S.n + a]));
+    s_io[b * S.n + a] = s;
+    nn = cabs2(s);
+  }
+  nn = block_sum_d(nn, sh);
+  if (threadIdx.x == 0) part[(int64_t)b * S.nblk + cb] = nn;
+}
+
+// after pass `pass`: norm of s; pass 0 decides re-orthogonalisation; the final pass
+// sets h_{j+1,j}, breakdown and 1/h.
+__global__ void __launch_bounds__(kT) reduce_norm(State S, int j, int pass, const double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x;
+  if (!S.active[b]) return;
+  if (pass == 1 && !S.reorth[b]) return;
+  const double* pb = part + (int64_t)b * S.nblk;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < S.nblk; k += blockDim.x) s += pb[k];
+  s = block_sum_d(s, sh);
+  if (threadIdx.x != 0) return;
+  const double nrm = sqrt(s);
+  if (pass == 0) {
+    S.norm1[b] = nrm;
+    S.reorth[b] = nrm < S.norm0[b] / sqrt(2.0);
+  }
+  if (pass == 1 || !S.reorth[b]) {
+    double2* Hc = S.H + ((int64_t)b * S.maxit + j) * (S.maxit + 1);
+    Hc[j + 1] = make_double2(nrm, 0.0);
+    S.hnext[b] = nrm;
+    S.breakdown[b] = nrm <= kBreakdownTol * S.norm0[b];
+  }
+}
+
+__global__ void __launch_bounds__(kT) normalize(State S, double2* __restrict__ v) {
+  const int b = blockIdx.x % S.B;
+  const int64_t cb = blockIdx.x / S.B;
+  if (!S.active[b] || S.breakdown[b]) return;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  if (a < S.n) {
+    const double inv = 1.0 / S.hnext[b];
+    v[b * S.n + a] = cscale(v[b * S.n + a], inv);
+  }
+}
+
+// hz(i, l) = h_{i,l} (z - tau_l) + delta_il, i <= l + 1
+__device__ __forceinline__ double2 hz_entry(const State& S, int b, int i, int l, double2 z) {
+  if (i > l + 1) return make_double2(0.0, 0.0);
+  const double2 h = S.H[((int64_t)b * S.maxit + l) * (S.maxit + 1) + i];
+  double2 v = cmul(h, csub(z, S.taus[(int64_t)b * S.maxit + l]));
+  if (i == l) v.x += 1.0;
+  return v;
+}
+
+// Per (item, shift): small least-squares (GMRES) / square (FOM) solve on Hbar_m(z; T_m),
+// history, verify decision.  force: best-effort pass for unconverged shifts at the end.
+__global__ void small_solve(State S, int m, int force) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= S.B * S.ns) return;
+  const int b = t / S.ns, k = t % S.ns;
+  S.flag[t] = 0;
+  if (!S.active[b]) return;
+  if (S.conv[t]) return;
+  const double2 z = S.shifts[t];
+  const double beta = S.beta[b];
+  const int ld = m + 1;
+  double2* W = S.scratch + (int64_t)t * (S.cap + 1) * S.cap;  // column-major (m+1) x m
+  for (int l = 0; l < m; ++l)
+    for (int i = 0; i <= m; ++i) W[(int64_t)l * ld + i] = hz_entry(S, b, i, l, z);
+  double2* y = S.Y + (int64_t)t * S.maxit;
+  bool valid = true;
+  double estimate = INFINITY;
+  if (S.variant == LT_VARIANT_GMRES) {
+    // Givens QR of the Hessenberg hz; rhs g = beta e1 (stored in y[0..m], y has maxit >= m+1? no)
+    // rotated rhs g = beta e1: g_0..g_{m-1} live in y, g_m in gm
+    double2 g[2];
+    y[0] = make_double2(beta, 0.0);
+    for (int l = 1; l < m; ++l) y[l] = make_double2(0.0, 0.0);
+    double2 gm = make_double2(0.0, 0.0);
+    for (int l = 0; l < m; ++l) {
+      const double2 x1 = W[(int64_t)l * ld + l];
+      const double2 x2 = W[(int64_t)l * ld + l + 1];
+      const double ax = sqrt(cabs2(x1)), r = sqrt(cabs2(x1) + cabs2(x2));
+      if (!(r > 0.0)) { valid = false; break; }
+      double cs;
+      double2 sn, ph;
+      if (ax == 0.0) {
+        cs = 0.0; sn = make_double2(1.0, 0.0); ph = make_double2(1.0, 0.0);
+      } else {
+        cs = ax / r;
+        ph = cscale(x1, 1.0 / ax);
+        sn = cmul(ph, cscale(cconj(x2), 1.0 / r));  // (a/|a|) conj(b) / r
+      }
+      // rows l, l+1:  [cs  sn; -conj(sn)  cs]
+      for (int c = l; c < m; ++c) {
+        const double2 a1 = W[(int64_t)c * ld + l], a2 = W[(int64_t)c * ld + l + 1];
+        W[(int64_t)c * ld + l] = cadd(cscale(a1, cs), cmul(sn, a2));
+        W[(int64_t)c * ld + l + 1] = csub(cscale(a2, cs), cmul(cconj(sn), a1));
+      }
+      const double2 g1 = y[l];
+      const double2 g2 = (l + 1 < m) ? y[l + 1] : gm;
+      g[0] = cadd(cscale(g1, cs), cmul(sn, g2));
+      g[1] = csub(cscale(g2, cs), cmul(cconj(sn), g1));
+      y[l] = g[0];
+      if (l + 1 < m) y[l + 1] = g[1]; else gm = g[1];
+    }
+    if (valid) {
+      for (int l = m - 1; l >= 0; --l) {
+        double2 acc = y[l];
+        for (int c = l + 1; c < m; ++c) acc = csub(acc, cmul(W[(int64_t)c * ld + l], y[c]));
+        y[l] = cdiv(acc, W[(int64_t)l * ld + l]);
+        if (!isfinite(y[l].x) || !isfinite(y[l].y)) valid = false;
+      }
+    }
+    if (valid) {
+      // explicit ||beta e1 - hz y|| (cpp:61)
+      double ss = 0.0;
+      for (int i = 0; i <= m; ++i) {
+        double2 r = make_double2(i == 0 ? beta : 0.0, 0.0);
+        const int l0 = i > 0 ? i - 1 : 0;
+        for (int l = l0; l < m; ++l) r = csub(r, cmul(hz_entry(S, b, i, l, z), y[l]));
+        ss += cabs2(r);
+      }
+      estimate = sqrt(ss);
+    }
+  } else {
+    // FOM: Hessenberg LU with partial pivoting on the m x m top (cpp:36-51)
+    y[0] = make_double2(beta, 0.0);
+    for (int l = 1; l < m; ++l) y[l] = make_double2(0.0, 0.0);
+    for (int l = 0; l < m && valid; ++l) {
+      if (l + 1 < m) {
+        const double2 p1 = W[(int64_t)l * ld + l], p2 = W[(int64_t)l * ld + l + 1];
+        if (cabs2(p2) > cabs2(p1)) {
+          for (int c = l; c < m; ++c) {
+            double2 tmp = W[(int64_t)c * ld + l];
+            W[(int64_t)c * ld + l] = W[(int64_t)c * ld + l + 1];
+            W[(int64_t)c * ld + l + 1] = tmp;
+          }
+          double2 tmp = y[l]; y[l] = y[l + 1]; y[l + 1] = tmp;
+        }
+        const double2 piv = W[(int64_t)l * ld + l];
+        if (!(cabs2(piv) > 0.0)) { valid = false; break; }
+        const double2 f = cdiv(W[(int64_t)l * ld + l + 1], piv);
+        for (int c = l; c < m; ++c)
+          W[(int64_t)c * ld + l + 1] = csub(W[(int64_t)c * ld + l + 1], cmul(f, W[(int64_t)c * ld + l]));
+        y[l + 1] = csub(y[l + 1], cmul(f, y[l]));
+      }
+    }
+    if (valid) {
+      for (int l = m - 1; l >= 0; --l) {
+        double2 acc = y[l];
+        for (int c = l + 1; c < m; ++c) acc = csub(acc, cmul(W[(int64_t)c * ld + l], y[c]));
+        y[l] = cdiv(acc, W[(int64_t)l * ld + l]);
+        if (!isfinite(y[l].x) || !isfinite(y[l].y)) valid = false;
+      }
+    }
+    if (valid) {
+      const double2 hmm = hz_entry(S, b, m, m - 1, z);
+      estimate = sqrt(cabs2(cmul(hmm, y[m - 1])));
+    }
+  }
+  if (!valid) {
+    if (!force && S.record_history) S.history[(int64_t)t * S.maxit + (m - 1)] = S.est[t];
+    return;
+  }
+  if (force) {
+    S.flag[t] = 1;
+    return;
+  }
+  S.est[t] = estimate / beta;
+  if (S.record_history) S.history[(int64_t)t * S.maxit + (m - 1)] = S.est[t];
+  if (S.est[t] <= S.verify_at[t] || S.breakdown[b]) S.flag[t] = 1;
+}
+
+// True residual r = b - (K + z M) U y for every flagged shift of an item:
+// partial ||r||^2 per (item, shift).  K u_j and M u_j are formed once per column.
+template <int DIM>
+__global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int m, const double2* __restrict__ rhs,
+                                                      const double2* const* __restrict__ Ucols, double* __restrict__ part) {
+  constexpr int KC = 8;  // shifts per register chunk
+  __shared__ double sh[32];
+  __shared__ int flagged[256];
+  __shared__ int nflag;
+  const int b = blockIdx.x % S.B;
+  const int64_t cb = blockIdx.x / S.B;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int k = 0; k < S.ns && c < 256; ++k)
+      if (S.flag[b * S.ns + k]) flagged[c++] = k;
+    nflag = c;
+  }
+  __syncthreads();
+  if (nflag == 0) return;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  const bool in = a < L.n;
+  int i = 0, jj = 0, kk = 0;
+  if (in) decode<DIM>(L, a, i, jj, kk);
+  const double2 bv = in ? rhs[b * L.n + a] : make_double2(0.0, 0.0);
+  const double mval = in ? __ldg(L.M + a) : 0.0;
+  for (int c0 = 0; c0 < nflag; c0 += KC) {
+    const int nc = min(KC, nflag - c0);
+    double2 acc[KC];
+#pragma unroll
+    for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
+    if (in) {
+      for (int j = 0; j < m; ++j) {
+        const double2* ub = Ucols[j] + b * L.n;
+        double2 off;
+        double dk;
+        gather<DIM>(L, ub, a, i, jj, kk, off, dk);
+        const double2 ua = ub[a];
+        const double2 Ku = csub(cscale(ua, dk), off);
+        const double2 Mu = cscale(ua, mval);
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          if (q < nc) {
+            const int t = b * S.ns + flagged[c0 + q];
+            const double2 y = S.Y[(int64_t)t * S.maxit + j];
+            acc[q] = cadd(acc[q], cmul(y, cadd(Ku, cmul(S.shifts[t], Mu))));
+          }
+        }
+      }
+    }
+    for (int q = 0; q < nc; ++q) {
+      const double2 r = csub(bv, acc[q]);
+      const double nn = block_sum_d(in ? cabs2(r) : 0.0, sh);
+      if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk + cb] = nn;
+    }
+  }
+}
+
+// per (item, shift) flagged: true_rel; freeze or back off.  best_effort: record only.
+__global__ void __launch_bounds__(kT) verify_finalize(State S, int m, const double* __restrict__ part, int best_effort) {
+  __shared__ double sh[32];
+  const int t = blockIdx.x;
+  if (!S.flag[t]) return;
+  const int b = t / S.ns;
+  const double* pb = part + (int64_t)t * S.nblk;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < S.nblk; k += blockDim.x) s += pb[k];
+  s = block_sum_d(s, sh);
+  if (threadIdx.x != 0) return;
+  const double true_rel = sqrt(s) / S.beta[b];
+  S.flag[t] = 0;
+  if (best_effort) {
+    S.true_res[t] = true_rel;
+    S.m_used[t] = m;
+    return;
+  }
+  if (true_rel <= S.tol || S.breakdown[b]) {
+    S.conv[t] = 1;
+    S.iter[t] = m;
+    S.true_res[t] = true_rel;
+    S.m_used[t] = m;
+  } else {
+    S.verify_at[t] = S.est[t] / 2.0;
+  }
+}
+
+__global__ void count_unconverged(State S, int m) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= S.B) return;
+  int c = 0;
+  for (int k = 0; k < S.ns; ++k) c += !S.conv[b * S.ns + k];
+  S.n_unconv[b] = c;
+}
+
+__global__ void __launch_bounds__(kT) norm_kernel(int64_t n, int B, const double2* __restrict__ x, double* __restrict__ part,
+                                                  int nblk) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x % B;
+  const int64_t cb = blockIdx.x / B;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  double s = a < n ? cabs2(x[b * n + a]) : 0.0;
+  s = block_sum_d(s, sh);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
+}
+
+__global__ void __launch_bounds__(kT) reduce_beta(int B, int nblk, const double* __restrict__ part, double* __restrict__ beta) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < nblk; k += blockDim.x) s += part[(int64_t)b * nblk + k];
+  s = block_sum_d(s, sh);
+  if (threadIdx.x == 0) beta[b] = sqrt(s);
+}
+
+__global__ void __launch_bounds__(kT) scale_to(int64_t n, int B, const double2* __restrict__ x, const double* __restrict__ beta,
+                                               double2* __restrict__ v) {
+  const int b = blockIdx.x % B;
+  const int64_t cb = blockIdx.x / B;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const double bt = beta[b];
+  v[b * n + a] = bt > 0.0 ? cscale(x[b * n + a], 1.0 / bt) : make_double2(0.0, 0.0);
+}
+
+// x_out[(b*ns + k)*n + a] = scale_{b,k} sum_{j < m_used} Y[b,k,j] U_j[b][a]
+__global__ void __launch_bounds__(kT) expand_kernel(int64_t n, int B, int ns, int maxit, const double2* const* __restrict__ Ucols,
+                                                    const double2* __restrict__ Y, const int* __restrict__ m_used,
+                                                    const double2* __restrict__ scale, double2* __restrict__ out) {
+  const int b = blockIdx.x % B;
+  const int64_t cb = blockIdx.x / B;
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  int mmax = 0;
+  for (int k = 0; k < ns; ++k) mmax = max(mmax, m_used[b * ns + k]);
+  constexpr int KC = 16;
+  for (int k0 = 0; k0 < ns; k0 += KC) {
+    double2 acc[KC];
+#pragma unroll
+    for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int j = 0; j < mmax; ++j) {
+      const double2 u = Ucols[j][b * n + a];
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        const int k = k0 + q;
+        if (k < ns && j < m_used[b * ns + k]) acc[q] = cfma(Y[((int64_t)b * ns + k) * maxit + j], u, acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      const int k = k0 + q;
+      if (k < ns) out[((int64_t)b * ns + k) * n + a] = scale ? cmul(scale[b * ns + k], acc[q]) : acc[q];
+    }
+  }
+}
+
+}  // namespace
+
+void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int B = prob.B, ns = prob.n_shifts;
+  const int64_t n = p->n;
+  const int nblk = (int)blocks_for(n, kT);
+  const int maxit = prob.maxit > 0 ? (int)std::min<int64_t>(n, prob.maxit) : (int)std::min<int64_t>(n, 10 * (int64_t)ns);
+  res.B = B;
+  res.n_shifts = ns;
+  res.maxit = maxit;
+  res.iterations.assign(B, 0);
+  res.status.assign((size_t)B * ns, lt_shift_status{0, 0, INFINITY, NAN});
+  res.m_used.assign((size_t)B * ns, 0);
+  res.U.clear();
+  if (prob.record_history) res.history.assign((size_t)B * ns * maxit, NAN);
+  if (B == 0 || ns == 0) return;
+
+  // ---- device state ----
+  int cap = std::min(maxit, 8);
+  const size_t n_bs = (size_t)B * ns;
+  DeviceBuffer dH(sizeof(double2) * (size_t)B * maxit * (maxit + 1), st);
+  LT_CUDA(cudaMemsetAsync(dH.get(), 0, dH.bytes(), st));
+  DeviceBuffer dTaus(sizeof(double2) * (size_t)B * maxit, st);
+  DeviceBuffer dShifts(sizeof(double2) * n_bs, st);
+  DeviceBuffer dY(sizeof(double2) * n_bs * maxit, st);
+  LT_CUDA(cudaMemsetAsync(dY.get(), 0, dY.bytes(), st));
+  DeviceBuffer dHist(prob.record_history ? sizeof(double) * n_bs * maxit : 8, st);
+  DeviceBuffer ints(sizeof(int) * (n_bs * 4 + (size_t)B * 5), st);
+  DeviceBuffer dbls(sizeof(double) * (n_bs * 3 + (size_t)B * 4), st);
+  int* conv = ints.as<int>();
+  int* iter = conv + n_bs;
+  int* flag = iter + n_bs;
+  int* m_used = flag + n_bs;
+  int* active = m_used + n_bs;
+  int* reorth = active + B;
+  int* brk = reorth + B;
+  int* n_unconv = brk + B;
+  double* est = dbls.as<double>();
+  double* true_res = est + n_bs;
+  double* verify_at = true_res + n_bs;
+  double* beta = verify_at + n_bs;
+  double* norm0 = beta + B;
+  double* norm1 = norm0 + B;
+  double* hnext = norm1 + B;
+  LT_CUDA(cudaMemsetAsync(ints.get(), 0, ints.bytes(), st));
+  {
+    std::vector<double> init(n_bs * 3);
+    for (size_t t = 0; t < n_bs; ++t) {
+      init[t] = INFINITY;
+      init[n_bs + t] = NAN;
+      init[2 * n_bs + t] = prob.tol;
+    }
+    LT_CUDA(cudaMemcpyAsync(est, init.data(), sizeof(double) * n_bs * 3, cudaMemcpyHostToDevice, st));
+    std::vector<double2> taus((size_t)B * maxit);
+    for (int b = 0; b < B; ++b)
+      for (int j = 0; j < maxit; ++j) taus[(size_t)b * maxit + j] = prob.tau_table[b][j];
+    LT_CUDA(cudaMemcpyAsync(dTaus.get(), taus.data(), sizeof(double2) * taus.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dShifts.get(), prob.shifts.data(), sizeof(double2) * n_bs, cudaMemcpyHostToDevice, st));
+    if (prob.record_history) {
+      std::vector<double> h(n_bs * maxit, NAN);
+      LT_CUDA(cudaMemcpyAsync(dHist.get(), h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st));
+    }
+  }
+  DeviceBuffer dScratch(sizeof(double2) * n_bs * (cap + 1) * cap, st);
+  DeviceBuffer dColPtr(sizeof(void*) * (maxit + 1) * 2, st);
+  const double2** dVcols = dColPtr.as<const double2*>();
+  const double2** dUcols = dVcols + (maxit + 1);
+  std::vector<DeviceBuffer> Vc;
+  std::vector<const double2*> vptr, uptr;
+  auto add_v = [&]() {
+    Vc.emplace_back(sizeof(double2) * (size_t)B * n, st);
+    vptr.push_back(Vc.back().as<double2>());
+  };
+  auto add_u = [&]() {
+    res.U.emplace_back(sizeof(double2) * (size_t)B * n, st);
+    uptr.push_back(res.U.back().as<double2>());
+  };
+  DeviceBuffer partials;
+  DeviceBuffer hcoef(sizeof(double2) * (size_t)B * (maxit + 1), st);
+
+  State S{};
+  S.B = B; S.ns = ns; S.maxit = maxit; S.cap = cap; S.n = n; S.nblk = nblk;
+  S.tol = prob.tol; S.variant = prob.variant; S.record_history = prob.record_history;
+  S.active = active; S.beta = beta; S.shifts = dShifts.as<double2>(); S.taus = dTaus.as<double2>();
+  S.H = dH.as<double2>(); S.conv = conv; S.iter = iter; S.est = est; S.true_res = true_res;
+  S.verify_at = verify_at; S.flag = flag; S.m_used = m_used; S.Y = dY.as<double2>();
+  S.history = prob.record_history ? dHist.as<double>() : nullptr; S.scratch = dScratch.as<double2>();
+  S.norm0 = norm0; S.norm1 = norm1; S.reorth = reorth; S.breakdown = brk; S.hnext = hnext; S.n_unconv = n_unconv;
+
+  const unsigned grid = (unsigned)nblk * (unsigned)B;
+  const double nb = (double)n * B;
+  LevelView L0 = p->view(0);
+
+  // beta = ||b||, v0 = b / beta
+  partials.ensure(sizeof(double2) * (size_t)B * nblk * 2, st);
+  launch(ctx, "fgmres_vec", nb * 16.0, [&] { norm_kernel<<<grid, kT, 0, st>>>(n, B, prob.b, partials.as<double>(), nblk); });
+  launch(ctx, "fgmres_small", 0.0, [&] { reduce_beta<<<B, kT, 0, st>>>(B, nblk, partials.as<double>(), beta); });
+  add_v();
+  launch(ctx, "fgmres_vec", nb * 32.0, [&] { scale_to<<<grid, kT, 0, st>>>(n, B, prob.b, beta, Vc[0].as<double2>()); });
+  std::vector<double> h_beta(B);
+  LT_CUDA(cudaMemcpyAsync(h_beta.data(), beta, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+
+  std::vector<int> h_active(B, 1);
+  {
+    // beta == 0: every shift converged with zero estimate / residual (cpp:147-156)
+    std::vector<int> conv0(n_bs, 0);
+    std::vector<double> est0(n_bs, 0.0);
+    bool any = false;
+    for (int b = 0; b < B; ++b)
+      if (!(h_beta[b] > 0.0)) {
+        h_active[b] = 0;
+        any = true;
+        for (int k = 0; k < ns; ++k) conv0[(size_t)b * ns + k] = 1;
+      }
+    if (any) {
+      for (int b = 0; b < B; ++b)
+        if (!h_active[b])
+          for (int k = 0; k < ns; ++k) {
+            res.status[(size_t)b * ns + k] = lt_shift_status{1, 0, 0.0, 0.0};
+          }
+      LT_CUDA(cudaMemcpyAsync(conv, conv0.data(), sizeof(int) * n_bs, cudaMemcpyHostToDevice, st));
+      std::vector<double> zero(n_bs, 0.0);
+      for (int b = 0; b < B; ++b)
+        if (h_active[b])
+          for (int k = 0; k < ns; ++k) { zero[(size_t)b * ns + k] = INFINITY; }
+      LT_CUDA(cudaMemcpyAsync(est, zero.data(), sizeof(double) * n_bs, cudaMemcpyHostToDevice, st));
+      for (int b = 0; b < B; ++b)
+        if (h_active[b])
+          for (int k = 0; k < ns; ++k) zero[(size_t)b * ns + k] = NAN;
+        else
+          for (int k = 0; k < ns; ++k) zero[(size_t)b * ns + k] = 0.0;
+      LT_CUDA(cudaMemcpyAsync(true_res, zero.data(), sizeof(double) * n_bs, cudaMemcpyHostToDevice, st));
+    }
+  }
+  LT_CUDA(cudaMemcpyAsync(active, h_active.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+
+  std::vector<int> h_brk(B, 0), h_unconv(B, 0);
+  std::vector<double2> taus_j(B);
+  DeviceBuffer gather_v, gather_u;
+  int m_global = 0;
+  for (int j = 0; j < maxit; ++j) {
+    int n_active = 0;
+    for (int b = 0; b < B; ++b) n_active += h_active[b];
+    if (n_active == 0) break;
+    if (j >= cap) {
+      const int new_cap = std::min(maxit, 2 * cap);
+      dScratch.allocate(sizeof(double2) * n_bs * (new_cap + 1) * new_cap, st);
+      cap = new_cap;
+      S.cap = cap;
+      S.scratch = dScratch.as<double2>();
+    }
+    // 1. u_j = (K + tau_j M)^{-1} v_j  for the active items
+    add_u();
+    LT_CUDA(cudaMemcpyAsync(dUcols + j, &uptr[j], sizeof(void*), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dVcols + j, &vptr[j], sizeof(void*), cudaMemcpyHostToDevice, st));
+    double2* Uj = const_cast<double2*>(uptr[j]);
+    const double2* Vj = vptr[j];
+    if (n_active == B) {
+      for (int b = 0; b < B; ++b) taus_j[b] = prob.tau_table[b][j];
+      inner_solve(p, B, taus_j.data(), Vj, n, Uj, n);
+    } else {
+      gather_v.ensure(sizeof(double2) * (size_t)n_active * n, st);
+      gather_u.ensure(sizeof(double2) * (size_t)n_active * n, st);
+      int q = 0;
+      for (int b = 0; b < B; ++b) {
+        if (!h_active[b]) continue;
+        taus_j[q] = prob.tau_table[b][j];
+        LT_CUDA(cudaMemcpyAsync(gather_v.as<double2>() + (size_t)q * n, Vj + (size_t)b * n, sizeof(double2) * n,
+                                cudaMemcpyDeviceToDevice, st));
+        ++q;
+      }
+      inner_solve(p, n_active, taus_j.data(), gather_v.as<double2>(), n, gather_u.as<double2>(), n);
+      q = 0;
+      for (int b = 0; b < B; ++b) {
+        if (!h_active[b]) continue;
+        LT_CUDA(cudaMemcpyAsync(Uj + (size_t)b * n, gather_u.as<double2>() + (size_t)q * n, sizeof(double2) * n,
+                                cudaMemcpyDeviceToDevice, st));
+        ++q;
+      }
+    }
+    // 2. s = M u_j into V_{j+1}; Gram-Schmidt with conditional re-orthogonalisation
+    add_v();
+    LT_CUDA(cudaMemcpyAsync(dVcols + j + 1, &vptr[j + 1], sizeof(void*), cudaMemcpyHostToDevice, st));
+    double2* s = const_cast<double2*>(vptr[j + 1]);
+    partials.ensure(sizeof(double2) * (size_t)B * (j + 2) * nblk, st);
+    launch(ctx, "fgmres_orth", nb * (16.0 * (j + 3)) + n * 8.0, [&] {
+      if (p->dim == 3)
+        mass_multidot<3><<<grid, kT, 0, st>>>(L0, S, j, Uj, s, dVcols, partials.as<double2>());
+      else
+        mass_multidot<2><<<grid, kT, 0, st>>>(L0, S, j, Uj, s, dVcols, partials.as<double2>());
+    });
+    launch(ctx, "fgmres_small", 0.0, [&] {
+      reduce_dots<<<B * (j + 2), kT, 0, st>>>(S, j, partials.as<double2>(), 0, hcoef.as<double2>());
+    });
+    launch(ctx, "fgmres_orth", nb * (16.0 * (j + 3)), [&] {
+      gs_update<<<grid, kT, 0, st>>>(S, j, 0, s, dVcols, hcoef.as<double2>(), partials.as<double>());
+    });
+    launch(ctx, "fgmres_small", 0.0, [&] { reduce_norm<<<B, kT, 0, st>>>(S, j, 0, partials.as<double>()); });
+    // re-orthogonalisation pass (items whose norm dropped by more than 1/sqrt(2))
+    launch(ctx, "fgmres_orth", 0.0, [&] { multidot<<<grid, kT, 0, st>>>(S, j, s, dVcols, partials.as<double2>()); });
+    launch(ctx, "fgmres_small", 0.0, [&] {
+      reduce_dots<<<B * (j + 2), kT, 0, st>>>(S, j, partials.as<double2>(), 1, hcoef.as<double2>());
+    });
+    launch(ctx, "fgmres_orth", 0.0, [&] {
+      gs_update<<<grid, kT, 0, st>>>(S, j, 1, s, dVcols, hcoef.as<double2>(), partials.as<double>());
+    });
+    launch(ctx, "fgmres_small", 0.0, [&] { reduce_norm<<<B, kT, 0, st>>>(S, j, 1, partials.as<double>()); });
+    launch(ctx, "fgmres_vec", nb * 32.0, [&] { normalize<<<grid, kT, 0, st>>>(S, s); });
+    const int m = j + 1;
+    // 3. per-shift small solves, verification, freeze
+    launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 0); });
+    partials.ensure(sizeof(double) * n_bs * nblk, st);
+    launch(ctx, "fgmres_verify", nb * (16.0 * (m + 1)) + n * 8.0 * (p->dim + 1), [&] {
+      if (p->dim == 3)
+        verify_residual<3><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+      else
+        verify_residual<2><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+    });
+    launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 0); });
+    launch(ctx, "fgmres_small", 0.0, [&] { count_unconverged<<<blocks_for(B, 128), 128, 0, st>>>(S, m); });
+    LT_CUDA(cudaMemcpyAsync(h_unconv.data(), n_unconv, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaMemcpyAsync(h_brk.data(), brk, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    m_global = m;
+    bool changed = false;
+    for (int b = 0; b < B; ++b) {
+      if (!h_active[b]) continue;
+      res.iterations[b] = m;
+      if (h_unconv[b] == 0 || h_brk[b]) { h_active[b] = 0; changed = true; }
+    }
+    if (changed) LT_CUDA(cudaMemcpyAsync(active, h_active.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+  }
+  res.cap = maxit;
+
+  // best-effort iterates for unconverged shifts (cpp:270-285), at each item's own m
+  bool any_unconv = false;
+  for (int b = 0; b < B; ++b) any_unconv |= (h_unconv[b] > 0 && res.iterations[b] > 0);
+  if (any_unconv && m_global > 0) {
+    // items may have stopped at different m; run per distinct m
+    std::vector<int> ms;
+    for (int b = 0; b < B; ++b)
+      if (h_unconv[b] > 0 && res.iterations[b] > 0) ms.push_back(res.iterations[b]);
+    std::sort(ms.begin(), ms.end());
+    ms.erase(std::unique(ms.begin(), ms.end()), ms.end());
+    for (int m : ms) {
+      std::vector<int> act(B, 0);
+      for (int b = 0; b < B; ++b) act[b] = (h_unconv[b] > 0 && res.iterations[b] == m);
+      LT_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+      launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 1); });
+      // restrict flags to the items of this m
+      launch(ctx, "fgmres_verify", 0.0, [&] {
+        if (p->dim == 3)
+          verify_residual<3><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+        else
+          verify_residual<2><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+      });
+      launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 1); });
+    }
+  }
+
+  // ---- read back status ----
+  std::vector<int> h_conv(n_bs), h_iter(n_bs), h_mu(n_bs);
+  std::vector<double> h_est(n_bs), h_true(n_bs);
+  LT_CUDA(cudaMemcpyAsync(h_conv.data(), conv, sizeof(int) * n_bs, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_iter.data(), iter, sizeof(int) * n_bs, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_mu.data(), m_used, sizeof(int) * n_bs, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_est.data(), est, sizeof(double) * n_bs, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_true.data(), true_res, sizeof(double) * n_bs, cudaMemcpyDeviceToHost, st));
+  if (prob.record_history)
+    LT_CUDA(cudaMemcpyAsync(res.history.data(), dHist.get(), sizeof(double) * n_bs * maxit, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  for (size_t t = 0; t < n_bs; ++t) {
+    res.status[t] = lt_shift_status{h_conv[t], h_iter[t], h_est[t], h_true[t]};
+    res.m_used[t] = h_mu[t];
+  }
+  res.Y = std::move(dY);
+  // column pointers for expand_solutions
+  res.cap = maxit;
+
+  if (prob.keep_basis) {
+    KeptBasis& kb = p->kept;
+    kb.n_rhs = B;
+    kb.steps = res.iterations;
+    kb.beta = h_beta;
+    kb.V.assign(B, {});
+    kb.U.assign(B, {});
+    kb.H.assign(B, {});
+    kb.taus.assign(B, {});
+    std::vector<double2> hH((size_t)B * maxit * (maxit + 1));
+    LT_CUDA(cudaMemcpyAsync(hH.data(), dH.get(), sizeof(double2) * hH.size(), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < B; ++b) {
+      const int m = res.iterations[b];
+      kb.V[b].assign((size_t)n * (m + 1), make_double2(0, 0));
+      kb.U[b].assign((size_t)n * m, make_double2(0, 0));
+      for (int jj = 0; jj <= m; ++jj) {
+        if (jj == m && h_brk[b]) break;  // V(:, m) zeroed on breakdown (cpp:259)
+        LT_CUDA(cudaMemcpyAsync(kb.V[b].data() + (size_t)jj * n, vptr[jj] + (size_t)b * n, sizeof(double2) * n,
+                                cudaMemcpyDeviceToHost, st));
+      }
+      for (int jj = 0; jj < m; ++jj)
+        LT_CUDA(cudaMemcpyAsync(kb.U[b].data() + (size_t)jj * n, uptr[jj] + (size_t)b * n, sizeof(double2) * n,
+                                cudaMemcpyDeviceToHost, st));
+      kb.H[b].assign((size_t)(m + 1) * m, make_double2(0, 0));
+      for (int jj = 0; jj < m; ++jj)
+        for (int i = 0; i <= m; ++i) kb.H[b][(size_t)jj * (m + 1) + i] = hH[((size_t)b * maxit + jj) * (maxit + 1) + i];
+      kb.taus[b].assign(prob.tau_table[b].begin(), prob.tau_table[b].begin() + m);
+    }
+    LT_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev, double2* x_out) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = p->n;
+  const int B = res.B, ns = res.n_shifts;
+  if (B == 0 || ns == 0) return;
+  const int ncols = (int)res.U.size();
+  std::vector<const double2*> cols(std::max(ncols, 1), nullptr);
+  for (int j = 0; j < ncols; ++j) cols[j] = res.U[j].as<double2>();
+  DeviceBuffer dcols(sizeof(void*) * cols.size(), st);
+  DeviceBuffer dmu(sizeof(int) * res.m_used.size(), st);
+  LT_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(void*) * cols.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dmu.get(), res.m_used.data(), sizeof(int) * res.m_used.size(), cudaMemcpyHostToDevice, st));
+  const int nblk = (int)blocks_for(n, kT);
+  launch(ctx, "expand", (double)n * B * 16.0 * (ncols + ns), [&] {
+    expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, res.maxit, dcols.as<const double2*>(), res.Y.as<double2>(),
+                                                      dmu.as<int>(), scale_dev, x_out);
+  });
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace lt

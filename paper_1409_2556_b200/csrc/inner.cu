@@ -1,0 +1,523 @@
+// The shift-and-invert preconditioner solve u = (K + tau M)^{-1} v on the device.
+//
+// Reference: SparseComplexFactorization::solve on an Eigen SparseLU<COLAMD> of K + tau M
+// (factorization.cpp:14-33, used at shifted_solver.cpp:192-193), exact to ~1e-15.  The LU
+// fill of K + tau M is infeasible in HBM for the 3-D configs, so the same
+// operator is inverted to tolerance instead: COCG (conjugate-orthogonal CG for the complex
+// symmetric K + tau M) preconditioned by a symmetric cell-centred multigrid V-cycle
+// (red-black Gauss-Seidel, multilinear prolongation, R = P^T, rediscretised coarse faces,
+// exact dense inverse of the coarsest operator per tau).  B right-hand sides (each its own
+// tau) run in lockstep; blocks are (cell block, item) with the item index fastest so the
+// face coefficients of a cell block are read from L2 once for all items.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "lt_internal.hpp"
+#include "stencil.cuh"
+
+namespace lt {
+
+namespace {
+
+constexpr int kT = 256;
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v);
+template <>
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffff, v, o);
+  return v;
+}
+template <>
+__device__ __forceinline__ double2 warp_sum(double2 v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffff, v.x, o);
+    v.y += __shfl_down_sync(0xffffffff, v.y, o);
+  }
+  return v;
+}
+
+// Block-wide sum; result valid in thread 0.
+template <class T>
+__device__ __forceinline__ T block_sum(T v) {
+  __shared__ T sh[32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? sh[lane] : T{};
+    v = warp_sum(v);
+  }
+  return v;
+}
+
+struct Batch {
+  int B;            // items in the batch
+  const int* done;  // per item: 1 -> skip
+};
+
+#define ITEM_PROLOGUE(n)                                          \
+  const int b = blockIdx.x % bt.B;                                \
+  const int64_t cb = blockIdx.x / bt.B;                           \
+  if (bt.done[b]) return;                                         \
+  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;       \
+  const bool in = a < (n);
+
+// ---- smoother / transfer / coarse solve --------------------------------------------------
+
+// One red-black Gauss-Seidel half sweep of colour `color` ((i+j+k) % 2).  zero_init: the
+// iterate is zero on entry (first half sweep of a V-cycle level): the colour cells get
+// f/d and the other cells are zero-filled.
+template <int DIM>
+__global__ void __launch_bounds__(kT) rbgs_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
+                                                  const double2* __restrict__ f, double2* __restrict__ x,
+                                                  int color, int zero_init) {
+  ITEM_PROLOGUE(L.n);
+  if (!in) return;
+  int i, j, k;
+  decode<DIM>(L, a, i, j, k);
+  double2* xb = x + b * L.n;
+  if (((i + j + k) & 1) != color) {
+    if (zero_init) xb[a] = make_double2(0.0, 0.0);
+    return;
+  }
+  const double2 tau = taus[b];
+  const double m = __ldg(L.M + a);
+  const double2 fa = f[b * L.n + a];
+  double2 off;
+  double dk;
+  if (zero_init) {
+    dk = diag_k(L, i, j, k);
+    off = make_double2(0.0, 0.0);
+  } else {
+    gather<DIM>(L, xb, a, i, j, k, off, dk);
+  }
+  const double2 d = make_double2(dk + tau.x * m, tau.y * m);
+  xb[a] = cdiv(cadd(fa, off), d);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) residual_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
+                                                      const double2* __restrict__ f, const double2* __restrict__ x,
+                                                      double2* __restrict__ r) {
+  ITEM_PROLOGUE(L.n);
+  if (!in) return;
+  int i, j, k;
+  decode<DIM>(L, a, i, j, k);
+  const double2 ax = stencil_apply<DIM>(L, x + b * L.n, a, i, j, k, taus[b]);
+  r[b * L.n + a] = csub(f[b * L.n + a], ax);
+}
+
+// 1-D cell-centred linear interpolation weight P[f, I] (aggregation 2, Dirichlet ghost = -e).
+__device__ __forceinline__ int p1d_terms(int fi, int agg, int nc, int* I, double* w) {
+  if (agg == 1) { I[0] = fi; w[0] = 1.0; return 1; }
+  const int c = fi >> 1;
+  if ((fi & 1) == 0) {
+    if (c == 0) { I[0] = 0; w[0] = 0.5; return 1; }
+    I[0] = c; w[0] = 0.75; I[1] = c - 1; w[1] = 0.25; return 2;
+  }
+  if (c == nc - 1) { I[0] = c; w[0] = 0.5; return 1; }
+  I[0] = c; w[0] = 0.75; I[1] = c + 1; w[1] = 0.25; return 2;
+}
+
+// Transpose weights: fine cells contributing to coarse I along one direction.
+__device__ __forceinline__ int r1d_terms(int I, int agg, int nc, int* F, double* w) {
+  if (agg == 1) { F[0] = I; w[0] = 1.0; return 1; }
+  int n = 0;
+  if (I > 0) { F[n] = 2 * I - 1; w[n] = 0.25; ++n; }
+  F[n] = 2 * I; w[n] = I == 0 ? 0.5 : 0.75; ++n;
+  F[n] = 2 * I + 1; w[n] = I == nc - 1 ? 0.5 : 0.75; ++n;
+  if (I < nc - 1) { F[n] = 2 * I + 2; w[n] = 0.25; ++n; }
+  return n;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) restrict_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
+                                                      const double2* __restrict__ rf, double2* __restrict__ fc) {
+  ITEM_PROLOGUE(Lc.n);
+  if (!in) return;
+  int I, J, K;
+  decode<DIM>(Lc, a, I, J, K);
+  int Fx[4], Fy[4], Fz[4];
+  double wx[4], wy[4], wz[4];
+  const int nxx = r1d_terms(I, ax, Lc.nx, Fx, wx);
+  const int nyy = r1d_terms(J, ay, Lc.ny, Fy, wy);
+  int nzz = 1;
+  Fz[0] = 0; wz[0] = 1.0;
+  if (DIM == 3) nzz = r1d_terms(K, az, Lc.nz, Fz, wz);
+  const double2* rb = rf + b * Lf.n;
+  double2 s = make_double2(0.0, 0.0);
+  for (int q = 0; q < nzz; ++q)
+    for (int p = 0; p < nyy; ++p) {
+      const double wzy = wz[q] * wy[p];
+      const int64_t row = ((int64_t)Fz[q] * Lf.ny + Fy[p]) * Lf.nx;
+      for (int o = 0; o < nxx; ++o) {
+        const double2 v = rb[row + Fx[o]];
+        const double w = wzy * wx[o];
+        s.x += w * v.x;
+        s.y += w * v.y;
+      }
+    }
+  fc[b * Lc.n + a] = s;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) prolong_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
+                                                     const double2* __restrict__ ec, double2* __restrict__ xf) {
+  ITEM_PROLOGUE(Lf.n);
+  if (!in) return;
+  int i, j, k;
+  decode<DIM>(Lf, a, i, j, k);
+  int Ix[2], Iy[2], Iz[2];
+  double wx[2], wy[2], wz[2];
+  const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
+  const int nyy = p1d_terms(j, ay, Lc.ny, Iy, wy);
+  int nzz = 1;
+  Iz[0] = 0; wz[0] = 1.0;
+  if (DIM == 3) nzz = p1d_terms(k, az, Lc.nz, Iz, wz);
+  const double2* eb = ec + b * Lc.n;
+  double2 s = xf[b * Lf.n + a];
+  for (int q = 0; q < nzz; ++q)
+    for (int p = 0; p < nyy; ++p) {
+      const double wzy = wz[q] * wy[p];
+      const int64_t row = ((int64_t)Iz[q] * Lc.ny + Iy[p]) * Lc.nx;
+      for (int o = 0; o < nxx; ++o) {
+        const double2 v = eb[row + Ix[o]];
+        const double w = wzy * wx[o];
+        s.x += w * v.x;
+        s.y += w * v.y;
+      }
+    }
+  xf[b * Lf.n + a] = s;
+}
+
+// e = A_c(tau_b)^{-1} f: one warp per row of the dense inverse (augmented, ld = 2n).
+__global__ void __launch_bounds__(kT) coarse_solve_kernel(int nc, Batch bt, const double2* const* __restrict__ inv,
+                                                          const double2* __restrict__ f, double2* __restrict__ e) {
+  const int b = blockIdx.y;
+  if (bt.done[b]) return;
+  const int row = blockIdx.x * (kT / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= nc) return;
+  const double2* Ar = inv[b] + (int64_t)row * 2 * nc + nc;
+  const double2* fb = f + (int64_t)b * nc;
+  double2 s = make_double2(0.0, 0.0);
+  for (int c = lane; c < nc; c += 32) s = cfma(Ar[c], fb[c], s);
+  s = warp_sum(s);
+  if (lane == 0) e[(int64_t)b * nc + row] = s;
+}
+
+// ---- COCG vector kernels (fused with their reductions) ----------------------------------
+
+// r = v, partial ||v||^2
+__global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ v, int64_t vs,
+                                                       double2* __restrict__ r, double* __restrict__ part, int nblk) {
+  ITEM_PROLOGUE(n);
+  double s = 0.0;
+  if (in) {
+    const double2 x = v[b * vs + a];
+    r[b * n + a] = x;
+    s = cabs2(x);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
+}
+
+// partial sum_a x_a y_a (bilinear, no conjugation)
+__global__ void __launch_bounds__(kT) bdot_kernel(int64_t n, Batch bt, const double2* __restrict__ x,
+                                                  const double2* __restrict__ y, double2* __restrict__ part, int nblk) {
+  ITEM_PROLOGUE(n);
+  double2 s = make_double2(0.0, 0.0);
+  if (in) s = cmul(x[b * n + a], y[b * n + a]);
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
+}
+
+// q = A p, partial p^T q
+template <int DIM>
+__global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
+                                                       const double2* __restrict__ p, double2* __restrict__ q,
+                                                       double2* __restrict__ part, int nblk) {
+  ITEM_PROLOGUE(L.n);
+  double2 s = make_double2(0.0, 0.0);
+  if (in) {
+    int i, j, k;
+    decode<DIM>(L, a, i, j, k);
+    const double2* pb = p + b * L.n;
+    const double2 qa = stencil_apply<DIM>(L, pb, a, i, j, k, taus[b]);
+    q[b * L.n + a] = qa;
+    s = cmul(pb[a], qa);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
+}
+
+// x += alpha p (x = alpha p on the first iteration), r -= alpha q, partial ||r||^2
+__global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
+                                                       const double2* __restrict__ p, const double2* __restrict__ q,
+                                                       double2* __restrict__ x, int64_t xs, double2* __restrict__ r,
+                                                       int first, double* __restrict__ part, int nblk) {
+  ITEM_PROLOGUE(n);
+  double s = 0.0;
+  if (in) {
+    const double2 al = alpha[b];
+    const double2 pa = p[b * n + a];
+    double2* xa = x + b * xs + a;
+    *xa = first ? cmul(al, pa) : cfma(al, pa, *xa);
+    double2 ra = csub(r[b * n + a], cmul(al, q[b * n + a]));
+    r[b * n + a] = ra;
+    s = cabs2(ra);
+  }
+  s = block_sum(s);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
+}
+
+// p = z + beta p (p = z when first)
+__global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const double2* __restrict__ beta,
+                                                     const double2* __restrict__ z, double2* __restrict__ p, int first) {
+  ITEM_PROLOGUE(n);
+  if (!in) return;
+  const double2 za = z[b * n + a];
+  p[b * n + a] = first ? za : cfma(beta[b], p[b * n + a], za);
+}
+
+// x = 0 for items whose right-hand side is zero
+__global__ void zero_kernel(int64_t n, const int* __restrict__ zero_item, double2* __restrict__ x, int64_t xs, int B) {
+  const int b = blockIdx.y;
+  if (!zero_item[b]) return;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+    x[b * xs + a] = make_double2(0.0, 0.0);
+}
+
+// ---- per-item scalar updates (one block per item, deterministic order) -----------------
+enum ScalarOp { OP_BB = 0, OP_RHO = 1, OP_ALPHA = 2, OP_RR = 3, OP_BETA = 4 };
+
+struct Scalars {
+  double* bb;
+  double* rr;
+  double2* rho;
+  double2* alpha;
+  double2* beta;
+};
+
+__global__ void __launch_bounds__(kT) scalar_kernel(int op, Batch bt, const void* part, int nblk, Scalars sc) {
+  const int b = blockIdx.x;
+  if (bt.done[b]) return;
+  if (op == OP_BB || op == OP_RR) {
+    const double* pp = static_cast<const double*>(part) + (int64_t)b * nblk;
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nblk; k += blockDim.x) s += pp[k];
+    s = block_sum(s);
+    if (threadIdx.x == 0) {
+      if (op == OP_BB) sc.bb[b] = s;
+      else sc.rr[b] = s;
+    }
+  } else {
+    const double2* pp = static_cast<const double2*>(part) + (int64_t)b * nblk;
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = threadIdx.x; k < nblk; k += blockDim.x) s = cadd(s, pp[k]);
+    s = block_sum(s);
+    if (threadIdx.x == 0) {
+      if (op == OP_RHO) sc.rho[b] = s;
+      else if (op == OP_ALPHA) sc.alpha[b] = cdiv(sc.rho[b], s);
+      else { sc.beta[b] = cdiv(s, sc.rho[b]); sc.rho[b] = s; }
+    }
+  }
+}
+
+}  // namespace
+
+void finalize_sums(lt_ctx, const double*, int, int, double*, int) {}
+
+namespace {
+
+struct VcycleWork {
+  std::vector<DeviceBuffer> x, f, r;  // per level: Bc x n_l (level 0: x = z, f = COCG r)
+};
+
+template <int DIM>
+void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, const double2* const* inv,
+            std::vector<double2*>& X, std::vector<const double2*>& F, std::vector<double2*>& R) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int last = (int)p->levels.size() - 1;
+  LevelView L = p->view(l);
+  const unsigned grid = blocks_for(L.n, kT) * (unsigned)Bc;
+  const double cell_bytes = (double)L.n * Bc;
+  const double coef = (double)L.n * 8.0 * (DIM + 1);
+  if (l == last) {
+    dim3 g(blocks_for(L.n, kT / 32), Bc);
+    launch(ctx, "mg_coarse_solve", cell_bytes * 32.0, [&] {
+      coarse_solve_kernel<<<g, kT, 0, st>>>((int)L.n, bt, inv, F[l], X[l]);
+    });
+    return;
+  }
+  LevelView Lc = p->view(l + 1);
+  const Level& lev = *p->levels[l];
+  // pre-smoothing (red, black) from a zero iterate
+  launch(ctx, "mg_smooth", cell_bytes * 24.0 + coef, [&] {
+    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 1);
+  });
+  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
+    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
+  });
+  launch(ctx, "mg_residual", cell_bytes * 48.0 + coef, [&] {
+    residual_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l]);
+  });
+  const unsigned gridc = blocks_for(Lc.n, kT) * (unsigned)Bc;
+  launch(ctx, "mg_restrict", cell_bytes * 16.0 + (double)Lc.n * Bc * 16.0, [&] {
+    restrict_kernel<DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, R[l],
+                                                const_cast<double2*>(F[l + 1]));
+  });
+  vcycle<DIM>(p, l + 1, Bc, bt, taus, inv, X, F, R);
+  launch(ctx, "mg_prolong", cell_bytes * 32.0 + (double)Lc.n * Bc * 16.0, [&] {
+    prolong_kernel<DIM><<<grid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, X[l + 1], X[l]);
+  });
+  // post-smoothing (black, red): the transpose of the pre-smoother
+  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
+    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
+  });
+  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
+    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 0);
+  });
+}
+
+template <int DIM>
+void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v, int64_t vs, double2* u,
+                 int64_t us) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int nl = (int)p->levels.size();
+  const int64_t n = p->n;
+  const int nblk = (int)blocks_for(n, kT);
+  LevelView L0 = p->view(0);
+
+  // coarse factors for each distinct tau (cached on the pencil)
+  std::vector<const double2*> inv_host(Bc);
+  for (int b = 0; b < Bc; ++b) inv_host[b] = p->factor(taus_host[b]).inverse.as<double2>();
+
+  // small per-item state: taus, inverse pointers, done flags, scalars
+  const size_t small_bytes = sizeof(double2) * Bc * 4 + sizeof(double) * Bc * 2 + sizeof(void*) * Bc +
+                             sizeof(int) * Bc + 64;
+  DeviceBuffer small(small_bytes, st);
+  char* sp = small.as<char>();
+  double2* d_taus = reinterpret_cast<double2*>(sp);
+  double2* d_rho = d_taus + Bc;
+  double2* d_alpha = d_rho + Bc;
+  double2* d_beta = d_alpha + Bc;
+  double* d_bb = reinterpret_cast<double*>(d_beta + Bc);
+  double* d_rr = d_bb + Bc;
+  const double2** d_inv = reinterpret_cast<const double2**>(d_rr + Bc);
+  int* d_done = reinterpret_cast<int*>(d_inv + Bc);
+  LT_CUDA(cudaMemcpyAsync(d_taus, taus_host, sizeof(double2) * Bc, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(d_inv, inv_host.data(), sizeof(void*) * Bc, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemsetAsync(d_done, 0, sizeof(int) * Bc, st));
+  Scalars sc{d_bb, d_rr, d_rho, d_alpha, d_beta};
+  Batch bt{Bc, d_done};
+
+  // workspace
+  DeviceBuffer partials(sizeof(double2) * (size_t)Bc * nblk, st);
+  DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 5, st);
+  double2* r = vec.as<double2>();
+  double2* z = r + Bc * n;
+  double2* pp = z + Bc * n;
+  double2* q = pp + Bc * n;
+  double2* res0 = q + Bc * n;
+  std::vector<DeviceBuffer> lvl(nl);
+  std::vector<double2*> X(nl), R(nl);
+  std::vector<const double2*> F(nl);
+  X[0] = z;
+  F[0] = r;
+  R[0] = res0;
+  for (int l = 1; l < nl; ++l) {
+    const int64_t nlv = p->levels[l]->n;
+    lvl[l].allocate(sizeof(double2) * (size_t)Bc * nlv * 3, st);
+    X[l] = lvl[l].as<double2>();
+    F[l] = X[l] + Bc * nlv;
+    R[l] = X[l] + 2 * Bc * nlv;
+  }
+  const unsigned grid = (unsigned)nblk * (unsigned)Bc;
+  const double nb = (double)n * Bc;
+  const double coef = (double)n * 8.0 * (DIM + 1);
+
+  launch(ctx, "cocg_vec", nb * 32.0, [&] { copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, (double*)partials.get(), nblk); });
+  launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), nblk, sc); });
+  std::vector<double> bb(Bc), rr(Bc), best(Bc);
+  LT_CUDA(cudaMemcpyAsync(bb.data(), d_bb, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> done(Bc, 0), zero(Bc, 0), stall(Bc, 0);
+  bool any_zero = false;
+  for (int b = 0; b < Bc; ++b)
+    if (!(bb[b] > 0.0)) { done[b] = 1; zero[b] = 1; any_zero = true; }
+  if (any_zero) {
+    DeviceBuffer dz(sizeof(int) * Bc, st);
+    LT_CUDA(cudaMemcpyAsync(dz.get(), zero.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
+    launch(ctx, "cocg_vec", nb * 16.0, [&] {
+      zero_kernel<<<dim3(blocks_for(n, kT), Bc), kT, 0, st>>>(n, dz.as<int>(), u, us, Bc);
+    });
+    LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
+  }
+  int active = 0;
+  for (int b = 0; b < Bc; ++b) active += !done[b];
+  if (active == 0) return;
+
+  const double tol2 = p->inner_tol * p->inner_tol;
+  for (int b = 0; b < Bc; ++b) best[b] = bb[b];
+  // z = B r ; rho = r^T z ; p = z
+  vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
+  launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
+  launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RHO, bt, partials.get(), nblk, sc); });
+  launch(ctx, "cocg_vec", nb * 32.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
+  for (int it = 0; it < p->inner_maxit; ++it) {
+    launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
+      apply_dot_kernel<DIM><<<grid, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(), nblk);
+    });
+    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk, sc); });
+    launch(ctx, "cocg_vec", nb * (it == 0 ? 64.0 : 80.0), [&] {
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, it == 0, (double*)partials.get(), nblk);
+    });
+    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
+    LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    bool changed = false;
+    for (int b = 0; b < Bc; ++b) {
+      if (done[b]) continue;
+      if (rr[b] <= tol2 * bb[b]) { done[b] = 1; changed = true; continue; }
+      // stagnation at the rounding floor: no halving of the residual in 4 iterations
+      if (rr[b] < 0.25 * best[b]) { best[b] = rr[b]; stall[b] = 0; }
+      else if (++stall[b] >= 4) { done[b] = 1; changed = true; }
+    }
+    if (changed) {
+      active = 0;
+      for (int b = 0; b < Bc; ++b) active += !done[b];
+      if (active == 0) break;
+      LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
+    }
+    vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
+    launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
+    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BETA, bt, partials.get(), nblk, sc); });
+    launch(ctx, "cocg_vec", nb * 48.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us) {
+  // Chunk so that the multigrid workspace stays bounded (~12 vectors per item).
+  const int64_t n = p->n;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double per_item = (double)n * sizeof(double2) * 8.0;
+  int chunk = (int)std::max(1.0, std::min(64.0, 0.5 * (double)free_b / per_item));
+  for (int b0 = 0; b0 < B; b0 += chunk) {
+    const int bc = std::min(chunk, B - b0);
+    if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);
+    else inner_chunk<2>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);
+  }
+}
+
+}  // namespace lt

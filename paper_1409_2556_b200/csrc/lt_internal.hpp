@@ -1,0 +1,211 @@
+// Internal C++ types of the laptomo B200 library (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "lt_common.cuh"
+
+namespace lt {
+
+// ---- stream-ordered device buffer -------------------------------------------------------
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  DeviceBuffer(size_t bytes, cudaStream_t s) { allocate(bytes, s); }
+  ~DeviceBuffer() { release(); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept { swap(o); }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) { release(); swap(o); }
+    return *this;
+  }
+  void allocate(size_t bytes, cudaStream_t s) {
+    release();
+    stream_ = s;
+    bytes_ = bytes;
+    if (bytes > 0) LT_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+  }
+  void ensure(size_t bytes, cudaStream_t s) {
+    if (bytes > bytes_) allocate(bytes, s);
+  }
+  void release() {
+    if (ptr_) cudaFreeAsync(ptr_, stream_);
+    ptr_ = nullptr;
+    bytes_ = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(ptr_); }
+  size_t bytes() const { return bytes_; }
+  void* get() const { return ptr_; }
+
+ private:
+  void swap(DeviceBuffer& o) {
+    std::swap(ptr_, o.ptr_);
+    std::swap(bytes_, o.bytes_);
+    std::swap(stream_, o.stream_);
+  }
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+  cudaStream_t stream_ = nullptr;
+};
+
+struct ProfileEntry {
+  double ms = 0.0;
+  int64_t launches = 0;
+  double bytes = 0.0;
+};
+
+struct PendingEvent {
+  std::string name;
+  cudaEvent_t start, stop;
+  double bytes;
+};
+
+}  // namespace lt
+
+struct lt_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool profiling = false;
+  int64_t launches = 0;
+  std::map<std::string, lt::ProfileEntry> profile;
+  std::vector<lt::PendingEvent> pending;
+  std::vector<cudaEvent_t> event_pool;
+  int num_sms = 148;
+
+  void resolve_profile();
+  cudaEvent_t take_event();
+};
+
+namespace lt {
+
+// Launch a kernel (callable issuing exactly one launch on ctx->stream) with accounting.
+template <class F>
+inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f) {
+  ctx->launches++;
+  if (ctx->profiling) {
+    cudaEvent_t a = ctx->take_event(), b = ctx->take_event();
+    cudaEventRecord(a, ctx->stream);
+    f();
+    cudaEventRecord(b, ctx->stream);
+    ctx->pending.push_back({name, a, b, algorithmic_bytes});
+    if (ctx->pending.size() > 8192) ctx->resolve_profile();
+  } else {
+    f();
+  }
+  check_launch(name);
+}
+
+// ---- discretisation levels -----------------------------------------------------------
+// Cell-centred FD level: face transmissibilities including the Dirichlet boundary faces,
+//   Tx[(k*ny + j)*(nx+1) + i]  face between cells i-1 and i (i = 0, nx: boundary)
+//   Ty[(k*(ny+1) + j)*nx + i]  face between rows j-1 and j
+//   Tz[(k*ny + j)*nx + i]      face between planes k-1 and k  (k in [0, nz])
+//   M[a]                       diagonal mass (S h^d, summed on coarse levels)
+struct Level {
+  int nx = 1, ny = 1, nz = 1;
+  int64_t n = 0;
+  double* Tx = nullptr;
+  double* Ty = nullptr;
+  double* Tz = nullptr;
+  double* M = nullptr;
+  DeviceBuffer storage;
+  int agg[3] = {1, 1, 1};  // aggregation to the next coarser level
+};
+
+// Device view of a level passed by value to kernels.
+struct LevelView {
+  int nx, ny, nz, dim;
+  int64_t n;
+  const double* Tx;
+  const double* Ty;
+  const double* Tz;
+  const double* M;
+};
+
+struct CoarseFactor {
+  double2 tau;
+  DeviceBuffer inverse;  // n_c x n_c complex, row-major
+};
+
+// Per-solve FGMRES basis kept for keep_basis queries.
+struct KeptBasis {
+  int n_rhs = 0;
+  std::vector<int> steps;
+  std::vector<double> beta;
+  std::vector<std::vector<double2>> V, U, H, taus;  // per rhs
+};
+
+}  // namespace lt
+
+struct lt_pencil_s {
+  lt_ctx ctx = nullptr;
+  lt_grid grid{};
+  int dim = 2;
+  int64_t n = 0;
+  std::vector<std::unique_ptr<lt::Level>> levels;
+  std::vector<std::unique_ptr<lt::CoarseFactor>> factors;  // keyed by exact tau
+  lt::DeviceBuffer kappa;         // per cell (fine), for Jacobian
+  lt::DeviceBuffer storativity;   // per cell (fine)
+  double inner_tol = 1e-12;
+  int inner_maxit = 200;
+  lt::KeptBasis kept;
+
+  lt::LevelView view(int l) const;
+  const lt::CoarseFactor& factor(double2 tau);  // prepares on miss
+};
+
+namespace lt {
+
+// pencil.cu
+void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int mem);
+void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2* x, int64_t xs,
+                 double2* y, int64_t ys, int B, bool mass_only, const char* name);
+void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count);
+
+// inner.cu: u_b = (K + tau_b M)^{-1} v_b, b < B, strided vectors; taus on host.
+void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs,
+                 double2* u, int64_t us);
+
+// Batched deterministic reductions: out[b] = sum over blocks of partials[b * nblk + k].
+void finalize_sums(lt_ctx ctx, const double* partials, int nblk, int B, double* out,
+                   int stride_out);
+
+// fgmres.cu
+struct OuterProblem {
+  int B = 0;           // items (right-hand sides) in lockstep
+  int n_shifts = 0;
+  const double2* b = nullptr;  // device, B x n
+  std::vector<double2> shifts;        // B * n_shifts (host)
+  std::vector<std::vector<double2>> tau_table;  // per item: tau applied at iteration j
+  int variant = LT_VARIANT_GMRES;
+  double tol = 1e-10;
+  int maxit = 0;
+  bool record_history = false;
+  bool keep_basis = false;
+};
+
+struct OuterResult {
+  int B = 0, n_shifts = 0, cap = 0;
+  std::vector<int> iterations;             // per item
+  std::vector<lt_shift_status> status;     // B * n_shifts
+  std::vector<double> history;             // B * n_shifts * maxit (if recorded)
+  int maxit = 0;
+  // Basis form of the solutions: x_{b,k} = U_b[:, :m_bk] y_{b,k}
+  std::vector<DeviceBuffer> U;             // per column j: B x n
+  DeviceBuffer Y;                          // B * n_shifts * cap complex (device)
+  std::vector<int> m_used;                 // B * n_shifts: number of columns in y
+};
+
+void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res);
+
+// x_out[b][k] = scale[b][k] * U_b y_{b,k}  (device output, B * n_shifts * n)
+void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev,
+                      double2* x_out);
+
+}  // namespace lt

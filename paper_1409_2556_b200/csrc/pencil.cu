@@ -1,0 +1,453 @@
+// Grid pencil: device assembly of the cell-centred FD operator (the FD
+// analogue of assemble(), assembly.cpp:69-113), the multigrid hierarchy behind the
+// shift-and-invert preconditioner, the matrix-free stencil (K + zM)x / Mx
+// (ShiftedPencil::apply / apply_mass, shifted_solver.cpp:109-118) and the coarsest-level
+// exact inverses cached by tau (the ShiftedPencil::factorization cache, cpp:120-128).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "lt_internal.hpp"
+#include "stencil.cuh"
+
+namespace lt {
+
+namespace {
+
+constexpr int64_t kMaxCoarse = 128;  // stop coarsening at <= this many cells
+
+__global__ void exp_kernel(const double* __restrict__ logv, double* __restrict__ out, int64_t n) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < n) out[a] = exp(logv[a]);
+}
+
+// Fine-level faces from per-cell kappa: harmonic mean inside, 2 kappa at the Dirichlet
+// boundary (ghost at h/2), all times h^(d-2).  M = S h^d.
+__global__ void assemble_x(const double* __restrict__ kap, double* __restrict__ Tx, int nx, int ny,
+                           int nz, double s) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)(nx + 1) * ny * nz;
+  if (f >= total) return;
+  int i = (int)(f % (nx + 1));
+  int64_t row = f / (nx + 1);
+  const double* kr = kap + row * nx;
+  double t;
+  if (i == 0) t = 2.0 * kr[0];
+  else if (i == nx) t = 2.0 * kr[nx - 1];
+  else { double a = kr[i - 1], b = kr[i]; t = 2.0 * a * b / (a + b); }
+  Tx[f] = t * s;
+}
+
+__global__ void assemble_y(const double* __restrict__ kap, double* __restrict__ Ty, int nx, int ny,
+                           int nz, double s) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)nx * (ny + 1) * nz;
+  if (f >= total) return;
+  int i = (int)(f % nx);
+  int64_t t1 = f / nx;
+  int j = (int)(t1 % (ny + 1));
+  int k = (int)(t1 / (ny + 1));
+  const double* kp = kap + (int64_t)k * ny * nx + i;
+  double t;
+  if (j == 0) t = 2.0 * kp[0];
+  else if (j == ny) t = 2.0 * kp[(int64_t)(ny - 1) * nx];
+  else { double a = kp[(int64_t)(j - 1) * nx], b = kp[(int64_t)j * nx]; t = 2.0 * a * b / (a + b); }
+  Ty[f] = t * s;
+}
+
+__global__ void assemble_z(const double* __restrict__ kap, double* __restrict__ Tz, int nx, int ny,
+                           int nz, double s) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t plane = (int64_t)nx * ny;
+  int64_t total = plane * (nz + 1);
+  if (f >= total) return;
+  int64_t p = f % plane;
+  int k = (int)(f / plane);
+  double t;
+  if (k == 0) t = 2.0 * kap[p];
+  else if (k == nz) t = 2.0 * kap[(int64_t)(nz - 1) * plane + p];
+  else { double a = kap[(int64_t)(k - 1) * plane + p], b = kap[(int64_t)k * plane + p]; t = 2.0 * a * b / (a + b); }
+  Tz[f] = t * s;
+}
+
+__global__ void scale_kernel(const double* __restrict__ in, double* __restrict__ out, int64_t n, double s) {
+  int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < n) out[a] = in[a] * s;
+}
+
+// Coarse faces: (1/a_dir) * sum of the fine faces that make up the coarse face
+// (rediscretisation of the Galerkin piecewise-constant sum), coarse M = sum over the aggregate.
+__global__ void coarsen_x(const double* __restrict__ Tf, double* __restrict__ Tc, int nxf, int nyf,
+                          int nxc, int nyc, int nzc, int ax, int ay, int az) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)(nxc + 1) * nyc * nzc;
+  if (f >= total) return;
+  int I = (int)(f % (nxc + 1));
+  int64_t t1 = f / (nxc + 1);
+  int J = (int)(t1 % nyc);
+  int K = (int)(t1 / nyc);
+  double s = 0.0;
+  for (int kk = 0; kk < az; ++kk)
+    for (int jj = 0; jj < ay; ++jj)
+      s += Tf[((int64_t)(K * az + kk) * nyf + (J * ay + jj)) * (nxf + 1) + (int64_t)I * ax];
+  Tc[f] = s / ax;
+}
+
+__global__ void coarsen_y(const double* __restrict__ Tf, double* __restrict__ Tc, int nxf, int nyf,
+                          int nxc, int nyc, int nzc, int ax, int ay, int az) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)nxc * (nyc + 1) * nzc;
+  if (f >= total) return;
+  int I = (int)(f % nxc);
+  int64_t t1 = f / nxc;
+  int J = (int)(t1 % (nyc + 1));
+  int K = (int)(t1 / (nyc + 1));
+  double s = 0.0;
+  for (int kk = 0; kk < az; ++kk)
+    for (int ii = 0; ii < ax; ++ii)
+      s += Tf[((int64_t)(K * az + kk) * (nyf + 1) + (int64_t)J * ay) * nxf + (I * ax + ii)];
+  Tc[f] = s / ay;
+}
+
+__global__ void coarsen_z(const double* __restrict__ Tf, double* __restrict__ Tc, int nxf, int nyf,
+                          int nxc, int nyc, int nzc, int ax, int ay, int az) {
+  int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)nxc * nyc * (nzc + 1);
+  if (f >= total) return;
+  int I = (int)(f % nxc);
+  int64_t t1 = f / nxc;
+  int J = (int)(t1 % nyc);
+  int K = (int)(t1 / nyc);
+  double s = 0.0;
+  for (int jj = 0; jj < ay; ++jj)
+    for (int ii = 0; ii < ax; ++ii)
+      s += Tf[((int64_t)K * az * nyf + (J * ay + jj)) * nxf + (I * ax + ii)];
+  Tc[f] = s / az;
+}
+
+__global__ void coarsen_m(const double* __restrict__ Mf, double* __restrict__ Mc, int nxf, int nyf,
+                          int nxc, int nyc, int nzc, int ax, int ay, int az) {
+  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t total = (int64_t)nxc * nyc * nzc;
+  if (c >= total) return;
+  int I = (int)(c % nxc);
+  int64_t t1 = c / nxc;
+  int J = (int)(t1 % nyc);
+  int K = (int)(t1 / nyc);
+  double s = 0.0;
+  for (int kk = 0; kk < az; ++kk)
+    for (int jj = 0; jj < ay; ++jj)
+      for (int ii = 0; ii < ax; ++ii)
+        s += Mf[((int64_t)(K * az + kk) * nyf + (J * ay + jj)) * nxf + (I * ax + ii)];
+  Mc[c] = s;
+}
+
+// Dense A_c(tau) = K_c + tau M_c, written into the left half of an n x 2n augmented
+// matrix [A | I] (row-major) for Gauss-Jordan inversion.
+__global__ void dense_coarse(LevelView L, double2 tau, double2* __restrict__ aug) {
+  int64_t n = L.n;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= n * 2 * n) return;
+  int64_t r = idx / (2 * n), c = idx % (2 * n);
+  double2 v = make_double2(0.0, 0.0);
+  if (c >= n) {
+    if (c - n == r) v.x = 1.0;
+  } else {
+    int i = (int)(r % L.nx);
+    int64_t t1 = r / L.nx;
+    int j = (int)(t1 % L.ny);
+    int k = (int)(t1 / L.ny);
+    if (c == r) {
+      double d = diag_k(L, i, j, k);
+      v = make_double2(d + tau.x * L.M[r], tau.y * L.M[r]);
+    } else {
+      int64_t plane = (int64_t)L.nx * L.ny;
+      if (c == r - 1 && i > 0) v.x = -L.Tx[fx(L, i, j, k)];
+      if (c == r + 1 && i < L.nx - 1) v.x = -L.Tx[fx(L, i + 1, j, k)];
+      if (c == r - L.nx && j > 0) v.x = -L.Ty[fy(L, i, j, k)];
+      if (c == r + L.nx && j < L.ny - 1) v.x = -L.Ty[fy(L, i, j + 1, k)];
+      if (L.dim == 3) {
+        if (c == r - plane && k > 0) v.x = -L.Tz[r];
+        if (c == r + plane && k < L.nz - 1) v.x = -L.Tz[r + plane];
+      }
+    }
+  }
+  aug[idx] = v;
+}
+
+// Single-CTA Gauss-Jordan with partial pivoting on [A | I] (n x 2n, row-major).
+// Leaves A^{-1} in the right half.  status[0] = 1 on a zero pivot.
+__global__ void __launch_bounds__(1024) gauss_jordan(double2* __restrict__ aug, int n, int* status) {
+  extern __shared__ double2 factors[];  // n
+  __shared__ double best_val[32];
+  __shared__ int best_idx[32];
+  __shared__ int piv;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t ld = 2 * (int64_t)n;
+  for (int c = 0; c < n; ++c) {
+    // pivot search over rows c..n-1
+    double bv = -1.0;
+    int bi = c;
+    for (int r = c + tid; r < n; r += nt) {
+      double v = cabs2(aug[r * ld + c]);
+      if (v > bv) { bv = v; bi = r; }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      double ov = __shfl_down_sync(0xffffffff, bv, off);
+      int oi = __shfl_down_sync(0xffffffff, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if ((tid & 31) == 0) { best_val[tid >> 5] = bv; best_idx[tid >> 5] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double v = best_val[0];
+      int i = best_idx[0];
+      for (int w = 1; w < (nt + 31) / 32; ++w)
+        if (best_val[w] > v || (best_val[w] == v && best_idx[w] < i)) { v = best_val[w]; i = best_idx[w]; }
+      piv = i;
+      if (!(v > 0.0)) status[0] = 1;
+    }
+    __syncthreads();
+    const int p = piv;
+    if (p != c) {
+      for (int64_t col = tid; col < ld; col += nt) {
+        double2 t = aug[c * ld + col];
+        aug[c * ld + col] = aug[p * ld + col];
+        aug[p * ld + col] = t;
+      }
+    }
+    __syncthreads();
+    const double2 inv = crecip(aug[c * ld + c]);
+    __syncthreads();
+    for (int64_t col = tid; col < ld; col += nt) aug[c * ld + col] = cmul(aug[c * ld + col], inv);
+    for (int r = tid; r < n; r += nt) factors[r] = aug[(int64_t)r * ld + c];
+    __syncthreads();
+    // eliminate column c from all other rows; columns < c of the left half are already
+    // reduced (zero outside the diagonal) and are not touched.
+    const int64_t width = ld - c;
+    const int64_t work = (int64_t)n * width;
+    for (int64_t w = tid; w < work; w += nt) {
+      int r = (int)(w / width);
+      if (r == c) continue;
+      int64_t col = c + w % width;
+      double2 f = factors[r];
+      if (f.x == 0.0 && f.y == 0.0) continue;
+      aug[r * ld + col] = csub(aug[r * ld + col], cmul(f, aug[(int64_t)c * ld + col]));
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+LevelView lt_pencil_view(const lt_pencil_s* p, int l) {
+  const Level& L = *p->levels[l];
+  return LevelView{L.nx, L.ny, L.nz, p->dim, L.n, L.Tx, L.Ty, L.Tz, L.M};
+}
+
+static void alloc_level(Level& L, int dim, cudaStream_t s) {
+  L.n = (int64_t)L.nx * L.ny * L.nz;
+  int64_t nfx = (int64_t)(L.nx + 1) * L.ny * L.nz;
+  int64_t nfy = (int64_t)L.nx * (L.ny + 1) * L.nz;
+  int64_t nfz = dim == 3 ? (int64_t)L.nx * L.ny * (L.nz + 1) : 0;
+  L.storage.allocate(sizeof(double) * (nfx + nfy + nfz + L.n), s);
+  double* base = L.storage.as<double>();
+  L.Tx = base;
+  L.Ty = base + nfx;
+  L.Tz = dim == 3 ? base + nfx + nfy : nullptr;
+  L.M = base + nfx + nfy + nfz;
+}
+
+void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int mem) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int dim = p->dim;
+  auto fine = std::make_unique<Level>();
+  fine->nx = p->grid.shape[0];
+  fine->ny = p->grid.shape[1];
+  fine->nz = dim == 3 ? p->grid.shape[2] : 1;
+  alloc_level(*fine, dim, st);
+  const int64_t n = fine->n;
+  p->n = n;
+  p->kappa.allocate(sizeof(double) * n, st);
+  p->storativity.allocate(sizeof(double) * n, st);
+  DeviceBuffer logs(sizeof(double) * 2 * n, st);
+  double* lk = logs.as<double>();
+  double* ls = lk + n;
+  auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  LT_CUDA(cudaMemcpyAsync(lk, log_kappa, sizeof(double) * n, kind, st));
+  LT_CUDA(cudaMemcpyAsync(ls, log_s, sizeof(double) * n, kind, st));
+  double* kap = p->kappa.as<double>();
+  double* sto = p->storativity.as<double>();
+  launch(ctx, "assemble", 32.0 * n, [&] { exp_kernel<<<blocks_for(n, kThreads), kThreads, 0, st>>>(lk, kap, n); });
+  launch(ctx, "assemble", 16.0 * n, [&] { exp_kernel<<<blocks_for(n, kThreads), kThreads, 0, st>>>(ls, sto, n); });
+  const double h = p->grid.h;
+  const double sface = dim == 3 ? h : 1.0;
+  const int nx = fine->nx, ny = fine->ny, nz = fine->nz;
+  Level* F = fine.get();
+  launch(ctx, "assemble", 16.0 * n, [&] {
+    assemble_x<<<blocks_for((int64_t)(nx + 1) * ny * nz, kThreads), kThreads, 0, st>>>(kap, F->Tx, nx, ny, nz, sface);
+  });
+  launch(ctx, "assemble", 16.0 * n, [&] {
+    assemble_y<<<blocks_for((int64_t)nx * (ny + 1) * nz, kThreads), kThreads, 0, st>>>(kap, F->Ty, nx, ny, nz, sface);
+  });
+  if (dim == 3)
+    launch(ctx, "assemble", 16.0 * n, [&] {
+      assemble_z<<<blocks_for((int64_t)nx * ny * (nz + 1), kThreads), kThreads, 0, st>>>(kap, F->Tz, nx, ny, nz, sface);
+    });
+  const double hd = dim == 3 ? h * h * h : h * h;
+  launch(ctx, "assemble", 16.0 * n, [&] { scale_kernel<<<blocks_for(n, kThreads), kThreads, 0, st>>>(sto, F->M, n, hd); });
+  p->levels.clear();
+  p->levels.push_back(std::move(fine));
+
+  // Hierarchy: halve every even dimension >= 4 until <= kMaxCoarse cells remain.
+  while (p->levels.back()->n > kMaxCoarse) {
+    Level& Fl = *p->levels.back();
+    int dims[3] = {Fl.nx, Fl.ny, Fl.nz};
+    int agg[3] = {1, 1, 1};
+    bool any = false;
+    for (int d = 0; d < dim; ++d) {
+      if (dims[d] % 2 == 0 && dims[d] >= 4) { agg[d] = 2; any = true; }
+    }
+    if (!any) break;
+    auto C = std::make_unique<Level>();
+    C->nx = Fl.nx / agg[0];
+    C->ny = Fl.ny / agg[1];
+    C->nz = Fl.nz / agg[2];
+    alloc_level(*C, dim, st);
+    for (int d = 0; d < 3; ++d) Fl.agg[d] = agg[d];
+    Level* Cp = C.get();
+    Level* Fp = &Fl;
+    launch(ctx, "coarsen", 0.0, [&] {
+      coarsen_x<<<blocks_for((int64_t)(Cp->nx + 1) * Cp->ny * Cp->nz, kThreads), kThreads, 0, st>>>(
+          Fp->Tx, Cp->Tx, Fp->nx, Fp->ny, Cp->nx, Cp->ny, Cp->nz, agg[0], agg[1], agg[2]);
+    });
+    launch(ctx, "coarsen", 0.0, [&] {
+      coarsen_y<<<blocks_for((int64_t)Cp->nx * (Cp->ny + 1) * Cp->nz, kThreads), kThreads, 0, st>>>(
+          Fp->Ty, Cp->Ty, Fp->nx, Fp->ny, Cp->nx, Cp->ny, Cp->nz, agg[0], agg[1], agg[2]);
+    });
+    if (dim == 3)
+      launch(ctx, "coarsen", 0.0, [&] {
+        coarsen_z<<<blocks_for((int64_t)Cp->nx * Cp->ny * (Cp->nz + 1), kThreads), kThreads, 0, st>>>(
+            Fp->Tz, Cp->Tz, Fp->nx, Fp->ny, Cp->nx, Cp->ny, Cp->nz, agg[0], agg[1], agg[2]);
+      });
+    launch(ctx, "coarsen", 0.0, [&] {
+      coarsen_m<<<blocks_for(Cp->n, kThreads), kThreads, 0, st>>>(Fp->M, Cp->M, Fp->nx, Fp->ny, Cp->nx,
+                                                                    Cp->ny, Cp->nz, agg[0], agg[1], agg[2]);
+    });
+    p->levels.push_back(std::move(C));
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace lt
+
+lt::LevelView lt_pencil_s::view(int l) const { return lt::lt_pencil_view(this, l); }
+
+const lt::CoarseFactor& lt_pencil_s::factor(double2 tau) {
+  for (auto& f : factors)
+    if (f->tau.x == tau.x && f->tau.y == tau.y) return *f;
+  using namespace lt;
+  const int lc = (int)levels.size() - 1;
+  LevelView L = view(lc);
+  const int64_t nc = L.n;
+  if (nc > 4096) throw Error(LT_ERR_PRECONDITIONER, "coarsest multigrid level too large for a dense inverse");
+  cudaStream_t st = ctx->stream;
+  auto f = std::make_unique<CoarseFactor>();
+  f->tau = tau;
+  f->inverse.allocate(sizeof(double2) * nc * 2 * nc, st);
+  DeviceBuffer status(sizeof(int), st);
+  LT_CUDA(cudaMemsetAsync(status.get(), 0, sizeof(int), st));
+  double2* aug = f->inverse.as<double2>();
+  launch(ctx, "coarse_factor", 0.0, [&] {
+    dense_coarse<<<blocks_for(nc * 2 * nc, kThreads), kThreads, 0, st>>>(L, tau, aug);
+  });
+  int nt = nc >= 1024 ? 1024 : (int)((nc + 31) / 32 * 32);
+  launch(ctx, "coarse_factor", 0.0, [&] {
+    gauss_jordan<<<1, nt, sizeof(double2) * nc, st>>>(aug, (int)nc, status.as<int>());
+  });
+  int h_status = 0;
+  LT_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  if (h_status != 0) throw Error(LT_ERR_PRECONDITIONER, "shift-and-invert factorization failed (singular coarse operator)");
+  factors.push_back(std::move(f));
+  return *factors.back();
+}
+
+namespace lt {
+
+namespace {
+
+template <int DIM, bool MASS_ONLY>
+__global__ void apply_kernel(LevelView L, const double2* __restrict__ taus, const double2* __restrict__ x,
+                             int64_t xs, double2* __restrict__ y, int64_t ys, int B) {
+  const int b = blockIdx.x % B;
+  const int64_t a = (int64_t)(blockIdx.x / B) * blockDim.x + threadIdx.x;
+  if (a >= L.n) return;
+  const double2* xb = x + b * xs;
+  double2 out;
+  if (MASS_ONLY) {
+    out = cscale(xb[a], L.M[a]);
+  } else {
+    int i, j, k;
+    decode<DIM>(L, a, i, j, k);
+    out = stencil_apply<DIM>(L, xb, a, i, j, k, taus[b]);
+  }
+  y[b * ys + a] = out;
+}
+
+}  // namespace
+
+void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2* x, int64_t xs,
+                 double2* y, int64_t ys, int B, bool mass_only, const char* name) {
+  LevelView L = p->view(level);
+  cudaStream_t st = p->ctx->stream;
+  unsigned grid = blocks_for(L.n, kThreads) * (unsigned)B;
+  double bytes = mass_only ? (double)L.n * (32.0 * B + 8.0) : (double)L.n * (32.0 * B + 8.0 * (p->dim + 1));
+  launch(p->ctx, name, bytes, [&] {
+    if (mass_only) {
+      if (p->dim == 3) apply_kernel<3, true><<<grid, kThreads, 0, st>>>(L, taus_dev, x, xs, y, ys, B);
+      else apply_kernel<2, true><<<grid, kThreads, 0, st>>>(L, taus_dev, x, xs, y, ys, B);
+    } else {
+      if (p->dim == 3) apply_kernel<3, false><<<grid, kThreads, 0, st>>>(L, taus_dev, x, xs, y, ys, B);
+      else apply_kernel<2, false><<<grid, kThreads, 0, st>>>(L, taus_dev, x, xs, y, ys, B);
+    }
+  });
+}
+
+void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count) {
+  const int dim = p->dim;
+  int base[3] = {0, 0, 0};
+  double frac[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) {
+    const int n = p->grid.shape[d];
+    double xi = point[d] / p->grid.h - 0.5;
+    const double tol = 1e-12 * n;
+    if (xi < -tol || xi > (n - 1) + tol)
+      throw Error(LT_ERR_INVALID_ARGUMENT, "point_weights: point lies outside the cell-centre hull");
+    xi = std::min(std::max(xi, 0.0), double(n - 1));
+    int i0 = std::min((int)std::floor(xi), std::max(n - 2, 0));
+    base[d] = i0;
+    frac[d] = xi - i0;
+  }
+  int c = 0;
+  for (int corner = 0; corner < (1 << dim); ++corner) {
+    double weight = 1.0;
+    int64_t flat = 0, stride = 1;
+    for (int d = 0; d < dim; ++d) {
+      int bit = (corner >> d) & 1;
+      weight *= bit ? frac[d] : 1.0 - frac[d];
+      flat += (int64_t)(base[d] + bit) * stride;
+      stride *= p->grid.shape[d];
+    }
+    if (weight == 0.0) continue;
+    // merge duplicates (degenerate 1-cell directions)
+    bool merged = false;
+    for (int q = 0; q < c; ++q)
+      if (idx[q] == flat) { w[q] += weight; merged = true; break; }
+    if (!merged) { idx[c] = flat; w[c] = weight; ++c; }
+  }
+  *count = c;
+}
+
+}  // namespace lt
