@@ -1,0 +1,373 @@
+"""Benchmark: shifted-system solves/s + Jacobian builds/s (FP64) on BASELINE configs[4]
+(3-D THT Jacobian, 128^3 cells, 16 sources x 64 receivers, Talbot N=32, 4 times) on one B200.
+
+One step = one full Jacobian build (ThtForwardModel::jacobian, jacobian.cpp:189-247):
+device assembly of the pencil from the log fields, forward + adjoint FGMRES-Sh solves of
+all 80 right-hand sides at each of the 4 times (5120 shifted-system solves), and the
+kappa + storativity Jacobian slices (4096 x 2*2,097,152, left on the device per time
+slice as SURVEY.md §8d defines a build), plus the 4096 predictions.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 4]
+
+N > 1 (torchrun): every rank builds the Jacobian of its own field realisation (replicas of
+the per-GPU workload, no data-path collective; scaling "weak"); value = all ranks' solves
+/ max-over-ranks time.  --impl reference times the CPU oracle port (SciPy/SuperLU
+restatement of the reference path; the C++ reference needs Eigen, absent) on a bounded
+sample with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "shifted-system solves/sec + Jacobian builds/sec (FP64), % HBM roofline"
+UNIT = "shifted-system solves/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def experiment_for(cfg, L):
+    g = L.Grid(tuple(cfg.shape), cfg.h)
+    return L.ThtExperiment(g, cfg.sources, cfg.rates, cfg.receivers, cfg.times, cfg.n_quad,
+                           solver=L.SolverConfig(kind=cfg.solver_kind), include_storativity=True)
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------------
+def _oracle_sample_cfg(config_index: int):
+    from paper_1409_2556_b200 import inputs
+    cfg = inputs.config(config_index)
+    if cfg.dim == 3:
+        return cfg.scaled((24, 24, 24 if cfg.shape[2] == cfg.shape[0] else 12), n_src=4, n_rec=4, n_times=1)
+    return cfg.scaled((128, 128), n_src=4, n_rec=4, n_times=1)
+
+
+def _oracle_worker(args):
+    """Forward/adjoint shifted-family solves of one RHS (own pencil + SuperLU cache)."""
+    cfg_index, which, idx = args
+    import numpy as np  # noqa
+    from oracle import fd as ofd
+    from oracle import forward as ofw
+    from oracle import jacobian as ojac
+    from oracle import shifted_solver as oss
+    from oracle import talbot as otal
+    cfg = _oracle_sample_cfg(cfg_index)
+    lk, ls = cfg.fields()
+    grid = ofd.Grid(tuple(cfg.shape), cfg.h)
+    ops = ofd.assemble_fd(grid, np.exp(lk), np.exp(ls))
+    pencil = oss.ShiftedPencil(ops.stiffness, ops.mass)
+    contour = otal.build_contour(cfg.n_quad, cfg.times[0])
+    solver = ofw.SolverConfig(kind=cfg.solver_kind)
+    if which == "src":
+        b = ofd.point_weights(grid, cfg.sources[idx]).astype(np.complex128)
+        x = ojac._solve_family_or_throw(pencil, b, list(contour.nodes), solver, "forward solve")
+        for k in range(contour.n_half()):
+            x[:, k] *= otal.qhat_step(cfg.rates[idx], contour.nodes[k])
+    else:
+        e = ofd.point_weights(grid, cfg.receivers[idx])
+        x = ojac.solve_adjoint_fields(pencil, e, contour, solver)
+    return which, idx, x
+
+
+def oracle_sample(config_index: int, workers: int):
+    """Runs the sample once; returns (solves, seconds, description)."""
+    from multiprocessing import get_context
+    from oracle import fd as ofd
+    from oracle import talbot as otal
+    cfg = _oracle_sample_cfg(config_index)
+    tasks = [(config_index, "src", s) for s in range(len(cfg.sources))] + \
+            [(config_index, "rec", r) for r in range(len(cfg.receivers))]
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"  # one core per worker process (spawned children inherit this)
+    t0 = time.perf_counter()
+    with get_context("spawn").Pool(workers) as pool:
+        out = pool.map(_oracle_worker, tasks)
+    fwd = {i: x for w, i, x in out if w == "src"}
+    adj = {i: x for w, i, x in out if w == "rec"}
+    lk, ls = cfg.fields()
+    grid = ofd.Grid(tuple(cfg.shape), cfg.h)
+    ops = ofd.assemble_fd(grid, np.exp(lk), np.exp(ls))
+    contour = otal.build_contour(cfg.n_quad, cfg.times[0])
+    for s in fwd:
+        for r in adj:
+            ofd.sensitivity_rows_fd(ops, fwd[s], adj[r], contour.weights, contour.nodes, True)
+    dt = time.perf_counter() - t0
+    solves = len(tasks) * (cfg.n_quad // 2)
+    desc = (f"oracle (SciPy SuperLU restatement) on configs[{config_index}] statistics at "
+            f"{'x'.join(map(str, cfg.shape))}: {len(cfg.sources)} sources + {len(cfg.receivers)} receivers, "
+            f"1 time, N={cfg.n_quad}: {solves} shifted solves + {len(fwd) * len(adj)} Jacobian rows, "
+            f"{workers} worker processes")
+    return solves, dt, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = min(os.cpu_count() or 1, 8)
+    vals, dts = [], []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        solves, dt, desc = oracle_sample(args.config, workers)
+        if i >= args.warmup:
+            vals.append(solves / dt)
+            dts.append(dt)
+    v = float(np.mean(vals))
+    from paper_1409_2556_b200 import inputs
+    cfg = inputs.config(args.config)
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(dts)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg.name, "sample": desc},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _sample_solves(config_index):
+    cfg = _oracle_sample_cfg(config_index)
+    return (len(cfg.sources) + len(cfg.receivers)) * (cfg.n_quad // 2)
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1409_2556_b200 import capi, inputs
+    from paper_1409_2556_b200 import laptomo as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    cfg = inputs.config(args.config)
+    if rank > 0:  # replica: own realisation of the same statistics
+        cfg.log_kappa = {**cfg.log_kappa, "seed": cfg.log_kappa["seed"] + 1000 * rank}
+    lk, ls = cfg.fields()
+    n = cfg.n_cells
+    n_src, n_rec, n_t = len(cfg.sources), len(cfg.receivers), len(cfg.times)
+    nh = cfg.n_quad // 2
+    solves_per_build = (n_src + n_rec) * n_t * nh
+    pairs = n_src * n_rec
+    n_param = 2 * n
+
+    ctx = L.Context(local)
+    lib = capi.lib()
+    ex = experiment_for(cfg, L)
+    exc, keep = ex.c()
+    grid_c = ex.grid.c()
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    # inputs resident in HBM; J slice buffer on the device
+    lk_d = torch.from_numpy(lk).cuda()
+    ls_d = torch.from_numpy(ls).cuda()
+    J = torch.empty((pairs, n_param), dtype=torch.float64, device="cuda")
+    pred = np.zeros(pairs)
+    preds = np.zeros((n_t, pairs))
+    lk_pin = torch.from_numpy(lk).pin_memory()
+    ls_pin = torch.from_numpy(ls).pin_memory()
+    torch.cuda.synchronize()
+
+    def build(mem_host: bool):
+        h = C.c_void_p()
+        if mem_host:
+            capi.check(lib.lt_pencil_create_grid(ctx.handle, C.byref(grid_c),
+                                                 C.cast(lk_pin.data_ptr(), capi.PD),
+                                                 C.cast(ls_pin.data_ptr(), capi.PD), capi.LT_MEM_HOST, C.byref(h)))
+        else:
+            capi.check(lib.lt_pencil_create_grid(ctx.handle, C.byref(grid_c),
+                                                 C.cast(lk_d.data_ptr(), capi.PD),
+                                                 C.cast(ls_d.data_ptr(), capi.PD), capi.LT_MEM_DEVICE, C.byref(h)))
+        sums = []
+        for t in range(n_t):
+            capi.check(lib.lt_jacobian_slice(h, C.byref(exc), t, capi.LT_MEM_DEVICE,
+                                             C.cast(J.data_ptr(), capi.PD), capi.dptr(pred)))
+            preds[t] = pred
+            if mem_host:
+                with torch.cuda.stream(stream):
+                    sums.append(torch.linalg.vector_norm(J, dim=1).cpu().numpy())
+        capi.check(lib.lt_pencil_destroy(h))
+        return sums
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        build(False)
+    # ---- device-resident timed region ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.reset_profile()
+    ctx.set_profiling(True)
+    launches0 = ctx.launch_count()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        build(False)
+    e1.record(stream)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    ctx.set_profiling(False)
+    clocks = sampler.stop()
+    prof = ctx.profile()
+    # ---- end-to-end through the public API with host inputs ----
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        build(True)
+    f1.record(stream)
+    barrier()
+    ms_e2e = f0.elapsed_time(f1)
+
+    t_max = ms
+    t_e2e = ms_e2e
+    if world > 1:
+        tt = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max, t_e2e = float(tt[0]), float(tt[1])
+    per_step = t_max / args.steps
+    value = world * solves_per_build * args.steps / (t_max * 1e-3)
+    e2e_value = world * solves_per_build * args.steps / (t_e2e * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    # dominant kernel class by device time
+    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dcnt, dbytes) = dom
+    achieved = (dbytes / dcnt) / (dms / dcnt * 1e-3) / 1e9 if dms > 0 else 0.0
+    breakdown = {k: {"ms": round(v[0], 3), "launches": v[1],
+                     "GBps_alg": round(v[2] / (v[0] * 1e-3) / 1e9, 1) if v[0] > 0 and v[2] > 0 else None}
+                 for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dname)
+        except Exception:
+            traffic = None
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        workers = min(os.cpu_count() or 1, 8)
+        solves, dt, desc = oracle_sample(args.config, workers)
+        cpu = {"value": solves / dt, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "jacobian_builds_per_s": world * args.steps / (t_max * 1e-3),
+        "config": {"workload": cfg.name, "grid": list(cfg.shape), "sources": n_src, "receivers": n_rec,
+                   "times": n_t, "n_quad": cfg.n_quad, "shifted_solves_per_build": solves_per_build,
+                   "jacobian": f"{pairs * n_t} x {n_param} FP64, per-time slices left on device",
+                   "l2": "inputs larger than L2 (one 128^3 complex vector = 33.5 MB; a basis/field set "
+                         "per time = tens of GB)",
+                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind},
+        "kernel_breakdown": breakdown,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n,
+                "d2h_bytes_per_step": 8 * pairs * n_t * 2},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

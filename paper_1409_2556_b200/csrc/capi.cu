@@ -95,7 +95,14 @@ void apply_common(lt_pencil p, double2 z, const lt_complex* x, lt_complex* y, in
   finish_out(y, yout, count, mem, st);
 }
 
-void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
+__global__ void conj_kernel(const double2* __restrict__ in, double2* __restrict__ out, int64_t n) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < n) out[a] = lt::cconj(in[a]);
+}
+
+// adjoint: (K + tau M)^{-H} v = conj((K + tau M)^{-1} conj(v)) since K, M are real symmetric,
+// so the adjoint solve reuses the factorisation of tau (factorization.hpp:25).
+void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem, bool adjoint) {
   check_pencil(p);
   LT_REQUIRE(n_rhs >= 0, "n_rhs must be nonnegative");
   if (n_rhs == 0) return;
@@ -105,7 +112,20 @@ void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, 
   Staged vin = stage_in(v, count, mem, st);
   Staged uout = stage_out(u, count, mem, st);
   std::vector<double2> taus(n_rhs, tau);
-  lt::inner_solve(p, n_rhs, taus.data(), vin.ptr, p->n, uout.ptr, p->n);
+  lt::DeviceBuffer vc;
+  const double2* vsrc = vin.ptr;
+  if (adjoint) {
+    vc.allocate(sizeof(double2) * count, st);
+    lt::launch(p->ctx, "conj", 32.0 * count, [&] {
+      conj_kernel<<<lt::blocks_for((int64_t)count, 256), 256, 0, st>>>(vin.ptr, vc.as<double2>(), (int64_t)count);
+    });
+    vsrc = vc.as<double2>();
+  }
+  lt::inner_solve(p, n_rhs, taus.data(), vsrc, p->n, uout.ptr, p->n);
+  if (adjoint)
+    lt::launch(p->ctx, "conj", 32.0 * count, [&] {
+      conj_kernel<<<lt::blocks_for((int64_t)count, 256), 256, 0, st>>>(uout.ptr, uout.ptr, (int64_t)count);
+    });
   finish_out(u, uout, count, mem, st);
 }
 
@@ -302,11 +322,11 @@ lt_status lt_pencil_set_inner_tolerance(lt_pencil p, double rel_tol, int max_ite
 }
 
 lt_status lt_pencil_solve(lt_pencil p, lt_complex tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
-  return guard([&] { solve_common(p, make_double2(tau.re, tau.im), v, u, n_rhs, mem); });
+  return guard([&] { solve_common(p, make_double2(tau.re, tau.im), v, u, n_rhs, mem, false); });
 }
 
 lt_status lt_pencil_solve_adjoint(lt_pencil p, lt_complex tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem) {
-  return guard([&] { solve_common(p, make_double2(tau.re, -tau.im), v, u, n_rhs, mem); });
+  return guard([&] { solve_common(p, make_double2(tau.re, tau.im), v, u, n_rhs, mem, true); });
 }
 
 lt_status lt_pencil_point_weights(lt_pencil p, const double* point, int64_t* indices, double* weights, int* count) {
