@@ -95,7 +95,7 @@ void apply_common(lt_pencil p, double2 z, const lt_complex* x, lt_complex* y, in
   finish_out(y, yout, count, mem, st);
 }
 
-__global__ void conj_kernel(const double2* __restrict__ in, double2* __restrict__ out, int64_t n) {
+__global__ void conj_kernel(const double2* in, double2* out, int64_t n) {
   const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (a < n) out[a] = lt::cconj(in[a]);
 }

@@ -70,13 +70,29 @@ __global__ void predict_kernel(int64_t n, int n_src, int n_rec, int ns, const do
   out[t] = 2.0 * acc.x;
 }
 
+// rhs[item*n + idx] += w for the sparse point weights of each item (zeroed beforehand)
+__global__ void scatter_points(int64_t n, int n_items, const int64_t* __restrict__ idx, const double* __restrict__ w,
+                               const int* __restrict__ cnt, double2* __restrict__ rhs) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_items * 8) return;
+  const int it = t / 8, q = t % 8;
+  if (q >= cnt[it]) return;
+  rhs[(int64_t)it * n + idx[it * 8 + q]].x += w[it * 8 + q];
+}
+
+__global__ void real_to_complex(int64_t n, const double* __restrict__ x, double2* __restrict__ y) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < n) y[a] = make_double2(x[a], 0.0);
+}
+
 // ---- Jacobian assembly -----------------------------------------------------------------
 // J_k[(s,r), a] = 2 Re sum_k w_k sum_{f in faces(a)} dT_f/dln k_a (phi_a - phi_b)(psi_a - psi_b)
 // J_S[(s,r), a] = 2 Re sum_k w_k z_k^p S_a h^d phi_a psi_a
-// A CTA owns TC consecutive cells and a range of (source-block x receiver-block) register
-// tiles; per (shift, face) stage the weighted face differences of all sources (P) and
-// receivers (Q) at its cells are staged in shared memory and every thread accumulates
-// its SB x RB tile of Re(P Q) for one cell.
+// A CTA owns TC consecutive cells of one row and all (source-block x receiver-block)
+// register tiles.  Per shift k, every field value at the tile (centre) and its 2d face
+// neighbours is loaded once, the 2d weighted face differences and the storativity term of
+// all sources (P) and receivers (Q) are staged in shared memory, and every thread
+// accumulates its SB x RB tile of Re(P Q) for one cell over the 2d+1 stages.
 constexpr int SB = 4;
 constexpr int RB = 8;
 
@@ -85,110 +101,121 @@ __global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double*
                                                       const double* __restrict__ stor, double hd, double face_scale,
                                                       const double2* __restrict__ fields, int n_src, int n_rec, int ns,
                                                       const double2* __restrict__ w, const double2* __restrict__ wz,
-                                                      int TC, int subs_per_cta, int nsub_r, int nsub_total,
+                                                      int TC, int tiles_x, int nsub_r, int nsub_total,
                                                       double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj) {
+  constexpr int NF = 2 * DIM + 1;  // faces + storativity stage
   extern __shared__ double2 smem[];
   const int n_items = n_src + n_rec;
-  double2* P = smem;                    // [n_src][TC]
-  double2* Q = smem + (size_t)n_src * TC;  // [n_rec][TC]
-  double* dT = reinterpret_cast<double*>(Q + (size_t)n_rec * TC);  // [TC]
+  double2* P = smem;                                    // [NF][n_src][TC]
+  double2* Q = smem + (size_t)NF * n_src * TC;          // [NF][n_rec][TC]
+  double* wt = reinterpret_cast<double*>(Q + (size_t)NF * n_rec * TC);  // [NF][TC]
+  int64_t* nb = reinterpret_cast<int64_t*>(wt + NF * TC);             // [2 DIM][TC] neighbour index or -1
   const int64_t n = L.n;
-  const int64_t a0 = (int64_t)blockIdx.x * TC;
+  // tile -> (row, x offset); cells of one tile are consecutive in x
+  const int tile = blockIdx.x;
+  const int tx = tile % tiles_x;
+  const int64_t row = tile / tiles_x;  // k * ny + j
+  const int i0 = tx * TC;
+  const int ncell = min(TC, L.nx - i0);
+  const int64_t a0 = row * L.nx + i0;
+  const int j = (int)(row % L.ny);
+  const int kz = (int)(row / L.ny);
   const int tid = threadIdx.x;
   const int c = tid % TC;
-  const int sub = blockIdx.y * subs_per_cta + tid / TC;
-  const bool owner = (tid / TC) < subs_per_cta && sub < nsub_total && a0 + c < n;
+  const int sub = tid / TC;
+  const bool owner = sub < nsub_total && c < ncell;
   const int s0 = owner ? (sub / nsub_r) * SB : 0;
   const int r0 = owner ? (sub % nsub_r) * RB : 0;
+
+  if (tid < NF * TC) {
+    const int f = tid / TC, cc = tid % TC;
+    double wv = 0.0;
+    int64_t nbi = -1;
+    if (cc < ncell) {
+      const int64_t a = a0 + cc;
+      if (f == 2 * DIM) {
+        wv = stor[a] * hd;
+      } else {
+        const int d = f >> 1, hi = f & 1;
+        const int coord = d == 0 ? i0 + cc : (d == 1 ? j : kz);
+        const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
+        const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : (int64_t)L.nx * L.ny);
+        const double ka = kappa[a];
+        const bool boundary = hi ? coord == ext - 1 : coord == 0;
+        if (boundary) {
+          wv = 2.0 * ka * face_scale;  // dT/dln k_a = T = 2 k_a h^(d-2); ghost value 0
+        } else {
+          nbi = hi ? a + stride : a - stride;
+          const double kb = kappa[nbi];
+          const double T = 2.0 * ka * kb / (ka + kb) * face_scale;
+          wv = T * kb / (ka + kb);
+        }
+      }
+    }
+    wt[f * TC + cc] = wv;
+    if (f < 2 * DIM) nb[f * TC + cc] = nbi;
+  }
+
   double accK[SB][RB], accS[SB][RB];
 #pragma unroll
   for (int i = 0; i < SB; ++i)
 #pragma unroll
-    for (int j = 0; j < RB; ++j) { accK[i][j] = 0.0; accS[i][j] = 0.0; }
+    for (int q = 0; q < RB; ++q) { accK[i][q] = 0.0; accS[i][q] = 0.0; }
+  __syncthreads();
 
-  const int nfaces = 2 * DIM;
   for (int k = 0; k < ns; ++k) {
     const double2 wk = w[k], wzk = wz[k];
-    for (int f = 0; f <= nfaces; ++f) {
-      // per-cell face weight dT_f/dln k_a (or S_a h^d for the storativity stage) and the
-      // neighbour offset (0 when the face is a Dirichlet boundary face)
-      if (tid < TC) {
-        const int64_t a = a0 + tid;
-        double wt = 0.0;
-        if (a < n) {
-          if (f == nfaces) {
-            wt = stor[a] * hd;
-          } else {
-            int i, j, kk;
-            decode<DIM>(L, a, i, j, kk);
-            const int d = f >> 1, hi = f & 1;
-            const int coord = d == 0 ? i : (d == 1 ? j : kk);
-            const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
-            const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : (int64_t)L.nx * L.ny);
-            const double ka = kappa[a];
-            const bool boundary = hi ? coord == ext - 1 : coord == 0;
-            if (boundary) {
-              wt = 2.0 * ka * face_scale;
-            } else {
-              const double kb = kappa[hi ? a + stride : a - stride];
-              const double T = 2.0 * ka * kb / (ka + kb) * face_scale;
-              wt = T * kb / (ka + kb);
-            }
-          }
+    // stage: one centre + 2d neighbour loads per (item, cell)
+    for (int e = tid; e < n_items * TC; e += blockDim.x) {
+      const int it = e / TC, cc = e % TC;
+      const double2* fld = fields + ((int64_t)it * ns + k) * n;
+      double2 fa = make_double2(0.0, 0.0);
+      double2 fn[2 * DIM];
+      if (cc < ncell) {
+        fa = fld[a0 + cc];
+#pragma unroll
+        for (int f = 0; f < 2 * DIM; ++f) {
+          const int64_t q = nb[f * TC + cc];
+          fn[f] = q >= 0 ? fld[q] : make_double2(0.0, 0.0);
         }
-        dT[tid] = wt;
+      } else {
+#pragma unroll
+        for (int f = 0; f < 2 * DIM; ++f) fn[f] = make_double2(0.0, 0.0);
       }
-      __syncthreads();
-      // stage P (sources, weighted) and Q (receivers)
-      for (int e = tid; e < n_items * TC; e += blockDim.x) {
-        const int it = e / TC, cc = e % TC;
-        const int64_t a = a0 + cc;
-        double2 v = make_double2(0.0, 0.0);
-        if (a < n) {
-          const double2* fld = fields + ((int64_t)it * ns + k) * n;
-          const double2 fa = fld[a];
-          if (f == nfaces) {
-            v = fa;
-          } else {
-            int i, j, kk;
-            decode<DIM>(L, a, i, j, kk);
-            const int d = f >> 1, hi = f & 1;
-            const int coord = d == 0 ? i : (d == 1 ? j : kk);
-            const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
-            const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : (int64_t)L.nx * L.ny);
-            const bool boundary = hi ? coord == ext - 1 : coord == 0;
-            v = boundary ? fa : csub(fa, fld[hi ? a + stride : a - stride]);
-          }
-        }
-        if (it < n_src) {
-          P[(size_t)it * TC + cc] = cscale(cmul(f == nfaces ? wzk : wk, v), dT[cc]);
-        } else {
-          Q[(size_t)(it - n_src) * TC + cc] = v;
-        }
+      if (it < n_src) {
+#pragma unroll
+        for (int f = 0; f < 2 * DIM; ++f)
+          P[((size_t)f * n_src + it) * TC + cc] = cscale(cmul(wk, csub(fa, fn[f])), wt[f * TC + cc]);
+        P[((size_t)(2 * DIM) * n_src + it) * TC + cc] = cscale(cmul(wzk, fa), wt[2 * DIM * TC + cc]);
+      } else {
+        const int r = it - n_src;
+#pragma unroll
+        for (int f = 0; f < 2 * DIM; ++f) Q[((size_t)f * n_rec + r) * TC + cc] = csub(fa, fn[f]);
+        Q[((size_t)(2 * DIM) * n_rec + r) * TC + cc] = fa;
       }
-      __syncthreads();
-      if (owner) {
+    }
+    __syncthreads();
+    if (owner) {
+#pragma unroll 1
+      for (int f = 0; f < NF; ++f) {
         double2 pv[SB];
 #pragma unroll
-        for (int i = 0; i < SB; ++i) pv[i] = (s0 + i < n_src) ? P[(size_t)(s0 + i) * TC + c] : make_double2(0.0, 0.0);
-        if (f == nfaces) {
+        for (int i = 0; i < SB; ++i)
+          pv[i] = (s0 + i < n_src) ? P[((size_t)f * n_src + s0 + i) * TC + c] : make_double2(0.0, 0.0);
 #pragma unroll
-          for (int j = 0; j < RB; ++j) {
-            const double2 qv = (r0 + j < n_rec) ? Q[(size_t)(r0 + j) * TC + c] : make_double2(0.0, 0.0);
+        for (int q = 0; q < RB; ++q) {
+          const double2 qv = (r0 + q < n_rec) ? Q[((size_t)f * n_rec + r0 + q) * TC + c] : make_double2(0.0, 0.0);
+          if (f < 2 * DIM) {
 #pragma unroll
-            for (int i = 0; i < SB; ++i) accS[i][j] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accS[i][j]));
-          }
-        } else {
+            for (int i = 0; i < SB; ++i) accK[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accK[i][q]));
+          } else {
 #pragma unroll
-          for (int j = 0; j < RB; ++j) {
-            const double2 qv = (r0 + j < n_rec) ? Q[(size_t)(r0 + j) * TC + c] : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int i = 0; i < SB; ++i) accK[i][j] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accK[i][j]));
+            for (int i = 0; i < SB; ++i) accS[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accS[i][q]));
           }
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
   }
   if (!owner) return;
   const int64_t a = a0 + c;
@@ -196,11 +223,11 @@ __global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double*
   for (int i = 0; i < SB; ++i) {
     if (s0 + i >= n_src) continue;
 #pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      if (r0 + j >= n_rec) continue;
-      const int64_t row = (int64_t)(s0 + i) * n_rec + (r0 + j);
-      Jk[row * ldj + a] = 2.0 * accK[i][j];
-      if (Js) Js[row * ldj + a] = 2.0 * accS[i][j];
+    for (int q = 0; q < RB; ++q) {
+      if (r0 + q >= n_rec) continue;
+      const int64_t rowj = (int64_t)(s0 + i) * n_rec + (r0 + q);
+      Jk[rowj * ldj + a] = 2.0 * accK[i][q];
+      if (Js) Js[rowj * ldj + a] = 2.0 * accS[i][q];
     }
   }
 }
@@ -219,12 +246,6 @@ PointSet make_points(lt_pencil p, const double* pts, int n_pts) {
   for (int r = 0; r < n_pts; ++r)
     point_weights(p, pts + (size_t)r * p->dim, ps.idx.data() + r * 8, ps.w.data() + r * 8, &ps.cnt[r]);
   return ps;
-}
-
-std::vector<double> dense_weights(lt_pencil p, const PointSet& ps, int r, double scale) {
-  std::vector<double> v(p->n, 0.0);
-  for (int q = 0; q < ps.cnt[r]; ++q) v[ps.idx[r * 8 + q]] += scale * ps.w[r * 8 + q];
-  return v;
 }
 
 void throw_unconverged(const OuterResult& res, const char* what) {
@@ -380,14 +401,14 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
   auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DeviceBuffer src_dev(sizeof(double) * (size_t)n * n_src, st);
   LT_CUDA(cudaMemcpyAsync(src_dev.get(), sources, sizeof(double) * n * n_src, kind, st));
-  std::vector<double> src_h((size_t)n * n_src);
-  LT_CUDA(cudaMemcpyAsync(src_h.data(), src_dev.get(), sizeof(double) * n * n_src, cudaMemcpyDeviceToHost, st));
   std::vector<double> ih_h;
   std::vector<int> with_initial(n_src, 0);
+  DeviceBuffer ih_dev;
   if (initial_head) {
+    ih_dev.allocate(sizeof(double) * (size_t)n * n_src, st);
+    LT_CUDA(cudaMemcpyAsync(ih_dev.get(), initial_head, sizeof(double) * n * n_src, kind, st));
     ih_h.resize((size_t)n * n_src);
-    LT_CUDA(cudaMemcpyAsync(ih_h.data(), initial_head, sizeof(double) * n * n_src,
-                            mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, st));
+    LT_CUDA(cudaMemcpyAsync(ih_h.data(), ih_dev.get(), sizeof(double) * n * n_src, cudaMemcpyDeviceToHost, st));
   }
   LT_CUDA(cudaStreamSynchronize(st));
   for (int s = 0; s < n_src && initial_head; ++s) {
@@ -429,31 +450,25 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
   for (int f0 = 0; f0 < F; f0 += chunk) {
     const int B = std::min(chunk, F - f0);
     // right-hand sides
-    std::vector<double2> rhs_h((size_t)B * n);
     DeviceBuffer rhs(sizeof(double2) * (size_t)B * n, st);
     std::vector<std::vector<cd>> shifts(B);
     for (int q = 0; q < B; ++q) {
       const Fam& fm = fams[f0 + q];
-      if (!fm.initial) {
-        for (int64_t a = 0; a < n; ++a) rhs_h[(size_t)q * n + a] = make_double2(src_h[(size_t)fm.s * n + a], 0.0);
-      }
       if (pooled) {
         for (int t = 0; t < n_times; ++t) shifts[q].insert(shifts[q].end(), nodes[t].begin(), nodes[t].end());
       } else {
         shifts[q] = nodes[fm.t];
       }
-    }
-    LT_CUDA(cudaMemcpyAsync(rhs.get(), rhs_h.data(), sizeof(double2) * rhs_h.size(), cudaMemcpyHostToDevice, st));
-    for (int q = 0; q < B; ++q) {
-      const Fam& fm = fams[f0 + q];
-      if (fm.initial) {
-        // rhs = M phi0 (apply_mass)
-        std::vector<double2> ih((size_t)n);
-        for (int64_t a = 0; a < n; ++a) ih[a] = make_double2(ih_h[(size_t)fm.s * n + a], 0.0);
+      double2* dst = rhs.as<double2>() + (size_t)q * n;
+      if (!fm.initial) {
+        const double* srcp = src_dev.as<double>() + (size_t)fm.s * n;
+        launch(ctx, "rhs", 24.0 * n, [&] { real_to_complex<<<blocks_for(n, kT), kT, 0, st>>>(n, srcp, dst); });
+      } else {
+        // rhs = M phi0 (apply_mass, forward.cpp:91-93)
         DeviceBuffer tmp(sizeof(double2) * n, st);
-        LT_CUDA(cudaMemcpyAsync(tmp.get(), ih.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, st));
-        apply_batch(p, 0, nullptr, tmp.as<double2>(), n, rhs.as<double2>() + (size_t)q * n, n, 1, true, "apply_mass");
-        LT_CUDA(cudaStreamSynchronize(st));
+        const double* ihp = ih_dev.as<double>() + (size_t)fm.s * n;
+        launch(ctx, "rhs", 24.0 * n, [&] { real_to_complex<<<blocks_for(n, kT), kT, 0, st>>>(n, ihp, tmp.as<double2>()); });
+        apply_batch(p, 0, nullptr, tmp.as<double2>(), n, dst, n, 1, true, "apply_mass");
       }
     }
     OuterResult res;
@@ -559,13 +574,33 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   PointSet rec = make_points(p, ex.receivers, n_rec);
   const int B = n_src + n_rec;
   // rhs: sources b_s, receivers -e_r  (jacobian.cpp:216, 227, solve_adjoint_fields cpp:49)
-  std::vector<double2> rhs_h((size_t)B * n, make_double2(0.0, 0.0));
-  for (int s = 0; s < n_src; ++s)
-    for (int q = 0; q < src.cnt[s]; ++q) rhs_h[(size_t)s * n + src.idx[s * 8 + q]].x += src.w[s * 8 + q];
-  for (int r = 0; r < n_rec; ++r)
-    for (int q = 0; q < rec.cnt[r]; ++q) rhs_h[(size_t)(n_src + r) * n + rec.idx[r * 8 + q]].x -= rec.w[r * 8 + q];
-  DeviceBuffer rhs(sizeof(double2) * rhs_h.size(), st);
-  LT_CUDA(cudaMemcpyAsync(rhs.get(), rhs_h.data(), sizeof(double2) * rhs_h.size(), cudaMemcpyHostToDevice, st));
+  // sparse point weights of all items (sources +w, receivers -w), scattered on the device
+  std::vector<int64_t> pidx((size_t)B * 8, 0);
+  std::vector<double> pw((size_t)B * 8, 0.0);
+  std::vector<int> pcnt(B, 0);
+  for (int s = 0; s < n_src; ++s) {
+    pcnt[s] = src.cnt[s];
+    for (int q = 0; q < src.cnt[s]; ++q) { pidx[s * 8 + q] = src.idx[s * 8 + q]; pw[s * 8 + q] = src.w[s * 8 + q]; }
+  }
+  for (int r = 0; r < n_rec; ++r) {
+    pcnt[n_src + r] = rec.cnt[r];
+    for (int q = 0; q < rec.cnt[r]; ++q) {
+      pidx[(n_src + r) * 8 + q] = rec.idx[r * 8 + q];
+      pw[(n_src + r) * 8 + q] = -rec.w[r * 8 + q];
+    }
+  }
+  DeviceBuffer rhs(sizeof(double2) * (size_t)B * n, st);
+  {
+    DeviceBuffer didx(sizeof(int64_t) * pidx.size(), st), dwt(sizeof(double) * pw.size(), st), dcnt(sizeof(int) * B, st);
+    LT_CUDA(cudaMemcpyAsync(didx.get(), pidx.data(), sizeof(int64_t) * pidx.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dwt.get(), pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dcnt.get(), pcnt.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemsetAsync(rhs.get(), 0, rhs.bytes(), st));
+    launch(ctx, "rhs", 0.0, [&] {
+      scatter_points<<<blocks_for((int64_t)B * 8, 128), 128, 0, st>>>(n, B, didx.as<int64_t>(), dwt.as<double>(),
+                                                                      dcnt.as<int>(), rhs.as<double2>());
+    });
+  }
   std::vector<std::vector<cd>> shifts(B, nodes);
   OuterResult res;
   solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
@@ -613,32 +648,29 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     }
     const int nsub_s = (n_src + SB - 1) / SB, nsub_r = (n_rec + RB - 1) / RB;
     const int nsub_total = nsub_s * nsub_r;
-    const int subs_per_cta = std::min(nsub_total, kT);
-    const int TC = std::max(1, kT / subs_per_cta);
-    dim3 grid((unsigned)((n + TC - 1) / TC), (unsigned)((nsub_total + subs_per_cta - 1) / subs_per_cta));
-    const size_t smem = sizeof(double2) * (size_t)B * TC + sizeof(double) * TC;
+    LT_REQUIRE(nsub_total <= kT, "jacobian: too many source/receiver blocks for one CTA (n_src*n_rec too large)");
+    const int nf = 2 * p->dim + 1;
+    int TC = std::max(1, kT / nsub_total);
     LevelView L = p->view(0);
+    TC = std::min(TC, L.nx);
+    auto smem_for = [&](int tc) {
+      return sizeof(double2) * (size_t)nf * B * tc + sizeof(double) * nf * tc + sizeof(int64_t) * 2 * p->dim * tc;
+    };
+    while (TC > 1 && smem_for(TC) > 200 * 1024) TC /= 2;
+    LT_REQUIRE(nf * TC <= kT, "jacobian: tile too wide");
+    const size_t smem = smem_for(TC);
+    const int tiles_x = (L.nx + TC - 1) / TC;
+    const unsigned grid = (unsigned)(tiles_x * (int64_t)L.ny * L.nz);
     const double h = p->grid.h;
     const double face_scale = p->dim == 3 ? h : 1.0;
     const double hd = p->dim == 3 ? h * h * h : h * h;
-    const double flops = 2.0 * 2.0 * (double)n * n_src * n_rec * ns * (2 * p->dim + 1);
-    (void)flops;
     const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
-    if (smem > 48 * 1024) {
-      auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
-      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
+    LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch(ctx, "jacobian", bytes, [&] {
-      if (p->dim == 3)
-        jacobian_kernel<3><<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
-                                                   fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(),
-                                                   dw.as<double2>() + ns, TC, subs_per_cta, nsub_r, nsub_total, J,
-                                                   ex.include_storativity ? J + n : nullptr, n_param);
-      else
-        jacobian_kernel<2><<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
-                                                   fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(),
-                                                   dw.as<double2>() + ns, TC, subs_per_cta, nsub_r, nsub_total, J,
-                                                   ex.include_storativity ? J + n : nullptr, n_param);
+      fn<<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
+                                 fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(), dw.as<double2>() + ns, TC,
+                                 tiles_x, nsub_r, nsub_total, J, ex.include_storativity ? J + n : nullptr, n_param);
     });
     if (mem != LT_MEM_DEVICE)
       LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));

@@ -65,6 +65,7 @@ struct State {
   int B, ns, maxit, cap;
   int64_t n;
   int nblk;
+  int nblk_tile;  // tiles per item of the fine level (verify_residual partials)
   double tol;
   int variant;
   int record_history;
@@ -230,7 +231,7 @@ __device__ __forceinline__ double2 hz_entry(const State& S, int b, int i, int l,
 __global__ void small_solve(State S, int m, int force) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= S.B * S.ns) return;
-  const int b = t / S.ns, k = t % S.ns;
+  const int b = t / S.ns;
   S.flag[t] = 0;
   if (!S.active[b]) return;
   if (S.conv[t]) return;
@@ -364,10 +365,9 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
   }
   __syncthreads();
   if (nflag == 0) return;
-  const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
-  const bool in = a < L.n;
-  int i = 0, jj = 0, kk = 0;
-  if (in) decode<DIM>(L, a, i, jj, kk);
+  int i, jj, kk;
+  int64_t a;
+  const bool in = tile_cell(L, (int)cb, i, jj, kk, a);
   const double2 bv = in ? rhs[b * L.n + a] : make_double2(0.0, 0.0);
   const double mval = in ? __ldg(L.M + a) : 0.0;
   for (int c0 = 0; c0 < nflag; c0 += KC) {
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
     for (int q = 0; q < nc; ++q) {
       const double2 r = csub(bv, acc[q]);
       const double nn = block_sum_d(in ? cabs2(r) : 0.0, sh);
-      if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk + cb] = nn;
+      if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = nn;
     }
   }
 }
@@ -408,9 +408,9 @@ __global__ void __launch_bounds__(kT) verify_finalize(State S, int m, const doub
   const int t = blockIdx.x;
   if (!S.flag[t]) return;
   const int b = t / S.ns;
-  const double* pb = part + (int64_t)t * S.nblk;
+  const double* pb = part + (int64_t)t * S.nblk_tile;
   double s = 0.0;
-  for (int k = threadIdx.x; k < S.nblk; k += blockDim.x) s += pb[k];
+  for (int k = threadIdx.x; k < S.nblk_tile; k += blockDim.x) s += pb[k];
   s = block_sum_d(s, sh);
   if (threadIdx.x != 0) return;
   const double true_rel = sqrt(s) / S.beta[b];
@@ -583,6 +583,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
 
   State S{};
   S.B = B; S.ns = ns; S.maxit = maxit; S.cap = cap; S.n = n; S.nblk = nblk;
+  S.nblk_tile = p->view(0).ntiles;
   S.tol = prob.tol; S.variant = prob.variant; S.record_history = prob.record_history;
   S.active = active; S.beta = beta; S.shifts = dShifts.as<double2>(); S.taus = dTaus.as<double2>();
   S.H = dH.as<double2>(); S.conv = conv; S.iter = iter; S.est = est; S.true_res = true_res;
@@ -713,12 +714,12 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
     const int m = j + 1;
     // 3. per-shift small solves, verification, freeze
     launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 0); });
-    partials.ensure(sizeof(double) * n_bs * nblk, st);
+    partials.ensure(sizeof(double) * n_bs * std::max(nblk, S.nblk_tile), st);
     launch(ctx, "fgmres_verify", nb * (16.0 * (m + 1)) + n * 8.0 * (p->dim + 1), [&] {
       if (p->dim == 3)
-        verify_residual<3><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+        verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
       else
-        verify_residual<2><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+        verify_residual<2><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
     });
     launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 0); });
     launch(ctx, "fgmres_small", 0.0, [&] { count_unconverged<<<blocks_for(B, 128), 128, 0, st>>>(S, m); });
@@ -754,9 +755,9 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
       // restrict flags to the items of this m
       launch(ctx, "fgmres_verify", 0.0, [&] {
         if (p->dim == 3)
-          verify_residual<3><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+          verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
         else
-          verify_residual<2><<<grid, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+          verify_residual<2><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
       });
       launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 1); });
     }

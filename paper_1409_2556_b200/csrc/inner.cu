@@ -59,6 +59,14 @@ struct Batch {
   const int* done;  // per item: 1 -> skip
 };
 
+#define TILE_PROLOGUE(LV)                  \
+  const int b = blockIdx.x % bt.B;          \
+  const int cb = blockIdx.x / bt.B;         \
+  if (bt.done[b]) return;                   \
+  int i, j, k;                              \
+  int64_t a;                                \
+  const bool in = tile_cell(LV, cb, i, j, k, a);
+
 #define ITEM_PROLOGUE(n)                                          \
   const int b = blockIdx.x % bt.B;                                \
   const int64_t cb = blockIdx.x / bt.B;                           \
@@ -75,16 +83,13 @@ template <int DIM>
 __global__ void __launch_bounds__(kT) rbgs_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
                                                   const double2* __restrict__ f, double2* __restrict__ x,
                                                   int color, int zero_init) {
-  ITEM_PROLOGUE(L.n);
+  TILE_PROLOGUE(L);
   if (!in) return;
-  int i, j, k;
-  decode<DIM>(L, a, i, j, k);
   double2* xb = x + b * L.n;
   if (((i + j + k) & 1) != color) {
     if (zero_init) xb[a] = make_double2(0.0, 0.0);
     return;
   }
-  const double2 tau = taus[b];
   const double m = __ldg(L.M + a);
   const double2 fa = f[b * L.n + a];
   double2 off;
@@ -95,18 +100,15 @@ __global__ void __launch_bounds__(kT) rbgs_kernel(LevelView L, Batch bt, const d
   } else {
     gather<DIM>(L, xb, a, i, j, k, off, dk);
   }
-  const double2 d = make_double2(dk + tau.x * m, tau.y * m);
-  xb[a] = cdiv(cadd(fa, off), d);
+  xb[a] = diag_solve(dk, m, taus[b], cadd(fa, off));
 }
 
 template <int DIM>
 __global__ void __launch_bounds__(kT) residual_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
                                                       const double2* __restrict__ f, const double2* __restrict__ x,
                                                       double2* __restrict__ r) {
-  ITEM_PROLOGUE(L.n);
+  TILE_PROLOGUE(L);
   if (!in) return;
-  int i, j, k;
-  decode<DIM>(L, a, i, j, k);
   const double2 ax = stencil_apply<DIM>(L, x + b * L.n, a, i, j, k, taus[b]);
   r[b * L.n + a] = csub(f[b * L.n + a], ax);
 }
@@ -137,10 +139,9 @@ __device__ __forceinline__ int r1d_terms(int I, int agg, int nc, int* F, double*
 template <int DIM>
 __global__ void __launch_bounds__(kT) restrict_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
                                                       const double2* __restrict__ rf, double2* __restrict__ fc) {
-  ITEM_PROLOGUE(Lc.n);
+  TILE_PROLOGUE(Lc);
   if (!in) return;
-  int I, J, K;
-  decode<DIM>(Lc, a, I, J, K);
+  const int I = i, J = j, K = k;
   int Fx[4], Fy[4], Fz[4];
   double wx[4], wy[4], wz[4];
   const int nxx = r1d_terms(I, ax, Lc.nx, Fx, wx);
@@ -167,10 +168,8 @@ __global__ void __launch_bounds__(kT) restrict_kernel(LevelView Lf, LevelView Lc
 template <int DIM>
 __global__ void __launch_bounds__(kT) prolong_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
                                                      const double2* __restrict__ ec, double2* __restrict__ xf) {
-  ITEM_PROLOGUE(Lf.n);
+  TILE_PROLOGUE(Lf);
   if (!in) return;
-  int i, j, k;
-  decode<DIM>(Lf, a, i, j, k);
   int Ix[2], Iy[2], Iz[2];
   double wx[2], wy[2], wz[2];
   const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
@@ -241,11 +240,9 @@ template <int DIM>
 __global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
                                                        const double2* __restrict__ p, double2* __restrict__ q,
                                                        double2* __restrict__ part, int nblk) {
-  ITEM_PROLOGUE(L.n);
+  TILE_PROLOGUE(L);
   double2 s = make_double2(0.0, 0.0);
   if (in) {
-    int i, j, k;
-    decode<DIM>(L, a, i, j, k);
     const double2* pb = p + b * L.n;
     const double2 qa = stencil_apply<DIM>(L, pb, a, i, j, k, taus[b]);
     q[b * L.n + a] = qa;
@@ -345,7 +342,7 @@ void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, co
   cudaStream_t st = ctx->stream;
   const int last = (int)p->levels.size() - 1;
   LevelView L = p->view(l);
-  const unsigned grid = blocks_for(L.n, kT) * (unsigned)Bc;
+  const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
   const double cell_bytes = (double)L.n * Bc;
   const double coef = (double)L.n * 8.0 * (DIM + 1);
   if (l == last) {
@@ -367,7 +364,7 @@ void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, co
   launch(ctx, "mg_residual", cell_bytes * 48.0 + coef, [&] {
     residual_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l]);
   });
-  const unsigned gridc = blocks_for(Lc.n, kT) * (unsigned)Bc;
+  const unsigned gridc = (unsigned)Lc.ntiles * (unsigned)Bc;
   launch(ctx, "mg_restrict", cell_bytes * 16.0 + (double)Lc.n * Bc * 16.0, [&] {
     restrict_kernel<DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, R[l],
                                                 const_cast<double2*>(F[l + 1]));
@@ -419,7 +416,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   Batch bt{Bc, d_done};
 
   // workspace
-  DeviceBuffer partials(sizeof(double2) * (size_t)Bc * nblk, st);
+  DeviceBuffer partials(sizeof(double2) * (size_t)Bc * std::max<int64_t>(nblk, L0.ntiles), st);
   DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 5, st);
   double2* r = vec.as<double2>();
   double2* z = r + Bc * n;
@@ -473,9 +470,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   launch(ctx, "cocg_vec", nb * 32.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
   for (int it = 0; it < p->inner_maxit; ++it) {
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
-      apply_dot_kernel<DIM><<<grid, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(), nblk);
+      apply_dot_kernel<DIM><<<(unsigned)L0.ntiles * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
+                                                                    L0.ntiles);
     });
-    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk, sc); });
+    launch(ctx, "cocg_scalar", 0.0, [&] {
+      scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), L0.ntiles, sc);
+    });
     launch(ctx, "cocg_vec", nb * (it == 0 ? 64.0 : 80.0), [&] {
       axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, it == 0, (double*)partials.get(), nblk);
     });

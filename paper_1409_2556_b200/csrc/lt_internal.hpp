@@ -126,6 +126,8 @@ struct LevelView {
   const double* Ty;
   const double* Tz;
   const double* M;
+  // 256-thread (x, y) tiles: tw x th cells, tw a power of two (tws = log2 tw)
+  int tw, tws, th, tiles_x, tiles_y, ntiles;
 };
 
 struct CoarseFactor {

@@ -242,7 +242,14 @@ __global__ void __launch_bounds__(1024) gauss_jordan(double2* __restrict__ aug, 
 
 LevelView lt_pencil_view(const lt_pencil_s* p, int l) {
   const Level& L = *p->levels[l];
-  return LevelView{L.nx, L.ny, L.nz, p->dim, L.n, L.Tx, L.Ty, L.Tz, L.M};
+  int tws = 0;
+  while ((1 << tws) < L.nx && tws < 5) ++tws;  // tile width: next power of two of nx, <= 32
+  const int tw = 1 << tws;
+  const int th = 256 / tw;
+  const int tiles_x = (L.nx + tw - 1) / tw;
+  const int tiles_y = (L.ny + th - 1) / th;
+  return LevelView{L.nx, L.ny, L.nz, p->dim, L.n, L.Tx, L.Ty, L.Tz, L.M,
+                   tw, tws, th, tiles_x, tiles_y, tiles_x * tiles_y * L.nz};
 }
 
 static void alloc_level(Level& L, int dim, cudaStream_t s) {
@@ -382,17 +389,13 @@ template <int DIM, bool MASS_ONLY>
 __global__ void apply_kernel(LevelView L, const double2* __restrict__ taus, const double2* __restrict__ x,
                              int64_t xs, double2* __restrict__ y, int64_t ys, int B) {
   const int b = blockIdx.x % B;
-  const int64_t a = (int64_t)(blockIdx.x / B) * blockDim.x + threadIdx.x;
-  if (a >= L.n) return;
+  int i, j, k;
+  int64_t a;
+  if (!tile_cell(L, blockIdx.x / B, i, j, k, a)) return;
   const double2* xb = x + b * xs;
   double2 out;
-  if (MASS_ONLY) {
-    out = cscale(xb[a], L.M[a]);
-  } else {
-    int i, j, k;
-    decode<DIM>(L, a, i, j, k);
-    out = stencil_apply<DIM>(L, xb, a, i, j, k, taus[b]);
-  }
+  if (MASS_ONLY) out = cscale(xb[a], L.M[a]);
+  else out = stencil_apply<DIM>(L, xb, a, i, j, k, taus[b]);
   y[b * ys + a] = out;
 }
 
@@ -402,7 +405,7 @@ void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2*
                  double2* y, int64_t ys, int B, bool mass_only, const char* name) {
   LevelView L = p->view(level);
   cudaStream_t st = p->ctx->stream;
-  unsigned grid = blocks_for(L.n, kThreads) * (unsigned)B;
+  unsigned grid = (unsigned)L.ntiles * (unsigned)B;
   double bytes = mass_only ? (double)L.n * (32.0 * B + 8.0) : (double)L.n * (32.0 * B + 8.0 * (p->dim + 1));
   launch(p->ctx, name, bytes, [&] {
     if (mass_only) {

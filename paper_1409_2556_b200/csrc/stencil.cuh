@@ -13,6 +13,26 @@ __device__ __forceinline__ int64_t fy(const LevelView& L, int i, int j, int k) {
   return ((int64_t)k * (L.ny + 1) + j) * L.nx + i;
 }
 
+// Cell of thread threadIdx.x in tile `cb` of a level (256-thread x-y tiles, one plane);
+// false for threads past the grid edge.
+__device__ __forceinline__ bool tile_cell(const LevelView& L, int cb, int& i, int& j, int& k, int64_t& a) {
+  const int bx = cb % L.tiles_x;
+  const int t = cb / L.tiles_x;
+  const int by = t % L.tiles_y;
+  k = t / L.tiles_y;
+  i = (bx << L.tws) + (threadIdx.x & (L.tw - 1));
+  j = by * L.th + (threadIdx.x >> L.tws);
+  a = ((int64_t)k * L.ny + j) * L.nx + i;
+  return i < L.nx && j < L.ny;
+}
+
+// (dk + tau m)^{-1} (f + off) with one real division
+__device__ __forceinline__ double2 diag_solve(double dk, double m, double2 tau, double2 rhs) {
+  const double dr = dk + tau.x * m, di = tau.y * m;
+  const double inv = 1.0 / (dr * dr + di * di);
+  return make_double2((rhs.x * dr + rhs.y * di) * inv, (rhs.y * dr - rhs.x * di) * inv);
+}
+
 template <int DIM>
 __device__ __forceinline__ void decode(const LevelView& L, int64_t a, int& i, int& j, int& k) {
   i = (int)(a % L.nx);
