@@ -41,10 +41,10 @@ def _needs(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = OBJ_DIR / (src.name + ".o")
+def _compile(src: Path, verbose: bool, defines=(), tag: str = "") -> Path:
+    obj = OBJ_DIR / (src.name + tag + ".o")
     if _needs(obj, [src] + headers()):
-        cmd = [NVCC, *ARCH, *COMMON, "-c", str(src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *COMMON, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,18 +55,21 @@ def _compile(src: Path, verbose: bool) -> Path:
     return obj
 
 
-def build(verbose: bool = False) -> Path:
+def build(verbose: bool = False, defines=(), variant: str = "") -> Path:
+    """variant != "": an experiment build with extra -D defines into liblaptomo_gpu_<variant>.so."""
     OBJ_DIR.mkdir(parents=True, exist_ok=True)
     OUT_DIR.mkdir(parents=True, exist_ok=True)
+    lib = LIB if not variant else OUT_DIR / f"liblaptomo_gpu_{variant}.so"
+    tag = f".{variant}" if variant else ""
     srcs = sources()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if _needs(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+        objs = list(ex.map(lambda s: _compile(s, verbose, defines, tag), srcs))
+    if _needs(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -12,7 +12,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblaptomo_gpu.so"
+LIB_PATH = Path(os.environ.get("LT_LIB") or Path(__file__).resolve().parent / "_lib" / "liblaptomo_gpu.so")
 
 LT_OK = 0
 LT_ERR_INVALID_ARGUMENT = 1

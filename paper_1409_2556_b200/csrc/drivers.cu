@@ -30,8 +30,8 @@ inline double2 d2(cd c) { return make_double2(c.real(), c.imag()); }
 __global__ void __launch_bounds__(kT) recombine_kernel(int64_t n, int B, int mc, const double2* const* __restrict__ Ucols,
                                                        const double2* __restrict__ c, const int64_t* __restrict__ dst,
                                                        double* __restrict__ heads) {
-  const int b = blockIdx.x % B;
-  const int64_t a = (int64_t)(blockIdx.x / B) * blockDim.x + threadIdx.x;
+  LT_ITEM_BLOCK(B, b, cb);
+  const int64_t a = (int64_t)cb * blockDim.x + threadIdx.x;
   if (a >= n || dst[b] < 0) return;
   double s = 0.0;
   for (int j = 0; j < mc; ++j) {

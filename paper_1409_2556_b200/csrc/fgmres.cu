@@ -98,8 +98,7 @@ __global__ void __launch_bounds__(kT) mass_multidot(LevelView L, State S, int j,
                                                     double2* __restrict__ s_out, const double2* const* __restrict__ Vcols,
                                                     double2* __restrict__ part) {
   __shared__ double2 sh[32];
-  const int b = blockIdx.x % S.B;
-  const int64_t cb = blockIdx.x / S.B;
+  LT_ITEM_BLOCK(S.B, b, cb);
   if (!S.active[b]) return;
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   const bool in = a < L.n;
@@ -122,8 +121,7 @@ __global__ void __launch_bounds__(kT) mass_multidot(LevelView L, State S, int j,
 __global__ void __launch_bounds__(kT) multidot(State S, int j, const double2* __restrict__ s_in,
                                                const double2* const* __restrict__ Vcols, double2* __restrict__ part) {
   __shared__ double2 sh[32];
-  const int b = blockIdx.x % S.B;
-  const int64_t cb = blockIdx.x / S.B;
+  LT_ITEM_BLOCK(S.B, b, cb);
   if (!S.active[b] || !S.reorth[b]) return;
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   const bool in = a < S.n;
@@ -165,8 +163,7 @@ __global__ void __launch_bounds__(kT) gs_update(State S, int j, int pass, double
                                                 const double2* const* __restrict__ Vcols,
                                                 const double2* __restrict__ hcoef, double* __restrict__ part) {
   __shared__ double sh[32];
-  const int b = blockIdx.x % S.B;
-  const int64_t cb = blockIdx.x / S.B;
+  LT_ITEM_BLOCK(S.B, b, cb);
   if (!S.active[b]) return;
   if (pass == 1 && !S.reorth[b]) return;
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
@@ -207,8 +204,7 @@ __global__ void __launch_bounds__(kT) reduce_norm(State S, int j, int pass, cons
 }
 
 __global__ void __launch_bounds__(kT) normalize(State S, double2* __restrict__ v) {
-  const int b = blockIdx.x % S.B;
-  const int64_t cb = blockIdx.x / S.B;
+  LT_ITEM_BLOCK(S.B, b, cb);
   if (!S.active[b] || S.breakdown[b]) return;
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   if (a < S.n) {
@@ -355,8 +351,7 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
   __shared__ double sh[32];
   __shared__ int flagged[256];
   __shared__ int nflag;
-  const int b = blockIdx.x % S.B;
-  const int64_t cb = blockIdx.x / S.B;
+  LT_ITEM_BLOCK(S.B, b, cb);
   if (threadIdx.x == 0) {
     int c = 0;
     for (int k = 0; k < S.ns && c < 256; ++k)
@@ -441,8 +436,7 @@ __global__ void count_unconverged(State S, int m) {
 __global__ void __launch_bounds__(kT) norm_kernel(int64_t n, int B, const double2* __restrict__ x, double* __restrict__ part,
                                                   int nblk) {
   __shared__ double sh[32];
-  const int b = blockIdx.x % B;
-  const int64_t cb = blockIdx.x / B;
+  LT_ITEM_BLOCK(B, b, cb);
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   double s = a < n ? cabs2(x[b * n + a]) : 0.0;
   s = block_sum_d(s, sh);
@@ -460,8 +454,7 @@ __global__ void __launch_bounds__(kT) reduce_beta(int B, int nblk, const double*
 
 __global__ void __launch_bounds__(kT) scale_to(int64_t n, int B, const double2* __restrict__ x, const double* __restrict__ beta,
                                                double2* __restrict__ v) {
-  const int b = blockIdx.x % B;
-  const int64_t cb = blockIdx.x / B;
+  LT_ITEM_BLOCK(B, b, cb);
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   const double bt = beta[b];
@@ -472,8 +465,7 @@ __global__ void __launch_bounds__(kT) scale_to(int64_t n, int B, const double2* 
 __global__ void __launch_bounds__(kT) expand_kernel(int64_t n, int B, int ns, int maxit, const double2* const* __restrict__ Ucols,
                                                     const double2* __restrict__ Y, const int* __restrict__ m_used,
                                                     const double2* __restrict__ scale, double2* __restrict__ out) {
-  const int b = blockIdx.x % B;
-  const int64_t cb = blockIdx.x / B;
+  LT_ITEM_BLOCK(B, b, cb);
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;
   if (a >= n) return;
   int mmax = 0;

@@ -60,16 +60,14 @@ struct Batch {
 };
 
 #define TILE_PROLOGUE(LV)                  \
-  const int b = blockIdx.x % bt.B;          \
-  const int cb = blockIdx.x / bt.B;         \
+  LT_ITEM_BLOCK(bt.B, b, cb)               \
   if (bt.done[b]) return;                   \
   int i, j, k;                              \
   int64_t a;                                \
   const bool in = tile_cell(LV, cb, i, j, k, a);
 
 #define ITEM_PROLOGUE(n)                                          \
-  const int b = blockIdx.x % bt.B;                                \
-  const int64_t cb = blockIdx.x / bt.B;                           \
+  LT_ITEM_BLOCK(bt.B, b, cb)                                      \
   if (bt.done[b]) return;                                         \
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;       \
   const bool in = a < (n);

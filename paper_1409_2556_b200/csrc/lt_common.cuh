@@ -74,6 +74,19 @@ inline void check_launch(const char* name) {
 
 constexpr int kThreads = 256;
 
+// Block -> (item, cell block) for batched kernels launched with B * blocks_per_item blocks.
+// Default: cell blocks of one item are consecutive (each item streams through contiguous
+// memory); -DLT_ITEM_FAST puts the item index fastest instead.
+#ifndef LT_ITEM_FAST
+#define LT_ITEM_BLOCK(B, b, cb)                            \
+  const int b = (int)(blockIdx.x / (gridDim.x / (B)));     \
+  const int cb = (int)(blockIdx.x % (gridDim.x / (B)));
+#else
+#define LT_ITEM_BLOCK(B, b, cb)         \
+  const int b = (int)(blockIdx.x % (B)); \
+  const int cb = (int)(blockIdx.x / (B));
+#endif
+
 inline unsigned blocks_for(int64_t n, int per_block) {
   int64_t b = (n + per_block - 1) / per_block;
   return static_cast<unsigned>(b < 1 ? 1 : b);

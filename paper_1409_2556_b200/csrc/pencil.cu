@@ -388,10 +388,10 @@ namespace {
 template <int DIM, bool MASS_ONLY>
 __global__ void apply_kernel(LevelView L, const double2* __restrict__ taus, const double2* __restrict__ x,
                              int64_t xs, double2* __restrict__ y, int64_t ys, int B) {
-  const int b = blockIdx.x % B;
+  LT_ITEM_BLOCK(B, b, cb);
   int i, j, k;
   int64_t a;
-  if (!tile_cell(L, blockIdx.x / B, i, j, k, a)) return;
+  if (!tile_cell(L, cb, i, j, k, a)) return;
   const double2* xb = x + b * xs;
   double2 out;
   if (MASS_ONLY) out = cscale(xb[a], L.M[a]);
