@@ -191,6 +191,133 @@ __global__ void __launch_bounds__(kT) prolong_kernel(LevelView Lf, LevelView Lc,
   xf[b * Lf.n + a] = s;
 }
 
+// ---- fused red-black Gauss-Seidel sweep ------------------------------------------------
+// One full sweep (colour `first`, then the other colour) of a 32 x 8 (x, y) tile, marching
+// through z with a 4-plane shared-memory ring (halo 2 in x/y): the first colour is updated
+// on the tile + 1-cell halo (from old second-colour values), the second colour on the tile
+// (from the new first-colour values), so each cell of x and f is read from HBM once and x is
+// written once.  zero_init: the iterate is zero on entry (no loads).  ec != null: the loaded
+// iterate is x + P ec (fused coarse-grid correction, cell-centred multilinear P).
+constexpr int SW_TX = 32, SW_TY = 8, SW_HX = SW_TX + 4, SW_HY = SW_TY + 4, SW_PL = SW_HX * SW_HY;
+
+__device__ __forceinline__ double2 prolong_at(const LevelView& Lc, int ax, int ay, int az, const double2* __restrict__ eb,
+                                              int i, int j, int k, int dim) {
+  int Ix[2], Iy[2], Iz[2];
+  double wx[2], wy[2], wz[2];
+  const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
+  const int nyy = p1d_terms(j, ay, Lc.ny, Iy, wy);
+  int nzz = 1;
+  Iz[0] = 0; wz[0] = 1.0;
+  if (dim == 3) nzz = p1d_terms(k, az, Lc.nz, Iz, wz);
+  double2 s = make_double2(0.0, 0.0);
+  for (int q = 0; q < nzz; ++q)
+    for (int p = 0; p < nyy; ++p) {
+      const double wzy = wz[q] * wy[p];
+      const int64_t row = ((int64_t)Iz[q] * Lc.ny + Iy[p]) * Lc.nx;
+      for (int o = 0; o < nxx; ++o) {
+        const double2 v = eb[row + Ix[o]];
+        const double w = wzy * wx[o];
+        s.x += w * v.x;
+        s.y += w * v.y;
+      }
+    }
+  return s;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
+                                                      const double2* __restrict__ f, const double2* __restrict__ xin,
+                                                      double2* __restrict__ x, int first, int zero_init, LevelView Lc,
+                                                      int ax, int ay, int az, const double2* __restrict__ ec) {
+  constexpr int NS = DIM == 3 ? 4 : 1;
+  __shared__ double2 U[NS][SW_PL];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int tiles_x = (L.nx + SW_TX - 1) / SW_TX;
+  const int i0 = (cb % tiles_x) * SW_TX, j0 = (cb / tiles_x) * SW_TY;
+  const int tid = threadIdx.x;
+  const double2 tau = taus[b];
+  const double2* fb = f + (int64_t)b * L.n;
+  double2* xb = x + (int64_t)b * L.n;  // out of place: halos of neighbouring tiles read xin
+  const double2* xib = zero_init ? nullptr : xin + (int64_t)b * L.n;
+  const double2* eb = ec ? ec + (int64_t)b * Lc.n : nullptr;
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  const int second = first ^ 1;
+  auto slot = [](int k) { return DIM == 3 ? (k & 3) : 0; };
+
+  auto load_plane = [&](int k) {
+    double2* S = U[slot(k)];
+    for (int e = tid; e < SW_PL; e += kT) {
+      const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
+      double2 v = make_double2(0.0, 0.0);
+      if (!zero_init && i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
+        const int64_t a = k * plane + (int64_t)j * L.nx + i;
+        v = xib[a];
+        if (eb) v = cadd(v, prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
+      }
+      S[e] = v;
+    }
+  };
+  // Gauss-Seidel update of colour `color` on plane k over the tile grown by `h` cells.
+  auto update = [&](int k, int color, int h) {
+    const int RX = SW_TX + 2 * h, RY = SW_TY + 2 * h;
+    double2* S = U[slot(k)];
+    for (int e = tid; e < RX * RY; e += kT) {
+      const int li = e % RX - h, lj = e / RX - h;
+      const int i = i0 + li, j = j0 + lj;
+      if (i < 0 || i >= L.nx || j < 0 || j >= L.ny || ((i + j + k) & 1) != color) continue;
+      const int s = (lj + 2) * SW_HX + (li + 2);
+      const int64_t a = k * plane + (int64_t)j * L.nx + i;
+      const int64_t ex = fx(L, i, j, k), ey = fy(L, i, j, k);
+      const double tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
+      const double ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
+      double dk = tw + te + ts + tn;
+      double2 o = fb[a];
+      if (i > 0) o = cadd(o, cscale(S[s - 1], tw));
+      if (i < L.nx - 1) o = cadd(o, cscale(S[s + 1], te));
+      if (j > 0) o = cadd(o, cscale(S[s - SW_HX], ts));
+      if (j < L.ny - 1) o = cadd(o, cscale(S[s + SW_HX], tn));
+      if (DIM == 3) {
+        const double tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+        dk += tb + tt;
+        if (k > 0) o = cadd(o, cscale(U[slot(k - 1)][s], tb));
+        if (k < L.nz - 1) o = cadd(o, cscale(U[slot(k + 1)][s], tt));
+      }
+      S[s] = diag_solve(dk, __ldg(L.M + a), tau, o);
+    }
+  };
+  auto store_plane = [&](int k) {
+    const double2* S = U[slot(k)];
+    const int li = tid % SW_TX, lj = tid / SW_TX;
+    const int i = i0 + li, j = j0 + lj;
+    if (i < L.nx && j < L.ny) xb[k * plane + (int64_t)j * L.nx + i] = S[(lj + 2) * SW_HX + (li + 2)];
+  };
+
+  if (DIM == 2) {
+    load_plane(0);
+    __syncthreads();
+    update(0, first, 1);
+    __syncthreads();
+    update(0, second, 0);
+    __syncthreads();
+    store_plane(0);
+    return;
+  }
+  load_plane(0);
+  if (L.nz > 1) load_plane(1);
+  __syncthreads();
+  update(0, first, 1);
+  for (int k = 0; k < L.nz; ++k) {
+    if (k + 2 < L.nz) load_plane(k + 2);
+    __syncthreads();
+    if (k + 1 < L.nz) update(k + 1, first, 1);
+    __syncthreads();
+    update(k, second, 0);
+    __syncthreads();
+    store_plane(k);
+  }
+}
+
 // e = A_c(tau_b)^{-1} f: one warp per row of the dense inverse (augmented, ld = 2n).
 __global__ void __launch_bounds__(kT) coarse_solve_kernel(int nc, Batch bt, const double2* const* __restrict__ inv,
                                                           const double2* __restrict__ f, double2* __restrict__ e) {
@@ -333,9 +460,10 @@ struct VcycleWork {
   std::vector<DeviceBuffer> x, f, r;  // per level: Bc x n_l (level 0: x = z, f = COCG r)
 };
 
+// Returns the buffer holding the level-l V-cycle output (Bc x n_l).
 template <int DIM>
-void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, const double2* const* inv,
-            std::vector<double2*>& X, std::vector<const double2*>& F, std::vector<double2*>& R) {
+const double2* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, const double2* const* inv,
+                      std::vector<double2*>& X, std::vector<const double2*>& F, std::vector<double2*>& R) {
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int last = (int)p->levels.size() - 1;
@@ -348,16 +476,15 @@ void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, co
     launch(ctx, "mg_coarse_solve", cell_bytes * 32.0, [&] {
       coarse_solve_kernel<<<g, kT, 0, st>>>((int)L.n, bt, inv, F[l], X[l]);
     });
-    return;
+    return X[l];
   }
   LevelView Lc = p->view(l + 1);
   const Level& lev = *p->levels[l];
-  // pre-smoothing (red, black) from a zero iterate
-  launch(ctx, "mg_smooth", cell_bytes * 24.0 + coef, [&] {
-    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 1);
-  });
+  const unsigned sgrid = (unsigned)(((L.nx + SW_TX - 1) / SW_TX) * ((L.ny + SW_TY - 1) / SW_TY)) * (unsigned)Bc;
+  // pre-smoothing: one red-black sweep (red first) from a zero iterate; algorithmic bytes
+  // per cell-item: f read + x written (coefficients once per item batch)
   launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
-    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
+    rb_sweep_kernel<DIM><<<sgrid, kT, 0, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
   });
   launch(ctx, "mg_residual", cell_bytes * 48.0 + coef, [&] {
     residual_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l]);
@@ -367,17 +494,14 @@ void vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, co
     restrict_kernel<DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, R[l],
                                                 const_cast<double2*>(F[l + 1]));
   });
-  vcycle<DIM>(p, l + 1, Bc, bt, taus, inv, X, F, R);
-  launch(ctx, "mg_prolong", cell_bytes * 32.0 + (double)Lc.n * Bc * 16.0, [&] {
-    prolong_kernel<DIM><<<grid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, X[l + 1], X[l]);
+  const double2* ec = vcycle<DIM>(p, l + 1, Bc, bt, taus, inv, X, F, R);
+  // post-smoothing: coarse correction x + P e_c fused into one black-first sweep (the
+  // transpose of the pre-smoother), written out of place into R[l]
+  launch(ctx, "mg_smooth", cell_bytes * 48.0 + (double)Lc.n * Bc * 16.0 + coef, [&] {
+    rb_sweep_kernel<DIM><<<sgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l], 1, 0, Lc, lev.agg[0], lev.agg[1],
+                                               lev.agg[2], ec);
   });
-  // post-smoothing (black, red): the transpose of the pre-smoother
-  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
-    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
-  });
-  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
-    rbgs_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 0);
-  });
+  return R[l];
 }
 
 template <int DIM>
@@ -417,14 +541,14 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   DeviceBuffer partials(sizeof(double2) * (size_t)Bc * std::max<int64_t>(nblk, L0.ntiles), st);
   DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 5, st);
   double2* r = vec.as<double2>();
-  double2* z = r + Bc * n;
-  double2* pp = z + Bc * n;
+  double2* zbuf = r + Bc * n;
+  double2* pp = zbuf + Bc * n;
   double2* q = pp + Bc * n;
   double2* res0 = q + Bc * n;
   std::vector<DeviceBuffer> lvl(nl);
   std::vector<double2*> X(nl), R(nl);
   std::vector<const double2*> F(nl);
-  X[0] = z;
+  X[0] = zbuf;
   F[0] = r;
   R[0] = res0;
   for (int l = 1; l < nl; ++l) {
@@ -462,7 +586,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   const double tol2 = p->inner_tol * p->inner_tol;
   for (int b = 0; b < Bc; ++b) best[b] = bb[b];
   // z = B r ; rho = r^T z ; p = z
-  vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
+  const double2* z = vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
   launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RHO, bt, partials.get(), nblk, sc); });
   launch(ctx, "cocg_vec", nb * 32.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
@@ -494,7 +618,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       if (active == 0) break;
       LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
     }
-    vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
+    z = vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
     launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BETA, bt, partials.get(), nblk, sc); });
     launch(ctx, "cocg_vec", nb * 48.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
