@@ -223,9 +223,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
 
-    cfg = inputs.config(args.config)
-    if rank > 0:  # replica: own realisation of the same statistics
-        cfg.log_kappa = {**cfg.log_kappa, "seed": cfg.log_kappa["seed"] + 1000 * rank}
+    from paper_1409_2556_b200.replicas import max_over_ranks, replica_config
+    cfg = replica_config(inputs.config(args.config), rank)  # rank > 0: own realisation
     lk, ls = cfg.fields()
     n = cfg.n_cells
     n_src, n_rec, n_t = len(cfg.sources), len(cfg.receivers), len(cfg.times)
@@ -309,12 +308,7 @@ def main():
     barrier()
     ms_e2e = f0.elapsed_time(f1)
 
-    t_max = ms
-    t_e2e = ms_e2e
-    if world > 1:
-        tt = torch.tensor([ms, ms_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max, t_e2e = float(tt[0]), float(tt[1])
+    t_max, t_e2e = max_over_ranks([ms, ms_e2e], device=torch.device("cuda", local))
     per_step = t_max / args.steps
     value = world * solves_per_build * args.steps / (t_max * 1e-3)
     e2e_value = world * solves_per_build * args.steps / (t_e2e * 1e-3)

@@ -229,8 +229,14 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
                                                       const double2* __restrict__ f, const double2* __restrict__ xin,
                                                       double2* __restrict__ x, int first, int zero_init, LevelView Lc,
                                                       int ax, int ay, int az, const double2* __restrict__ ec) {
-  constexpr int NS = DIM == 3 ? 4 : 1;
-  __shared__ double2 U[NS][SW_PL];
+  // x planes (halo 2) in a 5-slot ring, f planes (halo 1) in a 3-slot ring, both filled
+  // one step ahead with cp.async so HBM latency overlaps the Gauss-Seidel updates.
+  constexpr int NS = DIM == 3 ? 5 : 1;
+  constexpr int NF = DIM == 3 ? 3 : 1;
+  constexpr int FX = SW_TX + 2, FPL = FX * (SW_TY + 2);
+  extern __shared__ __align__(16) double2 sw_smem[];  // U[NS][SW_PL] then Fr[NF][FPL]
+  double2 (*U)[SW_PL] = reinterpret_cast<double2 (*)[SW_PL]>(sw_smem);
+  double2 (*Fr)[FPL] = reinterpret_cast<double2 (*)[FPL]>(sw_smem + NS * SW_PL);
   LT_ITEM_BLOCK(bt.B, b, cb);
   if (bt.done[b]) return;
   const int tiles_x = (L.nx + SW_TX - 1) / SW_TX;
@@ -243,25 +249,52 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
   const double2* eb = ec ? ec + (int64_t)b * Lc.n : nullptr;
   const int64_t plane = (int64_t)L.nx * L.ny;
   const int second = first ^ 1;
-  auto slot = [](int k) { return DIM == 3 ? (k & 3) : 0; };
+  auto slot = [](int k) { return DIM == 3 ? k % 5 : 0; };
+  auto fslot = [](int k) { return DIM == 3 ? k % 3 : 0; };
 
-  auto load_plane = [&](int k) {
+  auto cp16 = [](void* dst, const void* src, bool valid) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
+  };
+  auto commit = [] { asm volatile("cp.async.commit_group;\n" ::); };
+  auto wait1 = [] { asm volatile("cp.async.wait_group 1;\n" ::); };
+  auto wait0 = [] { asm volatile("cp.async.wait_group 0;\n" ::); };
+
+  // issue the copies of x plane k (or zero it) and of f plane kf (halo 1)
+  auto issue_x = [&](int k) {
     double2* S = U[slot(k)];
     for (int e = tid; e < SW_PL; e += kT) {
       const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
-      double2 v = make_double2(0.0, 0.0);
-      if (!zero_init && i >= 0 && i < L.nx && j >= 0 && j < L.ny) {
-        const int64_t a = k * plane + (int64_t)j * L.nx + i;
-        v = xib[a];
-        if (eb) v = cadd(v, prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
+      if (zero_init) {
+        S[e] = make_double2(0.0, 0.0);
+      } else {
+        const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
+        cp16(S + e, ok ? xib + (k * plane + (int64_t)j * L.nx + i) : xib, ok);
       }
-      S[e] = v;
+    }
+  };
+  auto issue_f = [&](int k) {
+    double2* S = Fr[fslot(k)];
+    for (int e = tid; e < FPL; e += kT) {
+      const int i = i0 - 1 + e % FX, j = j0 - 1 + e / FX;
+      const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
+      cp16(S + e, ok ? fb + (k * plane + (int64_t)j * L.nx + i) : fb, ok);
+    }
+  };
+  // coarse-grid correction x += P e_c on a landed x plane (post-smoother)
+  auto add_prolong = [&](int k) {
+    double2* S = U[slot(k)];
+    for (int e = tid; e < SW_PL; e += kT) {
+      const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
+      if (i >= 0 && i < L.nx && j >= 0 && j < L.ny)
+        S[e] = cadd(S[e], prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
     }
   };
   // Gauss-Seidel update of colour `color` on plane k over the tile grown by `h` cells.
   auto update = [&](int k, int color, int h) {
     const int RX = SW_TX + 2 * h, RY = SW_TY + 2 * h;
     double2* S = U[slot(k)];
+    const double2* Fk = Fr[fslot(k)];
     for (int e = tid; e < RX * RY; e += kT) {
       const int li = e % RX - h, lj = e / RX - h;
       const int i = i0 + li, j = j0 + lj;
@@ -272,7 +305,7 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
       const double tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
       const double ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
       double dk = tw + te + ts + tn;
-      double2 o = fb[a];
+      double2 o = Fk[(lj + 1) * FX + (li + 1)];
       if (i > 0) o = cadd(o, cscale(S[s - 1], tw));
       if (i < L.nx - 1) o = cadd(o, cscale(S[s + 1], te));
       if (j > 0) o = cadd(o, cscale(S[s - SW_HX], ts));
@@ -294,8 +327,15 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
   };
 
   if (DIM == 2) {
-    load_plane(0);
+    issue_x(0);
+    issue_f(0);
+    commit();
+    wait0();
     __syncthreads();
+    if (eb) {
+      add_prolong(0);
+      __syncthreads();
+    }
     update(0, first, 1);
     __syncthreads();
     update(0, second, 0);
@@ -303,19 +343,40 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
     store_plane(0);
     return;
   }
-  load_plane(0);
-  if (L.nz > 1) load_plane(1);
+  // prologue: group A = {x0, x1, f0}, group B = {x2, f1}
+  issue_x(0);
+  if (L.nz > 1) issue_x(1);
+  issue_f(0);
+  commit();
+  if (L.nz > 2) issue_x(2);
+  if (L.nz > 1) issue_f(1);
+  commit();
+  wait1();
   __syncthreads();
+  if (eb) {
+    add_prolong(0);
+    if (L.nz > 1) add_prolong(1);
+    __syncthreads();
+  }
   update(0, first, 1);
   for (int k = 0; k < L.nz; ++k) {
-    if (k + 2 < L.nz) load_plane(k + 2);
+    // prefetch x(k+3), f(k+2); then wait for x(k+2), f(k+1) issued one step earlier
+    if (k + 3 < L.nz) issue_x(k + 3);
+    if (k + 2 < L.nz) issue_f(k + 2);
+    commit();
+    wait1();
     __syncthreads();
+    if (eb && k + 2 < L.nz) {
+      add_prolong(k + 2);
+      __syncthreads();
+    }
     if (k + 1 < L.nz) update(k + 1, first, 1);
     __syncthreads();
     update(k, second, 0);
     __syncthreads();
     store_plane(k);
   }
+  wait0();
 }
 
 // e = A_c(tau_b)^{-1} f: one warp per row of the dense inverse (augmented, ld = 2n).
@@ -481,10 +542,16 @@ const double2* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2
   LevelView Lc = p->view(l + 1);
   const Level& lev = *p->levels[l];
   const unsigned sgrid = (unsigned)(((L.nx + SW_TX - 1) / SW_TX) * ((L.ny + SW_TY - 1) / SW_TY)) * (unsigned)Bc;
+  const size_t ssmem = sizeof(double2) * ((DIM == 3 ? 5 : 1) * SW_PL + (DIM == 3 ? 3 : 1) * (SW_TX + 2) * (SW_TY + 2));
+  static bool attr_set = false;
+  if (!attr_set) {
+    LT_CUDA(cudaFuncSetAttribute(rb_sweep_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+    attr_set = true;
+  }
   // pre-smoothing: one red-black sweep (red first) from a zero iterate; algorithmic bytes
   // per cell-item: f read + x written (coefficients once per item batch)
   launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
-    rb_sweep_kernel<DIM><<<sgrid, kT, 0, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
+    rb_sweep_kernel<DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
   });
   launch(ctx, "mg_residual", cell_bytes * 48.0 + coef, [&] {
     residual_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l]);
@@ -498,7 +565,7 @@ const double2* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2
   // post-smoothing: coarse correction x + P e_c fused into one black-first sweep (the
   // transpose of the pre-smoother), written out of place into R[l]
   launch(ctx, "mg_smooth", cell_bytes * 48.0 + (double)Lc.n * Bc * 16.0 + coef, [&] {
-    rb_sweep_kernel<DIM><<<sgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l], 1, 0, Lc, lev.agg[0], lev.agg[1],
+    rb_sweep_kernel<DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], X[l], R[l], 1, 0, Lc, lev.agg[0], lev.agg[1],
                                                lev.agg[2], ec);
   });
   return R[l];
