@@ -4,11 +4,12 @@
 // (factorization.cpp:14-33, used at shifted_solver.cpp:192-193), exact to ~1e-15.  The LU
 // fill of K + tau M is infeasible in HBM for the 3-D configs, so the same
 // operator is inverted to tolerance instead: COCG (conjugate-orthogonal CG for the complex
-// symmetric K + tau M) preconditioned by a symmetric cell-centred multigrid V-cycle
+// symmetric K + tau M) in FP64, preconditioned by a symmetric cell-centred multigrid V-cycle
 // (red-black Gauss-Seidel, multilinear prolongation, R = P^T, rediscretised coarse faces,
-// exact dense inverse of the coarsest operator per tau).  B right-hand sides (each its own
-// tau) run in lockstep; blocks are (cell block, item) with the item index fastest so the
-// face coefficients of a cell block are read from L2 once for all items.
+// exact dense inverse of the coarsest operator per tau).  The V-cycle runs in FP32 (complex64
+// vectors, FP32 copies of the faces; -DLT_MG_FP64 selects FP64): it only has to approximate
+// the inverse, while the FP64 COCG recursion (r -= alpha A p with the FP64 operator) keeps the
+// solve exact to the 1e-12 tolerance.  B right-hand sides (each its own tau) run in lockstep.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -22,6 +23,25 @@ namespace {
 
 constexpr int kT = 256;
 
+#ifdef LT_MG_FP64
+using MgReal = double;
+#else
+using MgReal = float;
+#endif
+
+template <class R> struct CT;
+template <> struct CT<double> { using V = double2; };
+template <> struct CT<float> { using V = float2; };
+
+template <class V> __device__ __forceinline__ V vzero() { return V{0, 0}; }
+template <class V> __device__ __forceinline__ V vadd(V a, V b) { return V{a.x + b.x, a.y + b.y}; }
+template <class V> __device__ __forceinline__ V vsub(V a, V b) { return V{a.x - b.x, a.y - b.y}; }
+template <class V, class R> __device__ __forceinline__ V vscale(V a, R s) { return V{a.x * s, a.y * s}; }
+template <class V> __device__ __forceinline__ V vfrom(double2 a) {
+  return V{static_cast<decltype(V::x)>(a.x), static_cast<decltype(V::x)>(a.y)};
+}
+template <class V> __device__ __forceinline__ double2 vto(V a) { return make_double2((double)a.x, (double)a.y); }
+
 template <class T>
 __device__ __forceinline__ T warp_sum(T v);
 template <>
@@ -31,6 +51,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 template <>
 __device__ __forceinline__ double2 warp_sum(double2 v) {
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffff, v.x, o);
+    v.y += __shfl_down_sync(0xffffffff, v.y, o);
+  }
+  return v;
+}
+template <>
+__device__ __forceinline__ float2 warp_sum(float2 v) {
   for (int o = 16; o > 0; o >>= 1) {
     v.x += __shfl_down_sync(0xffffffff, v.x, o);
     v.y += __shfl_down_sync(0xffffffff, v.y, o);
@@ -72,229 +100,200 @@ struct Batch {
   const int64_t a = cb * (int64_t)blockDim.x + threadIdx.x;       \
   const bool in = a < (n);
 
-// ---- smoother / transfer / coarse solve --------------------------------------------------
-
-// One red-black Gauss-Seidel half sweep of colour `color` ((i+j+k) % 2).  zero_init: the
-// iterate is zero on entry (first half sweep of a V-cycle level): the colour cells get
-// f/d and the other cells are zero-filled.
-template <int DIM>
-__global__ void __launch_bounds__(kT) rbgs_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
-                                                  const double2* __restrict__ f, double2* __restrict__ x,
-                                                  int color, int zero_init) {
-  TILE_PROLOGUE(L);
-  if (!in) return;
-  double2* xb = x + b * L.n;
-  if (((i + j + k) & 1) != color) {
-    if (zero_init) xb[a] = make_double2(0.0, 0.0);
-    return;
-  }
-  const double m = __ldg(L.M + a);
-  const double2 fa = f[b * L.n + a];
-  double2 off;
-  double dk;
-  if (zero_init) {
-    dk = diag_k(L, i, j, k);
-    off = make_double2(0.0, 0.0);
-  } else {
-    gather<DIM>(L, xb, a, i, j, k, off, dk);
-  }
-  xb[a] = diag_solve(dk, m, taus[b], cadd(fa, off));
+// (dk + tau m)^{-1} rhs in precision R with one real division
+template <class R, class V>
+__device__ __forceinline__ V diag_solve_r(R dk, R m, R tr, R ti, V rhs) {
+  const R dr = dk + tr * m, di = ti * m;
+  const R inv = R(1) / (dr * dr + di * di);
+  return V{(rhs.x * dr + rhs.y * di) * inv, (rhs.y * dr - rhs.x * di) * inv};
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kT) residual_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
-                                                      const double2* __restrict__ f, const double2* __restrict__ x,
-                                                      double2* __restrict__ r) {
-  TILE_PROLOGUE(L);
-  if (!in) return;
-  const double2 ax = stencil_apply<DIM>(L, x + b * L.n, a, i, j, k, taus[b]);
-  r[b * L.n + a] = csub(f[b * L.n + a], ax);
-}
+// ---- multigrid kernels (precision R) ---------------------------------------------------
 
 // 1-D cell-centred linear interpolation weight P[f, I] (aggregation 2, Dirichlet ghost = -e).
-__device__ __forceinline__ int p1d_terms(int fi, int agg, int nc, int* I, double* w) {
-  if (agg == 1) { I[0] = fi; w[0] = 1.0; return 1; }
+__device__ __forceinline__ int p1d_terms(int fi, int agg, int nc, int* I, float* w) {
+  if (agg == 1) { I[0] = fi; w[0] = 1.0f; return 1; }
   const int c = fi >> 1;
   if ((fi & 1) == 0) {
-    if (c == 0) { I[0] = 0; w[0] = 0.5; return 1; }
-    I[0] = c; w[0] = 0.75; I[1] = c - 1; w[1] = 0.25; return 2;
+    if (c == 0) { I[0] = 0; w[0] = 0.5f; return 1; }
+    I[0] = c; w[0] = 0.75f; I[1] = c - 1; w[1] = 0.25f; return 2;
   }
-  if (c == nc - 1) { I[0] = c; w[0] = 0.5; return 1; }
-  I[0] = c; w[0] = 0.75; I[1] = c + 1; w[1] = 0.25; return 2;
+  if (c == nc - 1) { I[0] = c; w[0] = 0.5f; return 1; }
+  I[0] = c; w[0] = 0.75f; I[1] = c + 1; w[1] = 0.25f; return 2;
 }
 
 // Transpose weights: fine cells contributing to coarse I along one direction.
-__device__ __forceinline__ int r1d_terms(int I, int agg, int nc, int* F, double* w) {
-  if (agg == 1) { F[0] = I; w[0] = 1.0; return 1; }
+__device__ __forceinline__ int r1d_terms(int I, int agg, int nc, int* F, float* w) {
+  if (agg == 1) { F[0] = I; w[0] = 1.0f; return 1; }
   int n = 0;
-  if (I > 0) { F[n] = 2 * I - 1; w[n] = 0.25; ++n; }
-  F[n] = 2 * I; w[n] = I == 0 ? 0.5 : 0.75; ++n;
-  F[n] = 2 * I + 1; w[n] = I == nc - 1 ? 0.5 : 0.75; ++n;
-  if (I < nc - 1) { F[n] = 2 * I + 2; w[n] = 0.25; ++n; }
+  if (I > 0) { F[n] = 2 * I - 1; w[n] = 0.25f; ++n; }
+  F[n] = 2 * I; w[n] = I == 0 ? 0.5f : 0.75f; ++n;
+  F[n] = 2 * I + 1; w[n] = I == nc - 1 ? 0.5f : 0.75f; ++n;
+  if (I < nc - 1) { F[n] = 2 * I + 2; w[n] = 0.25f; ++n; }
   return n;
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kT) restrict_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
-                                                      const double2* __restrict__ rf, double2* __restrict__ fc) {
+// r = f - A(tau) x
+template <class R, int DIM>
+__global__ void __launch_bounds__(kT) residual_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                      const typename CT<R>::V* __restrict__ f,
+                                                      const typename CT<R>::V* __restrict__ x,
+                                                      typename CT<R>::V* __restrict__ r) {
+  using V = typename CT<R>::V;
+  TILE_PROLOGUE(L);
+  if (!in) return;
+  const V* xb = x + (int64_t)b * L.n;
+  const int64_t ex = fx(L, i, j, k), ey = fy(L, i, j, k);
+  const R tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
+  const R ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
+  R dk = tw + te + ts + tn;
+  V o = vzero<V>();
+  if (i > 0) o = vadd(o, vscale(xb[a - 1], tw));
+  if (i < L.nx - 1) o = vadd(o, vscale(xb[a + 1], te));
+  if (j > 0) o = vadd(o, vscale(xb[a - L.nx], ts));
+  if (j < L.ny - 1) o = vadd(o, vscale(xb[a + L.nx], tn));
+  if (DIM == 3) {
+    const int64_t plane = (int64_t)L.nx * L.ny;
+    const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+    dk += tb + tt;
+    if (k > 0) o = vadd(o, vscale(xb[a - plane], tb));
+    if (k < L.nz - 1) o = vadd(o, vscale(xb[a + plane], tt));
+  }
+  const double2 tau = taus[b];
+  const R m = __ldg(L.M + a);
+  const R dr = dk + (R)tau.x * m, di = (R)tau.y * m;
+  const V xa = xb[a];
+  const V ax = V{dr * xa.x - di * xa.y - o.x, dr * xa.y + di * xa.x - o.y};
+  r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
+}
+
+template <class R, int DIM>
+__global__ void __launch_bounds__(kT) restrict_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, int ax, int ay, int az,
+                                                      Batch bt, const typename CT<R>::V* __restrict__ rf,
+                                                      typename CT<R>::V* __restrict__ fc) {
+  using V = typename CT<R>::V;
   TILE_PROLOGUE(Lc);
   if (!in) return;
-  const int I = i, J = j, K = k;
   int Fx[4], Fy[4], Fz[4];
-  double wx[4], wy[4], wz[4];
-  const int nxx = r1d_terms(I, ax, Lc.nx, Fx, wx);
-  const int nyy = r1d_terms(J, ay, Lc.ny, Fy, wy);
+  float wx[4], wy[4], wz[4];
+  const int nxx = r1d_terms(i, ax, Lc.nx, Fx, wx);
+  const int nyy = r1d_terms(j, ay, Lc.ny, Fy, wy);
   int nzz = 1;
-  Fz[0] = 0; wz[0] = 1.0;
-  if (DIM == 3) nzz = r1d_terms(K, az, Lc.nz, Fz, wz);
-  const double2* rb = rf + b * Lf.n;
-  double2 s = make_double2(0.0, 0.0);
+  Fz[0] = 0; wz[0] = 1.0f;
+  if (DIM == 3) nzz = r1d_terms(k, az, Lc.nz, Fz, wz);
+  const V* rb = rf + (int64_t)b * Lf.n;
+  V s = vzero<V>();
   for (int q = 0; q < nzz; ++q)
     for (int p = 0; p < nyy; ++p) {
-      const double wzy = wz[q] * wy[p];
+      const R wzy = (R)(wz[q] * wy[p]);
       const int64_t row = ((int64_t)Fz[q] * Lf.ny + Fy[p]) * Lf.nx;
-      for (int o = 0; o < nxx; ++o) {
-        const double2 v = rb[row + Fx[o]];
-        const double w = wzy * wx[o];
-        s.x += w * v.x;
-        s.y += w * v.y;
-      }
+      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(rb[row + Fx[o]], wzy * (R)wx[o]));
     }
-  fc[b * Lc.n + a] = s;
+  fc[(int64_t)b * Lc.n + a] = s;
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kT) prolong_kernel(LevelView Lf, LevelView Lc, int ax, int ay, int az, Batch bt,
-                                                     const double2* __restrict__ ec, double2* __restrict__ xf) {
-  TILE_PROLOGUE(Lf);
-  if (!in) return;
+template <class R, class V>
+__device__ __forceinline__ V prolong_at(const LevelViewT<R>& Lc, int ax, int ay, int az, const V* __restrict__ eb,
+                                        int i, int j, int k, int dim) {
   int Ix[2], Iy[2], Iz[2];
-  double wx[2], wy[2], wz[2];
+  float wx[2], wy[2], wz[2];
   const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
   const int nyy = p1d_terms(j, ay, Lc.ny, Iy, wy);
   int nzz = 1;
-  Iz[0] = 0; wz[0] = 1.0;
-  if (DIM == 3) nzz = p1d_terms(k, az, Lc.nz, Iz, wz);
-  const double2* eb = ec + b * Lc.n;
-  double2 s = xf[b * Lf.n + a];
-  for (int q = 0; q < nzz; ++q)
-    for (int p = 0; p < nyy; ++p) {
-      const double wzy = wz[q] * wy[p];
-      const int64_t row = ((int64_t)Iz[q] * Lc.ny + Iy[p]) * Lc.nx;
-      for (int o = 0; o < nxx; ++o) {
-        const double2 v = eb[row + Ix[o]];
-        const double w = wzy * wx[o];
-        s.x += w * v.x;
-        s.y += w * v.y;
-      }
-    }
-  xf[b * Lf.n + a] = s;
-}
-
-// ---- fused red-black Gauss-Seidel sweep ------------------------------------------------
-// One full sweep (colour `first`, then the other colour) of a 32 x 8 (x, y) tile, marching
-// through z with a 4-plane shared-memory ring (halo 2 in x/y): the first colour is updated
-// on the tile + 1-cell halo (from old second-colour values), the second colour on the tile
-// (from the new first-colour values), so each cell of x and f is read from HBM once and x is
-// written once.  zero_init: the iterate is zero on entry (no loads).  ec != null: the loaded
-// iterate is x + P ec (fused coarse-grid correction, cell-centred multilinear P).
-constexpr int SW_TX = 32, SW_TY = 8, SW_HX = SW_TX + 4, SW_HY = SW_TY + 4, SW_PL = SW_HX * SW_HY;
-
-__device__ __forceinline__ double2 prolong_at(const LevelView& Lc, int ax, int ay, int az, const double2* __restrict__ eb,
-                                              int i, int j, int k, int dim) {
-  int Ix[2], Iy[2], Iz[2];
-  double wx[2], wy[2], wz[2];
-  const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
-  const int nyy = p1d_terms(j, ay, Lc.ny, Iy, wy);
-  int nzz = 1;
-  Iz[0] = 0; wz[0] = 1.0;
+  Iz[0] = 0; wz[0] = 1.0f;
   if (dim == 3) nzz = p1d_terms(k, az, Lc.nz, Iz, wz);
-  double2 s = make_double2(0.0, 0.0);
+  V s = vzero<V>();
   for (int q = 0; q < nzz; ++q)
     for (int p = 0; p < nyy; ++p) {
-      const double wzy = wz[q] * wy[p];
+      const R wzy = (R)(wz[q] * wy[p]);
       const int64_t row = ((int64_t)Iz[q] * Lc.ny + Iy[p]) * Lc.nx;
-      for (int o = 0; o < nxx; ++o) {
-        const double2 v = eb[row + Ix[o]];
-        const double w = wzy * wx[o];
-        s.x += w * v.x;
-        s.y += w * v.y;
-      }
+      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(eb[row + Ix[o]], wzy * (R)wx[o]));
     }
   return s;
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
-                                                      const double2* __restrict__ f, const double2* __restrict__ xin,
-                                                      double2* __restrict__ x, int first, int zero_init, LevelView Lc,
-                                                      int ax, int ay, int az, const double2* __restrict__ ec) {
-  // x planes (halo 2) in a 5-slot ring, f planes (halo 1) in a 3-slot ring, both filled
-  // one step ahead with cp.async so HBM latency overlaps the Gauss-Seidel updates.
+// ---- fused red-black Gauss-Seidel sweep ------------------------------------------------
+// One full sweep (colour `first`, then the other colour) of a 32 x 8 (x, y) tile, marching
+// through z: x planes (halo 2) in a 5-slot shared-memory ring and f planes (halo 1) in a
+// 3-slot ring are filled one step ahead with cp.async; the first colour is updated on the
+// tile + 1-cell halo (from old second-colour values), the second colour on the tile (from
+// the new first-colour values).  Each cell of x and f is read from HBM once and x is written
+// once.  zero_init: the iterate is zero on entry.  ec != null: the iterate is xin + P ec
+// (fused coarse-grid correction).  Out of place (x != xin): halos of neighbouring tiles read xin.
+constexpr int SW_TX = 32, SW_TY = 8, SW_HX = SW_TX + 4, SW_HY = SW_TY + 4, SW_PL = SW_HX * SW_HY;
+constexpr int SW_FX = SW_TX + 2, SW_FPL = SW_FX * (SW_TY + 2);
+
+template <class V>
+__device__ __forceinline__ void cp_async_v(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (sizeof(V) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+
+template <class R, int DIM>
+__global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                      const typename CT<R>::V* __restrict__ f,
+                                                      const typename CT<R>::V* __restrict__ xin,
+                                                      typename CT<R>::V* __restrict__ x, int first, int zero_init,
+                                                      LevelViewT<R> Lc, int ax, int ay, int az,
+                                                      const typename CT<R>::V* __restrict__ ec) {
+  using V = typename CT<R>::V;
   constexpr int NS = DIM == 3 ? 5 : 1;
-  constexpr int NF = DIM == 3 ? 3 : 1;
-  constexpr int FX = SW_TX + 2, FPL = FX * (SW_TY + 2);
-  extern __shared__ __align__(16) double2 sw_smem[];  // U[NS][SW_PL] then Fr[NF][FPL]
-  double2 (*U)[SW_PL] = reinterpret_cast<double2 (*)[SW_PL]>(sw_smem);
-  double2 (*Fr)[FPL] = reinterpret_cast<double2 (*)[FPL]>(sw_smem + NS * SW_PL);
+  extern __shared__ __align__(16) unsigned char sw_raw[];
+  V (*U)[SW_PL] = reinterpret_cast<V (*)[SW_PL]>(sw_raw);
+  V (*Fr)[SW_FPL] = reinterpret_cast<V (*)[SW_FPL]>(sw_raw + sizeof(V) * NS * SW_PL);
   LT_ITEM_BLOCK(bt.B, b, cb);
   if (bt.done[b]) return;
   const int tiles_x = (L.nx + SW_TX - 1) / SW_TX;
   const int i0 = (cb % tiles_x) * SW_TX, j0 = (cb / tiles_x) * SW_TY;
   const int tid = threadIdx.x;
-  const double2 tau = taus[b];
-  const double2* fb = f + (int64_t)b * L.n;
-  double2* xb = x + (int64_t)b * L.n;  // out of place: halos of neighbouring tiles read xin
-  const double2* xib = zero_init ? nullptr : xin + (int64_t)b * L.n;
-  const double2* eb = ec ? ec + (int64_t)b * Lc.n : nullptr;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  const V* fb = f + (int64_t)b * L.n;
+  V* xb = x + (int64_t)b * L.n;
+  const V* xib = zero_init ? nullptr : xin + (int64_t)b * L.n;
+  const V* eb = ec ? ec + (int64_t)b * Lc.n : nullptr;
   const int64_t plane = (int64_t)L.nx * L.ny;
   const int second = first ^ 1;
   auto slot = [](int k) { return DIM == 3 ? k % 5 : 0; };
   auto fslot = [](int k) { return DIM == 3 ? k % 3 : 0; };
-
-  auto cp16 = [](void* dst, const void* src, bool valid) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
-  };
   auto commit = [] { asm volatile("cp.async.commit_group;\n" ::); };
   auto wait1 = [] { asm volatile("cp.async.wait_group 1;\n" ::); };
   auto wait0 = [] { asm volatile("cp.async.wait_group 0;\n" ::); };
 
-  // issue the copies of x plane k (or zero it) and of f plane kf (halo 1)
   auto issue_x = [&](int k) {
-    double2* S = U[slot(k)];
+    V* S = U[slot(k)];
     for (int e = tid; e < SW_PL; e += kT) {
       const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
       if (zero_init) {
-        S[e] = make_double2(0.0, 0.0);
+        S[e] = vzero<V>();
       } else {
         const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
-        cp16(S + e, ok ? xib + (k * plane + (int64_t)j * L.nx + i) : xib, ok);
+        cp_async_v<V>(S + e, ok ? xib + (k * plane + (int64_t)j * L.nx + i) : xib, ok);
       }
     }
   };
   auto issue_f = [&](int k) {
-    double2* S = Fr[fslot(k)];
-    for (int e = tid; e < FPL; e += kT) {
-      const int i = i0 - 1 + e % FX, j = j0 - 1 + e / FX;
+    V* S = Fr[fslot(k)];
+    for (int e = tid; e < SW_FPL; e += kT) {
+      const int i = i0 - 1 + e % SW_FX, j = j0 - 1 + e / SW_FX;
       const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
-      cp16(S + e, ok ? fb + (k * plane + (int64_t)j * L.nx + i) : fb, ok);
+      cp_async_v<V>(S + e, ok ? fb + (k * plane + (int64_t)j * L.nx + i) : fb, ok);
     }
   };
-  // coarse-grid correction x += P e_c on a landed x plane (post-smoother)
   auto add_prolong = [&](int k) {
-    double2* S = U[slot(k)];
+    V* S = U[slot(k)];
     for (int e = tid; e < SW_PL; e += kT) {
       const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
-      if (i >= 0 && i < L.nx && j >= 0 && j < L.ny)
-        S[e] = cadd(S[e], prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
+      if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) S[e] = vadd(S[e], prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
     }
   };
-  // Gauss-Seidel update of colour `color` on plane k over the tile grown by `h` cells.
+  // Gauss-Seidel update of colour `color` on plane k over the tile grown by `h` cells
   auto update = [&](int k, int color, int h) {
     const int RX = SW_TX + 2 * h, RY = SW_TY + 2 * h;
-    double2* S = U[slot(k)];
-    const double2* Fk = Fr[fslot(k)];
+    V* S = U[slot(k)];
+    const V* Fk = Fr[fslot(k)];
     for (int e = tid; e < RX * RY; e += kT) {
       const int li = e % RX - h, lj = e / RX - h;
       const int i = i0 + li, j = j0 + lj;
@@ -302,25 +301,25 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
       const int s = (lj + 2) * SW_HX + (li + 2);
       const int64_t a = k * plane + (int64_t)j * L.nx + i;
       const int64_t ex = fx(L, i, j, k), ey = fy(L, i, j, k);
-      const double tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
-      const double ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
-      double dk = tw + te + ts + tn;
-      double2 o = Fk[(lj + 1) * FX + (li + 1)];
-      if (i > 0) o = cadd(o, cscale(S[s - 1], tw));
-      if (i < L.nx - 1) o = cadd(o, cscale(S[s + 1], te));
-      if (j > 0) o = cadd(o, cscale(S[s - SW_HX], ts));
-      if (j < L.ny - 1) o = cadd(o, cscale(S[s + SW_HX], tn));
+      const R tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
+      const R ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
+      R dk = tw + te + ts + tn;
+      V o = Fk[(lj + 1) * SW_FX + (li + 1)];
+      if (i > 0) o = vadd(o, vscale(S[s - 1], tw));
+      if (i < L.nx - 1) o = vadd(o, vscale(S[s + 1], te));
+      if (j > 0) o = vadd(o, vscale(S[s - SW_HX], ts));
+      if (j < L.ny - 1) o = vadd(o, vscale(S[s + SW_HX], tn));
       if (DIM == 3) {
-        const double tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+        const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
         dk += tb + tt;
-        if (k > 0) o = cadd(o, cscale(U[slot(k - 1)][s], tb));
-        if (k < L.nz - 1) o = cadd(o, cscale(U[slot(k + 1)][s], tt));
+        if (k > 0) o = vadd(o, vscale(U[slot(k - 1)][s], tb));
+        if (k < L.nz - 1) o = vadd(o, vscale(U[slot(k + 1)][s], tt));
       }
-      S[s] = diag_solve(dk, __ldg(L.M + a), tau, o);
+      S[s] = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
     }
   };
   auto store_plane = [&](int k) {
-    const double2* S = U[slot(k)];
+    const V* S = U[slot(k)];
     const int li = tid % SW_TX, lj = tid / SW_TX;
     const int i = i0 + li, j = j0 + lj;
     if (i < L.nx && j < L.ny) xb[k * plane + (int64_t)j * L.nx + i] = S[(lj + 2) * SW_HX + (li + 2)];
@@ -379,44 +378,59 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelView L, Batch bt, con
   wait0();
 }
 
-// e = A_c(tau_b)^{-1} f: one warp per row of the dense inverse (augmented, ld = 2n).
-__global__ void __launch_bounds__(kT) coarse_solve_kernel(int nc, Batch bt, const double2* const* __restrict__ inv,
-                                                          const double2* __restrict__ f, double2* __restrict__ e) {
+template <class R>
+size_t sweep_smem(int dim) {
+  using V = typename CT<R>::V;
+  return sizeof(V) * ((dim == 3 ? 5 : 1) * SW_PL + (dim == 3 ? 3 : 1) * SW_FPL);
+}
+
+// e = A_c(tau_b)^{-1} f: one warp per row of the dense complex inverse (row stride ld, column
+// offset off).
+template <class V>
+__global__ void __launch_bounds__(kT) coarse_solve_kernel(int nc, Batch bt, const V* const* __restrict__ inv,
+                                                          int64_t ld, int64_t off, const V* __restrict__ f,
+                                                          V* __restrict__ e) {
   const int b = blockIdx.y;
   if (bt.done[b]) return;
   const int row = blockIdx.x * (kT / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= nc) return;
-  const double2* Ar = inv[b] + (int64_t)row * 2 * nc + nc;
-  const double2* fb = f + (int64_t)b * nc;
-  double2 s = make_double2(0.0, 0.0);
-  for (int c = lane; c < nc; c += 32) s = cfma(Ar[c], fb[c], s);
+  const V* Ar = inv[b] + (int64_t)row * ld + off;
+  const V* fb = f + (int64_t)b * nc;
+  V s = vzero<V>();
+  for (int c = lane; c < nc; c += 32) {
+    const V m = Ar[c], x = fb[c];
+    s = V{s.x + m.x * x.x - m.y * x.y, s.y + m.x * x.y + m.y * x.x};
+  }
   s = warp_sum(s);
   if (lane == 0) e[(int64_t)b * nc + row] = s;
 }
 
-// ---- COCG vector kernels (fused with their reductions) ----------------------------------
+// ---- COCG vector kernels (FP64, fused with their reductions) ----------------------------
+using VM = CT<MgReal>::V;
 
-// r = v, partial ||v||^2
+// r = v, rmg = (VM) v, partial ||v||^2
 __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ v, int64_t vs,
-                                                       double2* __restrict__ r, double* __restrict__ part, int nblk) {
+                                                       double2* __restrict__ r, VM* __restrict__ rmg,
+                                                       double* __restrict__ part, int nblk) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
     const double2 x = v[b * vs + a];
     r[b * n + a] = x;
+    rmg[b * n + a] = vfrom<VM>(x);
     s = cabs2(x);
   }
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
 
-// partial sum_a x_a y_a (bilinear, no conjugation)
+// partial sum_a r_a z_a (bilinear, no conjugation), z from the V-cycle
 __global__ void __launch_bounds__(kT) bdot_kernel(int64_t n, Batch bt, const double2* __restrict__ x,
-                                                  const double2* __restrict__ y, double2* __restrict__ part, int nblk) {
+                                                  const VM* __restrict__ y, double2* __restrict__ part, int nblk) {
   ITEM_PROLOGUE(n);
   double2 s = make_double2(0.0, 0.0);
-  if (in) s = cmul(x[b * n + a], y[b * n + a]);
+  if (in) s = cmul(x[b * n + a], vto(y[b * n + a]));
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
@@ -438,11 +452,12 @@ __global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, co
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
 
-// x += alpha p (x = alpha p on the first iteration), r -= alpha q, partial ||r||^2
+// x += alpha p (x = alpha p on the first iteration), r -= alpha q, rmg = (VM) r, partial ||r||^2
 __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
                                                        const double2* __restrict__ p, const double2* __restrict__ q,
                                                        double2* __restrict__ x, int64_t xs, double2* __restrict__ r,
-                                                       int first, double* __restrict__ part, int nblk) {
+                                                       VM* __restrict__ rmg, int first, double* __restrict__ part,
+                                                       int nblk) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
@@ -452,6 +467,7 @@ __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, cons
     *xa = first ? cmul(al, pa) : cfma(al, pa, *xa);
     double2 ra = csub(r[b * n + a], cmul(al, q[b * n + a]));
     r[b * n + a] = ra;
+    rmg[b * n + a] = vfrom<VM>(ra);
     s = cabs2(ra);
   }
   s = block_sum(s);
@@ -460,10 +476,10 @@ __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, cons
 
 // p = z + beta p (p = z when first)
 __global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const double2* __restrict__ beta,
-                                                     const double2* __restrict__ z, double2* __restrict__ p, int first) {
+                                                     const VM* __restrict__ z, double2* __restrict__ p, int first) {
   ITEM_PROLOGUE(n);
   if (!in) return;
-  const double2 za = z[b * n + a];
+  const double2 za = vto(z[b * n + a]);
   p[b * n + a] = first ? za : cfma(beta[b], p[b * n + a], za);
 }
 
@@ -511,69 +527,72 @@ __global__ void __launch_bounds__(kT) scalar_kernel(int op, Batch bt, const void
   }
 }
 
-}  // namespace
-
-void finalize_sums(lt_ctx, const double*, int, int, double*, int) {}
-
-namespace {
-
-struct VcycleWork {
-  std::vector<DeviceBuffer> x, f, r;  // per level: Bc x n_l (level 0: x = z, f = COCG r)
-};
+// ---- V-cycle driver --------------------------------------------------------------------
+template <class R>
+LevelViewT<R> mg_view(lt_pencil p, int l);
+template <>
+LevelViewT<double> mg_view<double>(lt_pencil p, int l) { return p->view(l); }
+template <>
+LevelViewT<float> mg_view<float>(lt_pencil p, int l) { return p->view32(l); }
 
 // Returns the buffer holding the level-l V-cycle output (Bc x n_l).
-template <int DIM>
-const double2* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus, const double2* const* inv,
-                      std::vector<double2*>& X, std::vector<const double2*>& F, std::vector<double2*>& R) {
+template <class R, int DIM>
+const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus,
+                                const typename CT<R>::V* const* inv, int64_t inv_ld, int64_t inv_off,
+                                std::vector<typename CT<R>::V*>& X, std::vector<typename CT<R>::V*>& F,
+                                std::vector<typename CT<R>::V*>& Rr) {
+  using V = typename CT<R>::V;
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int last = (int)p->levels.size() - 1;
-  LevelView L = p->view(l);
-  const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
+  LevelViewT<R> L = mg_view<R>(p, l);
+  const double vb = sizeof(V), rb = sizeof(R);
   const double cell_bytes = (double)L.n * Bc;
-  const double coef = (double)L.n * 8.0 * (DIM + 1);
+  const double coef = (double)L.n * rb * (DIM + 1);
   if (l == last) {
     dim3 g(blocks_for(L.n, kT / 32), Bc);
-    launch(ctx, "mg_coarse_solve", cell_bytes * 32.0, [&] {
-      coarse_solve_kernel<<<g, kT, 0, st>>>((int)L.n, bt, inv, F[l], X[l]);
+    launch(ctx, "mg_coarse_solve", cell_bytes * 2 * vb, [&] {
+      coarse_solve_kernel<V><<<g, kT, 0, st>>>((int)L.n, bt, inv, inv_ld, inv_off, F[l], X[l]);
     });
     return X[l];
   }
-  LevelView Lc = p->view(l + 1);
+  LevelViewT<R> Lc = mg_view<R>(p, l + 1);
   const Level& lev = *p->levels[l];
+  const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
   const unsigned sgrid = (unsigned)(((L.nx + SW_TX - 1) / SW_TX) * ((L.ny + SW_TY - 1) / SW_TY)) * (unsigned)Bc;
-  const size_t ssmem = sizeof(double2) * ((DIM == 3 ? 5 : 1) * SW_PL + (DIM == 3 ? 3 : 1) * (SW_TX + 2) * (SW_TY + 2));
+  const size_t ssmem = sweep_smem<R>(DIM);
   static bool attr_set = false;
   if (!attr_set) {
-    LT_CUDA(cudaFuncSetAttribute(rb_sweep_kernel<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+    LT_CUDA(cudaFuncSetAttribute(rb_sweep_kernel<R, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
     attr_set = true;
   }
-  // pre-smoothing: one red-black sweep (red first) from a zero iterate; algorithmic bytes
-  // per cell-item: f read + x written (coefficients once per item batch)
-  launch(ctx, "mg_smooth", cell_bytes * 32.0 + coef, [&] {
-    rb_sweep_kernel<DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
+  // pre-smoothing: one red-black sweep (red first) from a zero iterate
+  // (algorithmic bytes per cell-item: f read + x written; faces once per launch)
+  launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
+    rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
   });
-  launch(ctx, "mg_residual", cell_bytes * 48.0 + coef, [&] {
-    residual_kernel<DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], R[l]);
+  launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
+    residual_kernel<R, DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
   });
   const unsigned gridc = (unsigned)Lc.ntiles * (unsigned)Bc;
-  launch(ctx, "mg_restrict", cell_bytes * 16.0 + (double)Lc.n * Bc * 16.0, [&] {
-    restrict_kernel<DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, R[l],
-                                                const_cast<double2*>(F[l + 1]));
+  launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
+    restrict_kernel<R, DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, Rr[l], F[l + 1]);
   });
-  const double2* ec = vcycle<DIM>(p, l + 1, Bc, bt, taus, inv, X, F, R);
+  const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr);
   // post-smoothing: coarse correction x + P e_c fused into one black-first sweep (the
-  // transpose of the pre-smoother), written out of place into R[l]
-  launch(ctx, "mg_smooth", cell_bytes * 48.0 + (double)Lc.n * Bc * 16.0 + coef, [&] {
-    rb_sweep_kernel<DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], X[l], R[l], 1, 0, Lc, lev.agg[0], lev.agg[1],
-                                               lev.agg[2], ec);
+  // transpose of the pre-smoother), written out of place into Rr[l]
+  launch(ctx, "mg_smooth", cell_bytes * 3 * vb + (double)Lc.n * Bc * vb + coef, [&] {
+    rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], X[l], Rr[l], 1, 0, Lc, lev.agg[0],
+                                                      lev.agg[1], lev.agg[2], ec);
   });
-  return R[l];
+  return Rr[l];
 }
 
 template <int DIM>
 void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v, int64_t vs, double2* u,
                  int64_t us) {
+  using R = MgReal;
+  using V = VM;
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int nl = (int)p->levels.size();
@@ -582,8 +601,14 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   LevelView L0 = p->view(0);
 
   // coarse factors for each distinct tau (cached on the pencil)
-  std::vector<const double2*> inv_host(Bc);
-  for (int b = 0; b < Bc; ++b) inv_host[b] = p->factor(taus_host[b]).inverse.as<double2>();
+  std::vector<const V*> inv_host(Bc);
+  const int64_t nc = p->levels.back()->n;
+  const bool fp64 = sizeof(R) == 8;
+  for (int b = 0; b < Bc; ++b) {
+    const CoarseFactor& fc = p->factor(taus_host[b]);
+    inv_host[b] = fp64 ? reinterpret_cast<const V*>(fc.inverse.get()) : reinterpret_cast<const V*>(fc.inverse32.get());
+  }
+  const int64_t inv_ld = fp64 ? 2 * nc : nc, inv_off = fp64 ? nc : 0;
 
   // small per-item state: taus, inverse pointers, done flags, scalars
   const size_t small_bytes = sizeof(double2) * Bc * 4 + sizeof(double) * Bc * 2 + sizeof(void*) * Bc +
@@ -596,7 +621,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   double2* d_beta = d_alpha + Bc;
   double* d_bb = reinterpret_cast<double*>(d_beta + Bc);
   double* d_rr = d_bb + Bc;
-  const double2** d_inv = reinterpret_cast<const double2**>(d_rr + Bc);
+  const V** d_inv = reinterpret_cast<const V**>(d_rr + Bc);
   int* d_done = reinterpret_cast<int*>(d_inv + Bc);
   LT_CUDA(cudaMemcpyAsync(d_taus, taus_host, sizeof(double2) * Bc, cudaMemcpyHostToDevice, st));
   LT_CUDA(cudaMemcpyAsync(d_inv, inv_host.data(), sizeof(void*) * Bc, cudaMemcpyHostToDevice, st));
@@ -604,32 +629,30 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   Scalars sc{d_bb, d_rr, d_rho, d_alpha, d_beta};
   Batch bt{Bc, d_done};
 
-  // workspace
+  // workspace: FP64 Krylov vectors r, p, q; multigrid vectors (precision R) per level
   DeviceBuffer partials(sizeof(double2) * (size_t)Bc * std::max<int64_t>(nblk, L0.ntiles), st);
-  DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 5, st);
+  DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 3, st);
   double2* r = vec.as<double2>();
-  double2* zbuf = r + Bc * n;
-  double2* pp = zbuf + Bc * n;
+  double2* pp = r + Bc * n;
   double2* q = pp + Bc * n;
-  double2* res0 = q + Bc * n;
   std::vector<DeviceBuffer> lvl(nl);
-  std::vector<double2*> X(nl), R(nl);
-  std::vector<const double2*> F(nl);
-  X[0] = zbuf;
-  F[0] = r;
-  R[0] = res0;
-  for (int l = 1; l < nl; ++l) {
+  std::vector<V*> X(nl), F(nl), Rr(nl);
+  for (int l = 0; l < nl; ++l) {
     const int64_t nlv = p->levels[l]->n;
-    lvl[l].allocate(sizeof(double2) * (size_t)Bc * nlv * 3, st);
-    X[l] = lvl[l].as<double2>();
+    lvl[l].allocate(sizeof(V) * (size_t)Bc * nlv * 3, st);
+    X[l] = lvl[l].as<V>();
     F[l] = X[l] + Bc * nlv;
-    R[l] = X[l] + 2 * Bc * nlv;
+    Rr[l] = X[l] + 2 * Bc * nlv;
   }
+  V* rmg = F[0];  // the multigrid copy of the COCG residual
   const unsigned grid = (unsigned)nblk * (unsigned)Bc;
   const double nb = (double)n * Bc;
   const double coef = (double)n * 8.0 * (DIM + 1);
+  const double vb = sizeof(V);
 
-  launch(ctx, "cocg_vec", nb * 32.0, [&] { copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, (double*)partials.get(), nblk); });
+  launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] {
+    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, (double*)partials.get(), nblk);
+  });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), nblk, sc); });
   std::vector<double> bb(Bc), rr(Bc), best(Bc);
   LT_CUDA(cudaMemcpyAsync(bb.data(), d_bb, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
@@ -653,10 +676,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   const double tol2 = p->inner_tol * p->inner_tol;
   for (int b = 0; b < Bc; ++b) best[b] = bb[b];
   // z = B r ; rho = r^T z ; p = z
-  const double2* z = vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
-  launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
+  const V* z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
+  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+    bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
+  });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RHO, bt, partials.get(), nblk, sc); });
-  launch(ctx, "cocg_vec", nb * 32.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
+  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
   for (int it = 0; it < p->inner_maxit; ++it) {
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
       apply_dot_kernel<DIM><<<(unsigned)L0.ntiles * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
@@ -665,8 +690,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     launch(ctx, "cocg_scalar", 0.0, [&] {
       scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), L0.ntiles, sc);
     });
-    launch(ctx, "cocg_vec", nb * (it == 0 ? 64.0 : 80.0), [&] {
-      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, it == 0, (double*)partials.get(), nblk);
+    launch(ctx, "cocg_vec", nb * ((it == 0 ? 64.0 : 80.0) + vb), [&] {
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, rmg, it == 0, (double*)partials.get(),
+                                            nblk);
     });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
     LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
@@ -685,10 +711,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       if (active == 0) break;
       LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
     }
-    z = vcycle<DIM>(p, 0, Bc, bt, d_taus, d_inv, X, F, R);
-    launch(ctx, "cocg_vec", nb * 32.0, [&] { bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk); });
+    z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
+    launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+      bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
+    });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BETA, bt, partials.get(), nblk, sc); });
-    launch(ctx, "cocg_vec", nb * 48.0, [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
+    launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
   }
   LT_CUDA(cudaStreamSynchronize(st));
 }
@@ -696,11 +724,11 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
 }  // namespace
 
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us) {
-  // Chunk so that the multigrid workspace stays bounded (~12 vectors per item).
+  // Chunk so that the Krylov + multigrid workspace stays bounded.
   const int64_t n = p->n;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const double per_item = (double)n * sizeof(double2) * 8.0;
+  const double per_item = (double)n * (sizeof(double2) * 3.0 + sizeof(VM) * 3.0 * 1.2);
   int chunk = (int)std::max(1.0, std::min(64.0, 0.5 * (double)free_b / per_item));
   for (int b0 = 0; b0 < B; b0 += chunk) {
     const int bc = std::min(chunk, B - b0);

@@ -115,24 +115,35 @@ struct Level {
   double* Tz = nullptr;
   double* M = nullptr;
   DeviceBuffer storage;
+  // FP32 copy of the same arrays (same layout) for the mixed-precision V-cycle
+  float* Tx32 = nullptr;
+  float* Ty32 = nullptr;
+  float* Tz32 = nullptr;
+  float* M32 = nullptr;
+  DeviceBuffer storage32;
   int agg[3] = {1, 1, 1};  // aggregation to the next coarser level
 };
 
-// Device view of a level passed by value to kernels.
-struct LevelView {
+// Device view of a level passed by value to kernels (R = double: the operator; R = float:
+// the preconditioner copy).
+template <class R>
+struct LevelViewT {
   int nx, ny, nz, dim;
   int64_t n;
-  const double* Tx;
-  const double* Ty;
-  const double* Tz;
-  const double* M;
+  const R* Tx;
+  const R* Ty;
+  const R* Tz;
+  const R* M;
   // 256-thread (x, y) tiles: tw x th cells, tw a power of two (tws = log2 tw)
   int tw, tws, th, tiles_x, tiles_y, ntiles;
 };
+using LevelView = LevelViewT<double>;
+using LevelView32 = LevelViewT<float>;
 
 struct CoarseFactor {
   double2 tau;
-  DeviceBuffer inverse;  // n_c x n_c complex, row-major
+  DeviceBuffer inverse;    // [A | A^{-1}] n_c x 2n_c complex128, row-major (Gauss-Jordan work)
+  DeviceBuffer inverse32;  // A^{-1} n_c x n_c complex64, row-major (V-cycle coarsest solve)
 };
 
 // Per-solve FGMRES basis kept for keep_basis queries.
@@ -159,6 +170,7 @@ struct lt_pencil_s {
   lt::KeptBasis kept;
 
   lt::LevelView view(int l) const;
+  lt::LevelView32 view32(int l) const;
   const lt::CoarseFactor& factor(double2 tau);  // prepares on miss
 };
 
@@ -173,10 +185,6 @@ void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, doub
 // inner.cu: u_b = (K + tau_b M)^{-1} v_b, b < B, strided vectors; taus on host.
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs,
                  double2* u, int64_t us);
-
-// Batched deterministic reductions: out[b] = sum over blocks of partials[b * nblk + k].
-void finalize_sums(lt_ctx ctx, const double* partials, int nblk, int B, double* out,
-                   int stride_out);
 
 // fgmres.cu
 struct OuterProblem {

@@ -252,6 +252,27 @@ LevelView lt_pencil_view(const lt_pencil_s* p, int l) {
                    tw, tws, th, tiles_x, tiles_y, tiles_x * tiles_y * L.nz};
 }
 
+LevelView32 lt_pencil_view32(const lt_pencil_s* p, int l) {
+  const LevelView v = lt_pencil_view(p, l);
+  const Level& L = *p->levels[l];
+  return LevelView32{v.nx, v.ny, v.nz, v.dim, v.n, L.Tx32, L.Ty32, L.Tz32, L.M32,
+                     v.tw, v.tws, v.th, v.tiles_x, v.tiles_y, v.ntiles};
+}
+
+namespace {
+__global__ void d2f_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t n) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a < n) out[a] = (float)in[a];
+}
+__global__ void inverse_to_c64(const double2* __restrict__ aug, float2* __restrict__ out, int64_t n) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n * n) return;
+  const int64_t r = t / n, c = t % n;
+  const double2 v = aug[r * 2 * n + n + c];
+  out[t] = make_float2((float)v.x, (float)v.y);
+}
+}  // namespace
+
 static void alloc_level(Level& L, int dim, cudaStream_t s) {
   L.n = (int64_t)L.nx * L.ny * L.nz;
   int64_t nfx = (int64_t)(L.nx + 1) * L.ny * L.nz;
@@ -344,12 +365,26 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
     });
     p->levels.push_back(std::move(C));
   }
+  // FP32 copies of every level for the mixed-precision V-cycle (same layout)
+  for (auto& lv : p->levels) {
+    Level& Lv = *lv;
+    const int64_t cnt = (int64_t)(Lv.storage.bytes() / sizeof(double));
+    Lv.storage32.allocate(sizeof(float) * cnt, st);
+    float* base = Lv.storage32.as<float>();
+    const double* src = Lv.storage.as<double>();
+    Lv.Tx32 = base + (Lv.Tx - src);
+    Lv.Ty32 = base + (Lv.Ty - src);
+    Lv.Tz32 = Lv.Tz ? base + (Lv.Tz - src) : nullptr;
+    Lv.M32 = base + (Lv.M - src);
+    launch(ctx, "assemble", 12.0 * cnt, [&] { d2f_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(src, base, cnt); });
+  }
   LT_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace lt
 
 lt::LevelView lt_pencil_s::view(int l) const { return lt::lt_pencil_view(this, l); }
+lt::LevelView32 lt_pencil_s::view32(int l) const { return lt::lt_pencil_view32(this, l); }
 
 const lt::CoarseFactor& lt_pencil_s::factor(double2 tau) {
   for (auto& f : factors)
@@ -377,6 +412,11 @@ const lt::CoarseFactor& lt_pencil_s::factor(double2 tau) {
   LT_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   LT_CUDA(cudaStreamSynchronize(st));
   if (h_status != 0) throw Error(LT_ERR_PRECONDITIONER, "shift-and-invert factorization failed (singular coarse operator)");
+  f->inverse32.allocate(sizeof(float2) * nc * nc, st);
+  launch(ctx, "coarse_factor", 0.0, [&] {
+    inverse_to_c64<<<blocks_for(nc * nc, kThreads), kThreads, 0, st>>>(aug, f->inverse32.as<float2>(), nc);
+  });
+  LT_CUDA(cudaStreamSynchronize(st));
   factors.push_back(std::move(f));
   return *factors.back();
 }

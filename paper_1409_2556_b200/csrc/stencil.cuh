@@ -6,16 +6,19 @@
 
 namespace lt {
 
-__device__ __forceinline__ int64_t fx(const LevelView& L, int i, int j, int k) {
+template <class VW>
+__device__ __forceinline__ int64_t fx(const VW& L, int i, int j, int k) {
   return ((int64_t)k * L.ny + j) * (L.nx + 1) + i;
 }
-__device__ __forceinline__ int64_t fy(const LevelView& L, int i, int j, int k) {
+template <class VW>
+__device__ __forceinline__ int64_t fy(const VW& L, int i, int j, int k) {
   return ((int64_t)k * (L.ny + 1) + j) * L.nx + i;
 }
 
 // Cell of thread threadIdx.x in tile `cb` of a level (256-thread x-y tiles, one plane);
 // false for threads past the grid edge.
-__device__ __forceinline__ bool tile_cell(const LevelView& L, int cb, int& i, int& j, int& k, int64_t& a) {
+template <class VW>
+__device__ __forceinline__ bool tile_cell(const VW& L, int cb, int& i, int& j, int& k, int64_t& a) {
   const int bx = cb % L.tiles_x;
   const int t = cb / L.tiles_x;
   const int by = t % L.tiles_y;
@@ -46,7 +49,8 @@ __device__ __forceinline__ void decode(const LevelView& L, int64_t a, int& i, in
   }
 }
 
-__device__ __forceinline__ double diag_k(const LevelView& L, int i, int j, int k) {
+template <class VW>
+__device__ __forceinline__ double diag_k(const VW& L, int i, int j, int k) {
   double d = L.Tx[fx(L, i, j, k)] + L.Tx[fx(L, i + 1, j, k)] + L.Ty[fy(L, i, j, k)] + L.Ty[fy(L, i, j + 1, k)];
   if (L.dim == 3) {
     int64_t a = ((int64_t)k * L.ny + j) * L.nx + i;
