@@ -1,0 +1,473 @@
+// laptomo/laptomo.hpp — C++ mirror of the reference's public solver API
+// (/root/reference/proj/include/laptomo/{talbot,shifted_solver,forward,jacobian,errors}.hpp)
+// over the C ABI of include/laptomo_gpu.h.  Header-only; link liblaptomo_gpu.so.
+//
+// Same names, argument meaning and exceptions as the reference:
+//   std::invalid_argument, laptomo::FactorizationError, laptomo::ConvergenceError
+//   (unconverged_shifts).  Vectors are std::vector<double> / std::vector<Complex>;
+//   matrices are column-major (n rows), like the Eigen objects they replace.  With Eigen
+//   available, the Eigen overloads at the end accept/return Eigen types.
+//
+// Difference at the boundary: a pencil is built from a structured cell-centred grid and
+// per-cell log fields (assembled on the device) instead of assembled sparse (K, M).
+#pragma once
+
+#include <complex>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "laptomo_gpu.h"
+
+namespace laptomo {
+
+using Complex = std::complex<double>;
+
+// ---- errors (errors.hpp:14-31) ------------------------------------------------------------
+class FactorizationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+class ConvergenceError : public std::runtime_error {
+ public:
+  ConvergenceError(const std::string& what, std::vector<int> unconverged)
+      : std::runtime_error(what), unconverged_shifts(std::move(unconverged)) {}
+  std::vector<int> unconverged_shifts;
+};
+
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(lt_status s) {
+  if (s == LT_OK) return;
+  const std::string msg = lt_last_error();
+  switch (s) {
+    case LT_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case LT_ERR_PRECONDITIONER: throw FactorizationError(msg);
+    case LT_ERR_NOT_CONVERGED: {
+      std::vector<int> idx(4096);
+      const int n = lt_last_unconverged(idx.data(), (int)idx.size());
+      idx.resize(n < 4096 ? n : 4096);
+      throw ConvergenceError(msg, idx);
+    }
+    default: throw DeviceError(msg);
+  }
+}
+inline const lt_complex* c(const Complex* p) { return reinterpret_cast<const lt_complex*>(p); }
+inline lt_complex* c(Complex* p) { return reinterpret_cast<lt_complex*>(p); }
+inline lt_complex c(Complex z) { return lt_complex{z.real(), z.imag()}; }
+}  // namespace detail
+
+// ---- context --------------------------------------------------------------------------
+class Context {
+ public:
+  explicit Context(int device = 0) { detail::check(lt_ctx_create(device, &h_)); }
+  ~Context() { if (h_) lt_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  lt_ctx handle() const { return h_; }
+
+ private:
+  lt_ctx h_ = nullptr;
+};
+
+// ---- talbot (talbot.hpp:23-63) --------------------------------------------------------
+struct TalbotParams {
+  double sigma0 = -0.6122;
+  double mu0 = 0.5017;
+  double nu = 0.2645 / 0.5017;
+  double alpha = 0.6407;
+  lt_talbot_params c() const { return lt_talbot_params{sigma0, mu0, nu, alpha}; }
+};
+
+struct TalbotContour {
+  int n_quad = 0;
+  double time = 0.0;
+  double sigma = 0.0, mu = 0.0, nu = 0.0, alpha = 0.0;
+  std::vector<double> thetas;
+  std::vector<Complex> nodes, dnodes, weights;
+  int n_half() const { return static_cast<int>(nodes.size()); }
+};
+
+inline TalbotContour build_contour(int n_quad, double time, const TalbotParams& params = {}) {
+  TalbotContour out;
+  const int nh = n_quad > 0 ? n_quad / 2 : 0;
+  out.thetas.resize(nh);
+  out.nodes.resize(nh);
+  out.dnodes.resize(nh);
+  out.weights.resize(nh);
+  const lt_talbot_params p = params.c();
+  detail::check(lt_talbot_build(n_quad, time, &p, out.thetas.data(), detail::c(out.nodes.data()),
+                                detail::c(out.dnodes.data()), detail::c(out.weights.data())));
+  out.n_quad = n_quad;
+  out.time = time;
+  out.sigma = params.sigma0 * n_quad / time;
+  out.mu = params.mu0 * n_quad / time;
+  out.nu = params.nu;
+  out.alpha = params.alpha;
+  return out;
+}
+
+inline double inverse_laplace_sum(const TalbotContour& contour, const std::vector<Complex>& values) {
+  if ((int)values.size() != contour.n_half())
+    throw std::invalid_argument("inverse_laplace_sum: one value per retained node required");
+  Complex s = 0.0;
+  for (int k = 0; k < contour.n_half(); ++k) s += contour.weights[k] * values[k];
+  return 2.0 * s.real();
+}
+
+inline Complex qhat_step(double q0, Complex z) {
+  lt_complex out;
+  detail::check(lt_qhat_step(q0, detail::c(z), &out));
+  return {out.re, out.im};
+}
+
+// ---- shifted solver (shifted_solver.hpp:21-132) ---------------------------------------
+enum class KrylovVariant { Fom, Gmres };
+
+struct PreconditionerSchedule {
+  std::vector<Complex> taus;
+  std::vector<int> pattern;
+  Complex tau_at(int iteration) const { return taus[pattern[iteration % pattern.size()]]; }
+};
+
+inline PreconditionerSchedule single_tau_schedule(Complex tau) { return {{tau}, {0}}; }
+
+inline PreconditionerSchedule select_preconditioner_shifts(const std::vector<Complex>& shifts) {
+  lt_complex taus[2];
+  int nt = 0, pat[5], pl = 0;
+  detail::check(lt_select_preconditioner_shifts(detail::c(shifts.data()), (int)shifts.size(), taus, &nt, pat, &pl));
+  PreconditionerSchedule s;
+  for (int i = 0; i < nt; ++i) s.taus.emplace_back(taus[i].re, taus[i].im);
+  s.pattern.assign(pat, pat + pl);
+  return s;
+}
+
+struct ShiftedSolveOptions {
+  KrylovVariant variant = KrylovVariant::Gmres;
+  double tol = 1e-10;
+  int maxit = 0;
+  bool keep_basis = false;
+  bool record_history = true;
+};
+
+struct ShiftStatus {
+  bool converged = false;
+  int iteration = 0;
+  double estimate = 0.0;
+  double true_residual = 0.0;
+  std::vector<double> history;
+};
+
+struct ShiftedSolveResult {
+  std::vector<Complex> solutions;  // n x n_shifts, column-major
+  int iterations = 0;
+  bool all_converged = false;
+  std::vector<ShiftStatus> shifts;
+  std::vector<int> unconverged() const {
+    std::vector<int> out;
+    for (int k = 0; k < (int)shifts.size(); ++k)
+      if (!shifts[k].converged) out.push_back(k);
+    return out;
+  }
+};
+
+/// Cell-centred grid (x fastest): dims 2 or 3.
+struct Grid {
+  int dim = 2;
+  int shape[3] = {1, 1, 1};
+  double h = 1.0;
+  lt_grid c() const { return lt_grid{LT_GRID_FD_CELL, dim, {shape[0], shape[1], shape[2]}, h}; }
+};
+
+class ShiftedPencil;
+
+/// SparseComplexFactorization view of a prepared tau (factorization.hpp:19-27).
+class Factorization {
+ public:
+  Factorization(const ShiftedPencil* p, Complex tau) : p_(p), tau_(tau) {}
+  long rows() const;
+  std::vector<Complex> solve(const std::vector<Complex>& rhs) const;
+  std::vector<Complex> solve_adjoint(const std::vector<Complex>& rhs) const;
+
+ private:
+  const ShiftedPencil* p_;
+  Complex tau_;
+};
+
+class ShiftedPencil {
+ public:
+  ShiftedPencil(const Context& ctx, const Grid& grid, const std::vector<double>& log_kappa,
+                const std::vector<double>& log_storativity) {
+    const lt_grid g = grid.c();
+    detail::check(lt_pencil_create_grid(ctx.handle(), &g, log_kappa.data(), log_storativity.data(), LT_MEM_HOST, &h_));
+  }
+  ~ShiftedPencil() { if (h_) lt_pencil_destroy(h_); }
+  ShiftedPencil(const ShiftedPencil&) = delete;
+  ShiftedPencil& operator=(const ShiftedPencil&) = delete;
+
+  long rows() const { return (long)lt_pencil_rows(h_); }
+  std::vector<Complex> apply(Complex z, const std::vector<Complex>& x) const {
+    std::vector<Complex> y(x.size());
+    detail::check(lt_pencil_apply(h_, detail::c(z), detail::c(x.data()), detail::c(y.data()), 1, LT_MEM_HOST));
+    return y;
+  }
+  std::vector<Complex> apply_adjoint(Complex z, const std::vector<Complex>& x) const {
+    std::vector<Complex> y(x.size());
+    detail::check(lt_pencil_apply_adjoint(h_, detail::c(z), detail::c(x.data()), detail::c(y.data()), 1, LT_MEM_HOST));
+    return y;
+  }
+  std::vector<Complex> apply_mass(const std::vector<Complex>& x) const {
+    std::vector<Complex> y(x.size());
+    detail::check(lt_pencil_apply_mass(h_, detail::c(x.data()), detail::c(y.data()), 1, LT_MEM_HOST));
+    return y;
+  }
+  Factorization factorization(Complex tau) const {
+    const lt_complex t = detail::c(tau);
+    detail::check(lt_pencil_prepare(h_, &t, 1));
+    return Factorization(this, tau);
+  }
+  int factorization_count() const { return lt_pencil_factorization_count(h_); }
+  lt_pencil handle() const { return h_; }
+
+ private:
+  lt_pencil h_ = nullptr;
+};
+
+inline long Factorization::rows() const { return p_->rows(); }
+inline std::vector<Complex> Factorization::solve(const std::vector<Complex>& rhs) const {
+  std::vector<Complex> u(rhs.size());
+  detail::check(lt_pencil_solve(p_->handle(), detail::c(tau_), detail::c(rhs.data()), detail::c(u.data()), 1, LT_MEM_HOST));
+  return u;
+}
+inline std::vector<Complex> Factorization::solve_adjoint(const std::vector<Complex>& rhs) const {
+  std::vector<Complex> u(rhs.size());
+  detail::check(lt_pencil_solve_adjoint(p_->handle(), detail::c(tau_), detail::c(rhs.data()), detail::c(u.data()), 1,
+                                        LT_MEM_HOST));
+  return u;
+}
+
+inline ShiftedSolveResult solve_shifted_flexible(const ShiftedPencil& pencil, const std::vector<Complex>& b,
+                                                 const std::vector<Complex>& shifts,
+                                                 const PreconditionerSchedule& schedule,
+                                                 const ShiftedSolveOptions& options = {}) {
+  if (schedule.taus.empty() || schedule.pattern.empty())
+    throw std::invalid_argument("solve_shifted_flexible: empty preconditioner schedule");
+  const long n = pencil.rows();
+  const int ns = (int)shifts.size();
+  lt_solve_options o{options.variant == KrylovVariant::Fom ? LT_VARIANT_FOM : LT_VARIANT_GMRES, options.tol,
+                     options.maxit, 0, options.record_history ? 1 : 0};
+  ShiftedSolveResult r;
+  r.solutions.assign((size_t)n * ns, Complex(0.0));
+  std::vector<lt_shift_status> st(ns > 0 ? ns : 1);
+  int iters = 0;
+  const int maxit = options.maxit > 0 ? options.maxit : 10 * ns;
+  std::vector<double> hist((size_t)(ns > 0 ? ns : 1) * (maxit > 0 ? maxit : 1));
+  detail::check(lt_solve_shifted(pencil.handle(), detail::c(b.data()), 1, detail::c(shifts.data()), ns,
+                                 detail::c(schedule.taus.data()), (int)schedule.taus.size(), schedule.pattern.data(),
+                                 (int)schedule.pattern.size(), &o, LT_MEM_HOST, detail::c(r.solutions.data()), st.data(),
+                                 &iters, options.record_history ? hist.data() : nullptr));
+  r.iterations = iters;
+  r.all_converged = true;
+  for (int k = 0; k < ns; ++k) {
+    ShiftStatus s{st[k].converged != 0, st[k].iteration, st[k].estimate, st[k].true_residual, {}};
+    if (options.record_history)
+      for (int j = 0; j < iters && j < maxit; ++j) {
+        const double v = hist[(size_t)k * maxit + j];
+        if (v == v) s.history.push_back(v);
+      }
+    r.all_converged = r.all_converged && s.converged;
+    r.shifts.push_back(std::move(s));
+  }
+  return r;
+}
+
+inline ShiftedSolveResult solve_shifted_single(const ShiftedPencil& pencil, const std::vector<Complex>& b,
+                                               const std::vector<Complex>& shifts, Complex tau,
+                                               const ShiftedSolveOptions& options = {}) {
+  return solve_shifted_flexible(pencil, b, shifts, single_tau_schedule(tau), options);
+}
+
+inline std::vector<Complex> solve_shifted_direct(const ShiftedPencil& pencil, const std::vector<Complex>& b,
+                                                 const std::vector<Complex>& shifts) {
+  std::vector<Complex> x((size_t)pencil.rows() * shifts.size());
+  detail::check(lt_solve_shifted_direct(pencil.handle(), detail::c(b.data()), 1, detail::c(shifts.data()),
+                                        (int)shifts.size(), LT_MEM_HOST, detail::c(x.data())));
+  return x;
+}
+
+// ---- forward (forward.hpp:16-61) ------------------------------------------------------
+enum class SolverKind { Single, Flexible, Direct };
+
+struct SolverConfig {
+  SolverKind kind = SolverKind::Flexible;
+  KrylovVariant variant = KrylovVariant::Gmres;
+  double tol = 1e-10;
+  int maxit = 0;
+  lt_solver_config c() const {
+    return lt_solver_config{kind == SolverKind::Single ? LT_SOLVER_SINGLE
+                                                       : (kind == SolverKind::Direct ? LT_SOLVER_DIRECT : LT_SOLVER_FLEXIBLE),
+                            variant == KrylovVariant::Fom ? LT_VARIANT_FOM : LT_VARIANT_GMRES, tol, maxit};
+  }
+};
+
+struct ForwardProblem {
+  std::vector<double> source;        // free-dof interpolation weights of the source
+  double rate = 0.0;
+  std::vector<double> initial_head;  // empty: zero
+  std::vector<double> times;
+  int n_quad = 40;
+  TalbotParams contour;
+};
+
+struct TimeDiagnostics {
+  int iterations = 0;
+  bool all_converged = true;
+  std::vector<double> shift_residuals;
+};
+
+struct HeadSolution {
+  std::vector<double> heads;  // n x n_times, column-major
+  std::vector<TimeDiagnostics> diagnostics;
+};
+
+namespace detail {
+inline HeadSolution forward(const ShiftedPencil& pencil, const ForwardProblem& pb, const SolverConfig& s, int pooled) {
+  const long n = pencil.rows();
+  const int nt = (int)pb.times.size();
+  HeadSolution out;
+  out.heads.assign((size_t)n * nt, 0.0);
+  std::vector<lt_time_diag> diag(nt > 0 ? nt : 1);
+  std::vector<double> res((size_t)(nt > 0 ? nt : 1) * (pb.n_quad > 1 ? pb.n_quad / 2 : 1));
+  const lt_talbot_params tp = pb.contour.c();
+  const lt_solver_config sc = s.c();
+  const double rate = pb.rate;
+  detail::check(lt_forward(pencil.handle(), pb.source.data(), &rate, 1,
+                           pb.initial_head.empty() ? nullptr : pb.initial_head.data(), pb.times.data(), nt, pb.n_quad, &tp,
+                           &sc, pooled, LT_MEM_HOST, out.heads.data(), nullptr, 0, nullptr, diag.data(), res.data()));
+  for (int t = 0; t < nt; ++t) {
+    TimeDiagnostics d{diag[t].iterations, diag[t].all_converged != 0, {}};
+    d.shift_residuals.assign(res.begin() + (size_t)t * (pb.n_quad / 2), res.begin() + (size_t)(t + 1) * (pb.n_quad / 2));
+    out.diagnostics.push_back(std::move(d));
+  }
+  return out;
+}
+}  // namespace detail
+
+inline HeadSolution solve_forward(const ShiftedPencil& pencil, const ForwardProblem& problem,
+                                  const SolverConfig& solver = {}) {
+  return detail::forward(pencil, problem, solver, 0);
+}
+
+inline HeadSolution solve_forward_batch(const ShiftedPencil& pencil, const ForwardProblem& problem,
+                                        const SolverConfig& solver = {}) {
+  return detail::forward(pencil, problem, solver, 1);
+}
+
+// ---- Jacobian (jacobian.hpp:22-101) ---------------------------------------------------
+struct ThtExperiment {
+  Grid grid;
+  std::vector<std::vector<double>> sources;    // points (dim coordinates each)
+  std::vector<double> rates;
+  std::vector<std::vector<double>> receivers;
+  std::vector<double> times;
+  int n_quad = 20;
+  TalbotParams contour;
+  SolverConfig solver;
+  bool include_storativity = false;
+  bool storativity_z_factor = true;
+
+  int n_measurements() const { return (int)(sources.size() * receivers.size() * times.size()); }
+  int measurement_index(int source, int receiver, int time) const {
+    return (source * (int)receivers.size() + receiver) * (int)times.size() + time;
+  }
+};
+
+struct JacobianResult {
+  std::vector<double> jacobian;  // n_measurements x n_parameters, row-major
+  std::vector<double> predictions;
+};
+
+class ThtForwardModel {
+ public:
+  ThtForwardModel(const Context& ctx, ThtExperiment experiment, std::vector<double> log_storativity)
+      : ctx_(ctx), ex_(std::move(experiment)), log_s_(std::move(log_storativity)) {
+    if (ex_.sources.empty() || ex_.receivers.empty() || ex_.times.empty())
+      throw std::invalid_argument("ThtForwardModel: experiment must be nonempty");
+    if (ex_.rates.size() != ex_.sources.size())
+      throw std::invalid_argument("ThtForwardModel: one rate per source required");
+  }
+  int n_measurements() const { return ex_.n_measurements(); }
+  long n_parameters(long n_cells) const { return ex_.include_storativity ? 2 * n_cells : n_cells; }
+
+  std::vector<double> predict(const std::vector<double>& log_kappa) const { return predict_with(log_kappa, log_s_); }
+  std::vector<double> predict_with(const std::vector<double>& log_kappa, const std::vector<double>& log_s) const {
+    ShiftedPencil p(ctx_, ex_.grid, log_kappa, log_s);
+    std::vector<double> src, rec;
+    lt_experiment e = c(src, rec);
+    std::vector<double> out(n_measurements());
+    detail::check(lt_predict(p.handle(), &e, out.data()));
+    return out;
+  }
+  JacobianResult jacobian(const std::vector<double>& log_kappa) const {
+    ShiftedPencil p(ctx_, ex_.grid, log_kappa, log_s_);
+    std::vector<double> src, rec;
+    lt_experiment e = c(src, rec);
+    JacobianResult r;
+    r.jacobian.assign((size_t)n_measurements() * n_parameters(p.rows()), 0.0);
+    r.predictions.assign(n_measurements(), 0.0);
+    detail::check(lt_jacobian(p.handle(), &e, r.jacobian.data(), r.predictions.data()));
+    return r;
+  }
+
+ private:
+  lt_experiment c(std::vector<double>& src, std::vector<double>& rec) const {
+    lt_experiment e;
+    lt_experiment_defaults(&e);
+    for (const auto& q : ex_.sources) src.insert(src.end(), q.begin(), q.end());
+    for (const auto& q : ex_.receivers) rec.insert(rec.end(), q.begin(), q.end());
+    e.sources = src.data();
+    e.rates = ex_.rates.data();
+    e.n_src = (int)ex_.sources.size();
+    e.receivers = rec.data();
+    e.n_rec = (int)ex_.receivers.size();
+    e.times = ex_.times.data();
+    e.n_times = (int)ex_.times.size();
+    e.n_quad = ex_.n_quad;
+    e.contour = ex_.contour.c();
+    e.solver = ex_.solver.c();
+    e.include_storativity = ex_.include_storativity ? 1 : 0;
+    e.storativity_z_factor = ex_.storativity_z_factor ? 1 : 0;
+    return e;
+  }
+  const Context& ctx_;
+  ThtExperiment ex_;
+  std::vector<double> log_s_;
+};
+
+inline JacobianResult assemble_jacobian(const Context& ctx, const ThtExperiment& experiment,
+                                        const std::vector<double>& log_kappa,
+                                        const std::vector<double>& log_storativity) {
+  return ThtForwardModel(ctx, experiment, log_storativity).jacobian(log_kappa);
+}
+
+}  // namespace laptomo
+
+#if defined(__has_include)
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Dense>
+namespace laptomo {
+// Eigen adapters (the reference's vector types): contiguous Eigen vectors map directly.
+inline Eigen::VectorXcd to_eigen(const std::vector<Complex>& v) {
+  return Eigen::Map<const Eigen::VectorXcd>(v.data(), (Eigen::Index)v.size());
+}
+inline std::vector<Complex> from_eigen(const Eigen::VectorXcd& v) { return {v.data(), v.data() + v.size()}; }
+}  // namespace laptomo
+#endif
+#endif

@@ -11,6 +11,7 @@
 // the inverse, while the FP64 COCG recursion (r -= alpha A p with the FP64 operator) keeps the
 // solve exact to the 1e-12 tolerance.  B right-hand sides (each its own tau) run in lockstep.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -289,35 +290,45 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt,
       if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) S[e] = vadd(S[e], prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
     }
   };
-  // Gauss-Seidel update of colour `color` on plane k over the tile grown by `h` cells
-  auto update = [&](int k, int color, int h) {
-    const int RX = SW_TX + 2 * h, RY = SW_TY + 2 * h;
+  // Gauss-Seidel update of colour `color` on plane k over the tile grown by H cells: one
+  // thread per cell of that colour (i0, j0 even, so the colour parity of a row is known),
+  // compile-time region widths, 32-bit in-plane indices.
+  const int nxp1 = L.nx + 1;
+  auto update = [&](int k, int color, auto Hc) {
+    constexpr int H = decltype(Hc)::value;
+    constexpr int RX = SW_TX + 2 * H, RY = SW_TY + 2 * H, HALF = RX / 2;
+    if (tid >= RY * HALF) return;
+    const int lj = tid / HALF - H;
+    const int par = (color + lj + k) & 1;
+    const int li = -H + ((par + H) & 1) + 2 * (tid % HALF);
+    const int i = i0 + li, j = j0 + lj;
+    if (i < 0 || i >= L.nx || j < 0 || j >= L.ny) return;
     V* S = U[slot(k)];
     const V* Fk = Fr[fslot(k)];
-    for (int e = tid; e < RX * RY; e += kT) {
-      const int li = e % RX - h, lj = e / RX - h;
-      const int i = i0 + li, j = j0 + lj;
-      if (i < 0 || i >= L.nx || j < 0 || j >= L.ny || ((i + j + k) & 1) != color) continue;
-      const int s = (lj + 2) * SW_HX + (li + 2);
-      const int64_t a = k * plane + (int64_t)j * L.nx + i;
-      const int64_t ex = fx(L, i, j, k), ey = fy(L, i, j, k);
-      const R tw = __ldg(L.Tx + ex), te = __ldg(L.Tx + ex + 1);
-      const R ts = __ldg(L.Ty + ey), tn = __ldg(L.Ty + ey + L.nx);
-      R dk = tw + te + ts + tn;
-      V o = Fk[(lj + 1) * SW_FX + (li + 1)];
-      if (i > 0) o = vadd(o, vscale(S[s - 1], tw));
-      if (i < L.nx - 1) o = vadd(o, vscale(S[s + 1], te));
-      if (j > 0) o = vadd(o, vscale(S[s - SW_HX], ts));
-      if (j < L.ny - 1) o = vadd(o, vscale(S[s + SW_HX], tn));
-      if (DIM == 3) {
-        const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
-        dk += tb + tt;
-        if (k > 0) o = vadd(o, vscale(U[slot(k - 1)][s], tb));
-        if (k < L.nz - 1) o = vadd(o, vscale(U[slot(k + 1)][s], tt));
-      }
-      S[s] = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
+    const int s = (lj + 2) * SW_HX + (li + 2);
+    const int ip = j * L.nx + i;                       // in-plane cell index
+    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;     // plane k of the x faces
+    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
+    const int ex = j * nxp1 + i, ey = ip;
+    const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
+    const R ts = __ldg(Tyk + ey), tn = __ldg(Tyk + ey + L.nx);
+    R dk = tw + te + ts + tn;
+    V o = Fk[(lj + 1) * SW_FX + (li + 1)];
+    if (i > 0) o = vadd(o, vscale(S[s - 1], tw));
+    if (i < L.nx - 1) o = vadd(o, vscale(S[s + 1], te));
+    if (j > 0) o = vadd(o, vscale(S[s - SW_HX], ts));
+    if (j < L.ny - 1) o = vadd(o, vscale(S[s + SW_HX], tn));
+    const int64_t a = k * plane + ip;
+    if (DIM == 3) {
+      const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+      dk += tb + tt;
+      if (k > 0) o = vadd(o, vscale(U[slot(k - 1)][s], tb));
+      if (k < L.nz - 1) o = vadd(o, vscale(U[slot(k + 1)][s], tt));
     }
+    S[s] = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
   };
+  using H1 = std::integral_constant<int, 1>;
+  using H0 = std::integral_constant<int, 0>;
   auto store_plane = [&](int k) {
     const V* S = U[slot(k)];
     const int li = tid % SW_TX, lj = tid / SW_TX;
@@ -335,9 +346,9 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt,
       add_prolong(0);
       __syncthreads();
     }
-    update(0, first, 1);
+    update(0, first, H1{});
     __syncthreads();
-    update(0, second, 0);
+    update(0, second, H0{});
     __syncthreads();
     store_plane(0);
     return;
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt,
     if (L.nz > 1) add_prolong(1);
     __syncthreads();
   }
-  update(0, first, 1);
+  update(0, first, H1{});
   for (int k = 0; k < L.nz; ++k) {
     // prefetch x(k+3), f(k+2); then wait for x(k+2), f(k+1) issued one step earlier
     if (k + 3 < L.nz) issue_x(k + 3);
@@ -369,9 +380,9 @@ __global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt,
       add_prolong(k + 2);
       __syncthreads();
     }
-    if (k + 1 < L.nz) update(k + 1, first, 1);
+    if (k + 1 < L.nz) update(k + 1, first, H1{});
     __syncthreads();
-    update(k, second, 0);
+    update(k, second, H0{});
     __syncthreads();
     store_plane(k);
   }
