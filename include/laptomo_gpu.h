@@ -69,6 +69,9 @@ void* lt_ctx_stream(lt_ctx ctx);
 /* Per-kernel-class device timing (CUDA events on the context stream) for roofline reporting. */
 lt_status lt_ctx_set_profiling(lt_ctx ctx, int enabled);
 lt_status lt_ctx_reset_profile(lt_ctx ctx);
+/* Time only 1 in `every` launches of each kernel class (default 1) to keep the event
+ * overhead out of long timed regions; profile entries then count the sampled launches. */
+lt_status lt_ctx_set_profile_sampling(lt_ctx ctx, int every);
 /* Returns the number of kernel classes; fills up to `capacity` entries. name_buf holds
  * capacity*64 chars (NUL-terminated names). */
 int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, int64_t* launches,

@@ -89,6 +89,7 @@ SIGNATURES = {
     "lt_ctx_stream": (P, [P]),
     "lt_ctx_set_profiling": (I, [P, I]),
     "lt_ctx_reset_profile": (I, [P]),
+    "lt_ctx_set_profile_sampling": (I, [P, I]),
     "lt_ctx_profile": (I, [P, I, C.c_char_p, PD, PI64, PD]),
     "lt_ctx_launch_count": (I64, [P]),
     "lt_talbot_default_params": (None, [C.POINTER(LtTalbotParams)]),

@@ -175,7 +175,15 @@ lt_status lt_ctx_reset_profile(lt_ctx ctx) {
     LT_REQUIRE(ctx, "null context");
     ctx->resolve_profile();
     ctx->profile.clear();
+    ctx->class_counter.clear();
     ctx->launches = 0;
+  });
+}
+
+lt_status lt_ctx_set_profile_sampling(lt_ctx ctx, int every) {
+  return guard([&] {
+    LT_REQUIRE(ctx && every >= 1, "lt_ctx_set_profile_sampling: every must be >= 1");
+    ctx->sample_every = every;
   });
 }
 

@@ -97,7 +97,7 @@ constexpr int SB = 4;
 constexpr int RB = 8;
 
 template <int DIM>
-__global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double* __restrict__ kappa,
+__global__ void __launch_bounds__(kT, 2) jacobian_kernel(LevelView L, const double* __restrict__ kappa,
                                                       const double* __restrict__ stor, double hd, double face_scale,
                                                       const double2* __restrict__ fields, int n_src, int n_rec, int ns,
                                                       const double2* __restrict__ w, const double2* __restrict__ wz,
@@ -106,9 +106,9 @@ __global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double*
   constexpr int NF = 2 * DIM + 1;  // faces + storativity stage
   extern __shared__ double2 smem[];
   const int n_items = n_src + n_rec;
-  double2* P = smem;                                    // [NF][n_src][TC]
-  double2* Q = smem + (size_t)NF * n_src * TC;          // [NF][n_rec][TC]
-  double* wt = reinterpret_cast<double*>(Q + (size_t)NF * n_rec * TC);  // [NF][TC]
+  double2* P = smem;                                    // [2 DIM][n_src][TC]
+  double2* Q = smem + (size_t)2 * DIM * n_src * TC;     // [2 DIM][n_rec][TC]
+  double* wt = reinterpret_cast<double*>(Q + (size_t)2 * DIM * n_rec * TC);  // [NF][TC]
   int64_t* nb = reinterpret_cast<int64_t*>(wt + NF * TC);             // [2 DIM][TC] neighbour index or -1
   const int64_t n = L.n;
   // tile -> (row, x offset); cells of one tile are consecutive in x
@@ -156,78 +156,75 @@ __global__ void __launch_bounds__(kT) jacobian_kernel(LevelView L, const double*
     if (f < 2 * DIM) nb[f * TC + cc] = nbi;
   }
 
-  double accK[SB][RB], accS[SB][RB];
-#pragma unroll
-  for (int i = 0; i < SB; ++i)
-#pragma unroll
-    for (int q = 0; q < RB; ++q) { accK[i][q] = 0.0; accS[i][q] = 0.0; }
   __syncthreads();
-
-  for (int k = 0; k < ns; ++k) {
-    const double2 wk = w[k], wzk = wz[k];
-    // stage: one centre + 2d neighbour loads per (item, cell)
-    for (int e = tid; e < n_items * TC; e += blockDim.x) {
-      const int it = e / TC, cc = e % TC;
-      const double2* fld = fields + ((int64_t)it * ns + k) * n;
-      double2 fa = make_double2(0.0, 0.0);
-      double2 fn[2 * DIM];
-      if (cc < ncell) {
-        fa = fld[a0 + cc];
+  // phase 0: kappa block over the 2d face stages; phase 1: storativity block (centre stage).
+  // Two phases keep one SB x RB accumulator tile per thread (2 CTAs per SM).
+  for (int phase = 0; phase < (Js ? 2 : 1); ++phase) {
+    double acc[SB][RB];
 #pragma unroll
-        for (int f = 0; f < 2 * DIM; ++f) {
-          const int64_t q = nb[f * TC + cc];
-          fn[f] = q >= 0 ? fld[q] : make_double2(0.0, 0.0);
-        }
-      } else {
+    for (int i = 0; i < SB; ++i)
 #pragma unroll
-        for (int f = 0; f < 2 * DIM; ++f) fn[f] = make_double2(0.0, 0.0);
-      }
-      if (it < n_src) {
+      for (int q = 0; q < RB; ++q) acc[i][q] = 0.0;
+    const int nstage = phase == 0 ? 2 * DIM : 1;
+    for (int k = 0; k < ns; ++k) {
+      const double2 wk = w[k], wzk = wz[k];
+      // stage: one centre (+ 2d neighbour) loads per (item, cell)
+      for (int e = tid; e < n_items * TC; e += blockDim.x) {
+        const int it = e / TC, cc = e % TC;
+        const double2* fld = fields + ((int64_t)it * ns + k) * n;
+        const double2 fa = cc < ncell ? fld[a0 + cc] : make_double2(0.0, 0.0);
+        if (phase == 0) {
+          double2 fn[2 * DIM];
 #pragma unroll
-        for (int f = 0; f < 2 * DIM; ++f)
-          P[((size_t)f * n_src + it) * TC + cc] = cscale(cmul(wk, csub(fa, fn[f])), wt[f * TC + cc]);
-        P[((size_t)(2 * DIM) * n_src + it) * TC + cc] = cscale(cmul(wzk, fa), wt[2 * DIM * TC + cc]);
-      } else {
-        const int r = it - n_src;
+          for (int f = 0; f < 2 * DIM; ++f) {
+            const int64_t q = cc < ncell ? nb[f * TC + cc] : -1;
+            fn[f] = q >= 0 ? fld[q] : make_double2(0.0, 0.0);
+          }
+          if (it < n_src) {
 #pragma unroll
-        for (int f = 0; f < 2 * DIM; ++f) Q[((size_t)f * n_rec + r) * TC + cc] = csub(fa, fn[f]);
-        Q[((size_t)(2 * DIM) * n_rec + r) * TC + cc] = fa;
-      }
-    }
-    __syncthreads();
-    if (owner) {
-#pragma unroll 1
-      for (int f = 0; f < NF; ++f) {
-        double2 pv[SB];
-#pragma unroll
-        for (int i = 0; i < SB; ++i)
-          pv[i] = (s0 + i < n_src) ? P[((size_t)f * n_src + s0 + i) * TC + c] : make_double2(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-          const double2 qv = (r0 + q < n_rec) ? Q[((size_t)f * n_rec + r0 + q) * TC + c] : make_double2(0.0, 0.0);
-          if (f < 2 * DIM) {
-#pragma unroll
-            for (int i = 0; i < SB; ++i) accK[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accK[i][q]));
+            for (int f = 0; f < 2 * DIM; ++f)
+              P[((size_t)f * n_src + it) * TC + cc] = cscale(cmul(wk, csub(fa, fn[f])), wt[f * TC + cc]);
           } else {
+            const int r = it - n_src;
 #pragma unroll
-            for (int i = 0; i < SB; ++i) accS[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, accS[i][q]));
+            for (int f = 0; f < 2 * DIM; ++f) Q[((size_t)f * n_rec + r) * TC + cc] = csub(fa, fn[f]);
+          }
+        } else {
+          if (it < n_src) P[(size_t)it * TC + cc] = cscale(cmul(wzk, fa), wt[2 * DIM * TC + cc]);
+          else Q[(size_t)(it - n_src) * TC + cc] = fa;
+        }
+      }
+      __syncthreads();
+      if (owner) {
+#pragma unroll 1
+        for (int f = 0; f < nstage; ++f) {
+          double2 pv[SB];
+#pragma unroll
+          for (int i = 0; i < SB; ++i)
+            pv[i] = (s0 + i < n_src) ? P[((size_t)f * n_src + s0 + i) * TC + c] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const double2 qv = (r0 + q < n_rec) ? Q[((size_t)f * n_rec + r0 + q) * TC + c] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < SB; ++i) acc[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, acc[i][q]));
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
-  }
-  if (!owner) return;
-  const int64_t a = a0 + c;
+    if (owner) {
+      double* Jout = phase == 0 ? Jk : Js;
+      const int64_t a = a0 + c;
 #pragma unroll
-  for (int i = 0; i < SB; ++i) {
-    if (s0 + i >= n_src) continue;
+      for (int i = 0; i < SB; ++i) {
+        if (s0 + i >= n_src) continue;
 #pragma unroll
-    for (int q = 0; q < RB; ++q) {
-      if (r0 + q >= n_rec) continue;
-      const int64_t rowj = (int64_t)(s0 + i) * n_rec + (r0 + q);
-      Jk[rowj * ldj + a] = 2.0 * accK[i][q];
-      if (Js) Js[rowj * ldj + a] = 2.0 * accS[i][q];
+        for (int q = 0; q < RB; ++q) {
+          if (r0 + q >= n_rec) continue;
+          const int64_t rowj = (int64_t)(s0 + i) * n_rec + (r0 + q);
+          Jout[rowj * ldj + a] = 2.0 * acc[i][q];
+        }
+      }
     }
   }
 }
@@ -654,9 +651,9 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     LevelView L = p->view(0);
     TC = std::min(TC, L.nx);
     auto smem_for = [&](int tc) {
-      return sizeof(double2) * (size_t)nf * B * tc + sizeof(double) * nf * tc + sizeof(int64_t) * 2 * p->dim * tc;
+      return sizeof(double2) * (size_t)(nf - 1) * B * tc + sizeof(double) * nf * tc + sizeof(int64_t) * 2 * p->dim * tc;
     };
-    while (TC > 1 && smem_for(TC) > 200 * 1024) TC /= 2;
+    while (TC > 1 && smem_for(TC) > 110 * 1024) TC /= 2;  // two CTAs per SM
     LT_REQUIRE(nf * TC <= kT, "jacobian: tile too wide");
     const size_t smem = smem_for(TC);
     const int tiles_x = (L.nx + TC - 1) / TC;

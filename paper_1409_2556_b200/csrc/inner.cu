@@ -446,6 +446,130 @@ __global__ void __launch_bounds__(kT) bdot_kernel(int64_t n, Batch bt, const dou
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
 
+// ---- z-marching 7-point kernels (3-D) -------------------------------------------------
+// CTA = 32 x 8 (x, y) tile x a chunk of ZM_ZC planes; each thread keeps its column's
+// x[k-1], x[k], x[k+1] in registers (x[k+2] prefetched one step ahead), so every value of x
+// is read from HBM once; in-plane neighbours come from L1.
+constexpr int ZM_TX = 32, ZM_TY = 8, ZM_ZC = 32;
+
+struct ZmMap {
+  int i, j, k0, k1, ip;
+  bool in;
+};
+
+template <class VW>
+__device__ __forceinline__ ZmMap zm_map(const VW& L, int cb) {
+  const int tiles_x = (L.nx + ZM_TX - 1) / ZM_TX, tiles_y = (L.ny + ZM_TY - 1) / ZM_TY;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  ZmMap m;
+  m.i = (tile % tiles_x) * ZM_TX + (threadIdx.x & (ZM_TX - 1));
+  m.j = (tile / tiles_x) * ZM_TY + (threadIdx.x / ZM_TX);
+  m.in = m.i < L.nx && m.j < L.ny;
+  m.k0 = chunk * ZM_ZC;
+  m.k1 = min(L.nz, m.k0 + ZM_ZC);
+  m.ip = m.j * L.nx + m.i;
+  return m;
+}
+
+template <class VW>
+inline int zm_blocks(const VW& L) {
+  return ((L.nx + ZM_TX - 1) / ZM_TX) * ((L.ny + ZM_TY - 1) / ZM_TY) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+}
+
+// r = f - A(tau) x (precision R), z-marching
+template <class R>
+__global__ void __launch_bounds__(kT) residual_zm_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                         const typename CT<R>::V* __restrict__ f,
+                                                         const typename CT<R>::V* __restrict__ x,
+                                                         typename CT<R>::V* __restrict__ r) {
+  using V = typename CT<R>::V;
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZmMap m = zm_map(L, cb);
+  if (!m.in) return;
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  const V* xb = x + (int64_t)b * L.n;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  const int nxp1 = L.nx + 1;
+  V xm = m.k0 > 0 ? xb[(m.k0 - 1) * plane + m.ip] : vzero<V>();
+  V xc = xb[m.k0 * plane + m.ip];
+  V xp = m.k0 + 1 < L.nz ? xb[(m.k0 + 1) * plane + m.ip] : vzero<V>();
+  for (int k = m.k0; k < m.k1; ++k) {
+    const V xn = (k + 1 < m.k1 && k + 2 < L.nz) ? xb[(k + 2) * plane + m.ip] : vzero<V>();
+    const int64_t a = k * plane + m.ip;
+    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
+    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
+    const int ex = m.j * nxp1 + m.i;
+    const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
+    const R ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
+    const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+    const R dk = tw + te + ts + tn + tb + tt;
+    V o = vzero<V>();
+    if (m.i > 0) o = vadd(o, vscale(xb[a - 1], tw));
+    if (m.i < L.nx - 1) o = vadd(o, vscale(xb[a + 1], te));
+    if (m.j > 0) o = vadd(o, vscale(xb[a - L.nx], ts));
+    if (m.j < L.ny - 1) o = vadd(o, vscale(xb[a + L.nx], tn));
+    if (k > 0) o = vadd(o, vscale(xm, tb));
+    if (k < L.nz - 1) o = vadd(o, vscale(xp, tt));
+    const R mm = __ldg(L.M + a);
+    const R dr = dk + tr * mm, di = ti * mm;
+    const V ax = V{dr * xc.x - di * xc.y - o.x, dr * xc.y + di * xc.x - o.y};
+    r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
+    xm = xc;
+    xc = xp;
+    xp = xn;
+  }
+}
+
+// q = A p, partial p^T q (FP64), z-marching
+__global__ void __launch_bounds__(kT) apply_dot_zm_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
+                                                          const double2* __restrict__ p, double2* __restrict__ q,
+                                                          double2* __restrict__ part, int nblk) {
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZmMap m = zm_map(L, cb);
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  const double2* pb = p + (int64_t)b * L.n;
+  double2* qb = q + (int64_t)b * L.n;
+  const double2 tau = taus[b];
+  const int nxp1 = L.nx + 1;
+  double2 acc = make_double2(0.0, 0.0);
+  if (m.in) {
+    double2 xm = m.k0 > 0 ? pb[(m.k0 - 1) * plane + m.ip] : make_double2(0.0, 0.0);
+    double2 xc = pb[m.k0 * plane + m.ip];
+    double2 xp = m.k0 + 1 < L.nz ? pb[(m.k0 + 1) * plane + m.ip] : make_double2(0.0, 0.0);
+    for (int k = m.k0; k < m.k1; ++k) {
+      const double2 xn = (k + 1 < m.k1 && k + 2 < L.nz) ? pb[(k + 2) * plane + m.ip] : make_double2(0.0, 0.0);
+      const int64_t a = k * plane + m.ip;
+      const double* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
+      const double* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
+      const int ex = m.j * nxp1 + m.i;
+      const double tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
+      const double ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
+      const double tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+      const double dk = tw + te + ts + tn + tb + tt;
+      double2 o = make_double2(0.0, 0.0);
+      if (m.i > 0) o = cfma(make_double2(tw, 0.0), pb[a - 1], o);
+      if (m.i < L.nx - 1) o = cfma(make_double2(te, 0.0), pb[a + 1], o);
+      if (m.j > 0) o = cfma(make_double2(ts, 0.0), pb[a - L.nx], o);
+      if (m.j < L.ny - 1) o = cfma(make_double2(tn, 0.0), pb[a + L.nx], o);
+      if (k > 0) o = cfma(make_double2(tb, 0.0), xm, o);
+      if (k < L.nz - 1) o = cfma(make_double2(tt, 0.0), xp, o);
+      const double mm = __ldg(L.M + a);
+      const double2 d = make_double2(dk + tau.x * mm, tau.y * mm);
+      const double2 qa = csub(cmul(d, xc), o);
+      qb[a] = qa;
+      acc = cadd(acc, cmul(xc, qa));
+      xm = xc;
+      xc = xp;
+      xp = xn;
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
+}
+
 // q = A p, partial p^T q
 template <int DIM>
 __global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
@@ -583,7 +707,10 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
   });
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
-    residual_kernel<R, DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+    if (DIM == 3)
+      residual_zm_kernel<R><<<(unsigned)zm_blocks(L) * Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+    else
+      residual_kernel<R, DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
   });
   const unsigned gridc = (unsigned)Lc.ntiles * (unsigned)Bc;
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
@@ -641,7 +768,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   Batch bt{Bc, d_done};
 
   // workspace: FP64 Krylov vectors r, p, q; multigrid vectors (precision R) per level
-  DeviceBuffer partials(sizeof(double2) * (size_t)Bc * std::max<int64_t>(nblk, L0.ntiles), st);
+  DeviceBuffer partials(sizeof(double2) * (size_t)Bc *
+                            std::max<int64_t>(std::max<int64_t>(nblk, L0.ntiles), zm_blocks(L0)), st);
   DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 3, st);
   double2* r = vec.as<double2>();
   double2* pp = r + Bc * n;
@@ -694,12 +822,17 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RHO, bt, partials.get(), nblk, sc); });
   launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
   for (int it = 0; it < p->inner_maxit; ++it) {
+    const int nblk_apply = DIM == 3 ? zm_blocks(L0) : L0.ntiles;
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
-      apply_dot_kernel<DIM><<<(unsigned)L0.ntiles * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
-                                                                    L0.ntiles);
+      if (DIM == 3)
+        apply_dot_zm_kernel<<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
+                                                                      nblk_apply);
+      else
+        apply_dot_kernel<DIM><<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q,
+                                                                        partials.as<double2>(), nblk_apply);
     });
     launch(ctx, "cocg_scalar", 0.0, [&] {
-      scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), L0.ntiles, sc);
+      scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk_apply, sc);
     });
     launch(ctx, "cocg_vec", nb * ((it == 0 ? 64.0 : 80.0) + vb), [&] {
       axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, rmg, it == 0, (double*)partials.get(),
@@ -740,7 +873,7 @@ void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v,
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   const double per_item = (double)n * (sizeof(double2) * 3.0 + sizeof(VM) * 3.0 * 1.2);
-  int chunk = (int)std::max(1.0, std::min(64.0, 0.5 * (double)free_b / per_item));
+  int chunk = (int)std::max(1.0, std::min(128.0, 0.5 * (double)free_b / per_item));
   for (int b0 = 0; b0 < B; b0 += chunk) {
     const int bc = std::min(chunk, B - b0);
     if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);

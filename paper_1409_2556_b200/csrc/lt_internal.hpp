@@ -77,6 +77,8 @@ struct lt_ctx_s {
   std::vector<lt::PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   int num_sms = 148;
+  int sample_every = 1;                              // time 1 in N launches of each class
+  std::map<const char*, int64_t> class_counter;      // keyed by the (literal) class name
 
   void resolve_profile();
   cudaEvent_t take_event();
@@ -88,13 +90,13 @@ namespace lt {
 template <class F>
 inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f) {
   ctx->launches++;
-  if (ctx->profiling) {
+  if (ctx->profiling && (ctx->class_counter[name]++ % ctx->sample_every) == 0) {
     cudaEvent_t a = ctx->take_event(), b = ctx->take_event();
     cudaEventRecord(a, ctx->stream);
     f();
     cudaEventRecord(b, ctx->stream);
     ctx->pending.push_back({name, a, b, algorithmic_bytes});
-    if (ctx->pending.size() > 8192) ctx->resolve_profile();
+    if (ctx->pending.size() > 65536) ctx->resolve_profile();
   } else {
     f();
   }

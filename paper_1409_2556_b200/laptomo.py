@@ -68,6 +68,9 @@ class Context:
     def reset_profile(self):
         check(lib().lt_ctx_reset_profile(self._h))
 
+    def set_profile_sampling(self, every: int):
+        check(lib().lt_ctx_set_profile_sampling(self._h, int(every)))
+
     def launch_count(self) -> int:
         return int(lib().lt_ctx_launch_count(self._h))
 
