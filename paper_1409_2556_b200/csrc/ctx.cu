@@ -15,6 +15,24 @@ cudaEvent_t lt_ctx_s::take_event() {
   return e;
 }
 
+void lt_ctx_s::resolve_completed() {
+  size_t done = 0;
+  for (; done < pending.size(); ++done) {
+    if (cudaEventQuery(pending[done].stop) != cudaSuccess) break;
+    auto& pe = pending[done];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pe.start, pe.stop);
+    auto& e = profile[pe.name];
+    e.ms += ms;
+    e.launches += 1;
+    e.bytes += pe.bytes;
+    event_pool.push_back(pe.start);
+    event_pool.push_back(pe.stop);
+  }
+  cudaGetLastError();  // cudaErrorNotReady from the query is not an error
+  if (done) pending.erase(pending.begin(), pending.begin() + done);
+}
+
 void lt_ctx_s::resolve_profile() {
   if (pending.empty()) return;
   LT_CUDA(cudaEventSynchronize(pending.back().stop));

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <type_traits>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "lt_internal.hpp"
@@ -522,6 +524,133 @@ __global__ void __launch_bounds__(kT) residual_zm_kernel(LevelViewT<R> L, Batch 
   }
 }
 
+// One red-black Gauss-Seidel half sweep of colour `color`, in place and z-marching: a cell of
+// that colour reads only other-colour neighbours, which this launch does not change, so the
+// in-place update is race free; every cell is written (other colour unchanged) so stores are
+// full sectors.  zero_init: x = 0 on entry (colour cells get f/d, the others 0, x not read).
+template <class R>
+__global__ void __launch_bounds__(kT) rbhalf_zm_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                       const typename CT<R>::V* __restrict__ f,
+                                                       typename CT<R>::V* x, int color, int zero_init) {
+  using V = typename CT<R>::V;
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZmMap m = zm_map(L, cb);
+  if (!m.in) return;
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  V* xb = x + (int64_t)b * L.n;
+  const V* fb = f + (int64_t)b * L.n;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  const int nxp1 = L.nx + 1;
+  V xm = vzero<V>(), xc = vzero<V>(), xp = vzero<V>();
+  if (!zero_init) {
+    xm = m.k0 > 0 ? xb[(m.k0 - 1) * plane + m.ip] : vzero<V>();
+    xc = xb[m.k0 * plane + m.ip];
+    xp = m.k0 + 1 < L.nz ? xb[(m.k0 + 1) * plane + m.ip] : vzero<V>();
+  }
+  for (int k = m.k0; k < m.k1; ++k) {
+    V xn = vzero<V>();
+    if (!zero_init && k + 1 < m.k1 && k + 2 < L.nz) xn = xb[(k + 2) * plane + m.ip];
+    const int64_t a = k * plane + m.ip;
+    V out = xc;
+    if (((m.i + m.j + k) & 1) == color) {
+      const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
+      const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
+      const int ex = m.j * nxp1 + m.i;
+      const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
+      const R ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
+      R dk = tw + te + ts + tn;
+      V o = fb[a];
+      if (L.dim == 3) {
+        const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
+        dk += tb + tt;
+        if (!zero_init) {
+          if (k > 0) o = vadd(o, vscale(xm, tb));
+          if (k < L.nz - 1) o = vadd(o, vscale(xp, tt));
+        }
+      }
+      if (!zero_init) {
+        if (m.i > 0) o = vadd(o, vscale(xb[a - 1], tw));
+        if (m.i < L.nx - 1) o = vadd(o, vscale(xb[a + 1], te));
+        if (m.j > 0) o = vadd(o, vscale(xb[a - L.nx], ts));
+        if (m.j < L.ny - 1) o = vadd(o, vscale(xb[a + L.nx], tn));
+      }
+      out = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
+    }
+    xb[a] = out;
+    xm = xc;
+    xc = xp;
+    xp = xn;
+  }
+}
+
+// f_c = P^T r_f, z-marching over the coarse grid: each fine plane's in-plane (4 x 4) weighted
+// sum is formed once and added to the two coarse planes it belongs to (register ring).
+template <class R>
+__global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, int ax, int ay, int az,
+                                                         Batch bt, const typename CT<R>::V* __restrict__ rf,
+                                                         typename CT<R>::V* __restrict__ fc) {
+  using V = typename CT<R>::V;
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZmMap m = zm_map(Lc, cb);  // coarse column (I, J), coarse planes [k0, k1)
+  if (!m.in) return;
+  int Fx[4], Fy[4];
+  float wx[4], wy[4];
+  const int nxx = r1d_terms(m.i, ax, Lc.nx, Fx, wx);
+  const int nyy = r1d_terms(m.j, ay, Lc.ny, Fy, wy);
+  const V* rb = rf + (int64_t)b * Lf.n;
+  V* fb = fc + (int64_t)b * Lc.n;
+  const int64_t fplane = (int64_t)Lf.nx * Lf.ny, cplane = (int64_t)Lc.nx * Lc.ny;
+  auto inplane = [&](int kf) {
+    V s = vzero<V>();
+    const V* pl = rb + kf * fplane;
+    for (int p = 0; p < nyy; ++p) {
+      const V* row = pl + (int64_t)Fy[p] * Lf.nx;
+      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(row[Fx[o]], (R)(wy[p] * wx[o])));
+    }
+    return s;
+  };
+  if (az == 1 || Lf.dim == 2) {
+    for (int K = m.k0; K < m.k1; ++K) fb[K * cplane + m.ip] = inplane(K);
+    return;
+  }
+  // coarse K collects fine planes 2K-1 (1/4), 2K (3/4 | 1/2 at K = 0), 2K+1 (3/4 | 1/2 at the
+  // top), 2K+2 (1/4)
+  V sa = m.k0 > 0 ? inplane(2 * m.k0 - 1) : vzero<V>();  // S(2K-1)
+  V sb = inplane(2 * m.k0);                              // S(2K)
+  for (int K = m.k0; K < m.k1; ++K) {
+    const V sc = inplane(2 * K + 1);
+    const V sd = K < Lc.nz - 1 ? inplane(2 * K + 2) : vzero<V>();
+    const R w0 = K > 0 ? R(0.25) : R(0);
+    const R w1 = K == 0 ? R(0.5) : R(0.75);
+    const R w2 = K == Lc.nz - 1 ? R(0.5) : R(0.75);
+    const R w3 = K < Lc.nz - 1 ? R(0.25) : R(0);
+    fb[K * cplane + m.ip] = vadd(vadd(vscale(sa, w0), vscale(sb, w1)), vadd(vscale(sc, w2), vscale(sd, w3)));
+    sa = sc;
+    sb = sd;
+  }
+}
+
+// x += P e_c (cell-centred multilinear prolongation), z-marching over the fine grid
+template <class R>
+__global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, int ax, int ay, int az,
+                                                        Batch bt, const typename CT<R>::V* __restrict__ ec,
+                                                        typename CT<R>::V* __restrict__ xf) {
+  using V = typename CT<R>::V;
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZmMap m = zm_map(Lf, cb);
+  if (!m.in) return;
+  const int64_t plane = (int64_t)Lf.nx * Lf.ny;
+  const V* eb = ec + (int64_t)b * Lc.n;
+  V* xb = xf + (int64_t)b * Lf.n;
+  for (int k = m.k0; k < m.k1; ++k) {
+    const int64_t a = k * plane + m.ip;
+    xb[a] = vadd(xb[a], prolong_at(Lc, ax, ay, az, eb, m.i, m.j, k, Lf.dim));
+  }
+}
+
 // q = A p, partial p^T q (FP64), z-marching
 __global__ void __launch_bounds__(kT) apply_dot_zm_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
                                                           const double2* __restrict__ p, double2* __restrict__ q,
@@ -701,11 +830,25 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     LT_CUDA(cudaFuncSetAttribute(rb_sweep_kernel<R, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
     attr_set = true;
   }
-  // pre-smoothing: one red-black sweep (red first) from a zero iterate
-  // (algorithmic bytes per cell-item: f read + x written; faces once per launch)
-  launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
-    rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
-  });
+  static const bool zm_smoother = [] {
+    const char* e = std::getenv("LT_SMOOTHER");
+    return !(e && std::string(e) == "smem");
+  }();
+  const unsigned zgrid = (unsigned)zm_blocks(L) * (unsigned)Bc;
+  if (zm_smoother) {
+    // pre-smoothing: red half sweep from zero (f read, x written), black half sweep
+    launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
+      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 1);
+    });
+    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
+      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
+    });
+  } else {
+    // pre-smoothing: one fused red-black sweep (red first) from a zero iterate
+    launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
+      rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
+    });
+  }
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
     if (DIM == 3)
       residual_zm_kernel<R><<<(unsigned)zm_blocks(L) * Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
@@ -714,9 +857,26 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   });
   const unsigned gridc = (unsigned)Lc.ntiles * (unsigned)Bc;
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
-    restrict_kernel<R, DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, Rr[l], F[l + 1]);
+    if (zm_smoother)
+      restrict_zm_kernel<R><<<(unsigned)zm_blocks(Lc) * Bc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt,
+                                                                        Rr[l], F[l + 1]);
+    else
+      restrict_kernel<R, DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, Rr[l], F[l + 1]);
   });
   const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr);
+  if (zm_smoother) {
+    // coarse correction, then the transpose of the pre-smoother (black, red), in place
+    launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+      prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
+    });
+    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
+      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
+    });
+    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
+      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 0);
+    });
+    return X[l];
+  }
   // post-smoothing: coarse correction x + P e_c fused into one black-first sweep (the
   // transpose of the pre-smoother), written out of place into Rr[l]
   launch(ctx, "mg_smooth", cell_bytes * 3 * vb + (double)Lc.n * Bc * vb + coef, [&] {

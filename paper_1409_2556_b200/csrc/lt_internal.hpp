@@ -80,7 +80,8 @@ struct lt_ctx_s {
   int sample_every = 1;                              // time 1 in N launches of each class
   std::map<const char*, int64_t> class_counter;      // keyed by the (literal) class name
 
-  void resolve_profile();
+  void resolve_profile();    // waits for all pending events
+  void resolve_completed();  // accumulates the already-completed prefix of pending events
   cudaEvent_t take_event();
 };
 
@@ -96,10 +97,11 @@ inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f
     f();
     cudaEventRecord(b, ctx->stream);
     ctx->pending.push_back({name, a, b, algorithmic_bytes});
-    if (ctx->pending.size() > 65536) ctx->resolve_profile();
-  } else {
-    f();
+    check_launch(name);
+    if (ctx->pending.size() >= 1024) ctx->resolve_completed();  // non-blocking, recycles events
+    return;
   }
+  f();
   check_launch(name);
 }
 
