@@ -281,10 +281,11 @@ def main():
         build(False)
     # ---- device-resident timed region ----
     sampler = ClockSampler(local)
-    sampler.start()
+    if not os.environ.get("LT_BENCH_NOSMI"):
+        sampler.start()
     ctx.reset_profile()
     ctx.set_profile_sampling(PROFILE_EVERY)  # events on 1 in 8 launches per kernel class
-    ctx.set_profiling(True)
+    ctx.set_profiling(not os.environ.get("LT_BENCH_NOPROF"))
     launches0 = ctx.launch_count()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -322,7 +323,7 @@ def main():
 
     peak, peak_kind = peaks()
     # dominant kernel class by device time
-    dom = max(prof.items(), key=lambda kv: kv[1][0])
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 1, 0.0))
     dname, (dms, dcnt, dbytes) = dom
     achieved = (dbytes / dcnt) / (dms / dcnt * 1e-3) / 1e9 if dms > 0 else 0.0
     # sampled classes: estimated totals over the timed region = sampled x PROFILE_EVERY
