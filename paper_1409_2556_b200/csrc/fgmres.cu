@@ -347,10 +347,13 @@ __global__ void small_solve(State S, int m, int force) {
 template <int DIM>
 __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int m, const double2* __restrict__ rhs,
                                                       const double2* const* __restrict__ Ucols, double* __restrict__ part) {
-  constexpr int KC = 8;  // shifts per register chunk
+  constexpr int KC = 16;  // shifts per register chunk
+  constexpr int MJ = 16;  // Krylov columns whose coefficients are staged in shared memory
   __shared__ double sh[32];
   __shared__ int flagged[256];
   __shared__ int nflag;
+  __shared__ double2 ysm[KC][MJ];
+  __shared__ double2 zsm[KC];
   LT_ITEM_BLOCK(S.B, b, cb);
   if (threadIdx.x == 0) {
     int c = 0;
@@ -367,6 +370,16 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
   const double mval = in ? __ldg(L.M + a) : 0.0;
   for (int c0 = 0; c0 < nflag; c0 += KC) {
     const int nc = min(KC, nflag - c0);
+    const bool staged = m <= MJ;
+    __syncthreads();
+    if (staged) {
+      for (int e = threadIdx.x; e < KC * MJ; e += blockDim.x) {
+        const int q = e / MJ, j = e % MJ;
+        if (q < nc && j < m) ysm[q][j] = S.Y[(int64_t)(b * S.ns + flagged[c0 + q]) * S.maxit + j];
+      }
+      if (threadIdx.x < nc) zsm[threadIdx.x] = S.shifts[b * S.ns + flagged[c0 + threadIdx.x]];
+    }
+    __syncthreads();
     double2 acc[KC];
 #pragma unroll
     for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
@@ -383,16 +396,20 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
         for (int q = 0; q < KC; ++q) {
           if (q < nc) {
             const int t = b * S.ns + flagged[c0 + q];
-            const double2 y = S.Y[(int64_t)t * S.maxit + j];
-            acc[q] = cadd(acc[q], cmul(y, cadd(Ku, cmul(S.shifts[t], Mu))));
+            const double2 y = staged ? ysm[q][j] : S.Y[(int64_t)t * S.maxit + j];
+            const double2 z = staged ? zsm[q] : S.shifts[t];
+            acc[q] = cadd(acc[q], cmul(y, cadd(Ku, cmul(z, Mu))));
           }
         }
       }
     }
-    for (int q = 0; q < nc; ++q) {
-      const double2 r = csub(bv, acc[q]);
-      const double nn = block_sum_d(in ? cabs2(r) : 0.0, sh);
-      if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = nn;
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      if (q < nc) {  // uniform across the block
+        const double2 r = csub(bv, acc[q]);
+        const double nn = block_sum_d(in ? cabs2(r) : 0.0, sh);
+        if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = nn;
+      }
     }
   }
 }

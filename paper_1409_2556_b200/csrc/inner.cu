@@ -494,33 +494,49 @@ __global__ void __launch_bounds__(kT) residual_zm_kernel(LevelViewT<R> L, Batch 
   const V* xb = x + (int64_t)b * L.n;
   const R tr = (R)taus[b].x, ti = (R)taus[b].y;
   const int nxp1 = L.nx + 1;
+  const V* fb = f + (int64_t)b * L.n;
   V xm = m.k0 > 0 ? xb[(m.k0 - 1) * plane + m.ip] : vzero<V>();
   V xc = xb[m.k0 * plane + m.ip];
   V xp = m.k0 + 1 < L.nz ? xb[(m.k0 + 1) * plane + m.ip] : vzero<V>();
-  for (int k = m.k0; k < m.k1; ++k) {
-    const V xn = (k + 1 < m.k1 && k + 2 < L.nz) ? xb[(k + 2) * plane + m.ip] : vzero<V>();
+  struct Ops {
+    R tw, te, ts, tn, tb, tt, mm;
+    V f, nw, ne, ns, nn;
+  };
+  auto load_ops = [&](int k, Ops& o) {
     const int64_t a = k * plane + m.ip;
     const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
     const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
     const int ex = m.j * nxp1 + m.i;
-    const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
-    const R ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
-    const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
-    const R dk = tw + te + ts + tn + tb + tt;
-    V o = vzero<V>();
-    if (m.i > 0) o = vadd(o, vscale(xb[a - 1], tw));
-    if (m.i < L.nx - 1) o = vadd(o, vscale(xb[a + 1], te));
-    if (m.j > 0) o = vadd(o, vscale(xb[a - L.nx], ts));
-    if (m.j < L.ny - 1) o = vadd(o, vscale(xb[a + L.nx], tn));
-    if (k > 0) o = vadd(o, vscale(xm, tb));
-    if (k < L.nz - 1) o = vadd(o, vscale(xp, tt));
-    const R mm = __ldg(L.M + a);
-    const R dr = dk + tr * mm, di = ti * mm;
+    o.tw = __ldg(Txk + ex);
+    o.te = __ldg(Txk + ex + 1);
+    o.ts = __ldg(Tyk + m.ip);
+    o.tn = __ldg(Tyk + m.ip + L.nx);
+    o.tb = __ldg(L.Tz + a);
+    o.tt = __ldg(L.Tz + a + plane);
+    o.mm = __ldg(L.M + a);
+    o.f = fb[a];
+    o.nw = m.i > 0 ? xb[a - 1] : vzero<V>();
+    o.ne = m.i < L.nx - 1 ? xb[a + 1] : vzero<V>();
+    o.ns = m.j > 0 ? xb[a - L.nx] : vzero<V>();
+    o.nn = m.j < L.ny - 1 ? xb[a + L.nx] : vzero<V>();
+  };
+  Ops cur, nxt;
+  load_ops(m.k0, cur);
+  for (int k = m.k0; k < m.k1; ++k) {
+    const V xn = (k + 1 < m.k1 && k + 2 < L.nz) ? xb[(k + 2) * plane + m.ip] : vzero<V>();
+    if (k + 1 < m.k1) load_ops(k + 1, nxt);
+    const int64_t a = k * plane + m.ip;
+    const R dk = cur.tw + cur.te + cur.ts + cur.tn + cur.tb + cur.tt;
+    V o = vadd(vadd(vscale(cur.nw, cur.tw), vscale(cur.ne, cur.te)), vadd(vscale(cur.ns, cur.ts), vscale(cur.nn, cur.tn)));
+    if (k > 0) o = vadd(o, vscale(xm, cur.tb));
+    if (k < L.nz - 1) o = vadd(o, vscale(xp, cur.tt));
+    const R dr = dk + tr * cur.mm, di = ti * cur.mm;
     const V ax = V{dr * xc.x - di * xc.y - o.x, dr * xc.y + di * xc.x - o.y};
-    r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
+    r[(int64_t)b * L.n + a] = vsub(cur.f, ax);
     xm = xc;
     xc = xp;
     xp = xn;
+    cur = nxt;
   }
 }
 
@@ -548,39 +564,58 @@ __global__ void __launch_bounds__(kT) rbhalf_zm_kernel(LevelViewT<R> L, Batch bt
     xc = xb[m.k0 * plane + m.ip];
     xp = m.k0 + 1 < L.nz ? xb[(m.k0 + 1) * plane + m.ip] : vzero<V>();
   }
+  // operands of the colour cell of plane k, loaded one step ahead (software pipeline)
+  struct Ops {
+    R tw, te, ts, tn, tb, tt, mm;
+    V f, nw, ne, ns, nn;
+  };
+  auto load_ops = [&](int k, Ops& o) {
+    const int64_t a = k * plane + m.ip;
+    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
+    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
+    const int ex = m.j * nxp1 + m.i;
+    o.tw = __ldg(Txk + ex);
+    o.te = __ldg(Txk + ex + 1);
+    o.ts = __ldg(Tyk + m.ip);
+    o.tn = __ldg(Tyk + m.ip + L.nx);
+    o.tb = L.dim == 3 ? __ldg(L.Tz + a) : R(0);
+    o.tt = L.dim == 3 ? __ldg(L.Tz + a + plane) : R(0);
+    o.mm = __ldg(L.M + a);
+    o.f = fb[a];
+    if (!zero_init) {
+      o.nw = m.i > 0 ? xb[a - 1] : vzero<V>();
+      o.ne = m.i < L.nx - 1 ? xb[a + 1] : vzero<V>();
+      o.ns = m.j > 0 ? xb[a - L.nx] : vzero<V>();
+      o.nn = m.j < L.ny - 1 ? xb[a + L.nx] : vzero<V>();
+    }
+  };
+  Ops cur, nxt;
+  bool cur_valid = ((m.i + m.j + m.k0) & 1) == color;
+  if (cur_valid) load_ops(m.k0, cur);
   for (int k = m.k0; k < m.k1; ++k) {
     V xn = vzero<V>();
     if (!zero_init && k + 1 < m.k1 && k + 2 < L.nz) xn = xb[(k + 2) * plane + m.ip];
+    const bool nxt_valid = k + 1 < m.k1 && ((m.i + m.j + k + 1) & 1) == color;
+    if (nxt_valid) load_ops(k + 1, nxt);
     const int64_t a = k * plane + m.ip;
     V out = xc;
-    if (((m.i + m.j + k) & 1) == color) {
-      const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
-      const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
-      const int ex = m.j * nxp1 + m.i;
-      const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
-      const R ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
-      R dk = tw + te + ts + tn;
-      V o = fb[a];
-      if (L.dim == 3) {
-        const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
-        dk += tb + tt;
-        if (!zero_init) {
-          if (k > 0) o = vadd(o, vscale(xm, tb));
-          if (k < L.nz - 1) o = vadd(o, vscale(xp, tt));
-        }
-      }
+    if (cur_valid) {
+      const R dk = cur.tw + cur.te + cur.ts + cur.tn + cur.tb + cur.tt;
+      V o = cur.f;
       if (!zero_init) {
-        if (m.i > 0) o = vadd(o, vscale(xb[a - 1], tw));
-        if (m.i < L.nx - 1) o = vadd(o, vscale(xb[a + 1], te));
-        if (m.j > 0) o = vadd(o, vscale(xb[a - L.nx], ts));
-        if (m.j < L.ny - 1) o = vadd(o, vscale(xb[a + L.nx], tn));
+        o = vadd(o, vadd(vadd(vscale(cur.nw, cur.tw), vscale(cur.ne, cur.te)),
+                         vadd(vscale(cur.ns, cur.ts), vscale(cur.nn, cur.tn))));
+        if (k > 0) o = vadd(o, vscale(xm, cur.tb));
+        if (k < L.nz - 1) o = vadd(o, vscale(xp, cur.tt));
       }
-      out = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
+      out = diag_solve_r<R, V>(dk, cur.mm, tr, ti, o);
     }
     xb[a] = out;
     xm = xc;
     xc = xp;
     xp = xn;
+    cur = nxt;
+    cur_valid = nxt_valid;
   }
 }
 

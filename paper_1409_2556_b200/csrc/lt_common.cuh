@@ -75,9 +75,10 @@ inline void check_launch(const char* name) {
 constexpr int kThreads = 256;
 
 // Block -> (item, cell block) for batched kernels launched with B * blocks_per_item blocks.
-// Default: cell blocks of one item are consecutive (each item streams through contiguous
-// memory); -DLT_ITEM_FAST puts the item index fastest instead.
-#ifndef LT_ITEM_FAST
+// Default: the item index is fastest, so the blocks of all items that touch one cell block
+// run together and share its face coefficients in L2; -DLT_CELL_FAST makes the cell blocks
+// of one item consecutive instead.
+#ifdef LT_CELL_FAST
 #define LT_ITEM_BLOCK(B, b, cb)                            \
   const int b = (int)(blockIdx.x / (gridDim.x / (B)));     \
   const int cb = (int)(blockIdx.x % (gridDim.x / (B)));
