@@ -48,8 +48,13 @@ enum { LT_MEM_HOST = 0, LT_MEM_DEVICE = 1 };
 enum { LT_VARIANT_FOM = 0, LT_VARIANT_GMRES = 1 };
 /* SolverKind (forward.hpp:16) */
 enum { LT_SOLVER_SINGLE = 0, LT_SOLVER_FLEXIBLE = 1, LT_SOLVER_DIRECT = 2 };
-/* Discretisations: FD_CELL = cell-centred finite volume (BASELINE configs). */
-enum { LT_GRID_FD_CELL = 0 };
+/* Discretisations:
+ *   FD_CELL = cell-centred finite volume (BASELINE configs), per-cell fields;
+ *   P1_TRI  = the reference's own P1 FEM on build_mesh(n, L) (mesh.cpp:14-52,
+ *             assembly.cpp:24-113): shape[0] = n_per_side nodes, h = L/(n-1), per-element
+ *             fields (element 2c lower / 2c+1 upper triangle of cell c), unknowns = interior
+ *             nodes in ascending node order (the reference's free dofs). */
+enum { LT_GRID_FD_CELL = 0, LT_GRID_P1_TRI = 1 };
 
 typedef struct lt_ctx_s* lt_ctx;
 typedef struct lt_pencil_s* lt_pencil;
@@ -109,6 +114,8 @@ lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* l
                                 const double* log_storativity, int mem, lt_pencil* out);
 lt_status lt_pencil_destroy(lt_pencil p);
 int64_t lt_pencil_rows(lt_pencil p);
+/* Number of per-parameter cells of the log fields: cells (FD) or elements (P1). */
+int64_t lt_pencil_parameters(lt_pencil p);
 int lt_pencil_levels(lt_pencil p);
 
 /* (K + z M) x, (K + conj(z) M) x, M x for n_rhs RHS (shifted_solver.cpp:109-118). */

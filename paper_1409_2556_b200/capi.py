@@ -29,6 +29,7 @@ LT_SOLVER_SINGLE = 0
 LT_SOLVER_FLEXIBLE = 1
 LT_SOLVER_DIRECT = 2
 LT_GRID_FD_CELL = 0
+LT_GRID_P1_TRI = 1
 
 
 class LtComplex(C.Structure):
@@ -99,6 +100,7 @@ SIGNATURES = {
     "lt_pencil_create_grid": (I, [P, C.POINTER(LtGrid), PD, PD, I, C.POINTER(P)]),
     "lt_pencil_destroy": (I, [P]),
     "lt_pencil_rows": (I64, [P]),
+    "lt_pencil_parameters": (I64, [P]),
     "lt_pencil_levels": (I, [P]),
     "lt_pencil_apply": (I, [P, LtComplex, PC, PC, I, I]),
     "lt_pencil_apply_adjoint": (I, [P, LtComplex, PC, PC, I, I]),

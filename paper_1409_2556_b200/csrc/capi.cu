@@ -263,16 +263,25 @@ lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* l
                                 int mem, lt_pencil* out) {
   return guard([&] {
     LT_REQUIRE(ctx && grid && out, "lt_pencil_create_grid: null argument");
-    LT_REQUIRE(grid->kind == LT_GRID_FD_CELL, "lt_pencil_create_grid: unsupported grid kind");
-    LT_REQUIRE(grid->dim == 2 || grid->dim == 3, "lt_pencil_create_grid: dim must be 2 or 3");
-    for (int d = 0; d < grid->dim; ++d) LT_REQUIRE(grid->shape[d] >= 1, "lt_pencil_create_grid: empty grid");
+    LT_REQUIRE(grid->kind == LT_GRID_FD_CELL || grid->kind == LT_GRID_P1_TRI,
+               "lt_pencil_create_grid: unsupported grid kind");
+    if (grid->kind == LT_GRID_P1_TRI) {
+      // build_mesh(n, L) (mesh.cpp:14-20): at least one interior node for a nonempty pencil
+      LT_REQUIRE(grid->dim == 2, "lt_pencil_create_grid: the P1 mesh is 2-D");
+      LT_REQUIRE(grid->shape[0] >= 3, "build_mesh: n_per_side must be at least 3 for interior unknowns");
+    } else {
+      LT_REQUIRE(grid->dim == 2 || grid->dim == 3, "lt_pencil_create_grid: dim must be 2 or 3");
+      for (int d = 0; d < grid->dim; ++d) LT_REQUIRE(grid->shape[d] >= 1, "lt_pencil_create_grid: empty grid");
+    }
     LT_REQUIRE(grid->h > 0.0, "lt_pencil_create_grid: spacing must be positive");
     LT_REQUIRE(log_kappa && log_storativity, "assemble: one kappa and one storativity value per element");
     set_device(ctx);
     auto* p = new lt_pencil_s();
     p->ctx = ctx;
     p->grid = *grid;
+    p->kind = grid->kind;
     if (grid->dim == 2) p->grid.shape[2] = 1;
+    if (grid->kind == LT_GRID_P1_TRI) p->grid.shape[1] = grid->shape[0];
     p->dim = grid->dim;
     try {
       lt::pencil_build(p, log_kappa, log_storativity, mem);
@@ -295,6 +304,15 @@ lt_status lt_pencil_destroy(lt_pencil p) {
 }
 
 int64_t lt_pencil_rows(lt_pencil p) { return p ? p->n : -1; }
+
+int64_t lt_pencil_parameters(lt_pencil p) {
+  if (!p) return -1;
+  if (p->kind == LT_GRID_P1_TRI) {
+    const int64_t nc = p->grid.shape[0] - 1;
+    return 2 * nc * nc;
+  }
+  return p->n;
+}
 int lt_pencil_levels(lt_pencil p) { return p ? (int)p->levels.size() : -1; }
 
 lt_status lt_pencil_apply(lt_pencil p, lt_complex z, const lt_complex* x, lt_complex* y, int n_rhs, int mem) {
@@ -486,7 +504,7 @@ lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out, do
     check_pencil(p);
     LT_REQUIRE(exp, "null experiment");
     set_device(p->ctx);
-    const int64_t n_param = exp->include_storativity ? 2 * p->n : p->n;
+    const int64_t n_param = exp->include_storativity ? 2 * lt_pencil_parameters(p) : lt_pencil_parameters(p);
     const int pairs = exp->n_src * exp->n_rec;
     std::vector<double> slice(jac_out ? (size_t)pairs * n_param : 0), pred(pairs);
     for (int t = 0; t < exp->n_times; ++t) {

@@ -229,6 +229,116 @@ __global__ void __launch_bounds__(kT, 2) jacobian_kernel(LevelView L, const doub
   }
 }
 
+// P1 rows (sensitivity_row_conductivity / _storativity, jacobian.cpp:57-125) on the node
+// grid of build_mesh: per element e (2c lower (a,b,c), 2c+1 upper (a,c,d) of cell c)
+//   J_k[e] = 2 Re sum_k w_k (kappa_e / 2) (D0 phi D0 psi + D1 phi D1 psi)
+//     (exact P1 gradients: area h^2/2, grad = edge differences / h)
+//   J_S[e] = 2 Re sum_k w_k z_k (S_e h^2 / 24) ((sum phi)(sum psi) + sum_i phi_i psi_i)
+//     (exact P1 product integral area/12 sum (1 + d_ij) phi_i psi_j)
+// Dirichlet nodes carry zero.  A CTA owns TC cells (2 TC elements) of one row.
+__global__ void __launch_bounds__(kT, 2) jacobian_p1_kernel(int nx, double h2, const double* __restrict__ kappa,
+                                                            const double* __restrict__ stor,
+                                                            const double2* __restrict__ fields, int n_src, int n_rec,
+                                                            int ns, const double2* __restrict__ w,
+                                                            const double2* __restrict__ wz, int TC, int tiles_x,
+                                                            int nsub_r, int nsub_total, double* __restrict__ Jk,
+                                                            double* __restrict__ Js, int64_t ldj) {
+  extern __shared__ double2 smem[];
+  const int n_items = n_src + n_rec;
+  const int U = 2 * TC;                                  // elements per tile
+  double2* P = smem;                                     // [4][n_src][U]
+  double2* Q = smem + (size_t)4 * n_src * U;             // [4][n_rec][U]
+  double* wt = reinterpret_cast<double*>(Q + (size_t)4 * n_rec * U);  // [2][U]: kappa_e/2, S_e h^2/24
+  const int nc = nx + 1;
+  const int64_t n = (int64_t)nx * nx;
+  const int cj = blockIdx.x / tiles_x;
+  const int ci0 = (blockIdx.x % tiles_x) * TC;
+  const int ncell = min(TC, nc - ci0);
+  const int tid = threadIdx.x;
+  const int c = tid % U;
+  const int sub = tid / U;
+  const bool owner = sub < nsub_total && (c >> 1) < ncell;
+  const int s0 = owner ? (sub / nsub_r) * SB : 0;
+  const int r0 = owner ? (sub % nsub_r) * RB : 0;
+  if (tid < U) {
+    const int ci = ci0 + (tid >> 1);
+    const int64_t e = 2 * ((int64_t)cj * nc + ci) + (tid & 1);
+    wt[tid] = (tid >> 1) < ncell ? 0.5 * kappa[e] : 0.0;
+    wt[U + tid] = (tid >> 1) < ncell ? stor[e] * h2 / 24.0 : 0.0;
+  }
+  __syncthreads();
+  auto nodev = [&](const double2* fld, int I, int J) {
+    return (I >= 1 && I <= nx && J >= 1 && J <= nx) ? fld[(int64_t)(J - 1) * nx + (I - 1)] : make_double2(0.0, 0.0);
+  };
+  for (int phase = 0; phase < (Js ? 2 : 1); ++phase) {
+    const int nstage = phase == 0 ? 2 : 4;
+    double acc[SB][RB];
+#pragma unroll
+    for (int i = 0; i < SB; ++i)
+#pragma unroll
+      for (int q = 0; q < RB; ++q) acc[i][q] = 0.0;
+    for (int k = 0; k < ns; ++k) {
+      const double2 wk = phase == 0 ? w[k] : wz[k];
+      for (int e = tid; e < n_items * TC; e += blockDim.x) {
+        const int it = e / TC, cc = e % TC;
+        double2 v[2][4];
+        if (cc < ncell) {
+          const double2* fld = fields + ((int64_t)it * ns + k) * n;
+          const int ci = ci0 + cc;
+          const double2 fa = nodev(fld, ci, cj), fb = nodev(fld, ci + 1, cj);
+          const double2 fc = nodev(fld, ci + 1, cj + 1), fd = nodev(fld, ci, cj + 1);
+          if (phase == 0) {
+            v[0][0] = csub(fb, fa); v[0][1] = csub(fc, fb);  // lower (a, b, c)
+            v[1][0] = csub(fc, fd); v[1][1] = csub(fd, fa);  // upper (a, c, d)
+          } else {
+            v[0][0] = cadd(cadd(fa, fb), fc); v[0][1] = fa; v[0][2] = fb; v[0][3] = fc;
+            v[1][0] = cadd(cadd(fa, fc), fd); v[1][1] = fa; v[1][2] = fc; v[1][3] = fd;
+          }
+        } else {
+          for (int q = 0; q < 4; ++q) v[0][q] = v[1][q] = make_double2(0.0, 0.0);
+        }
+        for (int el = 0; el < 2; ++el) {
+          const int u = 2 * cc + el;
+          for (int f = 0; f < nstage; ++f) {
+            if (it < n_src) P[((size_t)f * n_src + it) * U + u] = cscale(cmul(wk, v[el][f]), wt[phase * U + u]);
+            else Q[((size_t)f * n_rec + (it - n_src)) * U + u] = v[el][f];
+          }
+        }
+      }
+      __syncthreads();
+      if (owner) {
+#pragma unroll 1
+        for (int f = 0; f < nstage; ++f) {
+          double2 pv[SB];
+#pragma unroll
+          for (int i = 0; i < SB; ++i)
+            pv[i] = (s0 + i < n_src) ? P[((size_t)f * n_src + s0 + i) * U + c] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < RB; ++q) {
+            const double2 qv = (r0 + q < n_rec) ? Q[((size_t)f * n_rec + r0 + q) * U + c] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < SB; ++i) acc[i][q] = fma(pv[i].x, qv.x, fma(-pv[i].y, qv.y, acc[i][q]));
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (owner) {
+      double* Jout = phase == 0 ? Jk : Js;
+      const int64_t e = 2 * ((int64_t)cj * nc + ci0 + (c >> 1)) + (c & 1);
+#pragma unroll
+      for (int i = 0; i < SB; ++i) {
+        if (s0 + i >= n_src) continue;
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+          if (r0 + q >= n_rec) continue;
+          Jout[((int64_t)(s0 + i) * n_rec + (r0 + q)) * ldj + e] = 2.0 * acc[i][q];
+        }
+      }
+    }
+  }
+}
+
 struct PointSet {
   std::vector<int64_t> idx;  // n_pts * 8
   std::vector<double> w;
@@ -563,6 +673,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   LT_REQUIRE(t >= 0 && t < ex.n_times, "jacobian_slice: time index out of range");
   LT_REQUIRE(ex.n_quad >= 4 && ex.n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
   LT_REQUIRE(ex.times[t] > 0.0, "build_contour: time must be positive");
+  TraceScope trace_all(ctx, "jacobian_slice", t);
   const int ns = ex.n_quad / 2;
   std::vector<cd> nodes, weights;
   talbot_build(ex.n_quad, ex.times[t], ex.contour, nullptr, &nodes, nullptr, &weights);
@@ -600,7 +711,10 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   }
   std::vector<std::vector<cd>> shifts(B, nodes);
   OuterResult res;
-  solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
+  {
+    TraceScope tr(ctx, "  solve_families", B);
+    solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
+  }
   // forward failures first (jacobian.cpp:214-218), then adjoint
   {
     OuterResult* r = &res;
@@ -623,7 +737,10 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
   LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
   DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n, st);
-  expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>());
+  {
+    TraceScope tr(ctx, "  expand", B);
+    expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>());
+  }
   res.U.clear();  // free the bases before the slice
 
   std::vector<double2> w(ns), wz(ns);
@@ -635,7 +752,39 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   LT_CUDA(cudaMemcpyAsync(dw.get(), w.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
   LT_CUDA(cudaMemcpyAsync(dw.as<double2>() + ns, wz.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
 
-  if (jac_out) {
+  if (jac_out && p->kind == LT_GRID_P1_TRI) {
+    TraceScope tr(ctx, "  jacobian_p1", B);
+    const int nx = p->levels[0]->nx, nc = nx + 1;
+    const int64_t nelem = 2 * (int64_t)nc * nc;
+    const int64_t n_param = ex.include_storativity ? 2 * nelem : nelem;
+    double* J = jac_out;
+    DeviceBuffer jtmp;
+    if (mem != LT_MEM_DEVICE) {
+      jtmp.allocate(sizeof(double) * (size_t)n_src * n_rec * n_param, st);
+      J = jtmp.as<double>();
+    }
+    const int nsub_r = (n_rec + RB - 1) / RB;
+    const int nsub_total = ((n_src + SB - 1) / SB) * nsub_r;
+    LT_REQUIRE(nsub_total <= kT / 2, "jacobian: too many source/receiver blocks for one CTA (n_src*n_rec too large)");
+    int TC = std::max(1, kT / (2 * nsub_total));
+    TC = std::min(TC, nc);
+    auto smem_for = [&](int tc) { return sizeof(double2) * (size_t)4 * B * 2 * tc + sizeof(double) * 4 * tc; };
+    while (TC > 1 && smem_for(TC) > 110 * 1024) TC /= 2;
+    const size_t smem = smem_for(TC);
+    const int tiles_x = (nc + TC - 1) / TC;
+    LT_CUDA(cudaFuncSetAttribute(jacobian_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const double h = p->grid.h;
+    const double bytes = (double)n * 16.0 * ns * B + (double)nelem * 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1);
+    launch(ctx, "jacobian", bytes, [&] {
+      jacobian_p1_kernel<<<(unsigned)(tiles_x * (int64_t)nc), kT, smem, st>>>(
+          nx, h * h, p->kappa.as<double>(), p->storativity.as<double>(), fields.as<double2>(), n_src, n_rec, ns,
+          dw.as<double2>(), dw.as<double2>() + ns, TC, tiles_x, nsub_r, nsub_total, J,
+          ex.include_storativity ? J + nelem : nullptr, n_param);
+    });
+    if (mem != LT_MEM_DEVICE)
+      LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
+  } else if (jac_out) {
+    TraceScope tr(ctx, "  jacobian", B);
     const int64_t n_param = ex.include_storativity ? 2 * n : n;
     double* J = jac_out;
     DeviceBuffer jtmp;

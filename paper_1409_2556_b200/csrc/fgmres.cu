@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(kT) mass_multidot(LevelView L, State S, int j,
   double2 s = make_double2(0.0, 0.0);
   if (in) {
     s = cscale(u[b * L.n + a], __ldg(L.M + a));
+    if (L.Mx) s = cadd(s, mass_off(L, u + b * L.n, a, (int)(a % L.nx), (int)(a / L.nx)));  // P1 (2-D)
     s_out[b * L.n + a] = s;
   }
   double2* pb = part + (int64_t)b * (j + 2) * S.nblk;
@@ -391,7 +392,8 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
         gather<DIM>(L, ub, a, i, jj, kk, off, dk);
         const double2 ua = ub[a];
         const double2 Ku = csub(cscale(ua, dk), off);
-        const double2 Mu = cscale(ua, mval);
+        double2 Mu = cscale(ua, mval);
+        if (L.Mx) Mu = cadd(Mu, mass_off(L, ub, a, i, jj));
 #pragma unroll
         for (int q = 0; q < KC; ++q) {
           if (q < nc) {

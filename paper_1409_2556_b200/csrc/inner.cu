@@ -826,6 +826,110 @@ __global__ void __launch_bounds__(kT) scalar_kernel(int op, Batch bt, const void
   }
 }
 
+// ---- P1 node-grid multigrid (2-D, vertex-centred) ---------------------------------------
+// 7-point operator A = K + tau M (K: 5-point edges, M: E/W/N/S/NE/SW couplings); (i + j) % 3
+// is a valid colouring (no two same-colour nodes are coupled), so each colour is updated in
+// place without races.  Prolongation = linear interpolation on the nested coarse triangles,
+// restriction = its transpose, coarse operators = P1 assembly of the averaged element fields.
+template <class R>
+__device__ __forceinline__ typename CT<R>::V p1_offsum(const LevelViewT<R>& L, const typename CT<R>::V* u, int64_t a,
+                                                       int i, int j, R tr, R ti, R& dk) {
+  // returns sum_b T_ab u_b - tau sum_b M_ab u_b (the negated off-diagonal action of A)
+  using V = typename CT<R>::V;
+  const int64_t ex = (int64_t)j * (L.nx + 1) + i, ey = (int64_t)j * L.nx + i;
+  const R tw = L.Tx[ex], te = L.Tx[ex + 1], ts = L.Ty[ey], tn = L.Ty[ey + L.nx];
+  dk = tw + te + ts + tn;
+  V k{0, 0};
+  if (i > 0) k = vadd(k, vscale(u[a - 1], tw));
+  if (i < L.nx - 1) k = vadd(k, vscale(u[a + 1], te));
+  if (j > 0) k = vadd(k, vscale(u[a - L.nx], ts));
+  if (j < L.ny - 1) k = vadd(k, vscale(u[a + L.nx], tn));
+  const V mo = mass_off(L, u, a, i, j);
+  return V{k.x - (tr * mo.x - ti * mo.y), k.y - (tr * mo.y + ti * mo.x)};
+}
+
+template <class R>
+__global__ void __launch_bounds__(kT) p1_gs_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                   const typename CT<R>::V* __restrict__ f, typename CT<R>::V* x,
+                                                   int color, int zero_init) {
+  using V = typename CT<R>::V;
+  TILE_PROLOGUE(L);
+  if (!in) return;
+  V* xb = x + (int64_t)b * L.n;
+  const bool mine = (i + j) % 3 == color;
+  if (zero_init && !mine) {
+    xb[a] = vzero<V>();
+    return;
+  }
+  if (!mine) return;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  R dk;
+  V o = f[(int64_t)b * L.n + a];
+  if (zero_init) {
+    const int64_t ex = (int64_t)j * (L.nx + 1) + i, ey = (int64_t)j * L.nx + i;
+    dk = L.Tx[ex] + L.Tx[ex + 1] + L.Ty[ey] + L.Ty[ey + L.nx];
+  } else {
+    o = vadd(o, p1_offsum<R>(L, xb, a, i, j, tr, ti, dk));
+  }
+  xb[a] = diag_solve_r<R, V>(dk, L.M[a], tr, ti, o);
+}
+
+template <class R>
+__global__ void __launch_bounds__(kT) p1_residual_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                         const typename CT<R>::V* __restrict__ f,
+                                                         const typename CT<R>::V* __restrict__ x,
+                                                         typename CT<R>::V* __restrict__ r) {
+  using V = typename CT<R>::V;
+  TILE_PROLOGUE(L);
+  if (!in) return;
+  const V* xb = x + (int64_t)b * L.n;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  R dk;
+  const V o = p1_offsum<R>(L, xb, a, i, j, tr, ti, dk);
+  const R mm = L.M[a];
+  const R dr = dk + tr * mm, di = ti * mm;
+  const V xa = xb[a];
+  const V ax = V{dr * xa.x - di * xa.y - o.x, dr * xa.y + di * xa.x - o.y};
+  r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
+}
+
+// f_c = P^T r: coarse node C = fine free (2ic+1, 2jc+1) collects itself and 1/2 of its
+// E/W/N/S and NE/SW fine neighbours (the fine nodes interpolating from C).
+template <class R>
+__global__ void __launch_bounds__(kT) p1_restrict_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, Batch bt,
+                                                         const typename CT<R>::V* __restrict__ rf,
+                                                         typename CT<R>::V* __restrict__ fc) {
+  using V = typename CT<R>::V;
+  TILE_PROLOGUE(Lc);
+  if (!in) return;
+  const V* rb = rf + (int64_t)b * Lf.n;
+  const int fi = 2 * i + 1, fj = 2 * j + 1;
+  const int64_t c = (int64_t)fj * Lf.nx + fi;
+  V s = vadd(vadd(vadd(rb[c - 1], rb[c + 1]), vadd(rb[c - Lf.nx], rb[c + Lf.nx])),
+             vadd(rb[c + Lf.nx + 1], rb[c - Lf.nx - 1]));
+  fc[(int64_t)b * Lc.n + a] = vadd(rb[c], vscale(s, R(0.5)));
+}
+
+template <class R>
+__global__ void __launch_bounds__(kT) p1_prolong_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, Batch bt,
+                                                        const typename CT<R>::V* __restrict__ ec,
+                                                        typename CT<R>::V* __restrict__ xf) {
+  using V = typename CT<R>::V;
+  TILE_PROLOGUE(Lf);
+  if (!in) return;
+  const V* eb = ec + (int64_t)b * Lc.n;
+  auto cval = [&](int Ic, int Jc) {  // coarse node coordinates; Dirichlet nodes are zero
+    return (Ic >= 1 && Ic <= Lc.nx && Jc >= 1 && Jc <= Lc.ny) ? eb[(int64_t)(Jc - 1) * Lc.nx + (Ic - 1)] : vzero<V>();
+  };
+  const int I = i + 1, J = j + 1;
+  V v;
+  if ((I & 1) == 0 && (J & 1) == 0) v = cval(I >> 1, J >> 1);
+  else if ((J & 1) == 0) v = vscale(vadd(cval(I >> 1, J >> 1), cval((I + 1) >> 1, J >> 1)), R(0.5));
+  else if ((I & 1) == 0) v = vscale(vadd(cval(I >> 1, J >> 1), cval(I >> 1, (J + 1) >> 1)), R(0.5));
+  else v = vscale(vadd(cval(I >> 1, J >> 1), cval((I + 1) >> 1, (J + 1) >> 1)), R(0.5));
+  xf[(int64_t)b * Lf.n + a] = vadd(xf[(int64_t)b * Lf.n + a], v);
+}
+
 // ---- V-cycle driver --------------------------------------------------------------------
 template <class R>
 LevelViewT<R> mg_view(lt_pencil p, int l);
@@ -848,6 +952,31 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   const double vb = sizeof(V), rb = sizeof(R);
   const double cell_bytes = (double)L.n * Bc;
   const double coef = (double)L.n * rb * (DIM + 1);
+  if (p->kind == LT_GRID_P1_TRI && l < last) {
+    // P1: symmetric 3-colour Gauss-Seidel V-cycle on the node grid
+    LevelViewT<R> Lc = mg_view<R>(p, l + 1);
+    const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
+    const double cb6 = coef + (double)L.n * rb * 3;  // + the three mass-coupling arrays
+    for (int c = 0; c < 3; ++c)
+      launch(ctx, "mg_smooth", cell_bytes * 3 * vb + cb6, [&] {
+        p1_gs_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], c, c == 0);
+      });
+    launch(ctx, "mg_residual", cell_bytes * 3 * vb + cb6, [&] {
+      p1_residual_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+    });
+    launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
+      p1_restrict_kernel<R><<<(unsigned)Lc.ntiles * Bc, kT, 0, st>>>(L, Lc, bt, Rr[l], F[l + 1]);
+    });
+    const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr);
+    launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+      p1_prolong_kernel<R><<<grid, kT, 0, st>>>(L, Lc, bt, ec, X[l]);
+    });
+    for (int c = 2; c >= 0; --c)
+      launch(ctx, "mg_smooth", cell_bytes * 3 * vb + cb6, [&] {
+        p1_gs_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], c, 0);
+      });
+    return X[l];
+  }
   if (l == last) {
     dim3 g(blocks_for(L.n, kT / 32), Bc);
     launch(ctx, "mg_coarse_solve", cell_bytes * 2 * vb, [&] {

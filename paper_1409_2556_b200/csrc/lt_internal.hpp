@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
@@ -105,6 +108,34 @@ inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f
   check_launch(name);
 }
 
+// ---- host-side phase tracing (LT_TRACE=1): synchronising wall-clock scopes on stderr ----
+inline bool trace_on() {
+  static const bool on = std::getenv("LT_TRACE") != nullptr;
+  return on;
+}
+
+class TraceScope {
+ public:
+  TraceScope(lt_ctx ctx, const char* what, int arg = -1) : ctx_(ctx), what_(what), arg_(arg) {
+    if (trace_on()) {
+      cudaStreamSynchronize(ctx_->stream);
+      t0_ = std::chrono::steady_clock::now();
+    }
+  }
+  ~TraceScope() {
+    if (!trace_on()) return;
+    cudaStreamSynchronize(ctx_->stream);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+    std::fprintf(stderr, "[lt] %-22s %4d %10.3f ms\n", what_, arg_, ms);
+  }
+
+ private:
+  lt_ctx ctx_;
+  const char* what_;
+  int arg_;
+  std::chrono::steady_clock::time_point t0_{};
+};
+
 // ---- discretisation levels -----------------------------------------------------------
 // Cell-centred FD level: face transmissibilities including the Dirichlet boundary faces,
 //   Tx[(k*ny + j)*(nx+1) + i]  face between cells i-1 and i (i = 0, nx: boundary)
@@ -118,14 +149,23 @@ struct Level {
   double* Ty = nullptr;
   double* Tz = nullptr;
   double* M = nullptr;
+  // P1 only: positive mass couplings of the 7-point M (E/W edges like Tx, N/S like Ty, the
+  // NE neighbour stored at the node); null for FD (diagonal M)
+  double* Mx = nullptr;
+  double* My = nullptr;
+  double* Md = nullptr;
   DeviceBuffer storage;
   // FP32 copy of the same arrays (same layout) for the mixed-precision V-cycle
   float* Tx32 = nullptr;
   float* Ty32 = nullptr;
   float* Tz32 = nullptr;
   float* M32 = nullptr;
+  float* Mx32 = nullptr;
+  float* My32 = nullptr;
+  float* Md32 = nullptr;
   DeviceBuffer storage32;
-  int agg[3] = {1, 1, 1};  // aggregation to the next coarser level
+  DeviceBuffer elem;       // P1: per-element kappa then S on this level (coarsening input)
+  int agg[3] = {1, 1, 1};  // aggregation to the next coarser level (FD)
 };
 
 // Device view of a level passed by value to kernels (R = double: the operator; R = float:
@@ -140,6 +180,9 @@ struct LevelViewT {
   const R* M;
   // 256-thread (x, y) tiles: tw x th cells, tw a power of two (tws = log2 tw)
   int tw, tws, th, tiles_x, tiles_y, ntiles;
+  const R* Mx;  // P1 mass couplings (null for FD)
+  const R* My;
+  const R* Md;
 };
 using LevelView = LevelViewT<double>;
 using LevelView32 = LevelViewT<float>;
@@ -164,6 +207,7 @@ struct lt_pencil_s {
   lt_ctx ctx = nullptr;
   lt_grid grid{};
   int dim = 2;
+  int kind = LT_GRID_FD_CELL;
   int64_t n = 0;
   std::vector<std::unique_ptr<lt::Level>> levels;
   std::vector<std::unique_ptr<lt::CoarseFactor>> factors;  // keyed by exact tau

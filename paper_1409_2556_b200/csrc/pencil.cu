@@ -170,6 +170,17 @@ __global__ void dense_coarse(LevelView L, double2 tau, double2* __restrict__ aug
         if (c == r - plane && k > 0) v.x = -L.Tz[r];
         if (c == r + plane && k < L.nz - 1) v.x = -L.Tz[r + plane];
       }
+      if (L.Mx) {  // P1: tau * the off-diagonal mass couplings
+        double mo = 0.0;
+        if (c == r - 1 && i > 0) mo = L.Mx[fx(L, i, j, k)];
+        if (c == r + 1 && i < L.nx - 1) mo = L.Mx[fx(L, i + 1, j, k)];
+        if (c == r - L.nx && j > 0) mo = L.My[fy(L, i, j, k)];
+        if (c == r + L.nx && j < L.ny - 1) mo = L.My[fy(L, i, j + 1, k)];
+        if (c == r + L.nx + 1 && i < L.nx - 1 && j < L.ny - 1) mo = L.Md[r];
+        if (c == r - L.nx - 1 && i > 0 && j > 0) mo = L.Md[c];
+        v.x += tau.x * mo;
+        v.y += tau.y * mo;
+      }
     }
   }
   aug[idx] = v;
@@ -249,14 +260,14 @@ LevelView lt_pencil_view(const lt_pencil_s* p, int l) {
   const int tiles_x = (L.nx + tw - 1) / tw;
   const int tiles_y = (L.ny + th - 1) / th;
   return LevelView{L.nx, L.ny, L.nz, p->dim, L.n, L.Tx, L.Ty, L.Tz, L.M,
-                   tw, tws, th, tiles_x, tiles_y, tiles_x * tiles_y * L.nz};
+                   tw, tws, th, tiles_x, tiles_y, tiles_x * tiles_y * L.nz, L.Mx, L.My, L.Md};
 }
 
 LevelView32 lt_pencil_view32(const lt_pencil_s* p, int l) {
   const LevelView v = lt_pencil_view(p, l);
   const Level& L = *p->levels[l];
   return LevelView32{v.nx, v.ny, v.nz, v.dim, v.n, L.Tx32, L.Ty32, L.Tz32, L.M32,
-                     v.tw, v.tws, v.th, v.tiles_x, v.tiles_y, v.ntiles};
+                     v.tw, v.tws, v.th, v.tiles_x, v.tiles_y, v.ntiles, L.Mx32, L.My32, L.Md32};
 }
 
 namespace {
@@ -286,7 +297,182 @@ static void alloc_level(Level& L, int dim, cudaStream_t s) {
   L.M = base + nfx + nfy + nfz;
 }
 
+// ---- P1 triangle discretisation (the reference's own operator) -------------------------
+// Node grid of build_mesh(n, L) (mesh.cpp:14-52): cell c = cj*nc + ci has the lower element
+// 2c = (a, b, c') and the upper element 2c+1 = (a, c', d); free unknowns are the interior
+// nodes (I, J) = (i+1, j+1), i, j < n-2.  Exact P1 integrals (assembly.cpp:24-41) per edge:
+//   K edge = (kappa_T1 + kappa_T2)/2 over the two triangles sharing it (hypotenuse: 0),
+//   M edge = h^2 (S_T1 + S_T2)/24, M node = h^2/12 sum of the six triangles' S,
+// laid out like the FD faces (Tx: E/W edges, Ty: N/S edges) plus Mx, My and Md (NE).
+namespace {
+
+__device__ __forceinline__ int64_t elem_lo(int ci, int cj, int nc) { return 2 * ((int64_t)cj * nc + ci); }
+
+__global__ void p1_assemble_x(const double* __restrict__ ek, const double* __restrict__ es, int nx, int ny,
+                              double h2, double* __restrict__ Tx, double* __restrict__ Mx) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)(nx + 1) * ny) return;
+  const int i = (int)(e % (nx + 1)), j = (int)(e / (nx + 1));
+  const int nc = nx + 1, I = i, J = j + 1;  // edge (I, J)-(I+1, J)
+  const int64_t lo = elem_lo(I, J, nc), up = elem_lo(I, J - 1, nc) + 1;
+  Tx[e] = 0.5 * (ek[lo] + ek[up]);
+  Mx[e] = h2 * (es[lo] + es[up]) / 24.0;
+}
+
+__global__ void p1_assemble_y(const double* __restrict__ ek, const double* __restrict__ es, int nx, int ny,
+                              double h2, double* __restrict__ Ty, double* __restrict__ My) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nx * (ny + 1)) return;
+  const int i = (int)(e % nx), j = (int)(e / nx);
+  const int nc = nx + 1, I = i + 1, J = j;  // edge (I, J)-(I, J+1)
+  const int64_t up = elem_lo(I, J, nc) + 1, lo = elem_lo(I - 1, J, nc);
+  Ty[e] = 0.5 * (ek[up] + ek[lo]);
+  My[e] = h2 * (es[up] + es[lo]) / 24.0;
+}
+
+__global__ void p1_assemble_node(const double* __restrict__ es, int nx, int ny, double h2, double* __restrict__ M,
+                                 double* __restrict__ Md) {
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= (int64_t)nx * ny) return;
+  const int i = (int)(a % nx), j = (int)(a / nx);
+  const int nc = nx + 1, I = i + 1, J = j + 1;
+  const double s = es[elem_lo(I, J, nc)] + es[elem_lo(I, J, nc) + 1] + es[elem_lo(I - 1, J, nc)] +
+                   es[elem_lo(I - 1, J - 1, nc)] + es[elem_lo(I - 1, J - 1, nc) + 1] + es[elem_lo(I, J - 1, nc) + 1];
+  M[a] = h2 * s / 12.0;
+  Md[a] = h2 * (es[elem_lo(I, J, nc)] + es[elem_lo(I, J, nc) + 1]) / 24.0;  // hypotenuse to (I+1, J+1)
+}
+
+// Coarse element fields: the mean over the four fine triangles inside each coarse triangle
+// (exact Galerkin P^T K P for the nested P1 spaces; the mass is approximated the same way).
+__global__ void p1_coarsen_elem(const double* __restrict__ ef, int ncf, double* __restrict__ ec, int ncc) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= (int64_t)ncc * ncc) return;
+  const int Ci = (int)(c % ncc), Cj = (int)(c / ncc);
+  const int fi = 2 * Ci, fj = 2 * Cj;
+  const double lo = ef[elem_lo(fi, fj, ncf)] + ef[elem_lo(fi + 1, fj, ncf)] + ef[elem_lo(fi + 1, fj, ncf) + 1] +
+                    ef[elem_lo(fi + 1, fj + 1, ncf)];
+  const double up = ef[elem_lo(fi, fj, ncf) + 1] + ef[elem_lo(fi, fj + 1, ncf)] + ef[elem_lo(fi, fj + 1, ncf) + 1] +
+                    ef[elem_lo(fi + 1, fj + 1, ncf) + 1];
+  ec[2 * c] = 0.25 * lo;
+  ec[2 * c + 1] = 0.25 * up;
+}
+
+}  // namespace
+
+static void alloc_level_p1(Level& L, cudaStream_t s) {
+  L.nz = 1;
+  L.n = (int64_t)L.nx * L.ny;
+  const int64_t nfx = (int64_t)(L.nx + 1) * L.ny, nfy = (int64_t)L.nx * (L.ny + 1);
+  L.storage.allocate(sizeof(double) * 2 * (nfx + nfy + L.n), s);
+  double* base = L.storage.as<double>();
+  L.Tx = base;
+  L.Ty = base + nfx;
+  L.Tz = nullptr;
+  L.M = base + nfx + nfy;
+  L.Mx = L.M + L.n;
+  L.My = L.Mx + nfx;
+  L.Md = L.My + nfy;
+  const int64_t nelem = 2 * (int64_t)(L.nx + 1) * (L.nx + 1);
+  L.elem.allocate(sizeof(double) * 2 * nelem, s);
+}
+
+static void assemble_p1(lt_ctx ctx, Level& L, double h) {
+  cudaStream_t st = ctx->stream;
+  const int64_t nelem = 2 * (int64_t)(L.nx + 1) * (L.nx + 1);
+  const double* ek = L.elem.as<double>();
+  const double* es = ek + nelem;
+  const double h2 = h * h;
+  const int nx = L.nx, ny = L.ny;
+  Level* Lp = &L;
+  launch(ctx, "assemble", 0.0, [&] {
+    p1_assemble_x<<<blocks_for((int64_t)(nx + 1) * ny, kThreads), kThreads, 0, st>>>(ek, es, nx, ny, h2, Lp->Tx, Lp->Mx);
+  });
+  launch(ctx, "assemble", 0.0, [&] {
+    p1_assemble_y<<<blocks_for((int64_t)nx * (ny + 1), kThreads), kThreads, 0, st>>>(ek, es, nx, ny, h2, Lp->Ty, Lp->My);
+  });
+  launch(ctx, "assemble", 0.0, [&] {
+    p1_assemble_node<<<blocks_for((int64_t)nx * ny, kThreads), kThreads, 0, st>>>(es, nx, ny, h2, Lp->M, Lp->Md);
+  });
+}
+
+static void make_fp32_copies(lt_pencil p) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  for (auto& lv : p->levels) {
+    Level& Lv = *lv;
+    const int64_t cnt = (int64_t)(Lv.storage.bytes() / sizeof(double));
+    Lv.storage32.allocate(sizeof(float) * cnt, st);
+    float* base = Lv.storage32.as<float>();
+    const double* src = Lv.storage.as<double>();
+    Lv.Tx32 = base + (Lv.Tx - src);
+    Lv.Ty32 = base + (Lv.Ty - src);
+    Lv.Tz32 = Lv.Tz ? base + (Lv.Tz - src) : nullptr;
+    Lv.M32 = base + (Lv.M - src);
+    Lv.Mx32 = Lv.Mx ? base + (Lv.Mx - src) : nullptr;
+    Lv.My32 = Lv.My ? base + (Lv.My - src) : nullptr;
+    Lv.Md32 = Lv.Md ? base + (Lv.Md - src) : nullptr;
+    launch(ctx, "assemble", 12.0 * cnt, [&] { d2f_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(src, base, cnt); });
+  }
+}
+
+static void pencil_build_p1(lt_pencil p, const double* log_kappa, const double* log_s, int mem) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int n_per_side = p->grid.shape[0];
+  const int nc = n_per_side - 1;
+  const int64_t nelem = 2 * (int64_t)nc * nc;
+  auto fine = std::make_unique<Level>();
+  fine->nx = fine->ny = n_per_side - 2;
+  alloc_level_p1(*fine, st);
+  p->n = fine->n;
+  p->kappa.allocate(sizeof(double) * nelem, st);
+  p->storativity.allocate(sizeof(double) * nelem, st);
+  DeviceBuffer logs(sizeof(double) * 2 * nelem, st);
+  double* lk = logs.as<double>();
+  double* ls = lk + nelem;
+  auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  LT_CUDA(cudaMemcpyAsync(lk, log_kappa, sizeof(double) * nelem, kind, st));
+  LT_CUDA(cudaMemcpyAsync(ls, log_s, sizeof(double) * nelem, kind, st));
+  double* kap = p->kappa.as<double>();
+  double* sto = p->storativity.as<double>();
+  launch(ctx, "assemble", 0.0, [&] { exp_kernel<<<blocks_for(nelem, kThreads), kThreads, 0, st>>>(lk, kap, nelem); });
+  launch(ctx, "assemble", 0.0, [&] { exp_kernel<<<blocks_for(nelem, kThreads), kThreads, 0, st>>>(ls, sto, nelem); });
+  LT_CUDA(cudaMemcpyAsync(fine->elem.as<double>(), kap, sizeof(double) * nelem, cudaMemcpyDeviceToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(fine->elem.as<double>() + nelem, sto, sizeof(double) * nelem, cudaMemcpyDeviceToDevice, st));
+  double h = p->grid.h;
+  assemble_p1(ctx, *fine, h);
+  p->levels.clear();
+  p->levels.push_back(std::move(fine));
+  // vertex-centred hierarchy: n-1 intervals -> (n-1)/2 while even and >= 4
+  while (p->levels.back()->n > kMaxCoarse) {
+    Level& Fl = *p->levels.back();
+    const int ncf = Fl.nx + 1;
+    if (ncf % 2 != 0 || ncf < 4) break;
+    const int ncc = ncf / 2;
+    auto C = std::make_unique<Level>();
+    C->nx = C->ny = ncc - 1;
+    alloc_level_p1(*C, st);
+    const int64_t nef = 2 * (int64_t)ncf * ncf, nec = 2 * (int64_t)ncc * ncc;
+    const double* ef = Fl.elem.as<double>();
+    double* ecp = C->elem.as<double>();
+    for (int f = 0; f < 2; ++f)
+      launch(ctx, "coarsen", 0.0, [&] {
+        p1_coarsen_elem<<<blocks_for((int64_t)ncc * ncc, kThreads), kThreads, 0, st>>>(ef + f * nef, ncf, ecp + f * nec,
+                                                                                      ncc);
+      });
+    h *= 2.0;
+    assemble_p1(ctx, *C, h);
+    p->levels.push_back(std::move(C));
+  }
+  make_fp32_copies(p);
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
 void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int mem) {
+  if (p->kind == LT_GRID_P1_TRI) {
+    pencil_build_p1(p, log_kappa, log_s, mem);
+    return;
+  }
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int dim = p->dim;
@@ -366,18 +552,7 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
     p->levels.push_back(std::move(C));
   }
   // FP32 copies of every level for the mixed-precision V-cycle (same layout)
-  for (auto& lv : p->levels) {
-    Level& Lv = *lv;
-    const int64_t cnt = (int64_t)(Lv.storage.bytes() / sizeof(double));
-    Lv.storage32.allocate(sizeof(float) * cnt, st);
-    float* base = Lv.storage32.as<float>();
-    const double* src = Lv.storage.as<double>();
-    Lv.Tx32 = base + (Lv.Tx - src);
-    Lv.Ty32 = base + (Lv.Ty - src);
-    Lv.Tz32 = Lv.Tz ? base + (Lv.Tz - src) : nullptr;
-    Lv.M32 = base + (Lv.M - src);
-    launch(ctx, "assemble", 12.0 * cnt, [&] { d2f_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(src, base, cnt); });
-  }
+  make_fp32_copies(p);
   LT_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -434,7 +609,7 @@ __global__ void apply_kernel(LevelView L, const double2* __restrict__ taus, cons
   if (!tile_cell(L, cb, i, j, k, a)) return;
   const double2* xb = x + b * xs;
   double2 out;
-  if (MASS_ONLY) out = cscale(xb[a], L.M[a]);
+  if (MASS_ONLY) out = mass_apply(L, xb, a, i, j);
   else out = stencil_apply<DIM>(L, xb, a, i, j, k, taus[b]);
   y[b * ys + a] = out;
 }
@@ -458,7 +633,48 @@ void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2*
   });
 }
 
+// P1 barycentric weights of the containing triangle (point_source, mesh.cpp:91-125),
+// restricted to the free (interior) nodes (restrict_to_free, assembly.cpp:45-51).
+static void point_weights_p1(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count) {
+  const int n = p->grid.shape[0];
+  const double h = p->grid.h;
+  const double L = h * (n - 1);
+  const double tol = 1e-12 * L;
+  double x = point[0], y = point[1];
+  if (x < -tol || x > L + tol || y < -tol || y > L + tol)
+    throw Error(LT_ERR_INVALID_ARGUMENT, "point_source: point lies outside the domain");
+  x = std::min(std::max(x, 0.0), L);
+  y = std::min(std::max(y, 0.0), L);
+  const int ci = std::min((int)std::floor(x / h), n - 2);
+  const int cj = std::min((int)std::floor(y / h), n - 2);
+  const double xi = x / h - ci, eta = y / h - cj;
+  int nodes[3][2];
+  double ws[3];
+  if (xi >= eta) {  // lower triangle (a, b, c)
+    nodes[0][0] = ci; nodes[0][1] = cj; ws[0] = 1.0 - xi;
+    nodes[1][0] = ci + 1; nodes[1][1] = cj; ws[1] = xi - eta;
+    nodes[2][0] = ci + 1; nodes[2][1] = cj + 1; ws[2] = eta;
+  } else {  // upper triangle (a, c, d)
+    nodes[0][0] = ci; nodes[0][1] = cj; ws[0] = 1.0 - eta;
+    nodes[1][0] = ci + 1; nodes[1][1] = cj + 1; ws[1] = xi;
+    nodes[2][0] = ci; nodes[2][1] = cj + 1; ws[2] = eta - xi;
+  }
+  int c = 0;
+  for (int q = 0; q < 3; ++q) {
+    const int I = nodes[q][0], J = nodes[q][1];
+    if (ws[q] == 0.0 || I <= 0 || J <= 0 || I >= n - 1 || J >= n - 1) continue;  // Dirichlet or zero
+    idx[c] = (int64_t)(J - 1) * (n - 2) + (I - 1);
+    w[c] = ws[q];
+    ++c;
+  }
+  *count = c;
+}
+
 void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count) {
+  if (p->kind == LT_GRID_P1_TRI) {
+    point_weights_p1(p, point, idx, w, count);
+    return;
+  }
   const int dim = p->dim;
   int base[3] = {0, 0, 0};
   double frac[3] = {0, 0, 0};

@@ -83,6 +83,30 @@ __device__ __forceinline__ void gather(const LevelView& L, const double2* __rest
   off = o;
 }
 
+// P1 only (2-D node grid): off-diagonal mass coupling sum_nb M_{a,nb} u_nb over the
+// E/W/N/S edges and the NE/SW diagonal; Dirichlet neighbours contribute nothing.
+template <class R, class V>
+__device__ __forceinline__ V mass_off(const LevelViewT<R>& L, const V* __restrict__ u, int64_t a, int i, int j) {
+  V o{0, 0};
+  const int64_t ex = (int64_t)j * (L.nx + 1) + i;
+  const int64_t ey = (int64_t)j * L.nx + i;
+  if (i > 0) { const R w = L.Mx[ex]; const V v = u[a - 1]; o.x += w * v.x; o.y += w * v.y; }
+  if (i < L.nx - 1) { const R w = L.Mx[ex + 1]; const V v = u[a + 1]; o.x += w * v.x; o.y += w * v.y; }
+  if (j > 0) { const R w = L.My[ey]; const V v = u[a - L.nx]; o.x += w * v.x; o.y += w * v.y; }
+  if (j < L.ny - 1) { const R w = L.My[ey + L.nx]; const V v = u[a + L.nx]; o.x += w * v.x; o.y += w * v.y; }
+  if (i < L.nx - 1 && j < L.ny - 1) { const R w = L.Md[a]; const V v = u[a + L.nx + 1]; o.x += w * v.x; o.y += w * v.y; }
+  if (i > 0 && j > 0) { const R w = L.Md[a - L.nx - 1]; const V v = u[a - L.nx - 1]; o.x += w * v.x; o.y += w * v.y; }
+  return o;
+}
+
+// (M u)_a, including the P1 off-diagonal couplings when present
+__device__ __forceinline__ double2 mass_apply(const LevelView& L, const double2* __restrict__ u, int64_t a, int i,
+                                              int j) {
+  double2 r = cscale(u[a], __ldg(L.M + a));
+  if (L.Mx) r = cadd(r, mass_off(L, u, a, i, j));
+  return r;
+}
+
 template <int DIM>
 __device__ __forceinline__ double2 stencil_apply(const LevelView& L, const double2* __restrict__ u, int64_t a,
                                                  int i, int j, int k, double2 tau) {
@@ -91,9 +115,11 @@ __device__ __forceinline__ double2 stencil_apply(const LevelView& L, const doubl
   gather<DIM>(L, u, a, i, j, k, off, dk);
   const double m = __ldg(L.M + a);
   const double2 ua = u[a];
-  // (dk + tau m) ua - off
+  // (dk + tau m) ua - off  (+ tau * P1 mass couplings)
   const double2 d = make_double2(dk + tau.x * m, tau.y * m);
-  return csub(cmul(d, ua), off);
+  double2 r = csub(cmul(d, ua), off);
+  if (L.Mx) r = cadd(r, cmul(tau, mass_off(L, u, a, i, j)));
+  return r;
 }
 
 }  // namespace lt

@@ -36,7 +36,8 @@ from .capi import (ConvergenceError, FactorizationError, LtComplex, check, cptr,
 __all__ = [
     "ConvergenceError", "FactorizationError", "Context", "TalbotParams", "TalbotContour", "build_contour",
     "inverse_laplace_sum", "qhat_step", "PreconditionerSchedule", "single_tau_schedule",
-    "select_preconditioner_shifts", "Grid", "ShiftedPencil", "ShiftedSolveOptions", "ShiftStatus",
+    "select_preconditioner_shifts", "Grid", "Mesh2D", "build_mesh", "ShiftedPencil", "ShiftedSolveOptions",
+    "ShiftStatus",
     "FlexibleBasisState", "ShiftedSolveResult", "solve_shifted_flexible", "solve_shifted_single",
     "solve_shifted_direct", "residual_estimate", "SolverConfig", "ForwardProblem", "TimeDiagnostics",
     "HeadSolution", "solve_forward", "solve_forward_batch", "solve_adjoint_fields", "ThtExperiment",
@@ -217,6 +218,48 @@ class Grid:
     def c(self) -> capi.LtGrid:
         shp = (C.c_int * 3)(*(list(self.shape) + [1] * (3 - len(self.shape))))
         return capi.LtGrid(capi.LT_GRID_FD_CELL, self.dim, shp, float(self.h))
+
+
+@dataclass(frozen=True)
+class Mesh2D:
+    """The reference's structured P1 mesh (build_mesh, mesh.hpp:17-27 / mesh.cpp:14-52) as a
+    device pencil geometry: per-element log fields (element 2c lower, 2c+1 upper triangle of
+    cell c), unknowns = interior nodes in ascending node order (the reference's free dofs)."""
+
+    n_per_side: int
+    side_length: float
+
+    @property
+    def dim(self) -> int:
+        return 2
+
+    @property
+    def n_elements(self) -> int:
+        return 2 * (self.n_per_side - 1) ** 2
+
+    @property
+    def n_cells(self) -> int:  # parameters per log field
+        return self.n_elements
+
+    @property
+    def n_free(self) -> int:
+        return (self.n_per_side - 2) ** 2
+
+    def spacing(self) -> float:
+        return self.side_length / (self.n_per_side - 1)
+
+    def c(self) -> capi.LtGrid:
+        shp = (C.c_int * 3)(self.n_per_side, self.n_per_side, 1)
+        return capi.LtGrid(capi.LT_GRID_P1_TRI, 2, shp, float(self.spacing()))
+
+
+def build_mesh(n_per_side: int, side_length: float) -> Mesh2D:
+    """mesh.cpp:14-20 argument checks."""
+    if n_per_side < 2:
+        raise ValueError("build_mesh: n_per_side must be at least 2")
+    if not (side_length > 0.0):
+        raise ValueError("build_mesh: side length must be positive")
+    return Mesh2D(int(n_per_side), float(side_length))
 
 
 class _Factorization:
