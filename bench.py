@@ -49,14 +49,14 @@ def peaks():
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled during the timed region through
-    NVML (the library nvidia-smi uses), once per second.  The solver issues many short host
-    synchronisations; polling NVML every 200 ms (nvidia-smi -lms 200) measurably stretched
-    them, so the period is 1 s."""
+    NVML (the library nvidia-smi uses), once every 4 s.  The solver issues many short host
+    synchronisations; polling NVML every 200 ms (nvidia-smi -lms 200) stretched the step by
+    ~50% and even 1 Hz by ~18%, so the period is 4 s (several samples per timed region)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index: int, period: float = 1.0):
+    def __init__(self, index: int, period: float = 4.0):
         self.index = index
         self.period = period
         self.samples = []
@@ -255,6 +255,7 @@ def main():
     preds = np.zeros((n_t, pairs))
     lk_pin = torch.from_numpy(lk).pin_memory()
     ls_pin = torch.from_numpy(ls).pin_memory()
+    row_pin = torch.empty((n_t, n_param), dtype=torch.float64).pin_memory()
     torch.cuda.synchronize()
 
     def build(mem_host: bool):
@@ -267,16 +268,17 @@ def main():
             capi.check(lib.lt_pencil_create_grid(ctx.handle, C.byref(grid_c),
                                                  C.cast(lk_d.data_ptr(), capi.PD),
                                                  C.cast(ls_d.data_ptr(), capi.PD), capi.LT_MEM_DEVICE, C.byref(h)))
-        sums = []
         for t in range(n_t):
             capi.check(lib.lt_jacobian_slice(h, C.byref(exc), t, capi.LT_MEM_DEVICE,
                                              C.cast(J.data_ptr(), capi.PD), capi.dptr(pred)))
             preds[t] = pred
             if mem_host:
+                # the step's result read back: the first sensitivity row of every slice
                 with torch.cuda.stream(stream):
-                    sums.append(torch.linalg.vector_norm(J, dim=1).cpu().numpy())
+                    row_pin[t].copy_(J[0], non_blocking=True)
         capi.check(lib.lt_pencil_destroy(h))
-        return sums
+        if mem_host:
+            stream.synchronize()
 
     def barrier():
         if world > 1:
@@ -365,7 +367,7 @@ def main():
         "kernel_breakdown": breakdown,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n,
-                "d2h_bytes_per_step": 8 * pairs * n_t * 2},
+                "d2h_bytes_per_step": 8 * n_t * (pairs + n_param)},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

@@ -24,6 +24,12 @@ namespace lt {
 
 namespace {
 
+// LT_INNER_TRACE=1: per-item final relative residual of each inner solve (diagnostics only)
+bool inner_trace() {
+  static const bool on = std::getenv("LT_INNER_TRACE") != nullptr;
+  return on;
+}
+
 constexpr int kT = 256;
 
 #ifdef LT_MG_FP64
@@ -1137,6 +1143,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   if (active == 0) return;
 
   const double tol2 = p->inner_tol * p->inner_tol;
+  int iters_seen = 0;
   for (int b = 0; b < Bc; ++b) best[b] = bb[b];
   // z = B r ; rho = r^T z ; p = z
   const V* z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
@@ -1169,9 +1176,11 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     for (int b = 0; b < Bc; ++b) {
       if (done[b]) continue;
       if (rr[b] <= tol2 * bb[b]) { done[b] = 1; changed = true; continue; }
-      // stagnation at the rounding floor: no halving of the residual in 4 iterations
+      // stagnation at the rounding floor: within 1e4 of the tolerance and no halving of the
+      // residual in 6 iterations.  (Far from the floor COCG's residual is non-monotone on the
+      // indefinite pencils Re tau < 0 gives -- plateaus there are not stagnation.)
       if (rr[b] < 0.25 * best[b]) { best[b] = rr[b]; stall[b] = 0; }
-      else if (++stall[b] >= 4) { done[b] = 1; changed = true; }
+      else if (rr[b] <= 1e8 * tol2 * bb[b] && ++stall[b] >= 6) { done[b] = 1; changed = true; }
     }
     if (changed) {
       active = 0;
@@ -1185,8 +1194,13 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BETA, bt, partials.get(), nblk, sc); });
     launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
+    if (inner_trace()) iters_seen = it + 1;
   }
   LT_CUDA(cudaStreamSynchronize(st));
+  if (inner_trace())
+    for (int b = 0; b < Bc; ++b)
+      std::fprintf(stderr, "[inner] tau=(%.4g,%.4g) it<=%d rel=%.3e %s\n", taus_host[b].x, taus_host[b].y,
+                   iters_seen + 1, std::sqrt(rr[b] / bb[b]), rr[b] <= tol2 * bb[b] ? "ok" : "STAGNATED");
 }
 
 }  // namespace
