@@ -75,7 +75,8 @@ void* lt_ctx_stream(lt_ctx ctx);
 lt_status lt_ctx_set_profiling(lt_ctx ctx, int enabled);
 lt_status lt_ctx_reset_profile(lt_ctx ctx);
 /* Time only 1 in `every` launches of each kernel class (default 1) to keep the event
- * overhead out of long timed regions; profile entries then count the sampled launches. */
+ * overhead out of long timed regions; lt_ctx_profile then scales each class's timed
+ * launches to all of its launches (estimated totals; `launches` = all launches). */
 lt_status lt_ctx_set_profile_sampling(lt_ctx ctx, int every);
 /* Returns the number of kernel classes; fills up to `capacity` entries. name_buf holds
  * capacity*64 chars (NUL-terminated names). */

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <map>
 #include <new>
 #include <string>
 #include <vector>
@@ -196,6 +197,9 @@ int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, i
     g_err = e.what();
     return -1;
   }
+  // with 1-in-N sampling, scale the timed launches of a class to all its launches
+  std::map<std::string, int64_t> total;
+  for (const auto& kv : ctx->class_counter) total[kv.first] += kv.second;
   int i = 0;
   for (const auto& kv : ctx->profile) {
     if (i < capacity) {
@@ -203,9 +207,12 @@ int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, i
         std::strncpy(name_buf + 64 * i, kv.first.c_str(), 63);
         name_buf[64 * i + 63] = 0;
       }
-      if (total_ms) total_ms[i] = kv.second.ms;
-      if (launches) launches[i] = kv.second.launches;
-      if (algorithmic_bytes) algorithmic_bytes[i] = kv.second.bytes;
+      const int64_t timed = kv.second.launches;
+      const int64_t all = std::max<int64_t>(timed, total.count(kv.first) ? total[kv.first] : timed);
+      const double f = timed > 0 ? (double)all / (double)timed : 1.0;
+      if (total_ms) total_ms[i] = kv.second.ms * f;
+      if (launches) launches[i] = all;
+      if (algorithmic_bytes) algorithmic_bytes[i] = kv.second.bytes * f;
     }
     ++i;
   }

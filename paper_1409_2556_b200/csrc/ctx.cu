@@ -50,6 +50,22 @@ void lt_ctx_s::resolve_profile() {
 }
 
 namespace lt {
+double available_device_bytes(lt_ctx ctx) {
+  // device free memory + what the stream-ordered pool holds reserved but unused + the block
+  // cache: freed buffers stay reserved, so cudaMemGetInfo alone would shrink chunk sizes (and
+  // the batching efficiency) as a run goes on; a request the cache cannot serve drains it
+  size_t free_b = 0, total_b = 0;
+  LT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  cudaMemPool_t pool;
+  uint64_t reserved = 0, used = 0;
+  if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) {
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  }
+  cudaGetLastError();
+  return (double)free_b + (double)(reserved > used ? reserved - used : 0) + (double)cache_cached_bytes();
+}
+
 lt_ctx ctx_create(int device) {
   int count = 0;
   LT_CUDA(cudaGetDeviceCount(&count));
@@ -80,6 +96,8 @@ void ctx_destroy(lt_ctx ctx) {
     cudaEventDestroy(pe.stop);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  cache_release_stream(ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

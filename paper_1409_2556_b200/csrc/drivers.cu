@@ -549,10 +549,8 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
     for (size_t q = 0; q < (size_t)n_src * n_times * nh; ++q) shift_residuals[q] = NAN;
 
   // item chunks bounded by memory: ~ (2 maxit-columns) vectors per item
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
   const double per_item = (double)n * sizeof(double2) * 14.0;
-  const int chunk = std::max(1, (int)std::min<double>(F, 0.6 * (double)free_b / per_item));
+  const int chunk = std::max(1, (int)std::min<double>(F, 0.6 * available_device_bytes(p->ctx) / per_item));
 
   for (int f0 = 0; f0 < F; f0 += chunk) {
     const int B = std::min(chunk, F - f0);

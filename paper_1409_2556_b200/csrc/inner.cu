@@ -24,10 +24,11 @@ namespace lt {
 
 namespace {
 
-// LT_INNER_TRACE=1: per-item final relative residual of each inner solve (diagnostics only)
-bool inner_trace() {
-  static const bool on = std::getenv("LT_INNER_TRACE") != nullptr;
-  return on;
+// LT_INNER_TRACE=1: chunking of each inner solve; =2 also the per-item final relative
+// residual (diagnostics only)
+int inner_trace() {
+  static const int level = std::getenv("LT_INNER_TRACE") ? std::atoi(std::getenv("LT_INNER_TRACE")) : 0;
+  return level;
 }
 
 constexpr int kT = 256;
@@ -1144,6 +1145,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
 
   const double tol2 = p->inner_tol * p->inner_tol;
   int iters_seen = 0;
+  double sync_ms = 0.0;
+  const auto wall0 = std::chrono::steady_clock::now();
   for (int b = 0; b < Bc; ++b) best[b] = bb[b];
   // z = B r ; rho = r^T z ; p = z
   const V* z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
@@ -1171,7 +1174,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
     LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    {
+      const auto s0 = std::chrono::steady_clock::now();
+      LT_CUDA(cudaStreamSynchronize(st));
+      if (inner_trace())
+        sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
+    }
     bool changed = false;
     for (int b = 0; b < Bc; ++b) {
       if (done[b]) continue;
@@ -1198,6 +1206,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
   LT_CUDA(cudaStreamSynchronize(st));
   if (inner_trace())
+    std::fprintf(stderr, "[inner] chunk B=%d iters=%d wall=%.3f ms sync-wait=%.3f ms\n", Bc, iters_seen + 1,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(), sync_ms);
+  if (inner_trace() >= 2)
     for (int b = 0; b < Bc; ++b)
       std::fprintf(stderr, "[inner] tau=(%.4g,%.4g) it<=%d rel=%.3e %s\n", taus_host[b].x, taus_host[b].y,
                    iters_seen + 1, std::sqrt(rr[b] / bb[b]), rr[b] <= tol2 * bb[b] ? "ok" : "STAGNATED");
@@ -1208,10 +1219,11 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us) {
   // Chunk so that the Krylov + multigrid workspace stays bounded.
   const int64_t n = p->n;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
+  const double avail = available_device_bytes(p->ctx);
   const double per_item = (double)n * (sizeof(double2) * 3.0 + sizeof(VM) * 3.0 * 1.2);
-  int chunk = (int)std::max(1.0, std::min(128.0, 0.5 * (double)free_b / per_item));
+  int chunk = (int)std::max(1.0, std::min(128.0, 0.5 * avail / per_item));
+  if (inner_trace())
+    std::fprintf(stderr, "[inner] B=%d chunk=%d available=%.1fGB\n", B, chunk, avail / 1e9);
   for (int b0 = 0; b0 < B; b0 += chunk) {
     const int bc = std::min(chunk, B - b0);
     if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);

@@ -15,6 +15,19 @@
 
 namespace lt {
 
+// ---- device block cache -----------------------------------------------------------------
+// Every buffer of a context lives on the context's single stream, so a freed block can be
+// handed to the next request of the same rounded size on that stream with no driver call and
+// no synchronisation (stream order is the only order).  The solver's request sizes repeat
+// exactly from one time slice / build to the next (one vector per item, basis columns, the
+// multigrid hierarchy, the field slab), so after the first slice it never touches the driver:
+// growing the stream-ordered pool instead costs 15 ms - 1.7 s of host time per large request.
+// On an out-of-memory the cache is returned to the pool and the request retried.  (allocator.cu)
+void* cache_alloc(size_t bytes, cudaStream_t s);
+void cache_free(void* p, size_t bytes, cudaStream_t s);
+void cache_release_stream(cudaStream_t s);  // return a stream's cached blocks to the pool
+size_t cache_cached_bytes();                // bytes held in free lists
+
 // ---- stream-ordered device buffer -------------------------------------------------------
 class DeviceBuffer {
  public:
@@ -32,13 +45,14 @@ class DeviceBuffer {
     release();
     stream_ = s;
     bytes_ = bytes;
-    if (bytes > 0) LT_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+    if (bytes == 0) return;
+    ptr_ = cache_alloc(bytes, s);
   }
   void ensure(size_t bytes, cudaStream_t s) {
     if (bytes > bytes_) allocate(bytes, s);
   }
   void release() {
-    if (ptr_) cudaFreeAsync(ptr_, stream_);
+    if (ptr_) cache_free(ptr_, bytes_, stream_);
     ptr_ = nullptr;
     bytes_ = 0;
   }
@@ -231,6 +245,9 @@ void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2*
 void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count);
 
 // inner.cu: u_b = (K + tau_b M)^{-1} v_b, b < B, strided vectors; taus on host.
+// device bytes a solve may still take: free + the pool's reserved-but-unused memory (ctx.cu)
+double available_device_bytes(lt_ctx ctx);
+
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs,
                  double2* u, int64_t us);
 
