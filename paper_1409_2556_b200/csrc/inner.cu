@@ -693,7 +693,9 @@ __global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelV
   }
 }
 
-// q = A p, partial p^T q (FP64), z-marching
+// q = A p, partial p^T q (FP64), z-marching; the operands of plane k + 1 (coefficients and the
+// in-plane neighbours) are loaded while plane k is computed (software pipeline), the in-row
+// neighbours come from the adjacent lanes
 __global__ void __launch_bounds__(kT) apply_dot_zm_kernel(LevelView L, Batch bt, const double2* __restrict__ taus,
                                                           const double2* __restrict__ p, double2* __restrict__ q,
                                                           double2* __restrict__ part, int nblk) {
@@ -705,41 +707,619 @@ __global__ void __launch_bounds__(kT) apply_dot_zm_kernel(LevelView L, Batch bt,
   double2* qb = q + (int64_t)b * L.n;
   const double2 tau = taus[b];
   const int nxp1 = L.nx + 1;
-  double2 acc = make_double2(0.0, 0.0);
+  const int lane = threadIdx.x & 31;
+  const bool d3 = L.dim == 3;
+  const double2 zero = make_double2(0.0, 0.0);
+  double2 pm = zero, pc = zero, pp = zero;
   if (m.in) {
-    double2 xm = m.k0 > 0 ? pb[(m.k0 - 1) * plane + m.ip] : make_double2(0.0, 0.0);
-    double2 xc = pb[m.k0 * plane + m.ip];
-    double2 xp = m.k0 + 1 < L.nz ? pb[(m.k0 + 1) * plane + m.ip] : make_double2(0.0, 0.0);
-    for (int k = m.k0; k < m.k1; ++k) {
-      const double2 xn = (k + 1 < m.k1 && k + 2 < L.nz) ? pb[(k + 2) * plane + m.ip] : make_double2(0.0, 0.0);
+    if (m.k0 > 0) pm = pb[(m.k0 - 1) * plane + m.ip];
+    pc = pb[m.k0 * plane + m.ip];
+    if (m.k0 + 1 < L.nz) pp = pb[(m.k0 + 1) * plane + m.ip];
+  }
+  struct Ops {
+    double tw, te, ts, tn, tb, tt, mm;
+    double2 ps, pn, pw, pe;  // y neighbours, x neighbours across the tile edge
+  };
+  auto load_ops = [&](int k, Ops& o) {
+    const int64_t a = k * plane + m.ip;
+    const double* Txk = L.Tx + (int64_t)k * L.ny * nxp1 + (int64_t)m.j * nxp1 + m.i;
+    const double* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx + m.ip;
+    o.tw = __ldg(Txk);
+    o.te = __ldg(Txk + 1);
+    o.ts = __ldg(Tyk);
+    o.tn = __ldg(Tyk + L.nx);
+    o.tb = d3 ? __ldg(L.Tz + a) : 0.0;
+    o.tt = d3 ? __ldg(L.Tz + a + plane) : 0.0;
+    o.mm = __ldg(L.M + a);
+    o.ps = m.j > 0 ? pb[a - L.nx] : zero;
+    o.pn = m.j < L.ny - 1 ? pb[a + L.nx] : zero;
+    o.pw = (lane == 0 && m.i > 0) ? pb[a - 1] : zero;
+    o.pe = (lane == 31 && m.i + 1 < L.nx) ? pb[a + 1] : zero;
+  };
+  Ops cur, nxt;
+  if (m.in) load_ops(m.k0, cur);
+  double2 acc = zero;
+  for (int k = m.k0; k < m.k1; ++k) {
+    double2 pq = zero;
+    if (m.in && k + 2 < L.nz && k + 1 < m.k1) pq = pb[(k + 2) * plane + m.ip];
+    if (m.in && k + 1 < m.k1) load_ops(k + 1, nxt);
+    const double2 up = make_double2(__shfl_up_sync(0xffffffffu, pc.x, 1), __shfl_up_sync(0xffffffffu, pc.y, 1));
+    const double2 dn = make_double2(__shfl_down_sync(0xffffffffu, pc.x, 1), __shfl_down_sync(0xffffffffu, pc.y, 1));
+    if (m.in) {
       const int64_t a = k * plane + m.ip;
-      const double* Txk = L.Tx + (int64_t)k * L.ny * nxp1;
-      const double* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
-      const int ex = m.j * nxp1 + m.i;
-      const double tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
-      const double ts = __ldg(Tyk + m.ip), tn = __ldg(Tyk + m.ip + L.nx);
-      const double tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
-      const double dk = tw + te + ts + tn + tb + tt;
-      double2 o = make_double2(0.0, 0.0);
-      if (m.i > 0) o = cfma(make_double2(tw, 0.0), pb[a - 1], o);
-      if (m.i < L.nx - 1) o = cfma(make_double2(te, 0.0), pb[a + 1], o);
-      if (m.j > 0) o = cfma(make_double2(ts, 0.0), pb[a - L.nx], o);
-      if (m.j < L.ny - 1) o = cfma(make_double2(tn, 0.0), pb[a + L.nx], o);
-      if (k > 0) o = cfma(make_double2(tb, 0.0), xm, o);
-      if (k < L.nz - 1) o = cfma(make_double2(tt, 0.0), xp, o);
-      const double mm = __ldg(L.M + a);
-      const double2 d = make_double2(dk + tau.x * mm, tau.y * mm);
-      const double2 qa = csub(cmul(d, xc), o);
+      const double2 west = lane > 0 ? up : cur.pw;
+      const double2 east = lane < 31 ? dn : cur.pe;
+      const double dk = cur.tw + cur.te + cur.ts + cur.tn + cur.tb + cur.tt;
+      double2 o = cscale(west, cur.tw);
+      o = cfma(make_double2(cur.te, 0.0), east, o);
+      o = cfma(make_double2(cur.ts, 0.0), cur.ps, o);
+      o = cfma(make_double2(cur.tn, 0.0), cur.pn, o);
+      o = cfma(make_double2(cur.tb, 0.0), pm, o);
+      o = cfma(make_double2(cur.tt, 0.0), pp, o);
+      const double2 d = make_double2(dk + tau.x * cur.mm, tau.y * cur.mm);
+      const double2 qa = csub(cmul(d, pc), o);
       qb[a] = qa;
-      acc = cadd(acc, cmul(xc, qa));
-      xm = xc;
-      xc = xp;
-      xp = xn;
+      acc = cfma(pc, qa, acc);
     }
+    pm = pc;
+    pc = pp;
+    pp = pq;
+    cur = nxt;
   }
   acc = block_sum(acc);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
 }
+
+// ---- pair z-marching kernels (nx even) ----------------------------------------------------
+// A thread owns two x-adjacent cells (i0, i0 + 1), i0 even.  In a red-black half sweep exactly
+// one of the two has the sweep's colour on every plane, so every lane does useful work (the
+// one-cell kernel idles half its lanes and was issue-bound), the pair moves as one 16-byte
+// access, and the in-row neighbours come from the adjacent lanes by shuffle (a warp is one
+// row of 64 cells).  CTA = 32 pairs x 8 rows x a chunk of ZM_ZC planes.
+constexpr int ZP_TX = 32;
+
+template <class VW>
+inline int zp_blocks(const VW& L) {
+  return ((L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX)) * ((L.ny + ZM_TY - 1) / ZM_TY) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+}
+
+template <class V>
+struct Pair {
+  V a, c;  // cells i0, i0 + 1
+};
+
+template <class V>
+__device__ __forceinline__ Pair<V> ld_pair(const V* p) {
+  if constexpr (sizeof(V) == 8) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    return {V{t.x, t.y}, V{t.z, t.w}};
+  } else {
+    return {p[0], p[1]};
+  }
+}
+
+template <class V>
+__device__ __forceinline__ void st_pair(V* p, const Pair<V>& v) {
+  if constexpr (sizeof(V) == 8) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.a.x, v.a.y, v.c.x, v.c.y);
+  } else {
+    p[0] = v.a;
+    p[1] = v.c;
+  }
+}
+
+template <class V>
+__device__ __forceinline__ V shfl_up1(V v) {
+  return V{__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1)};
+}
+template <class V>
+__device__ __forceinline__ V shfl_down1(V v) {
+  return V{__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1)};
+}
+
+template <class V>
+__device__ __forceinline__ V pick(const Pair<V>& p, int o) {
+  return o ? p.c : p.a;
+}
+
+struct ZpMap {
+  int i0, j, k0, k1, lane;
+  bool in;
+  int64_t ip;
+};
+
+template <class VW>
+__device__ __forceinline__ ZpMap zp_map(const VW& L, int cb) {
+  const int tiles_x = (L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX), tiles_y = (L.ny + ZM_TY - 1) / ZM_TY;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  ZpMap m;
+  m.lane = threadIdx.x & 31;
+  m.i0 = (tile % tiles_x) * 2 * ZP_TX + 2 * m.lane;
+  m.j = (tile / tiles_x) * ZM_TY + (threadIdx.x >> 5);
+  m.in = m.i0 < L.nx && m.j < L.ny;
+  m.k0 = chunk * ZM_ZC;
+  m.k1 = min(L.nz, m.k0 + ZM_ZC);
+  m.ip = (int64_t)m.j * L.nx + m.i0;
+  return m;
+}
+
+// Red-black half sweep of colour `color` on cell pairs, in place (see rbhalf_zm_kernel for why
+// in place is race free).  zero_init: x = 0 on entry.  dot != null: also the partial
+// sum_a f_a x_a over all cells after the sweep (the COCG rho = r^T z fused into the last
+// sweep of the V-cycle: f is the multigrid copy of r on the finest level).
+template <class R>
+__global__ void __launch_bounds__(kT, 3) rbpair_zm_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
+                                                       const typename CT<R>::V* __restrict__ f,
+                                                       typename CT<R>::V* x, int color, int zero_init,
+                                                       double2* __restrict__ dot, int nblk) {
+  using V = typename CT<R>::V;
+  using PV = Pair<V>;
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZpMap m = zp_map(L, cb);
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  V* xb = x + (int64_t)b * L.n;
+  const V* fb = f + (int64_t)b * L.n;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  const int nxp1 = L.nx + 1;
+  const bool d3 = L.dim == 3;
+  const PV pz{vzero<V>(), vzero<V>()};
+  PV xm = pz, xc = pz, xp = pz;
+  if (m.in && !zero_init) {
+    if (m.k0 > 0) xm = ld_pair(xb + (m.k0 - 1) * plane + m.ip);
+    xc = ld_pair(xb + m.k0 * plane + m.ip);
+    if (m.k0 + 1 < L.nz) xp = ld_pair(xb + (m.k0 + 1) * plane + m.ip);
+  }
+  struct Ops {
+    R tw, te, ts, tn, tb, tt, mm;
+    PV fv, ns, nn;
+    V xw, xe;  // x-neighbours across the tile edge (lanes 0 / 31 only)
+  };
+  auto load_ops = [&](int k, Ops& o) {
+    const int off = (m.j + k + color) & 1;
+    const int64_t a = k * plane + m.ip;
+    const int ic = m.i0 + off;
+    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1 + (int64_t)m.j * nxp1 + ic;
+    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx + (int64_t)m.j * L.nx + ic;
+    o.tw = __ldg(Txk);
+    o.te = __ldg(Txk + 1);
+    o.ts = __ldg(Tyk);
+    o.tn = __ldg(Tyk + L.nx);
+    o.tb = d3 ? __ldg(L.Tz + a + off) : R(0);
+    o.tt = d3 ? __ldg(L.Tz + a + off + plane) : R(0);
+    o.mm = __ldg(L.M + a + off);
+    o.fv = ld_pair(fb + a);
+    o.ns = pz;
+    o.nn = pz;
+    o.xw = vzero<V>();
+    o.xe = vzero<V>();
+    if (!zero_init) {
+      if (m.j > 0) o.ns = ld_pair(xb + a - L.nx);
+      if (m.j < L.ny - 1) o.nn = ld_pair(xb + a + L.nx);
+      if (off == 0 && m.lane == 0 && m.i0 > 0) o.xw = xb[a - 1];
+      if (off == 1 && m.lane == 31 && m.i0 + 2 < L.nx) o.xe = xb[a + 2];
+    }
+  };
+  Ops cur, nxt;
+  if (m.in) load_ops(m.k0, cur);
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = m.k0; k < m.k1; ++k) {
+    PV xn = pz;
+    if (m.in && !zero_init && k + 2 < L.nz && k + 1 < m.k1) xn = ld_pair(xb + (k + 2) * plane + m.ip);
+    if (m.in && k + 1 < m.k1) load_ops(k + 1, nxt);
+    const int off = (m.j + k + color) & 1;
+    // in-row neighbours of the colour cell from the adjacent lanes (every lane shuffles)
+    const V up = shfl_up1(xc.c), dn = shfl_down1(xc.a);
+    if (m.in) {
+      const V west = off ? xc.a : (m.lane > 0 ? up : cur.xw);
+      const V east = off ? (m.lane < 31 ? dn : cur.xe) : xc.c;
+      const R dk = cur.tw + cur.te + cur.ts + cur.tn + cur.tb + cur.tt;
+      V o = pick(cur.fv, off);
+      o = vadd(o, vadd(vadd(vscale(west, cur.tw), vscale(east, cur.te)),
+                       vadd(vscale(pick(cur.ns, off), cur.ts), vscale(pick(cur.nn, off), cur.tn))));
+      o = vadd(o, vadd(vscale(pick(xm, off), cur.tb), vscale(pick(xp, off), cur.tt)));
+      const V nv = diag_solve_r<R, V>(dk, cur.mm, tr, ti, o);
+      PV out = xc;
+      if (off) out.c = nv;
+      else out.a = nv;
+      st_pair(xb + k * plane + m.ip, out);
+      if (dot) {
+        const double2 fa = vto(cur.fv.a), fc = vto(cur.fv.c);
+        acc = cfma(fa, vto(out.a), acc);
+        acc = cfma(fc, vto(out.c), acc);
+      }
+    }
+    xm = xc;
+    xc = xp;
+    xp = xn;
+    cur = nxt;
+  }
+  if (dot) {
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) dot[(int64_t)b * nblk + cb] = acc;
+  }
+}
+
+// r = f - A(tau) x on cell pairs (precision R)
+template <class R>
+__global__ void __launch_bounds__(kT, 3) residual_pair_zm_kernel(LevelViewT<R> L, Batch bt,
+                                                              const double2* __restrict__ taus,
+                                                              const typename CT<R>::V* __restrict__ f,
+                                                              const typename CT<R>::V* __restrict__ x,
+                                                              typename CT<R>::V* __restrict__ r) {
+  using V = typename CT<R>::V;
+  using PV = Pair<V>;
+  using R2 = typename CT<R>::V;  // two coefficients of a pair
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const ZpMap m = zp_map(L, cb);
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  const V* xb = x + (int64_t)b * L.n;
+  const V* fb = f + (int64_t)b * L.n;
+  V* rb = r + (int64_t)b * L.n;
+  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
+  const int nxp1 = L.nx + 1;
+  const bool d3 = L.dim == 3;
+  const PV pz{vzero<V>(), vzero<V>()};
+  PV xm = pz, xc = pz, xp = pz;
+  if (m.in) {
+    if (m.k0 > 0) xm = ld_pair(xb + (m.k0 - 1) * plane + m.ip);
+    xc = ld_pair(xb + m.k0 * plane + m.ip);
+    if (m.k0 + 1 < L.nz) xp = ld_pair(xb + (m.k0 + 1) * plane + m.ip);
+  }
+  struct Ops {
+    R tx0, tx1, tx2;
+    R2 ts, tn, tb, tt, mm;
+    PV fv, ns, nn;
+    V xw, xe;
+  };
+  auto ld_r2 = [](const R* p) { return R2{__ldg(p), __ldg(p + 1)}; };
+  auto load_ops = [&](int k, Ops& o) {
+    const int64_t a = k * plane + m.ip;
+    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1 + (int64_t)m.j * nxp1 + m.i0;
+    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx + m.ip;
+    o.tx0 = __ldg(Txk);
+    o.tx1 = __ldg(Txk + 1);
+    o.tx2 = __ldg(Txk + 2);
+    o.ts = ld_r2(Tyk);
+    o.tn = ld_r2(Tyk + L.nx);
+    o.tb = d3 ? ld_r2(L.Tz + a) : R2{0, 0};
+    o.tt = d3 ? ld_r2(L.Tz + a + plane) : R2{0, 0};
+    o.mm = ld_r2(L.M + a);
+    o.fv = ld_pair(fb + a);
+    o.ns = m.j > 0 ? ld_pair(xb + a - L.nx) : pz;
+    o.nn = m.j < L.ny - 1 ? ld_pair(xb + a + L.nx) : pz;
+    o.xw = (m.lane == 0 && m.i0 > 0) ? xb[a - 1] : vzero<V>();
+    o.xe = (m.lane == 31 && m.i0 + 2 < L.nx) ? xb[a + 2] : vzero<V>();
+  };
+  Ops cur, nxt;
+  if (m.in) load_ops(m.k0, cur);
+  for (int k = m.k0; k < m.k1; ++k) {
+    PV xn = pz;
+    if (m.in && k + 2 < L.nz && k + 1 < m.k1) xn = ld_pair(xb + (k + 2) * plane + m.ip);
+    if (m.in && k + 1 < m.k1) load_ops(k + 1, nxt);
+    const V up = shfl_up1(xc.c), dn = shfl_down1(xc.a);
+    if (m.in) {
+      const V west = m.lane > 0 ? up : cur.xw;
+      const V east = m.lane < 31 ? dn : cur.xe;
+      PV out;
+      {  // cell i0: neighbours west, xc.c
+        const R dk = cur.tx0 + cur.tx1 + cur.ts.x + cur.tn.x + cur.tb.x + cur.tt.x;
+        V o = vadd(vadd(vscale(west, cur.tx0), vscale(xc.c, cur.tx1)),
+                   vadd(vscale(cur.ns.a, cur.ts.x), vscale(cur.nn.a, cur.tn.x)));
+        o = vadd(o, vadd(vscale(xm.a, cur.tb.x), vscale(xp.a, cur.tt.x)));
+        const R dr = dk + tr * cur.mm.x, di = ti * cur.mm.x;
+        out.a = V{cur.fv.a.x - (dr * xc.a.x - di * xc.a.y - o.x), cur.fv.a.y - (dr * xc.a.y + di * xc.a.x - o.y)};
+      }
+      {  // cell i0 + 1: neighbours xc.a, east
+        const R dk = cur.tx1 + cur.tx2 + cur.ts.y + cur.tn.y + cur.tb.y + cur.tt.y;
+        V o = vadd(vadd(vscale(xc.a, cur.tx1), vscale(east, cur.tx2)),
+                   vadd(vscale(cur.ns.c, cur.ts.y), vscale(cur.nn.c, cur.tn.y)));
+        o = vadd(o, vadd(vscale(xm.c, cur.tb.y), vscale(xp.c, cur.tt.y)));
+        const R dr = dk + tr * cur.mm.y, di = ti * cur.mm.y;
+        out.c = V{cur.fv.c.x - (dr * xc.c.x - di * xc.c.y - o.x), cur.fv.c.y - (dr * xc.c.y + di * xc.c.x - o.y)};
+      }
+      st_pair(rb + k * plane + m.ip, out);
+    }
+    xm = xc;
+    xc = xp;
+    xp = xn;
+    cur = nxt;
+  }
+}
+
+// ---- TMA-fed z-marching kernels (large levels, nx even) -----------------------------------
+// A CTA owns an (x, y) tile and marches a chunk of planes.  One thread issues the tensor-memory
+// copies of each plane's operand tiles -- the iterate with a halo, the right-hand side and the
+// packed coefficients -- into a ring of TZ_D plane slots in shared memory, TZ_D - 2 planes
+// ahead of the plane being computed, each slot signalled by an mbarrier.  The bytes in flight
+// no longer depend on registers and occupancy (the register-pipelined kernels reached only
+// ~50% of HBM bandwidth), neighbours come from shared memory (no shuffles or edge loads), and
+// the domain boundary is the TMA out-of-bounds zero fill.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* m, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Ring bookkeeping shared by the kernels: plane p (k0 - 1 <= p <= k1) lives in slot
+// (p - k0 + 1) % D, and its barrier phase parity is ((p - k0 + 1) / D) & 1.
+template <int D>
+struct ZRing {
+  int k0;
+  __device__ __forceinline__ int slot(int p) const { return (p - k0 + 1) % D; }
+  __device__ __forceinline__ uint32_t parity(int p) const { return (uint32_t)(((p - k0 + 1) / D) & 1); }
+};
+
+struct TzDims {
+  int nx, ny, nz;
+  int64_t n;
+};
+
+// FP32 multigrid tiles: 64 x 8 cells (32 pairs x 8 rows)
+constexpr int TZ_W = 64, TZ_H = 8;
+constexpr int TZ_XW = TZ_W + 4, TZ_XH = TZ_H + 2;  // iterate x0-2 .. x0+65, y0-1 .. y0+8
+constexpr int TZ_CW = TZ_W + 1, TZ_CH = TZ_H + 1;  // packed coefficients x0 .. x0+64, y0 .. y0+8
+constexpr int TZ_D = 5;
+constexpr uint32_t TZ_XB = sizeof(float2) * TZ_XW * TZ_XH;  // 5440
+constexpr uint32_t TZ_FB = sizeof(float2) * TZ_W * TZ_H;    // 4096
+constexpr uint32_t TZ_CB = sizeof(float4) * TZ_CW * TZ_CH;  // 9360
+constexpr uint32_t TZ_OFF_F = 5504, TZ_OFF_C = TZ_OFF_F + 4096, TZ_SLOT = TZ_OFF_C + 9472;  // 128-byte aligned
+constexpr size_t TZ_SMEM = (size_t)TZ_SLOT * TZ_D;
+
+template <class VW>
+inline int tz_blocks(const VW& L) {
+  return ((L.nx + TZ_W - 1) / TZ_W) * ((L.ny + TZ_H - 1) / TZ_H) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+}
+
+// mode 0: red-black half sweep of `color` in place on x (zero_init: x = 0 on entry; dot: also
+// the partials of f^T x after the sweep); mode 1: r = f - A x.
+template <int MODE>
+__global__ void __launch_bounds__(kT, 2) mg_tma_kernel(const __grid_constant__ CUtensorMap mx,
+                                                       const __grid_constant__ CUtensorMap mf,
+                                                       const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                       const double2* __restrict__ taus, float2* __restrict__ out,
+                                                       int color, int zero_init, double2* __restrict__ dot, int nblk) {
+  extern __shared__ __align__(128) unsigned char tz_smem[];
+  __shared__ __align__(8) uint64_t bar[TZ_D];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int tiles_x = (L.nx + TZ_W - 1) / TZ_W, tiles_y = (L.ny + TZ_H - 1) / TZ_H;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  const int x0 = (tile % tiles_x) * TZ_W, y0 = (tile / tiles_x) * TZ_H;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  const int i0 = x0 + 2 * lane, j = y0 + wy;
+  const bool in = i0 < L.nx && j < L.ny;
+  const bool ldx = MODE == 1 || !zero_init;
+  const ZRing<TZ_D> ring{k0};
+  if (tid == 0) {
+    for (int s = 0; s < TZ_D; ++s) mbar_init(&bar[s], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  auto issue = [&](int p) {
+    unsigned char* s = tz_smem + (size_t)ring.slot(p) * TZ_SLOT;
+    uint64_t* br = &bar[ring.slot(p)];
+    const bool lf = p >= k0 && p < k1, lc = p >= k0;
+    mbar_arrive_tx(br, (ldx ? TZ_XB : 0u) + (lf ? TZ_FB : 0u) + (lc ? TZ_CB : 0u));
+    if (ldx) tma_load4(s, &mx, x0 - 2, y0 - 1, p, b, br);
+    if (lf) tma_load4(s + TZ_OFF_F, &mf, x0, y0, p, b, br);
+    if (lc) tma_load3(s + TZ_OFF_C, &mc, 2 * x0, y0, p, br);
+  };
+  if (tid == 0)
+    for (int p = k0 - 1; p <= min(k1, k0 - 2 + TZ_D); ++p) issue(p);
+  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  float2* ob = out + (int64_t)b * L.n;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = k0; k < k1; ++k) {
+    mbar_wait(&bar[ring.slot(k - 1)], ring.parity(k - 1));
+    mbar_wait(&bar[ring.slot(k)], ring.parity(k));
+    mbar_wait(&bar[ring.slot(k + 1)], ring.parity(k + 1));
+    const unsigned char* sm = tz_smem + (size_t)ring.slot(k - 1) * TZ_SLOT;
+    const unsigned char* s0 = tz_smem + (size_t)ring.slot(k) * TZ_SLOT;
+    const unsigned char* sp = tz_smem + (size_t)ring.slot(k + 1) * TZ_SLOT;
+    auto X = [](const unsigned char* s, int yy, int xx) { return reinterpret_cast<const float2*>(s)[yy * TZ_XW + xx]; };
+    auto F = [](const unsigned char* s, int yy, int xx) {
+      return reinterpret_cast<const float2*>(s + TZ_OFF_F)[yy * TZ_W + xx];
+    };
+    auto Cf = [](const unsigned char* s, int yy, int xx) {
+      return reinterpret_cast<const float4*>(s + TZ_OFF_C)[yy * TZ_CW + xx];
+    };
+    if (in) {
+      const int c0 = 2 * lane;  // pair's first cell in F / C tile coordinates (X: + 2, + 1 row)
+      float2* dst = ob + k * plane + (int64_t)j * L.nx + i0;
+      if (MODE == 0) {
+        const int off = (j + k + color) & 1;
+        const int cx = c0 + off, xx = cx + 2;
+        const float4 cc = Cf(s0, wy, cx);
+        const float te = Cf(s0, wy, cx + 1).x, tn = Cf(s0, wy + 1, cx).y, tt = Cf(sp, wy, cx).z;
+        const float dk = cc.x + te + cc.y + tn + cc.z + tt;
+        float2 o = F(s0, wy, cx);
+        float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!zero_init) {
+          pr = *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
+          const float2 w = X(s0, wy + 1, xx - 1), e = X(s0, wy + 1, xx + 1);
+          const float2 so = X(s0, wy, xx), no = X(s0, wy + 2, xx);
+          const float2 dn = X(sm, wy + 1, xx), up = X(sp, wy + 1, xx);
+          o.x += cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
+          o.y += cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
+        }
+        const float2 nv = diag_solve_r<float, float2>(dk, cc.w, tr, ti, o);
+        if (off) {
+          pr.z = nv.x;
+          pr.w = nv.y;
+        } else {
+          pr.x = nv.x;
+          pr.y = nv.y;
+        }
+        *reinterpret_cast<float4*>(dst) = pr;
+        if (dot) {
+          const float2 fa = F(s0, wy, c0), fc = F(s0, wy, c0 + 1);
+          acc = cfma(make_double2(fa.x, fa.y), make_double2(pr.x, pr.y), acc);
+          acc = cfma(make_double2(fc.x, fc.y), make_double2(pr.z, pr.w), acc);
+        }
+      } else {
+        const float4 pr = *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
+        const float2 xa = make_float2(pr.x, pr.y), xc = make_float2(pr.z, pr.w);
+        float4 res;
+        {
+          const float4 ca = Cf(s0, wy, c0);
+          const float te = Cf(s0, wy, c0 + 1).x, tn = Cf(s0, wy + 1, c0).y, tt = Cf(sp, wy, c0).z;
+          const float2 w = X(s0, wy + 1, c0 + 1), so = X(s0, wy, c0 + 2), no = X(s0, wy + 2, c0 + 2);
+          const float2 dn = X(sm, wy + 1, c0 + 2), up = X(sp, wy + 1, c0 + 2);
+          const float dk = ca.x + te + ca.y + tn + ca.z + tt;
+          const float dr = dk + tr * ca.w, di = ti * ca.w;
+          const float ox = ca.x * w.x + te * xc.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
+          const float oy = ca.x * w.y + te * xc.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
+          const float2 f = F(s0, wy, c0);
+          res.x = f.x - (dr * xa.x - di * xa.y - ox);
+          res.y = f.y - (dr * xa.y + di * xa.x - oy);
+        }
+        {
+          const float4 ca = Cf(s0, wy, c0 + 1);
+          const float te = Cf(s0, wy, c0 + 2).x, tn = Cf(s0, wy + 1, c0 + 1).y, tt = Cf(sp, wy, c0 + 1).z;
+          const float2 e = X(s0, wy + 1, c0 + 4), so = X(s0, wy, c0 + 3), no = X(s0, wy + 2, c0 + 3);
+          const float2 dn = X(sm, wy + 1, c0 + 3), up = X(sp, wy + 1, c0 + 3);
+          const float dk = ca.x + te + ca.y + tn + ca.z + tt;
+          const float dr = dk + tr * ca.w, di = ti * ca.w;
+          const float ox = ca.x * xa.x + te * e.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
+          const float oy = ca.x * xa.y + te * e.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
+          const float2 f = F(s0, wy, c0 + 1);
+          res.z = f.x - (dr * xc.x - di * xc.y - ox);
+          res.w = f.y - (dr * xc.y + di * xc.x - oy);
+        }
+        *reinterpret_cast<float4*>(dst) = res;
+      }
+    }
+    __syncthreads();  // every thread is done with plane k - 1's slot
+    if (tid == 0 && k - 1 + TZ_D <= k1) issue(k - 1 + TZ_D);
+  }
+  if (MODE == 0 && dot) {
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) dot[(int64_t)b * nblk + cb] = acc;
+  }
+}
+
+// FP64 operator tiles: 32 x 8 cells, one per thread
+constexpr int TA_W = 32, TA_H = 8;
+constexpr int TA_XW = TA_W + 2, TA_XH = TA_H + 2;  // p: x0-1 .. x0+32, y0-1 .. y0+8
+constexpr int TA_CW = TA_W + 1, TA_CH = TA_H + 1;  // packed coefficients x0 .. x0+32, y0 .. y0+8
+constexpr int TA_D = 4;
+constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;  // 5440
+constexpr uint32_t TA_CB = sizeof(double4) * TA_CW * TA_CH;  // 9504
+constexpr uint32_t TA_OFF_C = 5504, TA_SLOT = TA_OFF_C + 9600;
+constexpr size_t TA_SMEM = (size_t)TA_SLOT * TA_D;
+
+// q = A(tau) p, partial p^T q (FP64)
+__global__ void __launch_bounds__(kT, 3) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
+                                                          const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                          const double2* __restrict__ taus, double2* __restrict__ q,
+                                                          double2* __restrict__ part, int nblk) {
+  extern __shared__ __align__(128) unsigned char ta_smem[];
+  __shared__ __align__(8) uint64_t bar[TA_D];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int tiles_x = (L.nx + TA_W - 1) / TA_W, tiles_y = (L.ny + TA_H - 1) / TA_H;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  const int x0 = (tile % tiles_x) * TA_W, y0 = (tile / tiles_x) * TA_H;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  const int i = x0 + lane, j = y0 + wy;
+  const bool in = i < L.nx && j < L.ny;
+  const ZRing<TA_D> ring{k0};
+  if (tid == 0) {
+    for (int s = 0; s < TA_D; ++s) mbar_init(&bar[s], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  auto issue = [&](int p) {
+    unsigned char* s = ta_smem + (size_t)ring.slot(p) * TA_SLOT;
+    uint64_t* br = &bar[ring.slot(p)];
+    const bool lc = p >= k0;
+    mbar_arrive_tx(br, TA_XB + (lc ? TA_CB : 0u));
+    tma_load4(s, &mp, 2 * (x0 - 1), y0 - 1, p, b, br);
+    if (lc) tma_load3(s + TA_OFF_C, &mc, 4 * x0, y0, p, br);
+  };
+  if (tid == 0)
+    for (int p = k0 - 1; p <= min(k1, k0 - 2 + TA_D); ++p) issue(p);
+  const double2 tau = taus[b];
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  double2* qb = q + (int64_t)b * L.n;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = k0; k < k1; ++k) {
+    mbar_wait(&bar[ring.slot(k - 1)], ring.parity(k - 1));
+    mbar_wait(&bar[ring.slot(k)], ring.parity(k));
+    mbar_wait(&bar[ring.slot(k + 1)], ring.parity(k + 1));
+    if (in) {
+      const unsigned char* sm = ta_smem + (size_t)ring.slot(k - 1) * TA_SLOT;
+      const unsigned char* s0 = ta_smem + (size_t)ring.slot(k) * TA_SLOT;
+      const unsigned char* sp = ta_smem + (size_t)ring.slot(k + 1) * TA_SLOT;
+      auto X = [](const unsigned char* s, int yy, int xx) { return reinterpret_cast<const double2*>(s)[yy * TA_XW + xx]; };
+      auto Cf = [](const unsigned char* s, int yy, int xx) {
+        return reinterpret_cast<const double4*>(s + TA_OFF_C)[yy * TA_CW + xx];
+      };
+      const double4 cc = Cf(s0, wy, lane);
+      const double te = Cf(s0, wy, lane + 1).x, tn = Cf(s0, wy + 1, lane).y, tt = Cf(sp, wy, lane).z;
+      const double2 pc = X(s0, wy + 1, lane + 1);
+      const double2 w = X(s0, wy + 1, lane), e = X(s0, wy + 1, lane + 2);
+      const double2 so = X(s0, wy, lane + 1), no = X(s0, wy + 2, lane + 1);
+      const double2 dn = X(sm, wy + 1, lane + 1), up = X(sp, wy + 1, lane + 1);
+      const double dk = cc.x + te + cc.y + tn + cc.z + tt;
+      const double ox = cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
+      const double oy = cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
+      const double dr = dk + tau.x * cc.w, di = tau.y * cc.w;
+      const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
+      qb[k * plane + (int64_t)j * L.nx + i] = qa;
+      acc = cfma(pc, qa, acc);
+    }
+    __syncthreads();
+    if (tid == 0 && k - 1 + TA_D <= k1) issue(k - 1 + TA_D);
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
+}
+
+// per-level tensor maps of one inner solve (ok = the level runs the TMA kernels)
+struct TzMaps {
+  bool ok = false;
+  CUtensorMap x, f, c;
+};
 
 // q = A p, partial p^T q
 template <int DIM>
@@ -947,10 +1527,14 @@ LevelViewT<float> mg_view<float>(lt_pencil p, int l) { return p->view32(l); }
 
 // Returns the buffer holding the level-l V-cycle output (Bc x n_l).
 template <class R, int DIM>
+// dot_part != null (finest level only): the last sweep also writes per-block partials of
+// f^T x, and *dot_nblk their count per item (0 when this level could not fuse them).
 const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, const double2* taus,
                                 const typename CT<R>::V* const* inv, int64_t inv_ld, int64_t inv_off,
                                 std::vector<typename CT<R>::V*>& X, std::vector<typename CT<R>::V*>& F,
-                                std::vector<typename CT<R>::V*>& Rr) {
+                                std::vector<typename CT<R>::V*>& Rr, double2* dot_part, int* dot_nblk,
+                                const TzMaps* tz) {
+  if (dot_nblk) *dot_nblk = 0;
   using V = typename CT<R>::V;
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
@@ -974,7 +1558,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
       p1_restrict_kernel<R><<<(unsigned)Lc.ntiles * Bc, kT, 0, st>>>(L, Lc, bt, Rr[l], F[l + 1]);
     });
-    const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr);
+    const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr, nullptr, nullptr, tz);
     launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
       p1_prolong_kernel<R><<<grid, kT, 0, st>>>(L, Lc, bt, ec, X[l]);
     });
@@ -993,68 +1577,64 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   }
   LevelViewT<R> Lc = mg_view<R>(p, l + 1);
   const Level& lev = *p->levels[l];
-  const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
-  const unsigned sgrid = (unsigned)(((L.nx + SW_TX - 1) / SW_TX) * ((L.ny + SW_TY - 1) / SW_TY)) * (unsigned)Bc;
-  const size_t ssmem = sweep_smem<R>(DIM);
-  static bool attr_set = false;
-  if (!attr_set) {
-    LT_CUDA(cudaFuncSetAttribute(rb_sweep_kernel<R, DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-    attr_set = true;
-  }
-  static const bool zm_smoother = [] {
-    const char* e = std::getenv("LT_SMOOTHER");
-    return !(e && std::string(e) == "smem");
+  // red-black sweeps per pre/post smoothing (LT_MG_NU, default 2)
+  static const int nu = [] {
+    const char* e = std::getenv("LT_MG_NU");
+    return e ? std::max(1, std::atoi(e)) : 2;
   }();
+  // half sweeps on cell pairs when the rows have even length, else one cell per thread
+  const bool pairs = (L.nx & 1) == 0;
   const unsigned zgrid = (unsigned)zm_blocks(L) * (unsigned)Bc;
-  if (zm_smoother) {
-    // pre-smoothing: red half sweep from zero (f read, x written), black half sweep
-    launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
-      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 1);
+  const unsigned pgrid = (unsigned)zp_blocks(L) * (unsigned)Bc;
+  const bool tma = tz && tz[l].ok;
+  const unsigned tgrid = (unsigned)tz_blocks(L) * (unsigned)Bc;
+  const TzDims tdims{L.nx, L.ny, L.nz, L.n};
+  auto half = [&](int color, int zero_init, double2* dot) {
+    launch(ctx, "mg_smooth", cell_bytes * (zero_init ? 2 : 3) * vb + coef, [&] {
+      if (tma)
+        mg_tma_kernel<0><<<tgrid, kT, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
+                                                   zero_init, dot, tz_blocks(L));
+      else if (pairs)
+        rbpair_zm_kernel<R><<<pgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], color, zero_init, dot, zp_blocks(L));
+      else
+        rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], color, zero_init);
     });
-    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
-      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
-    });
-  } else {
-    // pre-smoothing: one fused red-black sweep (red first) from a zero iterate
-    launch(ctx, "mg_smooth", cell_bytes * 2 * vb + coef, [&] {
-      rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], nullptr, X[l], 0, 1, Lc, 1, 1, 1, nullptr);
-    });
+  };
+  // pre-smoothing: red half sweep from zero (f read, x written), then black, red, ...
+  half(0, 1, nullptr);
+  half(1, 0, nullptr);
+  for (int s = 1; s < nu; ++s) {
+    half(0, 0, nullptr);
+    half(1, 0, nullptr);
   }
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
-    if (DIM == 3)
-      residual_zm_kernel<R><<<(unsigned)zm_blocks(L) * Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+    if (tma)
+      mg_tma_kernel<1><<<tgrid, kT, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
+                                                 nullptr, 0);
+    else if (pairs)
+      residual_pair_zm_kernel<R><<<pgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+    else if (DIM == 3)
+      residual_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
     else
-      residual_kernel<R, DIM><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
+      residual_kernel<R, DIM><<<(unsigned)L.ntiles * (unsigned)Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
   });
-  const unsigned gridc = (unsigned)Lc.ntiles * (unsigned)Bc;
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
-    if (zm_smoother)
-      restrict_zm_kernel<R><<<(unsigned)zm_blocks(Lc) * Bc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt,
-                                                                        Rr[l], F[l + 1]);
-    else
-      restrict_kernel<R, DIM><<<gridc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, Rr[l], F[l + 1]);
+    restrict_zm_kernel<R><<<(unsigned)zm_blocks(Lc) * Bc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt,
+                                                                      Rr[l], F[l + 1]);
   });
-  const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr);
-  if (zm_smoother) {
-    // coarse correction, then the transpose of the pre-smoother (black, red), in place
-    launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
-      prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
-    });
-    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
-      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 1, 0);
-    });
-    launch(ctx, "mg_smooth", cell_bytes * 3 * vb + coef, [&] {
-      rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], 0, 0);
-    });
-    return X[l];
+  const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr, nullptr, nullptr, tz);
+  // coarse correction, then the transpose of the pre-smoother (black, red, ...), in place
+  launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+    prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
+  });
+  for (int s = 0; s < nu; ++s) {
+    half(1, 0, nullptr);
+    // the last half sweep also forms the partial sums of f^T x when asked (and possible)
+    const bool last_sweep = s == nu - 1;
+    half(0, 0, last_sweep && pairs ? dot_part : nullptr);
   }
-  // post-smoothing: coarse correction x + P e_c fused into one black-first sweep (the
-  // transpose of the pre-smoother), written out of place into Rr[l]
-  launch(ctx, "mg_smooth", cell_bytes * 3 * vb + (double)Lc.n * Bc * vb + coef, [&] {
-    rb_sweep_kernel<R, DIM><<<sgrid, kT, ssmem, st>>>(L, bt, taus, F[l], X[l], Rr[l], 1, 0, Lc, lev.agg[0],
-                                                      lev.agg[1], lev.agg[2], ec);
-  });
-  return Rr[l];
+  if (dot_nblk) *dot_nblk = (tma || pairs) && dot_part ? zp_blocks(L) : 0;
+  return X[l];
 }
 
 template <int DIM>
@@ -1100,7 +1680,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
 
   // workspace: FP64 Krylov vectors r, p, q; multigrid vectors (precision R) per level
   DeviceBuffer partials(sizeof(double2) * (size_t)Bc *
-                            std::max<int64_t>(std::max<int64_t>(nblk, L0.ntiles), zm_blocks(L0)), st);
+                            std::max<int64_t>(std::max<int64_t>(nblk, L0.ntiles),
+                                              std::max(zm_blocks(L0), zp_blocks(L0))),
+                        st);
   DeviceBuffer vec(sizeof(double2) * (size_t)Bc * n * 3, st);
   double2* r = vec.as<double2>();
   double2* pp = r + Bc * n;
@@ -1115,6 +1697,53 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     Rr[l] = X[l] + 2 * Bc * nlv;
   }
   V* rmg = F[0];  // the multigrid copy of the COCG residual
+
+  // TMA tensor maps (FD levels with even rows of >= 64 cells; FP32 V-cycle only) and the
+  // FP64 operator's maps on the finest level.  LT_NO_TMA=1 selects the register-pipelined
+  // kernels instead.
+  static const bool tma_on = std::getenv("LT_NO_TMA") == nullptr;
+  std::vector<TzMaps> tzm(nl);
+  if (tma_on) {
+    static bool attr = false;
+    if (!attr) {
+      LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
+      attr = true;
+    }
+  }
+  if (tma_on && p->kind != LT_GRID_P1_TRI && sizeof(R) == 4) {
+    for (int l = 0; l < nl - 1; ++l) {
+      const Level& Lv = *p->levels[l];
+      if (Lv.nx % 2 != 0 || Lv.nx < 64) continue;
+      const uint64_t nx = Lv.nx, ny = Lv.ny, nz = Lv.nz;
+      const uint64_t dims[4] = {nx, ny, nz, (uint64_t)Bc};
+      const uint64_t str[3] = {nx * 8, nx * ny * 8, nx * ny * nz * 8};
+      const uint32_t bx[4] = {TZ_XW, TZ_XH, 1, 1}, bf[4] = {TZ_W, TZ_H, 1, 1};
+      const uint64_t cd[3] = {2 * (nx + 1), ny + 1, nz + 1};
+      const uint64_t cs[2] = {(nx + 1) * 16, (nx + 1) * (ny + 1) * 16};
+      const uint32_t bc[3] = {2 * TZ_CW, TZ_CH, 1};
+      tzm[l].x = tma_map_8b(X[l], 4, dims, str, bx);
+      tzm[l].f = tma_map_8b(F[l], 4, dims, str, bf);
+      tzm[l].c = tma_map_8b(Lv.pack32.get(), 3, cd, cs, bc);
+      tzm[l].ok = true;
+    }
+  }
+  // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
+  // reads and writes X[l]
+  const bool ta_ok = tma_on && p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32;
+  CUtensorMap map_p{}, map_c64{};
+  if (ta_ok) {
+    const uint64_t nx = L0.nx, ny = L0.ny, nz = L0.nz;
+    const uint64_t dims[4] = {2 * nx, ny, nz, (uint64_t)Bc};
+    const uint64_t str[3] = {nx * 16, nx * ny * 16, nx * ny * nz * 16};
+    const uint32_t bx[4] = {2 * TA_XW, TA_XH, 1, 1};
+    const uint64_t cd[3] = {4 * (nx + 1), ny + 1, nz + 1};
+    const uint64_t cs[2] = {(nx + 1) * 32, (nx + 1) * (ny + 1) * 32};
+    const uint32_t bc[3] = {4 * TA_CW, TA_CH, 1};
+    map_p = tma_map_8b(pp, 4, dims, str, bx);
+    map_c64 = tma_map_8b(p->levels[0]->pack64.get(), 3, cd, cs, bc);
+  }
   const unsigned grid = (unsigned)nblk * (unsigned)Bc;
   const double nb = (double)n * Bc;
   const double coef = (double)n * 8.0 * (DIM + 1);
@@ -1148,28 +1777,46 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   double sync_ms = 0.0;
   const auto wall0 = std::chrono::steady_clock::now();
   for (int b = 0; b < Bc; ++b) best[b] = bb[b];
+  // FD: rho = r^T z is fused into the V-cycle's last sweep (partials of f^T x on the finest
+  // level, f the multigrid copy of r); P1 keeps the separate dot kernel
+  const bool fused = p->kind != LT_GRID_P1_TRI;
+  const V* z = nullptr;
+  auto precondition = [&](int op) {
+    int dnb = 0;
+    z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr, fused ? partials.as<double2>() : nullptr,
+                       &dnb, tzm.data());
+    if (dnb == 0) {
+      dnb = nblk;
+      launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+        bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
+      });
+    }
+    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(op, bt, partials.get(), dnb, sc); });
+  };
   // z = B r ; rho = r^T z ; p = z
-  const V* z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
-  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
-    bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
-  });
-  launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RHO, bt, partials.get(), nblk, sc); });
+  precondition(OP_RHO);
   launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
   for (int it = 0; it < p->inner_maxit; ++it) {
-    const int nblk_apply = DIM == 3 ? zm_blocks(L0) : L0.ntiles;
+    const bool zm = DIM == 3 || p->kind != LT_GRID_P1_TRI;
+    const int nblk_apply = zm ? zm_blocks(L0) : L0.ntiles;
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
-      if (DIM == 3)
+      if (ta_ok)
+        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kT, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
+                                                                         bt, d_taus, q, partials.as<double2>(),
+                                                                         nblk_apply);
+      else if (zm)
         apply_dot_zm_kernel<<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
                                                                       nblk_apply);
       else
         apply_dot_kernel<DIM><<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q,
                                                                         partials.as<double2>(), nblk_apply);
     });
+    const double2* pdir = pp;
     launch(ctx, "cocg_scalar", 0.0, [&] {
       scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk_apply, sc);
     });
     launch(ctx, "cocg_vec", nb * ((it == 0 ? 64.0 : 80.0) + vb), [&] {
-      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pp, q, u, us, r, rmg, it == 0, (double*)partials.get(),
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pdir, q, u, us, r, rmg, it == 0, (double*)partials.get(),
                                             nblk);
     });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
@@ -1196,11 +1843,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       if (active == 0) break;
       LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
     }
-    z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr);
-    launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
-      bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
-    });
-    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BETA, bt, partials.get(), nblk, sc); });
+    precondition(OP_BETA);
     launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
     if (inner_trace()) iters_seen = it + 1;
   }

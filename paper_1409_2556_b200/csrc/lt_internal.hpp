@@ -1,6 +1,7 @@
 // Internal C++ types of the laptomo B200 library (not part of the C ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -179,6 +180,10 @@ struct Level {
   float* Md32 = nullptr;
   DeviceBuffer storage32;
   DeviceBuffer elem;       // P1: per-element kappa then S on this level (coarsening input)
+  // FD: per-cell packed {west face, south face, bottom face, mass} over (nx+1) x (ny+1) x
+  // (nz+1) (the high boundary faces in the extra row / column / plane), FP32 and FP64: the
+  // operand tiles of the TMA-fed z-marching kernels
+  DeviceBuffer pack32, pack64;
   int agg[3] = {1, 1, 1};  // aggregation to the next coarser level (FD)
 };
 
@@ -245,6 +250,11 @@ void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2*
 void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count);
 
 // inner.cu: u_b = (K + tau_b M)^{-1} v_b, b < B, strided vectors; taus on host.
+// Tiled TMA tensor map over 8-byte elements (no swizzle, out-of-bounds boxes read as zero);
+// dims / box innermost first, strides_bytes for dims 1.. (tma.cu)
+CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box);
+
 // device bytes a solve may still take: free + the pool's reserved-but-unused memory (ctx.cu)
 double available_device_bytes(lt_ctx ctx);
 

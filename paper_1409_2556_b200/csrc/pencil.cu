@@ -395,6 +395,28 @@ static void assemble_p1(lt_ctx ctx, Level& L, double h) {
   });
 }
 
+// out[(k (ny+1) + j) (nx+1) + i] = {Tx west face of (i,j,k), Ty south face, Tz bottom face, M}
+// over i <= nx, j <= ny, k <= nz (faces past the last cell of a row / column / stack in the
+// extra entries, zero where no such face exists); Tz null in 2-D
+template <class T4>
+__global__ void pack_coef_kernel(const double* __restrict__ Tx, const double* __restrict__ Ty,
+                                 const double* __restrict__ Tz, const double* __restrict__ M, int nx, int ny, int nz,
+                                 T4* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t cnt = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+  if (t >= cnt) return;
+  const int i = (int)(t % (nx + 1));
+  const int j = (int)((t / (nx + 1)) % (ny + 1));
+  const int k = (int)(t / ((int64_t)(nx + 1) * (ny + 1)));
+  const bool ci = i < nx, cj = j < ny, ck = k < nz;
+  const double tw = (cj && ck) ? Tx[((int64_t)k * ny + j) * (nx + 1) + i] : 0.0;
+  const double ts = (ci && ck) ? Ty[((int64_t)k * (ny + 1) + j) * nx + i] : 0.0;
+  const double tb = (Tz && ci && cj) ? Tz[((int64_t)k * ny + j) * nx + i] : 0.0;
+  const double m = (ci && cj && ck) ? M[((int64_t)k * ny + j) * nx + i] : 0.0;
+  using E = decltype(T4::x);
+  out[t] = T4{(E)tw, (E)ts, (E)tb, (E)m};
+}
+
 static void make_fp32_copies(lt_pencil p) {
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
@@ -553,6 +575,24 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
   }
   // FP32 copies of every level for the mixed-precision V-cycle (same layout)
   make_fp32_copies(p);
+  // packed operand arrays of the TMA-fed kernels: FP32 for the V-cycle levels, FP64 for the
+  // finest level (the COCG operator)
+  for (size_t l = 0; l < p->levels.size(); ++l) {
+    Level& Lv = *p->levels[l];
+    const int64_t cnt = (int64_t)(Lv.nx + 1) * (Lv.ny + 1) * (Lv.nz + 1);
+    Lv.pack32.allocate(sizeof(float4) * cnt, st);
+    launch(ctx, "assemble", 20.0 * cnt, [&] {
+      pack_coef_kernel<float4><<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx, Lv.ny,
+                                                                               Lv.nz, Lv.pack32.as<float4>());
+    });
+    if (l == 0) {
+      Lv.pack64.allocate(sizeof(double4) * cnt, st);
+      launch(ctx, "assemble", 36.0 * cnt, [&] {
+        pack_coef_kernel<double4><<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx,
+                                                                                  Lv.ny, Lv.nz, Lv.pack64.as<double4>());
+      });
+    }
+  }
   LT_CUDA(cudaStreamSynchronize(st));
 }
 
