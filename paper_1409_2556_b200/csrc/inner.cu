@@ -177,31 +177,6 @@ __global__ void __launch_bounds__(kT) residual_kernel(LevelViewT<R> L, Batch bt,
   r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
 }
 
-template <class R, int DIM>
-__global__ void __launch_bounds__(kT) restrict_kernel(LevelViewT<R> Lf, LevelViewT<R> Lc, int ax, int ay, int az,
-                                                      Batch bt, const typename CT<R>::V* __restrict__ rf,
-                                                      typename CT<R>::V* __restrict__ fc) {
-  using V = typename CT<R>::V;
-  TILE_PROLOGUE(Lc);
-  if (!in) return;
-  int Fx[4], Fy[4], Fz[4];
-  float wx[4], wy[4], wz[4];
-  const int nxx = r1d_terms(i, ax, Lc.nx, Fx, wx);
-  const int nyy = r1d_terms(j, ay, Lc.ny, Fy, wy);
-  int nzz = 1;
-  Fz[0] = 0; wz[0] = 1.0f;
-  if (DIM == 3) nzz = r1d_terms(k, az, Lc.nz, Fz, wz);
-  const V* rb = rf + (int64_t)b * Lf.n;
-  V s = vzero<V>();
-  for (int q = 0; q < nzz; ++q)
-    for (int p = 0; p < nyy; ++p) {
-      const R wzy = (R)(wz[q] * wy[p]);
-      const int64_t row = ((int64_t)Fz[q] * Lf.ny + Fy[p]) * Lf.nx;
-      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(rb[row + Fx[o]], wzy * (R)wx[o]));
-    }
-  fc[(int64_t)b * Lc.n + a] = s;
-}
-
 template <class R, class V>
 __device__ __forceinline__ V prolong_at(const LevelViewT<R>& Lc, int ax, int ay, int az, const V* __restrict__ eb,
                                         int i, int j, int k, int dim) {
@@ -220,188 +195,6 @@ __device__ __forceinline__ V prolong_at(const LevelViewT<R>& Lc, int ax, int ay,
       for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(eb[row + Ix[o]], wzy * (R)wx[o]));
     }
   return s;
-}
-
-// ---- fused red-black Gauss-Seidel sweep ------------------------------------------------
-// One full sweep (colour `first`, then the other colour) of a 32 x 8 (x, y) tile, marching
-// through z: x planes (halo 2) in a 5-slot shared-memory ring and f planes (halo 1) in a
-// 3-slot ring are filled one step ahead with cp.async; the first colour is updated on the
-// tile + 1-cell halo (from old second-colour values), the second colour on the tile (from
-// the new first-colour values).  Each cell of x and f is read from HBM once and x is written
-// once.  zero_init: the iterate is zero on entry.  ec != null: the iterate is xin + P ec
-// (fused coarse-grid correction).  Out of place (x != xin): halos of neighbouring tiles read xin.
-constexpr int SW_TX = 32, SW_TY = 8, SW_HX = SW_TX + 4, SW_HY = SW_TY + 4, SW_PL = SW_HX * SW_HY;
-constexpr int SW_FX = SW_TX + 2, SW_FPL = SW_FX * (SW_TY + 2);
-
-template <class V>
-__device__ __forceinline__ void cp_async_v(void* dst, const void* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  if (sizeof(V) == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
-}
-
-template <class R, int DIM>
-__global__ void __launch_bounds__(kT) rb_sweep_kernel(LevelViewT<R> L, Batch bt, const double2* __restrict__ taus,
-                                                      const typename CT<R>::V* __restrict__ f,
-                                                      const typename CT<R>::V* __restrict__ xin,
-                                                      typename CT<R>::V* __restrict__ x, int first, int zero_init,
-                                                      LevelViewT<R> Lc, int ax, int ay, int az,
-                                                      const typename CT<R>::V* __restrict__ ec) {
-  using V = typename CT<R>::V;
-  constexpr int NS = DIM == 3 ? 5 : 1;
-  extern __shared__ __align__(16) unsigned char sw_raw[];
-  V (*U)[SW_PL] = reinterpret_cast<V (*)[SW_PL]>(sw_raw);
-  V (*Fr)[SW_FPL] = reinterpret_cast<V (*)[SW_FPL]>(sw_raw + sizeof(V) * NS * SW_PL);
-  LT_ITEM_BLOCK(bt.B, b, cb);
-  if (bt.done[b]) return;
-  const int tiles_x = (L.nx + SW_TX - 1) / SW_TX;
-  const int i0 = (cb % tiles_x) * SW_TX, j0 = (cb / tiles_x) * SW_TY;
-  const int tid = threadIdx.x;
-  const R tr = (R)taus[b].x, ti = (R)taus[b].y;
-  const V* fb = f + (int64_t)b * L.n;
-  V* xb = x + (int64_t)b * L.n;
-  const V* xib = zero_init ? nullptr : xin + (int64_t)b * L.n;
-  const V* eb = ec ? ec + (int64_t)b * Lc.n : nullptr;
-  const int64_t plane = (int64_t)L.nx * L.ny;
-  const int second = first ^ 1;
-  auto slot = [](int k) { return DIM == 3 ? k % 5 : 0; };
-  auto fslot = [](int k) { return DIM == 3 ? k % 3 : 0; };
-  auto commit = [] { asm volatile("cp.async.commit_group;\n" ::); };
-  auto wait1 = [] { asm volatile("cp.async.wait_group 1;\n" ::); };
-  auto wait0 = [] { asm volatile("cp.async.wait_group 0;\n" ::); };
-
-  auto issue_x = [&](int k) {
-    V* S = U[slot(k)];
-    for (int e = tid; e < SW_PL; e += kT) {
-      const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
-      if (zero_init) {
-        S[e] = vzero<V>();
-      } else {
-        const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
-        cp_async_v<V>(S + e, ok ? xib + (k * plane + (int64_t)j * L.nx + i) : xib, ok);
-      }
-    }
-  };
-  auto issue_f = [&](int k) {
-    V* S = Fr[fslot(k)];
-    for (int e = tid; e < SW_FPL; e += kT) {
-      const int i = i0 - 1 + e % SW_FX, j = j0 - 1 + e / SW_FX;
-      const bool ok = i >= 0 && i < L.nx && j >= 0 && j < L.ny;
-      cp_async_v<V>(S + e, ok ? fb + (k * plane + (int64_t)j * L.nx + i) : fb, ok);
-    }
-  };
-  auto add_prolong = [&](int k) {
-    V* S = U[slot(k)];
-    for (int e = tid; e < SW_PL; e += kT) {
-      const int i = i0 - 2 + e % SW_HX, j = j0 - 2 + e / SW_HX;
-      if (i >= 0 && i < L.nx && j >= 0 && j < L.ny) S[e] = vadd(S[e], prolong_at(Lc, ax, ay, az, eb, i, j, k, DIM));
-    }
-  };
-  // Gauss-Seidel update of colour `color` on plane k over the tile grown by H cells: one
-  // thread per cell of that colour (i0, j0 even, so the colour parity of a row is known),
-  // compile-time region widths, 32-bit in-plane indices.
-  const int nxp1 = L.nx + 1;
-  auto update = [&](int k, int color, auto Hc) {
-    constexpr int H = decltype(Hc)::value;
-    constexpr int RX = SW_TX + 2 * H, RY = SW_TY + 2 * H, HALF = RX / 2;
-    if (tid >= RY * HALF) return;
-    const int lj = tid / HALF - H;
-    const int par = (color + lj + k) & 1;
-    const int li = -H + ((par + H) & 1) + 2 * (tid % HALF);
-    const int i = i0 + li, j = j0 + lj;
-    if (i < 0 || i >= L.nx || j < 0 || j >= L.ny) return;
-    V* S = U[slot(k)];
-    const V* Fk = Fr[fslot(k)];
-    const int s = (lj + 2) * SW_HX + (li + 2);
-    const int ip = j * L.nx + i;                       // in-plane cell index
-    const R* Txk = L.Tx + (int64_t)k * L.ny * nxp1;     // plane k of the x faces
-    const R* Tyk = L.Ty + (int64_t)k * (L.ny + 1) * L.nx;
-    const int ex = j * nxp1 + i, ey = ip;
-    const R tw = __ldg(Txk + ex), te = __ldg(Txk + ex + 1);
-    const R ts = __ldg(Tyk + ey), tn = __ldg(Tyk + ey + L.nx);
-    R dk = tw + te + ts + tn;
-    V o = Fk[(lj + 1) * SW_FX + (li + 1)];
-    if (i > 0) o = vadd(o, vscale(S[s - 1], tw));
-    if (i < L.nx - 1) o = vadd(o, vscale(S[s + 1], te));
-    if (j > 0) o = vadd(o, vscale(S[s - SW_HX], ts));
-    if (j < L.ny - 1) o = vadd(o, vscale(S[s + SW_HX], tn));
-    const int64_t a = k * plane + ip;
-    if (DIM == 3) {
-      const R tb = __ldg(L.Tz + a), tt = __ldg(L.Tz + a + plane);
-      dk += tb + tt;
-      if (k > 0) o = vadd(o, vscale(U[slot(k - 1)][s], tb));
-      if (k < L.nz - 1) o = vadd(o, vscale(U[slot(k + 1)][s], tt));
-    }
-    S[s] = diag_solve_r<R, V>(dk, __ldg(L.M + a), tr, ti, o);
-  };
-  using H1 = std::integral_constant<int, 1>;
-  using H0 = std::integral_constant<int, 0>;
-  auto store_plane = [&](int k) {
-    const V* S = U[slot(k)];
-    const int li = tid % SW_TX, lj = tid / SW_TX;
-    const int i = i0 + li, j = j0 + lj;
-    if (i < L.nx && j < L.ny) xb[k * plane + (int64_t)j * L.nx + i] = S[(lj + 2) * SW_HX + (li + 2)];
-  };
-
-  if (DIM == 2) {
-    issue_x(0);
-    issue_f(0);
-    commit();
-    wait0();
-    __syncthreads();
-    if (eb) {
-      add_prolong(0);
-      __syncthreads();
-    }
-    update(0, first, H1{});
-    __syncthreads();
-    update(0, second, H0{});
-    __syncthreads();
-    store_plane(0);
-    return;
-  }
-  // prologue: group A = {x0, x1, f0}, group B = {x2, f1}
-  issue_x(0);
-  if (L.nz > 1) issue_x(1);
-  issue_f(0);
-  commit();
-  if (L.nz > 2) issue_x(2);
-  if (L.nz > 1) issue_f(1);
-  commit();
-  wait1();
-  __syncthreads();
-  if (eb) {
-    add_prolong(0);
-    if (L.nz > 1) add_prolong(1);
-    __syncthreads();
-  }
-  update(0, first, H1{});
-  for (int k = 0; k < L.nz; ++k) {
-    // prefetch x(k+3), f(k+2); then wait for x(k+2), f(k+1) issued one step earlier
-    if (k + 3 < L.nz) issue_x(k + 3);
-    if (k + 2 < L.nz) issue_f(k + 2);
-    commit();
-    wait1();
-    __syncthreads();
-    if (eb && k + 2 < L.nz) {
-      add_prolong(k + 2);
-      __syncthreads();
-    }
-    if (k + 1 < L.nz) update(k + 1, first, H1{});
-    __syncthreads();
-    update(k, second, H0{});
-    __syncthreads();
-    store_plane(k);
-  }
-  wait0();
-}
-
-template <class R>
-size_t sweep_smem(int dim) {
-  using V = typename CT<R>::V;
-  return sizeof(V) * ((dim == 3 ? 5 : 1) * SW_PL + (dim == 3 ? 3 : 1) * SW_FPL);
 }
 
 // e = A_c(tau_b)^{-1} f: one warp per row of the dense complex inverse (row stride ld, column
