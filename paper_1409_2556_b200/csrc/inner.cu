@@ -839,6 +839,9 @@ __device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t ok = 0;
   do {
@@ -897,16 +900,23 @@ inline int tz_blocks(const VW& L) {
   return ((L.nx + TZ_W - 1) / TZ_W) * ((L.ny + TZ_H - 1) / TZ_H) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
 }
 
+// Producer / consumer layout of the TMA kernels: warps 0..7 compute (one (x, y) cell or pair
+// each), warp 8 is the producer -- one lane issues each plane's copies into the ring once the
+// eight consumer warps have released that slot (per-slot "empty" barrier, one arrival per
+// consumer warp), so consumer warps never wait on each other and the loads run TZ_D - 2
+// planes ahead of the slowest warp.
+constexpr int kTP = kT + 32;
+
 // mode 0: red-black half sweep of `color` in place on x (zero_init: x = 0 on entry; dot: also
 // the partials of f^T x after the sweep); mode 1: r = f - A x.
 template <int MODE>
-__global__ void __launch_bounds__(kT, 2) mg_tma_kernel(const __grid_constant__ CUtensorMap mx,
-                                                       const __grid_constant__ CUtensorMap mf,
-                                                       const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
-                                                       const double2* __restrict__ taus, float2* __restrict__ out,
-                                                       int color, int zero_init, double2* __restrict__ dot, int nblk) {
+__global__ void __launch_bounds__(kTP, 2) mg_tma_kernel(const __grid_constant__ CUtensorMap mx,
+                                                        const __grid_constant__ CUtensorMap mf,
+                                                        const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                        const double2* __restrict__ taus, float2* __restrict__ out,
+                                                        int color, int zero_init, double2* __restrict__ dot, int nblk) {
   extern __shared__ __align__(128) unsigned char tz_smem[];
-  __shared__ __align__(8) uint64_t bar[TZ_D];
+  __shared__ __align__(8) uint64_t full[TZ_D], empty[TZ_D];
   LT_ITEM_BLOCK(bt.B, b, cb);
   if (bt.done[b]) return;
   const int tiles_x = (L.nx + TZ_W - 1) / TZ_W, tiles_y = (L.ny + TZ_H - 1) / TZ_H;
@@ -915,112 +925,120 @@ __global__ void __launch_bounds__(kT, 2) mg_tma_kernel(const __grid_constant__ C
   const int x0 = (tile % tiles_x) * TZ_W, y0 = (tile / tiles_x) * TZ_H;
   const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const int i0 = x0 + 2 * lane, j = y0 + wy;
-  const bool in = i0 < L.nx && j < L.ny;
-  const bool ldx = MODE == 1 || !zero_init;
   const ZRing<TZ_D> ring{k0};
   if (tid == 0) {
-    for (int s = 0; s < TZ_D; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < TZ_D; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
     mbar_init_fence();
   }
   __syncthreads();
-  auto issue = [&](int p) {
-    unsigned char* s = tz_smem + (size_t)ring.slot(p) * TZ_SLOT;
-    uint64_t* br = &bar[ring.slot(p)];
-    const bool lf = p >= k0 && p < k1, lc = p >= k0;
-    mbar_arrive_tx(br, (ldx ? TZ_XB : 0u) + (lf ? TZ_FB : 0u) + (lc ? TZ_CB : 0u));
-    if (ldx) tma_load4(s, &mx, x0 - 2, y0 - 1, p, b, br);
-    if (lf) tma_load4(s + TZ_OFF_F, &mf, x0, y0, p, b, br);
-    if (lc) tma_load3(s + TZ_OFF_C, &mc, 2 * x0, y0, p, br);
-  };
-  if (tid == 0)
-    for (int p = k0 - 1; p <= min(k1, k0 - 2 + TZ_D); ++p) issue(p);
-  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
-  const int64_t plane = (int64_t)L.nx * L.ny;
-  float2* ob = out + (int64_t)b * L.n;
   double2 acc = make_double2(0.0, 0.0);
-  for (int k = k0; k < k1; ++k) {
-    mbar_wait(&bar[ring.slot(k - 1)], ring.parity(k - 1));
-    mbar_wait(&bar[ring.slot(k)], ring.parity(k));
-    mbar_wait(&bar[ring.slot(k + 1)], ring.parity(k + 1));
-    const unsigned char* sm = tz_smem + (size_t)ring.slot(k - 1) * TZ_SLOT;
-    const unsigned char* s0 = tz_smem + (size_t)ring.slot(k) * TZ_SLOT;
-    const unsigned char* sp = tz_smem + (size_t)ring.slot(k + 1) * TZ_SLOT;
-    auto X = [](const unsigned char* s, int yy, int xx) { return reinterpret_cast<const float2*>(s)[yy * TZ_XW + xx]; };
-    auto F = [](const unsigned char* s, int yy, int xx) {
-      return reinterpret_cast<const float2*>(s + TZ_OFF_F)[yy * TZ_W + xx];
-    };
-    auto Cf = [](const unsigned char* s, int yy, int xx) {
-      return reinterpret_cast<const float4*>(s + TZ_OFF_C)[yy * TZ_CW + xx];
-    };
-    if (in) {
-      const int c0 = 2 * lane;  // pair's first cell in F / C tile coordinates (X: + 2, + 1 row)
-      float2* dst = ob + k * plane + (int64_t)j * L.nx + i0;
-      if (MODE == 0) {
-        const int off = (j + k + color) & 1;
-        const int cx = c0 + off, xx = cx + 2;
-        const float4 cc = Cf(s0, wy, cx);
-        const float te = Cf(s0, wy, cx + 1).x, tn = Cf(s0, wy + 1, cx).y, tt = Cf(sp, wy, cx).z;
-        const float dk = cc.x + te + cc.y + tn + cc.z + tt;
-        float2 o = F(s0, wy, cx);
-        float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!zero_init) {
-          pr = *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
-          const float2 w = X(s0, wy + 1, xx - 1), e = X(s0, wy + 1, xx + 1);
-          const float2 so = X(s0, wy, xx), no = X(s0, wy + 2, xx);
-          const float2 dn = X(sm, wy + 1, xx), up = X(sp, wy + 1, xx);
-          o.x += cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
-          o.y += cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
-        }
-        const float2 nv = diag_solve_r<float, float2>(dk, cc.w, tr, ti, o);
-        if (off) {
-          pr.z = nv.x;
-          pr.w = nv.y;
-        } else {
-          pr.x = nv.x;
-          pr.y = nv.y;
-        }
-        *reinterpret_cast<float4*>(dst) = pr;
-        if (dot) {
-          const float2 fa = F(s0, wy, c0), fc = F(s0, wy, c0 + 1);
-          acc = cfma(make_double2(fa.x, fa.y), make_double2(pr.x, pr.y), acc);
-          acc = cfma(make_double2(fc.x, fc.y), make_double2(pr.z, pr.w), acc);
-        }
-      } else {
-        const float4 pr = *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
-        const float2 xa = make_float2(pr.x, pr.y), xc = make_float2(pr.z, pr.w);
-        float4 res;
-        {
-          const float4 ca = Cf(s0, wy, c0);
-          const float te = Cf(s0, wy, c0 + 1).x, tn = Cf(s0, wy + 1, c0).y, tt = Cf(sp, wy, c0).z;
-          const float2 w = X(s0, wy + 1, c0 + 1), so = X(s0, wy, c0 + 2), no = X(s0, wy + 2, c0 + 2);
-          const float2 dn = X(sm, wy + 1, c0 + 2), up = X(sp, wy + 1, c0 + 2);
-          const float dk = ca.x + te + ca.y + tn + ca.z + tt;
-          const float dr = dk + tr * ca.w, di = ti * ca.w;
-          const float ox = ca.x * w.x + te * xc.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
-          const float oy = ca.x * w.y + te * xc.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
-          const float2 f = F(s0, wy, c0);
-          res.x = f.x - (dr * xa.x - di * xa.y - ox);
-          res.y = f.y - (dr * xa.y + di * xa.x - oy);
-        }
-        {
-          const float4 ca = Cf(s0, wy, c0 + 1);
-          const float te = Cf(s0, wy, c0 + 2).x, tn = Cf(s0, wy + 1, c0 + 1).y, tt = Cf(sp, wy, c0 + 1).z;
-          const float2 e = X(s0, wy + 1, c0 + 4), so = X(s0, wy, c0 + 3), no = X(s0, wy + 2, c0 + 3);
-          const float2 dn = X(sm, wy + 1, c0 + 3), up = X(sp, wy + 1, c0 + 3);
-          const float dk = ca.x + te + ca.y + tn + ca.z + tt;
-          const float dr = dk + tr * ca.w, di = ti * ca.w;
-          const float ox = ca.x * xa.x + te * e.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
-          const float oy = ca.x * xa.y + te * e.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
-          const float2 f = F(s0, wy, c0 + 1);
-          res.z = f.x - (dr * xc.x - di * xc.y - ox);
-          res.w = f.y - (dr * xc.y + di * xc.x - oy);
-        }
-        *reinterpret_cast<float4*>(dst) = res;
+  if (wy == kT / 32) {  // producer warp
+    if (lane == 0) {
+      const bool ldx = MODE == 1 || !zero_init;
+      for (int p = k0 - 1; p <= k1; ++p) {
+        const int use = (p - k0 + 1) / TZ_D, s = ring.slot(p);
+        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = tz_smem + (size_t)s * TZ_SLOT;
+        const bool lf = p >= k0 && p < k1, lc = p >= k0;
+        mbar_arrive_tx(&full[s], (ldx ? TZ_XB : 0u) + (lf ? TZ_FB : 0u) + (lc ? TZ_CB : 0u));
+        if (ldx) tma_load4(sp, &mx, x0 - 2, y0 - 1, p, b, &full[s]);
+        if (lf) tma_load4(sp + TZ_OFF_F, &mf, x0, y0, p, b, &full[s]);
+        if (lc) tma_load3(sp + TZ_OFF_C, &mc, 2 * x0, y0, p, &full[s]);
       }
     }
-    __syncthreads();  // every thread is done with plane k - 1's slot
-    if (tid == 0 && k - 1 + TZ_D <= k1) issue(k - 1 + TZ_D);
+  } else {
+    const int i0 = x0 + 2 * lane, j = y0 + wy;
+    const bool in = i0 < L.nx && j < L.ny;
+    const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+    const int64_t plane = (int64_t)L.nx * L.ny;
+    float2* ob = out + (int64_t)b * L.n;
+    for (int k = k0; k < k1; ++k) {
+      mbar_wait(&full[ring.slot(k - 1)], ring.parity(k - 1));
+      mbar_wait(&full[ring.slot(k)], ring.parity(k));
+      mbar_wait(&full[ring.slot(k + 1)], ring.parity(k + 1));
+      const unsigned char* sm = tz_smem + (size_t)ring.slot(k - 1) * TZ_SLOT;
+      const unsigned char* s0 = tz_smem + (size_t)ring.slot(k) * TZ_SLOT;
+      const unsigned char* sp = tz_smem + (size_t)ring.slot(k + 1) * TZ_SLOT;
+      auto X = [](const unsigned char* s, int yy, int xx) { return reinterpret_cast<const float2*>(s)[yy * TZ_XW + xx]; };
+      auto F = [](const unsigned char* s, int yy, int xx) {
+        return reinterpret_cast<const float2*>(s + TZ_OFF_F)[yy * TZ_W + xx];
+      };
+      auto Cf = [](const unsigned char* s, int yy, int xx) {
+        return reinterpret_cast<const float4*>(s + TZ_OFF_C)[yy * TZ_CW + xx];
+      };
+      if (in) {
+        const int c0 = 2 * lane;  // pair's first cell in F / C tile coordinates (X: + 2, + 1 row)
+        float2* dst = ob + k * plane + (int64_t)j * L.nx + i0;
+        if (MODE == 0) {
+          const int off = (j + k + color) & 1;
+          const int cx = c0 + off, xx = cx + 2;
+          const float4 cc = Cf(s0, wy, cx);
+          const float te = Cf(s0, wy, cx + 1).x, tn = Cf(s0, wy + 1, cx).y, tt = Cf(sp, wy, cx).z;
+          const float dk = cc.x + te + cc.y + tn + cc.z + tt;
+          float2 o = F(s0, wy, cx);
+          float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (!zero_init) {
+            pr = *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
+            const float2 w = X(s0, wy + 1, xx - 1), e = X(s0, wy + 1, xx + 1);
+            const float2 so = X(s0, wy, xx), no = X(s0, wy + 2, xx);
+            const float2 dn = X(sm, wy + 1, xx), up = X(sp, wy + 1, xx);
+            o.x += cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
+            o.y += cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
+          }
+          const float2 nv = diag_solve_r<float, float2>(dk, cc.w, tr, ti, o);
+          if (off) {
+            pr.z = nv.x;
+            pr.w = nv.y;
+          } else {
+            pr.x = nv.x;
+            pr.y = nv.y;
+          }
+          *reinterpret_cast<float4*>(dst) = pr;
+          if (dot) {
+            const float2 fa = F(s0, wy, c0), fc = F(s0, wy, c0 + 1);
+            acc = cfma(make_double2(fa.x, fa.y), make_double2(pr.x, pr.y), acc);
+            acc = cfma(make_double2(fc.x, fc.y), make_double2(pr.z, pr.w), acc);
+          }
+        } else {
+          const float4 pr =
+              *reinterpret_cast<const float4*>(&reinterpret_cast<const float2*>(s0)[(wy + 1) * TZ_XW + c0 + 2]);
+          const float2 xa = make_float2(pr.x, pr.y), xc = make_float2(pr.z, pr.w);
+          float4 res;
+          {
+            const float4 ca = Cf(s0, wy, c0);
+            const float te = Cf(s0, wy, c0 + 1).x, tn = Cf(s0, wy + 1, c0).y, tt = Cf(sp, wy, c0).z;
+            const float2 w = X(s0, wy + 1, c0 + 1), so = X(s0, wy, c0 + 2), no = X(s0, wy + 2, c0 + 2);
+            const float2 dn = X(sm, wy + 1, c0 + 2), up = X(sp, wy + 1, c0 + 2);
+            const float dk = ca.x + te + ca.y + tn + ca.z + tt;
+            const float dr = dk + tr * ca.w, di = ti * ca.w;
+            const float ox = ca.x * w.x + te * xc.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
+            const float oy = ca.x * w.y + te * xc.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
+            const float2 f = F(s0, wy, c0);
+            res.x = f.x - (dr * xa.x - di * xa.y - ox);
+            res.y = f.y - (dr * xa.y + di * xa.x - oy);
+          }
+          {
+            const float4 ca = Cf(s0, wy, c0 + 1);
+            const float te = Cf(s0, wy, c0 + 2).x, tn = Cf(s0, wy + 1, c0 + 1).y, tt = Cf(sp, wy, c0 + 1).z;
+            const float2 e = X(s0, wy + 1, c0 + 4), so = X(s0, wy, c0 + 3), no = X(s0, wy + 2, c0 + 3);
+            const float2 dn = X(sm, wy + 1, c0 + 3), up = X(sp, wy + 1, c0 + 3);
+            const float dk = ca.x + te + ca.y + tn + ca.z + tt;
+            const float dr = dk + tr * ca.w, di = ti * ca.w;
+            const float ox = ca.x * xa.x + te * e.x + ca.y * so.x + tn * no.x + ca.z * dn.x + tt * up.x;
+            const float oy = ca.x * xa.y + te * e.y + ca.y * so.y + tn * no.y + ca.z * dn.y + tt * up.y;
+            const float2 f = F(s0, wy, c0 + 1);
+            res.z = f.x - (dr * xc.x - di * xc.y - ox);
+            res.w = f.y - (dr * xc.y + di * xc.x - oy);
+          }
+          *reinterpret_cast<float4*>(dst) = res;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ring.slot(k - 1)]);  // this warp is done with plane k - 1
+    }
   }
   if (MODE == 0 && dot) {
     acc = block_sum(acc);
@@ -1039,12 +1057,12 @@ constexpr uint32_t TA_OFF_C = 5504, TA_SLOT = TA_OFF_C + 9600;
 constexpr size_t TA_SMEM = (size_t)TA_SLOT * TA_D;
 
 // q = A(tau) p, partial p^T q (FP64)
-__global__ void __launch_bounds__(kT, 3) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
-                                                          const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
-                                                          const double2* __restrict__ taus, double2* __restrict__ q,
-                                                          double2* __restrict__ part, int nblk) {
+__global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
+                                                           const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                           const double2* __restrict__ taus, double2* __restrict__ q,
+                                                           double2* __restrict__ part, int nblk) {
   extern __shared__ __align__(128) unsigned char ta_smem[];
-  __shared__ __align__(8) uint64_t bar[TA_D];
+  __shared__ __align__(8) uint64_t full[TA_D], empty[TA_D];
   LT_ITEM_BLOCK(bt.B, b, cb);
   if (bt.done[b]) return;
   const int tiles_x = (L.nx + TA_W - 1) / TA_W, tiles_y = (L.ny + TA_H - 1) / TA_H;
@@ -1053,56 +1071,65 @@ __global__ void __launch_bounds__(kT, 3) apply_tma_kernel(const __grid_constant_
   const int x0 = (tile % tiles_x) * TA_W, y0 = (tile / tiles_x) * TA_H;
   const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const int i = x0 + lane, j = y0 + wy;
-  const bool in = i < L.nx && j < L.ny;
   const ZRing<TA_D> ring{k0};
   if (tid == 0) {
-    for (int s = 0; s < TA_D; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < TA_D; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
     mbar_init_fence();
   }
   __syncthreads();
-  auto issue = [&](int p) {
-    unsigned char* s = ta_smem + (size_t)ring.slot(p) * TA_SLOT;
-    uint64_t* br = &bar[ring.slot(p)];
-    const bool lc = p >= k0;
-    mbar_arrive_tx(br, TA_XB + (lc ? TA_CB : 0u));
-    tma_load4(s, &mp, 2 * (x0 - 1), y0 - 1, p, b, br);
-    if (lc) tma_load3(s + TA_OFF_C, &mc, 4 * x0, y0, p, br);
-  };
-  if (tid == 0)
-    for (int p = k0 - 1; p <= min(k1, k0 - 2 + TA_D); ++p) issue(p);
-  const double2 tau = taus[b];
-  const int64_t plane = (int64_t)L.nx * L.ny;
-  double2* qb = q + (int64_t)b * L.n;
   double2 acc = make_double2(0.0, 0.0);
-  for (int k = k0; k < k1; ++k) {
-    mbar_wait(&bar[ring.slot(k - 1)], ring.parity(k - 1));
-    mbar_wait(&bar[ring.slot(k)], ring.parity(k));
-    mbar_wait(&bar[ring.slot(k + 1)], ring.parity(k + 1));
-    if (in) {
-      const unsigned char* sm = ta_smem + (size_t)ring.slot(k - 1) * TA_SLOT;
-      const unsigned char* s0 = ta_smem + (size_t)ring.slot(k) * TA_SLOT;
-      const unsigned char* sp = ta_smem + (size_t)ring.slot(k + 1) * TA_SLOT;
-      auto X = [](const unsigned char* s, int yy, int xx) { return reinterpret_cast<const double2*>(s)[yy * TA_XW + xx]; };
-      auto Cf = [](const unsigned char* s, int yy, int xx) {
-        return reinterpret_cast<const double4*>(s + TA_OFF_C)[yy * TA_CW + xx];
-      };
-      const double4 cc = Cf(s0, wy, lane);
-      const double te = Cf(s0, wy, lane + 1).x, tn = Cf(s0, wy + 1, lane).y, tt = Cf(sp, wy, lane).z;
-      const double2 pc = X(s0, wy + 1, lane + 1);
-      const double2 w = X(s0, wy + 1, lane), e = X(s0, wy + 1, lane + 2);
-      const double2 so = X(s0, wy, lane + 1), no = X(s0, wy + 2, lane + 1);
-      const double2 dn = X(sm, wy + 1, lane + 1), up = X(sp, wy + 1, lane + 1);
-      const double dk = cc.x + te + cc.y + tn + cc.z + tt;
-      const double ox = cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
-      const double oy = cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
-      const double dr = dk + tau.x * cc.w, di = tau.y * cc.w;
-      const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
-      qb[k * plane + (int64_t)j * L.nx + i] = qa;
-      acc = cfma(pc, qa, acc);
+  if (wy == kT / 32) {  // producer warp
+    if (lane == 0) {
+      for (int p = k0 - 1; p <= k1; ++p) {
+        const int use = (p - k0 + 1) / TA_D, s = ring.slot(p);
+        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = ta_smem + (size_t)s * TA_SLOT;
+        const bool lc = p >= k0;
+        mbar_arrive_tx(&full[s], TA_XB + (lc ? TA_CB : 0u));
+        tma_load4(sp, &mp, 2 * (x0 - 1), y0 - 1, p, b, &full[s]);
+        if (lc) tma_load3(sp + TA_OFF_C, &mc, 4 * x0, y0, p, &full[s]);
+      }
     }
-    __syncthreads();
-    if (tid == 0 && k - 1 + TA_D <= k1) issue(k - 1 + TA_D);
+  } else {
+    const int i = x0 + lane, j = y0 + wy;
+    const bool in = i < L.nx && j < L.ny;
+    const double2 tau = taus[b];
+    const int64_t plane = (int64_t)L.nx * L.ny;
+    double2* qb = q + (int64_t)b * L.n;
+    for (int k = k0; k < k1; ++k) {
+      mbar_wait(&full[ring.slot(k - 1)], ring.parity(k - 1));
+      mbar_wait(&full[ring.slot(k)], ring.parity(k));
+      mbar_wait(&full[ring.slot(k + 1)], ring.parity(k + 1));
+      if (in) {
+        const unsigned char* sm = ta_smem + (size_t)ring.slot(k - 1) * TA_SLOT;
+        const unsigned char* s0 = ta_smem + (size_t)ring.slot(k) * TA_SLOT;
+        const unsigned char* sp = ta_smem + (size_t)ring.slot(k + 1) * TA_SLOT;
+        auto X = [](const unsigned char* s, int yy, int xx) {
+          return reinterpret_cast<const double2*>(s)[yy * TA_XW + xx];
+        };
+        auto Cf = [](const unsigned char* s, int yy, int xx) {
+          return reinterpret_cast<const double4*>(s + TA_OFF_C)[yy * TA_CW + xx];
+        };
+        const double4 cc = Cf(s0, wy, lane);
+        const double te = Cf(s0, wy, lane + 1).x, tn = Cf(s0, wy + 1, lane).y, tt = Cf(sp, wy, lane).z;
+        const double2 pc = X(s0, wy + 1, lane + 1);
+        const double2 w = X(s0, wy + 1, lane), e = X(s0, wy + 1, lane + 2);
+        const double2 so = X(s0, wy, lane + 1), no = X(s0, wy + 2, lane + 1);
+        const double2 dn = X(sm, wy + 1, lane + 1), up = X(sp, wy + 1, lane + 1);
+        const double dk = cc.x + te + cc.y + tn + cc.z + tt;
+        const double ox = cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
+        const double oy = cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
+        const double dr = dk + tau.x * cc.w, di = tau.y * cc.w;
+        const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
+        qb[k * plane + (int64_t)j * L.nx + i] = qa;
+        acc = cfma(pc, qa, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ring.slot(k - 1)]);
+    }
   }
   acc = block_sum(acc);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
@@ -1385,7 +1412,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   auto half = [&](int color, int zero_init, double2* dot) {
     launch(ctx, "mg_smooth", cell_bytes * (zero_init ? 2 : 3) * vb + coef, [&] {
       if (tma)
-        mg_tma_kernel<0><<<tgrid, kT, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
+        mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
       else if (pairs)
         rbpair_zm_kernel<R><<<pgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], color, zero_init, dot, zp_blocks(L));
@@ -1402,7 +1429,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   }
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
     if (tma)
-      mg_tma_kernel<1><<<tgrid, kT, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
+      mg_tma_kernel<1><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
                                                  nullptr, 0);
     else if (pairs)
       residual_pair_zm_kernel<R><<<pgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
@@ -1594,7 +1621,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     const int nblk_apply = zm ? zm_blocks(L0) : L0.ntiles;
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
       if (ta_ok)
-        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kT, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
+        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kTP, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
                                                                          bt, d_taus, q, partials.as<double2>(),
                                                                          nblk_apply);
       else if (zm)
