@@ -344,17 +344,20 @@ __global__ void small_solve(State S, int m, int force) {
 }
 
 // True residual r = b - (K + z M) U y for every flagged shift of an item:
-// partial ||r||^2 per (item, shift).  K u_j and M u_j are formed once per column.
+// partial ||r||^2 per (item, shift).  K u_j and M u_j are formed once per column and
+// accumulated as sum_j y_jq K u_j + (y_jq z_q) M u_j (y z staged in shared memory); the KC
+// per-shift partial norms are reduced together (one barrier per chunk, not one per shift).
 template <int DIM>
-__global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int m, const double2* __restrict__ rhs,
-                                                      const double2* const* __restrict__ Ucols, double* __restrict__ part) {
+__global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, int m, const double2* __restrict__ rhs,
+                                                         const double2* const* __restrict__ Ucols,
+                                                         double* __restrict__ part) {
   constexpr int KC = 16;  // shifts per register chunk
   constexpr int MJ = 16;  // Krylov columns whose coefficients are staged in shared memory
-  __shared__ double sh[32];
+  constexpr int NW = kT / 32;
   __shared__ int flagged[256];
   __shared__ int nflag;
-  __shared__ double2 ysm[KC][MJ];
-  __shared__ double2 zsm[KC];
+  __shared__ double2 ysm[MJ][KC], yzsm[MJ][KC];
+  __shared__ double red[NW][KC];
   LT_ITEM_BLOCK(S.B, b, cb);
   if (threadIdx.x == 0) {
     int c = 0;
@@ -364,6 +367,7 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
   }
   __syncthreads();
   if (nflag == 0) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int i, jj, kk;
   int64_t a;
   const bool in = tile_cell(L, (int)cb, i, jj, kk, a);
@@ -375,10 +379,16 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
     __syncthreads();
     if (staged) {
       for (int e = threadIdx.x; e < KC * MJ; e += blockDim.x) {
-        const int q = e / MJ, j = e % MJ;
-        if (q < nc && j < m) ysm[q][j] = S.Y[(int64_t)(b * S.ns + flagged[c0 + q]) * S.maxit + j];
+        const int j = e / KC, q = e % KC;
+        double2 y = make_double2(0.0, 0.0), yz = y;
+        if (q < nc && j < m) {
+          const int t = b * S.ns + flagged[c0 + q];
+          y = S.Y[(int64_t)t * S.maxit + j];
+          yz = cmul(y, S.shifts[t]);
+        }
+        ysm[j][q] = y;
+        yzsm[j][q] = yz;
       }
-      if (threadIdx.x < nc) zsm[threadIdx.x] = S.shifts[b * S.ns + flagged[c0 + threadIdx.x]];
     }
     __syncthreads();
     double2 acc[KC];
@@ -397,21 +407,33 @@ __global__ void __launch_bounds__(kT) verify_residual(LevelView L, State S, int 
 #pragma unroll
         for (int q = 0; q < KC; ++q) {
           if (q < nc) {
-            const int t = b * S.ns + flagged[c0 + q];
-            const double2 y = staged ? ysm[q][j] : S.Y[(int64_t)t * S.maxit + j];
-            const double2 z = staged ? zsm[q] : S.shifts[t];
-            acc[q] = cadd(acc[q], cmul(y, cadd(Ku, cmul(z, Mu))));
+            double2 y, yz;
+            if (staged) {
+              y = ysm[j][q];
+              yz = yzsm[j][q];
+            } else {
+              const int t = b * S.ns + flagged[c0 + q];
+              y = S.Y[(int64_t)t * S.maxit + j];
+              yz = cmul(y, S.shifts[t]);
+            }
+            acc[q] = cfma(y, Ku, cfma(yz, Mu, acc[q]));
           }
         }
       }
     }
+    // per-shift partial norms: warp sums, then one pass over the NW warp results
 #pragma unroll
     for (int q = 0; q < KC; ++q) {
-      if (q < nc) {  // uniform across the block
-        const double2 r = csub(bv, acc[q]);
-        const double nn = block_sum_d(in ? cabs2(r) : 0.0, sh);
-        if (threadIdx.x == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = nn;
-      }
+      double nn = 0.0;
+      if (q < nc && in) nn = cabs2(csub(bv, acc[q]));
+      nn = warp_sum_d(nn);
+      if (lane == 0) red[w][q] = nn;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      double t = 0.0;
+      for (int v = 0; v < NW; ++v) t += red[v][threadIdx.x];
+      part[((int64_t)b * S.ns + flagged[c0 + threadIdx.x]) * S.nblk_tile + cb] = t;
     }
   }
 }
