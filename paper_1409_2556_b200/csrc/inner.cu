@@ -1410,7 +1410,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   const unsigned tgrid = (unsigned)tz_blocks(L) * (unsigned)Bc;
   const TzDims tdims{L.nx, L.ny, L.nz, L.n};
   auto half = [&](int color, int zero_init, double2* dot) {
-    launch(ctx, "mg_smooth", cell_bytes * (zero_init ? 2 : 3) * vb + coef, [&] {
+    // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled
+    launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", cell_bytes * (zero_init ? 2 : 3) * vb + coef, [&] {
       if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));

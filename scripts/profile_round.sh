@@ -10,7 +10,7 @@ mkdir -p $OUT
 timeout 900 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err || { echo "bench failed"; tail -20 $OUT/${TAG}_bench.err; exit 1; }
 cat $OUT/${TAG}_bench.json
 # launch list: skip the warm-up build, record one timed build (~12k launches)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 12000 -c 12500 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 10000 -c 9500 --csv \
   --log-file $OUT/${TAG}_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline \
   > $OUT/${TAG}_ncu_launch.log 2>&1 || echo "launch list failed"
 for KS in "$@"; do   # kernel_regex:launches_to_skip
