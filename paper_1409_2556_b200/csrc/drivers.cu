@@ -54,17 +54,22 @@ __global__ void gather_points(int64_t n, int B, int n_pts, const double* __restr
 }
 
 // predictions[s][r] = 2 Re sum_k w_k sum_q wq phi_{s,k}[idx_q]
+// (cell_major fields: f[(k n + a) B + s], B = n_src + n_rec)
 __global__ void predict_kernel(int64_t n, int n_src, int n_rec, int ns, const double2* __restrict__ fields,
                                const double2* __restrict__ w, const int64_t* __restrict__ idx, const double* __restrict__ wt,
-                               const int* __restrict__ cnt, double* __restrict__ out) {
+                               const int* __restrict__ cnt, double* __restrict__ out, int cell_major) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_src * n_rec) return;
   const int s = t / n_rec, r = t % n_rec;
+  const int B = n_src + n_rec;
   double2 acc = make_double2(0.0, 0.0);
   for (int k = 0; k < ns; ++k) {
-    const double2* f = fields + ((int64_t)s * ns + k) * n;
     double2 v = make_double2(0.0, 0.0);
-    for (int q = 0; q < cnt[r]; ++q) v = cadd(v, cscale(f[idx[r * 8 + q]], wt[r * 8 + q]));
+    for (int q = 0; q < cnt[r]; ++q) {
+      const int64_t a = idx[r * 8 + q];
+      const double2 fv = cell_major ? fields[((int64_t)k * n + a) * B + s] : fields[((int64_t)s * ns + k) * n + a];
+      v = cadd(v, cscale(fv, wt[r * 8 + q]));
+    }
     acc = cadd(acc, cmul(w[k], v));
   }
   out[t] = 2.0 * acc.x;
@@ -223,6 +228,348 @@ __global__ void __launch_bounds__(kT, 2) jacobian_kernel(LevelView L, const doub
           if (r0 + q >= n_rec) continue;
           const int64_t rowj = (int64_t)(s0 + i) * n_rec + (r0 + q);
           Jout[rowj * ldj + a] = 2.0 * acc[i][q];
+        }
+      }
+    }
+  }
+}
+
+// ---- Jacobian on the FP64 tensor cores (mma.sync m8n8k4 .f64) ------------------------------
+// Per cell a the kappa and storativity rows are small real GEMMs.  With the 2d+1 points of the
+// cell (centre, face neighbours b_f) and the arrow transform of the source fields
+//   A_0 = w_k sum_f wt_f (phi_a - phi_bf),  A_f = -w_k wt_f (phi_a - phi_bf),
+// sum_f wt_f (phi_a - phi_bf)(psi_a - psi_bf) = sum_p A_p psi_p, so
+//   J_k[s, r] = 2 Re sum_{k, p} A_{k,p}[s] psi_{k,p}[r],   J_S[s, r] = 2 Re sum_k wz_k S_a h^d phi_a psi_a
+// = real GEMMs over K = (shift, point, re/im) whose B operand is the raw receiver field (no
+// difference pass for the receivers).  A persistent CTA walks tasks = (tile of 2 cells of a
+// row, pair of shifts), warp-specialised:
+//   producer warp 8 : bulk-copies each task's raw fields (all items at the tile's 12 points,
+//                     one contiguous B x 16-byte run per (shift, point) of the cell-major field
+//                     array) into a 4-deep ring, 3 tasks ahead;
+//   producer warps 8-15: the arrow transform of the 16 sources into mma A fragments
+//                     (double-buffered; 4 lanes per (cell, shift, source), faces split);
+//   consumer warps 0-7: warp = (cell, 16 receivers): 2 x 2 accumulator tiles per block.
+// mbarriers hand the stages over; J is written after a tile's last shift pair.
+// Requires n_src <= 16 and n_rec <= 64.
+constexpr int JW_TC = 2;  // cells per tile
+constexpr int JW_SMAX = 16, JW_RMAX = 64;
+constexpr int JW_NRAW = 4, JW_AHEAD = 3;
+constexpr int JW_CONS = 8, JW_PROD = 8;
+constexpr int JW_NA = 2;  // A-fragment buffers
+constexpr int JW_THREADS = 32 * (JW_CONS + JW_PROD);
+
+template <int DIM>
+struct JwGeom {
+  static constexpr int NPC = 2 * DIM + 1;          // points per cell
+  static constexpr int NCH = DIM == 3 ? 36 : 24;   // B-item chunks per ring slot (two TMA boxes)
+  static constexpr int KS = NPC;                    // K steps per shift pair (2 NPC 2 / 4)
+};
+
+// A ring slot holds two TMA boxes of the cell-major field array (x = cells of the row):
+//   box A: shifts kp..kp+1 x rows j-1..j+1 x cells i0-1..i0+2       (24 chunks, [s2][y][x])
+//   box B: shifts kp..kp+1 x planes kz-1..kz+1 x cells i0..i0+1     (12 chunks, [s2][z][x], 3-D)
+// each chunk = all B items of one (shift, cell); out-of-domain cells and the padding shift
+// arrive as zeros (TMA out-of-bounds fill).  Chunk of cell c's point p (0 centre, 1..6 faces):
+template <int DIM>
+__device__ __forceinline__ int jw_chunk(int s2, int c, int p) {
+  switch (p) {
+    case 0: return (s2 * 3 + 1) * 4 + c + 1;
+    case 1: return (s2 * 3 + 1) * 4 + c;
+    case 2: return (s2 * 3 + 1) * 4 + c + 2;
+    case 3: return (s2 * 3 + 0) * 4 + c + 1;
+    case 4: return (s2 * 3 + 2) * 4 + c + 1;
+    case 5: return 24 + (s2 * 3 + 0) * 2 + c;
+    default: return 24 + (s2 * 3 + 2) * 2 + c;
+  }
+}
+
+// ring slot layout (complex units): box A at 0, box B at jw_offb(B); both 128-byte aligned
+__host__ __device__ inline int jw_offb(int B) { return ((24 * B * 16 + 127) / 128) * 8; }
+template <int DIM>
+__host__ __device__ inline int jw_slot(int B) {
+  return (((jw_offb(B) + (DIM == 3 ? 12 * B : 0)) * 16 + 127) / 128) * 8;
+}
+
+template <int DIM>
+size_t jw_smem(int B) {
+  using G = JwGeom<DIM>;
+  return sizeof(double2) * JW_NRAW * (size_t)jw_slot<DIM>(B)        // raw ring
+         + sizeof(double) * JW_NA * JW_TC * 2 * (G::KS + 1) * 32     // A fragments [buf][cell][mt][ks][lane]
+         + sizeof(double) * 2 * JW_TC * G::NPC;                      // weights [tile parity]
+}
+
+__device__ __forceinline__ void tma5(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
+                                     uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"((uint32_t)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ uint32_t jw_s(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   jw_s(dst)),
+               "l"(src), "r"(bytes), "r"(jw_s(bar))
+               : "memory");
+}
+__device__ __forceinline__ void jw_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(jw_s(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void jw_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(jw_s(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void jw_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(jw_s(b)) : "memory");
+}
+__device__ __forceinline__ void jw_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(jw_s(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
+    const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, LevelView L,
+    const double* __restrict__ kappa, const double* __restrict__ stor, double hd, double face_scale, int n_src, int n_rec,
+    int ns, const double2* __restrict__ w,
+    const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj, int ntiles, int dbg) {
+  using G = JwGeom<DIM>;
+  constexpr int NPC = G::NPC, NCH = G::NCH, KS = G::KS;
+  constexpr int AF = JW_TC * 2 * (KS + 1) * 32;  // doubles per A-fragment buffer
+  extern __shared__ __align__(128) unsigned char jsm[];
+  __shared__ __align__(8) uint64_t raw_full[JW_NRAW], raw_empty[JW_NRAW], a_full[JW_NA], a_empty[JW_NA];
+  const int B = n_src + n_rec;
+  double2* raw = reinterpret_cast<double2*>(jsm);                       // [JW_NRAW][NCH][B]
+  const int SLOT = jw_slot<DIM>(B), OFFB = jw_offb(B);
+  auto chunk = [&](int ch) { return ch < 24 ? ch * B : OFFB + (ch - 24) * B; };  // complex offset in a slot
+  double* Af = reinterpret_cast<double*>(raw + JW_NRAW * SLOT);       // [JW_NA][AF]
+  double* wts = Af + JW_NA * AF;  // [tile parity][TC][NPC] (p = 0: S h^d)
+  const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
+  const int tiles_x = (L.nx + JW_TC - 1) / JW_TC;
+  const int64_t n = L.n, plane = (int64_t)L.nx * L.ny;
+  if ((int)blockIdx.x >= ntiles) return;
+  const int npair = (ns + 1) / 2;
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int T = my_tiles * npair;
+  struct TileXY {
+    int i0, j, kz;
+  };
+  // tile order: x segments fastest, then YB rows, then planes, then blocks of YB rows, so the
+  // CTAs in flight at any time cover YB rows x ~all planes' neighbours: the y and z face
+  // neighbours of a tile are loaded by concurrently running tiles (L2 hits, not HBM re-reads)
+  const int YB = (L.ny % 4 == 0) ? 4 : ((L.ny % 2 == 0) ? 2 : 1);
+  auto tile_at = [&](int t) {
+    const int tile = (int)blockIdx.x + (t / npair) * (int)gridDim.x;
+    const int tx = tile % tiles_x, r = tile / tiles_x;
+    const int yi = r % YB, r2 = r / YB;
+    const int kz = r2 % L.nz, yb = r2 / L.nz;
+    return TileXY{tx * JW_TC, yb * YB + yi, kz};
+  };
+  if (tid == 0) {
+    for (int q = 0; q < JW_NRAW; ++q) {
+      jw_init(&raw_full[q], 1);
+      jw_init(&raw_empty[q], JW_CONS + JW_PROD);
+    }
+    for (int q = 0; q < JW_NA; ++q) {
+      jw_init(&a_full[q], JW_PROD);
+      jw_init(&a_empty[q], JW_CONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (wc >= JW_CONS) {
+    // ------------------------------- producers -------------------------------------------
+    const int pw = wc - JW_CONS;  // 0 issues the copies
+    const int ptid = tid - 32 * JW_CONS;
+    // task t's two boxes into slot t % JW_NRAW (one thread)
+    auto issue = [&](int t) {
+      if (lane != 0) return;
+      const TileXY g = tile_at(t);
+      const int kp = (t % npair) * 2;
+      const int slot = t % JW_NRAW;
+      double2* dst = raw + slot * SLOT;
+      const uint32_t ca = (uint32_t)B * 16u;
+      jw_expect(&raw_full[slot], 24u * ca + (DIM == 3 ? 12u * ca : 0u));
+      tma5(dst, &mA, 0, g.i0 - 1, g.j - 1, g.kz, kp, &raw_full[slot]);
+      if (DIM == 3) tma5(dst + OFFB, &mB, 0, g.i0, g.j, g.kz - 1, kp, &raw_full[slot]);
+    };
+    if (pw == 0)
+      for (int t = 0; t < min(T, JW_AHEAD); ++t) issue(t);
+    // face / storativity weights of tile u into wts[u & 1] (loads issued a tile ahead of use)
+    auto weights = [&](int u) {
+      if ((dbg & 8) || ptid >= JW_TC * NPC || u * npair >= T) return;
+      const TileXY g = tile_at(u * npair);
+      const int c = ptid / NPC, p = ptid % NPC;
+      const int i = g.i0 + c;
+      double wv = 0.0;
+      if (i < L.nx) {
+        const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + i;
+        if (p == 0) {
+          wv = stor[a] * hd;
+        } else {
+          const int f = p - 1, d = f >> 1, hi = f & 1;
+          const int coord = d == 0 ? i : (d == 1 ? g.j : g.kz);
+          const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
+          const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : plane);
+          const double ka = kappa[a];
+          if (hi ? coord == ext - 1 : coord == 0) {
+            wv = 2.0 * ka * face_scale;  // dT/dln k_a = T = 2 k_a h^(d-2); ghost value 0
+          } else {
+            const double kb = kappa[hi ? a + stride : a - stride];
+            const double Tf = 2.0 * ka * kb / (ka + kb) * face_scale;
+            wv = Tf * kb / (ka + kb);
+          }
+        }
+      }
+      wts[(u & 1) * JW_TC * NPC + c * NPC + p] = wv;
+    };
+    weights(0);
+    for (int t = 0; t < T; ++t) {
+      const int kp = (t % npair) * 2;
+      const double* wt = wts + ((t / npair) & 1) * JW_TC * NPC;
+      if (t % npair == 0) {
+        // this tile's weights (stored a tile ago) are visible after the producers' barrier; the
+        // next tile's go into the other half (its previous user, tile - 1, is finished)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * JW_PROD) : "memory");
+        weights(t / npair + 1);
+      }
+      jw_wait(&raw_full[t % JW_NRAW], (uint32_t)((t / JW_NRAW) & 1));
+      if (t >= JW_NA) jw_wait(&a_empty[t % JW_NA], (uint32_t)(((t - JW_NA) / JW_NA) & 1));
+      // arrow transform: 4 lanes per (cell, shift of the pair, source), faces p - 1 = part mod 4
+      if (!(dbg & 2)) {
+        const double2* rw = raw + (t % JW_NRAW) * SLOT;
+        double* Ab = Af + (t % JW_NA) * AF;
+        const int combo = ptid >> 2, part = ptid & 3;
+        const int s = combo % JW_SMAX, s2 = (combo / JW_SMAX) % 2, c = combo / (2 * JW_SMAX);
+        const int k = kp + s2;
+        const bool live = s < n_src && k < ns;
+        const double2 wk = live ? w[k] : make_double2(0.0, 0.0);
+        const double2* R = rw + min(s, B - 1);
+        const double2 pa = R[chunk(jw_chunk<DIM>(s2, c, 0))];
+        const int mt = s >> 3, lrow = (s & 7) * 4;
+        double* Ac = Ab + (c * 2 + mt) * (KS + 1) * 32;
+        auto put = [&](int p, double2 v) {  // A'[s][K], K = (s2 NPC + p) 2 + comp (re, -im)
+          const int K0 = (s2 * NPC + p) * 2;
+          Ac[(K0 >> 2) * 32 + lrow + (K0 & 3)] = v.x;
+          Ac[((K0 + 1) >> 2) * 32 + lrow + ((K0 + 1) & 3)] = -v.y;
+        };
+        double2 a0 = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int p = 1; p < NPC; ++p) {
+          if ((p - 1) % 4 != part) continue;
+          const double2 d = live ? cscale(csub(pa, R[chunk(jw_chunk<DIM>(s2, c, p))]), wt[c * NPC + p]) : make_double2(0.0, 0.0);
+          a0 = cadd(a0, d);
+          put(p, cmul(wk, make_double2(-d.x, -d.y)));
+        }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          a0.x += __shfl_xor_sync(0xffffffffu, a0.x, o);
+          a0.y += __shfl_xor_sync(0xffffffffu, a0.y, o);
+        }
+        if (part == 0) put(0, cmul(wk, a0));
+        if (part == 1) {  // storativity block: K = s2 2 + comp in step KS
+          const double2 As = live ? cmul(wz[k], cscale(pa, wt[c * NPC])) : make_double2(0.0, 0.0);
+          Ac[KS * 32 + lrow + s2 * 2] = As.x;
+          Ac[KS * 32 + lrow + s2 * 2 + 1] = -As.y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jw_arrive(&a_full[t % JW_NA]);
+        jw_arrive(&raw_empty[t % JW_NRAW]);
+      }
+      // refill: task t + AHEAD goes into the slot task t - 1 used, once everyone is done with it
+      if (pw == 0 && t + JW_AHEAD < T) {
+        if (t >= 1) jw_wait(&raw_empty[(t - 1) % JW_NRAW], (uint32_t)(((t - 1) / JW_NRAW) & 1));
+        issue(t + JW_AHEAD);
+      }
+    }
+  } else {
+    // ------------------------------- consumers -------------------------------------------
+    // warp -> receivers wc*8 .. +7 of both cells (the two cells' J entries of one row are
+    // adjacent: one 16-byte store)
+    const int kq = lane & 3, rl = lane >> 2;
+    const int rcol = n_src + min(wc * 8 + rl, n_rec - 1);
+    double accK[2][2][2], accS[2][2][2];  // [cell][m tile][2]
+    for (int t = 0; t < T; ++t) {
+      const TileXY g = tile_at(t);
+      if (t % npair == 0) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) accK[c][mt][0] = accK[c][mt][1] = accS[c][mt][0] = accS[c][mt][1] = 0.0;
+      }
+      jw_wait(&raw_full[t % JW_NRAW], (uint32_t)((t / JW_NRAW) & 1));
+      jw_wait(&a_full[t % JW_NA], (uint32_t)((t / JW_NA) & 1));
+      const double2* rw = raw + (t % JW_NRAW) * SLOT;
+      const double* Ab = Af + (t % JW_NA) * AF;
+      if (!(dbg & 1)) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double* Ac = Ab + c * 2 * (KS + 1) * 32;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const int K = ks * 4 + kq, comp = K & 1, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
+            const double bv = reinterpret_cast<const double*>(rw + chunk(jw_chunk<DIM>(s2, c, p)))[2 * rcol + comp];
+            dmma(accK[c][0], Ac[ks * 32 + lane], bv);
+            dmma(accK[c][1], Ac[(KS + 1) * 32 + ks * 32 + lane], bv);
+          }
+          {  // storativity: K = s2 2 + comp at the centre point
+            const int s2 = kq >> 1, comp = kq & 1;
+            const double bv = reinterpret_cast<const double*>(rw + chunk(jw_chunk<DIM>(s2, c, 0)))[2 * rcol + comp];
+            dmma(accS[c][0], Ac[KS * 32 + lane], bv);
+            dmma(accS[c][1], Ac[(KS + 1) * 32 + KS * 32 + lane], bv);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jw_arrive(&a_empty[t % JW_NA]);
+        jw_arrive(&raw_empty[t % JW_NRAW]);
+      }
+      if (!(dbg & 4) && t % npair == npair - 1) {
+        const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + g.i0;
+        const bool both = g.i0 + 1 < L.nx;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int s = mt * 8 + (lane >> 2);
+          if (s >= n_src) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wc * 8 + (lane & 3) * 2 + h;
+            if (r >= n_rec) continue;
+            const int64_t o = ((int64_t)s * n_rec + r) * ldj + a;
+            double* pk = Jk + o;
+            if (both && ((reinterpret_cast<uintptr_t>(pk) & 15) == 0)) {
+              *reinterpret_cast<double2*>(pk) = make_double2(2.0 * accK[0][mt][h], 2.0 * accK[1][mt][h]);
+            } else {
+              pk[0] = 2.0 * accK[0][mt][h];
+              if (both) pk[1] = 2.0 * accK[1][mt][h];
+            }
+            if (Js) {
+              double* ps = Js + o;
+              if (both && ((reinterpret_cast<uintptr_t>(ps) & 15) == 0)) {
+                *reinterpret_cast<double2*>(ps) = make_double2(2.0 * accS[0][mt][h], 2.0 * accS[1][mt][h]);
+              } else {
+                ps[0] = 2.0 * accS[0][mt][h];
+                if (both) ps[1] = 2.0 * accS[1][mt][h];
+              }
+            }
+          }
         }
       }
     }
@@ -735,9 +1082,14 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
   LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
   DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n, st);
+  // FD with <= 16 sources and <= 64 receivers: tensor-core Jacobian on cell-major fields
+  // (LT_JAC_V2=1 selects the CUDA-core kernel)
+  static const bool mma_on = std::getenv("LT_JAC_V2") == nullptr;
+  const bool tensor_jac = mma_on && p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
+                          (p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B)) <= 227 * 1024;
   {
     TraceScope tr(ctx, "  expand", B);
-    expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>());
+    expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>(), tensor_jac);
   }
   res.U.clear();  // free the bases before the slice
 
@@ -790,6 +1142,33 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
       jtmp.allocate(sizeof(double) * (size_t)n_src * n_rec * n_param, st);
       J = jtmp.as<double>();
     }
+    const double h = p->grid.h;
+    const double face_scale = p->dim == 3 ? h : 1.0;
+    const double hd = p->dim == 3 ? h * h * h : h * h;
+    const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
+    if (tensor_jac) {
+      static const int jw_dbg = std::getenv("LT_JW_DBG") ? std::atoi(std::getenv("LT_JW_DBG")) : 0;
+      LevelView L = p->view(0);
+      const int ntiles = ((L.nx + JW_TC - 1) / JW_TC) * L.ny * L.nz;
+      const int grid = std::min(ntiles, ctx->num_sms);
+      const size_t smem = p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B);
+      auto fn = p->dim == 3 ? jacobian_mma_kernel<3> : jacobian_mma_kernel<2>;
+      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      // 5-D maps over the cell-major fields: (item re/im, x, y, z, shift)
+      const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
+      const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
+                                (uint64_t)n * B * 16};
+      const uint32_t boxA[5] = {2 * (uint32_t)B, 4, 3, 1, 2}, boxB[5] = {2 * (uint32_t)B, 2, 1, 3, 2};
+      const CUtensorMap mA = tma_map_8b(fields.get(), 5, dims, strd, boxA);
+      const CUtensorMap mB = tma_map_8b(fields.get(), 5, dims, strd, boxB);
+      launch(ctx, "jacobian", bytes, [&] {
+        fn<<<grid, JW_THREADS, smem, st>>>(mA, mB, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
+                                           face_scale, n_src, n_rec, ns, dw.as<double2>(), dw.as<double2>() + ns, J,
+                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles, jw_dbg);
+      });
+      if (mem != LT_MEM_DEVICE)
+        LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
+    } else {
     const int nsub_s = (n_src + SB - 1) / SB, nsub_r = (n_rec + RB - 1) / RB;
     const int nsub_total = nsub_s * nsub_r;
     LT_REQUIRE(nsub_total <= kT, "jacobian: too many source/receiver blocks for one CTA (n_src*n_rec too large)");
@@ -805,10 +1184,6 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     const size_t smem = smem_for(TC);
     const int tiles_x = (L.nx + TC - 1) / TC;
     const unsigned grid = (unsigned)(tiles_x * (int64_t)L.ny * L.nz);
-    const double h = p->grid.h;
-    const double face_scale = p->dim == 3 ? h : 1.0;
-    const double hd = p->dim == 3 ? h * h * h : h * h;
-    const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
     auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
     LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     launch(ctx, "jacobian", bytes, [&] {
@@ -818,6 +1193,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     });
     if (mem != LT_MEM_DEVICE)
       LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
+    }
   }
   if (pred_out) {
     DeviceBuffer didx(sizeof(int64_t) * rec.idx.size(), st), dwt(sizeof(double) * rec.w.size(), st),
@@ -828,7 +1204,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     launch(ctx, "predict", 0.0, [&] {
       predict_kernel<<<blocks_for((int64_t)n_src * n_rec, 128), 128, 0, st>>>(n, n_src, n_rec, ns, fields.as<double2>(),
                                                                              dw.as<double2>(), didx.as<int64_t>(),
-                                                                             dwt.as<double>(), dcnt.as<int>(), dout.as<double>());
+                                                                             dwt.as<double>(), dcnt.as<int>(), dout.as<double>(), tensor_jac ? 1 : 0);
     });
     LT_CUDA(cudaMemcpyAsync(pred_out, dout.get(), sizeof(double) * (size_t)n_src * n_rec, cudaMemcpyDeviceToHost, st));
   }

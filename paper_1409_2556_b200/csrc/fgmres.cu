@@ -532,6 +532,52 @@ __global__ void __launch_bounds__(kT) expand_kernel(int64_t n, int B, int ns, in
   }
 }
 
+// Cell-major variant for the Jacobian: out[(k n + a) B + b] (all items of a (shift, cell)
+// contiguous).  A block takes 32 cells x 8 items: basis reads are coalesced along the cells of
+// one item, each shift's 32 x 8 values are transposed through shared memory and written as
+// 8-item (128-byte) runs.
+__global__ void __launch_bounds__(256) expand_cm_kernel(int64_t n, int B, int ns, int maxit,
+                                                        const double2* const* __restrict__ Ucols,
+                                                        const double2* __restrict__ Y, const int* __restrict__ m_used,
+                                                        const double2* __restrict__ scale, double2* __restrict__ out) {
+  constexpr int CX = 32, IY = 8, KC = 16;
+  __shared__ double2 tile[CX][IY + 1];
+  const int cl = threadIdx.x % CX, il = threadIdx.x / CX;
+  const int64_t a0 = (int64_t)blockIdx.x * CX;
+  const int b0 = blockIdx.y * IY;
+  const int64_t a = a0 + cl;
+  const int b = b0 + il;
+  const bool in = a < n && b < B;
+  int mmax = 0;
+  if (b < B)
+    for (int k = 0; k < ns; ++k) mmax = max(mmax, m_used[b * ns + k]);
+  for (int k0 = 0; k0 < ns; k0 += KC) {
+    double2 acc[KC];
+#pragma unroll
+    for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
+    if (in)
+      for (int j = 0; j < mmax; ++j) {
+        const double2 u = Ucols[j][b * n + a];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          const int k = k0 + q;
+          if (k < ns && j < m_used[b * ns + k]) acc[q] = cfma(Y[((int64_t)b * ns + k) * maxit + j], u, acc[q]);
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      const int k = k0 + q;
+      if (k >= ns) break;  // uniform
+      __syncthreads();
+      tile[cl][il] = (in && scale) ? cmul(scale[b * ns + k], acc[q]) : acc[q];
+      __syncthreads();
+      // write: thread -> (cell c = t / IY, item i = t % IY): 8 consecutive items per cell
+      const int c = threadIdx.x / IY, i = threadIdx.x % IY;
+      if (a0 + c < n && b0 + i < B) out[((int64_t)k * n + a0 + c) * B + b0 + i] = tile[c][i];
+    }
+  }
+}
+
 }  // namespace
 
 void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
@@ -848,7 +894,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
   }
 }
 
-void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev, double2* x_out) {
+void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev, double2* x_out, bool cell_major) {
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int64_t n = p->n;
@@ -863,8 +909,12 @@ void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_
   LT_CUDA(cudaMemcpyAsync(dmu.get(), res.m_used.data(), sizeof(int) * res.m_used.size(), cudaMemcpyHostToDevice, st));
   const int nblk = (int)blocks_for(n, kT);
   launch(ctx, "expand", (double)n * B * 16.0 * (ncols + ns), [&] {
-    expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, res.maxit, dcols.as<const double2*>(), res.Y.as<double2>(),
-                                                      dmu.as<int>(), scale_dev, x_out);
+    if (cell_major)
+      expand_cm_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((B + 7) / 8)), 256, 0, st>>>(
+          n, B, ns, res.maxit, dcols.as<const double2*>(), res.Y.as<double2>(), dmu.as<int>(), scale_dev, x_out);
+    else
+      expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, res.maxit, dcols.as<const double2*>(),
+                                                        res.Y.as<double2>(), dmu.as<int>(), scale_dev, x_out);
   });
   LT_CUDA(cudaStreamSynchronize(st));
 }

@@ -290,7 +290,8 @@ struct OuterResult {
 void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res);
 
 // x_out[b][k] = scale[b][k] * U_b y_{b,k}  (device output, B * n_shifts * n)
+// cell_major: out[(k n + a) B + b] instead of out[(b ns + k) n + a]
 void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev,
-                      double2* x_out);
+                      double2* x_out, bool cell_major = false);
 
 }  // namespace lt
