@@ -177,26 +177,6 @@ __global__ void __launch_bounds__(kT) residual_kernel(LevelViewT<R> L, Batch bt,
   r[(int64_t)b * L.n + a] = vsub(f[(int64_t)b * L.n + a], ax);
 }
 
-template <class R, class V>
-__device__ __forceinline__ V prolong_at(const LevelViewT<R>& Lc, int ax, int ay, int az, const V* __restrict__ eb,
-                                        int i, int j, int k, int dim) {
-  int Ix[2], Iy[2], Iz[2];
-  float wx[2], wy[2], wz[2];
-  const int nxx = p1d_terms(i, ax, Lc.nx, Ix, wx);
-  const int nyy = p1d_terms(j, ay, Lc.ny, Iy, wy);
-  int nzz = 1;
-  Iz[0] = 0; wz[0] = 1.0f;
-  if (dim == 3) nzz = p1d_terms(k, az, Lc.nz, Iz, wz);
-  V s = vzero<V>();
-  for (int q = 0; q < nzz; ++q)
-    for (int p = 0; p < nyy; ++p) {
-      const R wzy = (R)(wz[q] * wy[p]);
-      const int64_t row = ((int64_t)Iz[q] * Lc.ny + Iy[p]) * Lc.nx;
-      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(eb[row + Ix[o]], wzy * (R)wx[o]));
-    }
-  return s;
-}
-
 // e = A_c(tau_b)^{-1} f: one warp per row of the dense complex inverse (row stride ld, column
 // offset off).
 template <class V>
@@ -447,7 +427,10 @@ __global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, Level
     return s;
   };
   if (az == 1 || Lf.dim == 2) {
-    for (int K = m.k0; K < m.k1; ++K) fb[K * cplane + m.ip] = inplane(K);
+    for (int K = m.k0; K < m.k1; ++K) {
+      const V v = inplane(K);
+      if (m.in) fb[K * cplane + m.ip] = v;
+    }
     return;
   }
   // coarse K collects fine planes 2K-1 (1/4), 2K (3/4 | 1/2 at K = 0), 2K+1 (3/4 | 1/2 at the
@@ -457,11 +440,12 @@ __global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, Level
   for (int K = m.k0; K < m.k1; ++K) {
     const V sc = inplane(2 * K + 1);
     const V sd = K < Lc.nz - 1 ? inplane(2 * K + 2) : vzero<V>();
-    const R w0 = K > 0 ? R(0.25) : R(0);
-    const R w1 = K == 0 ? R(0.5) : R(0.75);
-    const R w2 = K == Lc.nz - 1 ? R(0.5) : R(0.75);
-    const R w3 = K < Lc.nz - 1 ? R(0.25) : R(0);
-    fb[K * cplane + m.ip] = vadd(vadd(vscale(sa, w0), vscale(sb, w1)), vadd(vscale(sc, w2), vscale(sd, w3)));
+    const R z0 = K > 0 ? R(0.25) : R(0);
+    const R z1 = K == 0 ? R(0.5) : R(0.75);
+    const R z2 = K == Lc.nz - 1 ? R(0.5) : R(0.75);
+    const R z3 = K < Lc.nz - 1 ? R(0.25) : R(0);
+    const V v = vadd(vadd(vscale(sa, z0), vscale(sb, z1)), vadd(vscale(sc, z2), vscale(sd, z3)));
+    if (m.in) fb[K * cplane + m.ip] = v;
     sa = sc;
     sb = sd;
   }
@@ -480,9 +464,47 @@ __global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelV
   const int64_t plane = (int64_t)Lf.nx * Lf.ny;
   const V* eb = ec + (int64_t)b * Lc.n;
   V* xb = xf + (int64_t)b * Lf.n;
+  // the column's bilinear in-plane weights, applied once per coarse plane (register ring
+  // over the coarse planes instead of 8 coarse loads per fine cell)
+  int Ix[2], Iy[2];
+  float wx[2], wy[2];
+  const int nxx = p1d_terms(m.i, ax, Lc.nx, Ix, wx);
+  const int nyy = p1d_terms(m.j, ay, Lc.ny, Iy, wy);
+  const int64_t cplane = (int64_t)Lc.nx * Lc.ny;
+  auto inplane = [&](int K) {
+    V s = vzero<V>();
+    if (K < 0 || K >= Lc.nz) return s;
+    const V* pl = eb + K * cplane;
+    for (int p = 0; p < nyy; ++p)
+      for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(pl[(int64_t)Iy[p] * Lc.nx + Ix[o]], (R)(wy[p] * wx[o])));
+    return s;
+  };
+  if (Lf.dim == 2 || az == 1) {
+    for (int k = m.k0; k < m.k1; ++k) {
+      const int64_t a = k * plane + m.ip;
+      xb[a] = vadd(xb[a], inplane(Lf.dim == 2 ? 0 : k));
+    }
+    return;
+  }
+  // aggregation 2 in z: fine k takes 3/4 of coarse K = k / 2 and 1/4 of K - 1 (k even) or
+  // K + 1 (k odd); at the ends the Dirichlet ghost makes it 1/2 of K (p1d_terms)
+  int K = m.k0 >> 1;
+  V sm = inplane(K - 1), sc = inplane(K), sp = inplane(K + 1);
+  V xn = xb[m.k0 * plane + m.ip];
   for (int k = m.k0; k < m.k1; ++k) {
     const int64_t a = k * plane + m.ip;
-    xb[a] = vadd(xb[a], prolong_at(Lc, ax, ay, az, eb, m.i, m.j, k, Lf.dim));
+    const V xc = xn;
+    if (k + 1 < m.k1) xn = xb[a + plane];
+    if ((k >> 1) != K) {
+      K = k >> 1;
+      sm = sc;
+      sc = sp;
+      sp = inplane(K + 1);
+    }
+    V v;
+    if ((k & 1) == 0) v = K == 0 ? vscale(sc, R(0.5)) : vadd(vscale(sc, R(0.75)), vscale(sm, R(0.25)));
+    else v = K == Lc.nz - 1 ? vscale(sc, R(0.5)) : vadd(vscale(sc, R(0.75)), vscale(sp, R(0.25)));
+    xb[a] = vadd(xc, v);
   }
 }
 
