@@ -202,16 +202,18 @@ __global__ void __launch_bounds__(kT) coarse_solve_kernel(int nc, Batch bt, cons
 // ---- COCG vector kernels (FP64, fused with their reductions) ----------------------------
 using VM = CT<MgReal>::V;
 
-// r = v, rmg = (VM) v, partial ||v||^2
+// r = v, rmg = (VM) v, u = 0, partial ||v||^2
 __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ v, int64_t vs,
                                                        double2* __restrict__ r, VM* __restrict__ rmg,
-                                                       double* __restrict__ part, int nblk) {
+                                                       double2* __restrict__ u, int64_t us, double* __restrict__ part,
+                                                       int nblk) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
     const double2 x = v[b * vs + a];
     r[b * n + a] = x;
     rmg[b * n + a] = vfrom<VM>(x);
+    u[b * us + a] = make_double2(0.0, 0.0);
     s = cabs2(x);
   }
   s = block_sum(s);
@@ -1180,20 +1182,15 @@ __global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, co
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
 
-// x += alpha p (x = alpha p on the first iteration), r -= alpha q, rmg = (VM) r, partial ||r||^2
+// r -= alpha q, rmg = (VM) r, partial ||r||^2.  (The solution update u += alpha p is deferred
+// into the next direction update, which reads p anyway.)
 __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
-                                                       const double2* __restrict__ p, const double2* __restrict__ q,
-                                                       double2* __restrict__ x, int64_t xs, double2* __restrict__ r,
-                                                       VM* __restrict__ rmg, int first, double* __restrict__ part,
-                                                       int nblk) {
+                                                       const double2* __restrict__ q, double2* __restrict__ r,
+                                                       VM* __restrict__ rmg, double* __restrict__ part, int nblk) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
-    const double2 al = alpha[b];
-    const double2 pa = p[b * n + a];
-    double2* xa = x + b * xs + a;
-    *xa = first ? cmul(al, pa) : cfma(al, pa, *xa);
-    double2 ra = csub(r[b * n + a], cmul(al, q[b * n + a]));
+    const double2 ra = csub(r[b * n + a], cmul(alpha[b], q[b * n + a]));
     r[b * n + a] = ra;
     rmg[b * n + a] = vfrom<VM>(ra);
     s = cabs2(ra);
@@ -1202,13 +1199,32 @@ __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, cons
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
 
-// p = z + beta p (p = z when first)
-__global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const double2* __restrict__ beta,
-                                                     const VM* __restrict__ z, double2* __restrict__ p, int first) {
+// u += alpha p (the deferred solution update of this iteration), then p = z + beta p;
+// first: p = z only
+__global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
+                                                     const double2* __restrict__ beta, const VM* __restrict__ z,
+                                                     double2* __restrict__ p, double2* __restrict__ u, int64_t us,
+                                                     int first) {
   ITEM_PROLOGUE(n);
   if (!in) return;
   const double2 za = vto(z[b * n + a]);
-  p[b * n + a] = first ? za : cfma(beta[b], p[b * n + a], za);
+  if (first) {
+    p[b * n + a] = za;
+    return;
+  }
+  const double2 pa = p[b * n + a];
+  double2* ua = u + b * us + a;
+  *ua = cfma(alpha[b], pa, *ua);
+  p[b * n + a] = cfma(beta[b], pa, za);
+}
+
+// u += alpha p for the items whose last update is still pending (mask)
+__global__ void uupdate_kernel(int64_t n, const int* __restrict__ mask, const double2* __restrict__ alpha,
+                               const double2* __restrict__ p, double2* __restrict__ u, int64_t us) {
+  const int b = blockIdx.y;
+  if (!mask[b]) return;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+    u[b * us + a] = cfma(alpha[b], p[b * n + a], u[b * us + a]);
 }
 
 // x = 0 for items whose right-hand side is zero
@@ -1592,8 +1608,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   const double coef = (double)n * 8.0 * (DIM + 1);
   const double vb = sizeof(V);
 
-  launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] {
-    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, (double*)partials.get(), nblk);
+  launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
+    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), nblk);
   });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), nblk, sc); });
   std::vector<double> bb(Bc), rr(Bc), best(Bc);
@@ -1638,7 +1654,10 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   };
   // z = B r ; rho = r^T z ; p = z
   precondition(OP_RHO);
-  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 1); });
+  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+    pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 1);
+  });
+  std::vector<int> pending(Bc, 0);  // items whose u still lacks this iteration's alpha p
   for (int it = 0; it < p->inner_maxit; ++it) {
     const bool zm = DIM == 3 || p->kind != LT_GRID_P1_TRI;
     const int nblk_apply = zm ? zm_blocks(L0) : L0.ntiles;
@@ -1658,10 +1677,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     launch(ctx, "cocg_scalar", 0.0, [&] {
       scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk_apply, sc);
     });
-    launch(ctx, "cocg_vec", nb * ((it == 0 ? 64.0 : 80.0) + vb), [&] {
-      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, pdir, q, u, us, r, rmg, it == 0, (double*)partials.get(),
-                                            nblk);
+    (void)pdir;
+    launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), nblk);
     });
+    for (int b = 0; b < Bc; ++b)
+      if (!done[b]) pending[b] = 1;
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
     LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
     {
@@ -1687,8 +1708,22 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
     }
     precondition(OP_BETA);
-    launch(ctx, "cocg_vec", nb * (32.0 + vb), [&] { pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_beta, z, pp, 0); });
+    launch(ctx, "cocg_vec", nb * (64.0 + vb), [&] {
+      pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 0);
+    });
+    for (int b = 0; b < Bc; ++b)
+      if (!done[b]) pending[b] = 0;
     if (inner_trace()) iters_seen = it + 1;
+  }
+  // the last deferred solution update of the items that stopped after an r update
+  bool any_pending = false;
+  for (int b = 0; b < Bc; ++b) any_pending |= pending[b] != 0;
+  if (any_pending) {
+    DeviceBuffer dm(sizeof(int) * Bc, st);
+    LT_CUDA(cudaMemcpyAsync(dm.get(), pending.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
+    launch(ctx, "cocg_vec", nb * 48.0, [&] {
+      uupdate_kernel<<<dim3(blocks_for(n, kT), Bc), kT, 0, st>>>(n, dm.as<int>(), d_alpha, pp, u, us);
+    });
   }
   LT_CUDA(cudaStreamSynchronize(st));
   if (inner_trace())
