@@ -120,6 +120,24 @@ __device__ __forceinline__ V diag_solve_r(R dk, R m, R tr, R ti, V rhs) {
 
 // ---- multigrid kernels (precision R) ---------------------------------------------------
 
+// Storage index of cell (i, j, k) of a level: natural, or colour-split (see the colour-split
+// TMA kernels below)
+template <class VW>
+__device__ __forceinline__ int64_t rb_index(const VW& L, int i, int j, int k) {
+  const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+  return L.split ? row + (int64_t)(((i + j + k) & 1) * (L.nx >> 1)) + (i >> 1) : row + i;
+}
+// natural flat index a -> storage index (nx == 0: natural layout)
+__device__ __forceinline__ int64_t rb_flat(int64_t a, int nx, int ny) {
+  if (nx == 0) return a;
+  const int64_t t = a / nx;
+  const int i = (int)(a - t * nx);
+  const int64_t k = t / ny;
+  const int j = (int)(t - k * ny);
+  return t * nx + (int64_t)(((i + j + (int)(k & 1)) & 1) * (nx >> 1)) + (i >> 1);
+}
+
+
 // 1-D cell-centred linear interpolation weight P[f, I] (aggregation 2, Dirichlet ghost = -e).
 __device__ __forceinline__ int p1d_terms(int fi, int agg, int nc, int* I, float* w) {
   if (agg == 1) { I[0] = fi; w[0] = 1.0f; return 1; }
@@ -206,13 +224,13 @@ using VM = CT<MgReal>::V;
 __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ v, int64_t vs,
                                                        double2* __restrict__ r, VM* __restrict__ rmg,
                                                        double2* __restrict__ u, int64_t us, double* __restrict__ part,
-                                                       int nblk) {
+                                                       int nblk, int snx, int sny) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
     const double2 x = v[b * vs + a];
     r[b * n + a] = x;
-    rmg[b * n + a] = vfrom<VM>(x);
+    rmg[b * n + rb_flat(a, snx, sny)] = vfrom<VM>(x);
     u[b * us + a] = make_double2(0.0, 0.0);
     s = cabs2(x);
   }
@@ -222,10 +240,11 @@ __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, cons
 
 // partial sum_a r_a z_a (bilinear, no conjugation), z from the V-cycle
 __global__ void __launch_bounds__(kT) bdot_kernel(int64_t n, Batch bt, const double2* __restrict__ x,
-                                                  const VM* __restrict__ y, double2* __restrict__ part, int nblk) {
+                                                  const VM* __restrict__ y, double2* __restrict__ part, int nblk,
+                                                  int snx, int sny) {
   ITEM_PROLOGUE(n);
   double2 s = make_double2(0.0, 0.0);
-  if (in) s = cmul(x[b * n + a], vto(y[b * n + a]));
+  if (in) s = cmul(x[b * n + a], vto(y[b * n + rb_flat(a, snx, sny)]));
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
@@ -401,6 +420,228 @@ __global__ void __launch_bounds__(kT) rbhalf_zm_kernel(LevelViewT<R> L, Batch bt
   }
 }
 
+// ---- transfers for aggregation 2 in x, y and z (3-D), natural or colour-split levels ------
+// Both kernels work on fine cell PAIRS (2I, 2I + 1): they share the coarse x index I, and in
+// the colour-split layout they sit at position I of the two colour halves; in the natural
+// layout they are one 16-byte word.  Lanes are consecutive I, so every load is coalesced and
+// the x-neighbours 2I - 1 / 2I + 2 (restriction) or coarse I -+ 1 (prolongation) come from
+// the adjacent lanes by shuffle.  The z direction is a register ring as in the zm kernels.
+// (The per-cell zm kernels read 16 strided fine values per coarse cell and fine plane and
+// were latency-bound at 0.7-1.7 TB/s.)
+constexpr int TP_TY = 4, TP_ZC = 16;  // restriction: 32 x 4 coarse columns x 16 coarse planes
+
+// fine cells (2I, 2I + 1) of row (j, k) of a level
+__device__ __forceinline__ void pair_load(const LevelViewT<float>& L, const float2* __restrict__ v, int I, int j,
+                                          int k, float2& e, float2& o) {
+  const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+  if (L.split) {
+    const int s = (j + k) & 1, h = L.nx >> 1;  // even cells in colour half s
+    e = v[row + s * h + I];
+    o = v[row + (s ^ 1) * h + I];
+  } else {
+    const float4 p = *reinterpret_cast<const float4*>(v + row + 2 * I);
+    e = make_float2(p.x, p.y);
+    o = make_float2(p.z, p.w);
+  }
+}
+__device__ __forceinline__ void pair_store(const LevelViewT<float>& L, float2* __restrict__ v, int I, int j, int k,
+                                           float2 e, float2 o) {
+  const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+  if (L.split) {
+    const int s = (j + k) & 1, h = L.nx >> 1;
+    v[row + s * h + I] = e;
+    v[row + (s ^ 1) * h + I] = o;
+  } else {
+    *reinterpret_cast<float4*>(v + row + 2 * I) = make_float4(e.x, e.y, o.x, o.y);
+  }
+}
+__device__ __forceinline__ float2 shfl_f2(float2 v, int src) {
+  return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ float2 f2fma(float w, float2 a, float2 acc) {
+  return make_float2(fmaf(w, a.x, acc.x), fmaf(w, a.y, acc.y));
+}
+
+// f_c = P^T r_f.  Thread = coarse column (I, J), CTA = 32 x TP_TY columns x TP_ZC coarse
+// planes, z-marching over the fine planes with the loads of fine plane kf + 1 in flight while
+// plane kf is reduced (software pipeline; one coarse cell per thread with all loads
+// independent was bound by CTA turnover at 1 CTA per SM, the unpipelined march by its serial
+// plane chain).
+struct RowsRaw {
+  float2 e[4], o[4], m[4], p[4];  // fine rows 2J-1 .. 2J+2: cells 2I, 2I+1, 2I-1 (lane 0), 2I+2 (lane 31)
+};
+__global__ void __launch_bounds__(32 * TP_TY) restrict_pair_kernel(LevelViewT<float> Lf, LevelViewT<float> Lc,
+                                                                   Batch bt, const float2* __restrict__ rf,
+                                                                   float2* __restrict__ fc) {
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int tx = (Lc.nx + 31) / 32, ty = (Lc.ny + TP_TY - 1) / TP_TY;
+  const int tile = cb % (tx * ty), chunk = cb / (tx * ty);
+  const int lane = threadIdx.x & 31;
+  const int I = (tile % tx) * 32 + lane, J = (tile / tx) * TP_TY + (threadIdx.x >> 5);
+  if (J >= Lc.ny) return;  // whole warp
+  const bool in = I < Lc.nx;
+  const int K0 = chunk * TP_ZC, K1 = min(Lc.nz, K0 + TP_ZC);
+  const float2* rb = rf + (int64_t)b * Lf.n;
+  const float wxm = I > 0 ? 0.25f : 0.f, wx0 = I == 0 ? 0.5f : 0.75f;
+  const float wx1 = I == Lc.nx - 1 ? 0.5f : 0.75f, wxp = I < Lc.nx - 1 ? 0.25f : 0.f;
+  const float wyv[4] = {J > 0 ? 0.25f : 0.f, J == 0 ? 0.5f : 0.75f, J == Lc.ny - 1 ? 0.5f : 0.75f,
+                        J < Lc.ny - 1 ? 0.25f : 0.f};
+  auto load = [&](int kf, RowsRaw& R) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      R.e[r] = R.o[r] = R.m[r] = R.p[r] = make_float2(0.f, 0.f);
+      if (wyv[r] == 0.f) continue;  // warp-uniform
+      const int jf = 2 * J - 1 + r;
+      if (in) pair_load(Lf, rb, I, jf, kf, R.e[r], R.o[r]);
+      float2 t;
+      if (lane == 0 && in && I > 0) pair_load(Lf, rb, I - 1, jf, kf, t, R.m[r]);
+      if (lane == 31 && I + 1 < Lc.nx) pair_load(Lf, rb, I + 1, jf, kf, R.p[r], t);
+    }
+  };
+  auto reduce = [&](const RowsRaw& R) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (wyv[r] == 0.f) continue;
+      float2 om = shfl_f2(R.o[r], (lane + 31) & 31), ep = shfl_f2(R.e[r], (lane + 1) & 31);
+      if (lane == 0) om = R.m[r];
+      if (lane == 31) ep = R.p[r];
+      float2 xr = make_float2(0.f, 0.f);
+      xr = f2fma(wxm, om, xr);
+      xr = f2fma(wx0, R.e[r], xr);
+      xr = f2fma(wx1, R.o[r], xr);
+      xr = f2fma(wxp, ep, xr);
+      acc = f2fma(wyv[r], xr, acc);
+    }
+    return acc;
+  };
+  float2* fb = fc + (int64_t)b * Lc.n;
+  // coarse K collects fine planes 2K-1 (1/4), 2K (3/4 | 1/2 at K = 0), 2K+1 (3/4 | 1/2 at the
+  // top), 2K+2 (1/4)
+  const int kbeg = max(2 * K0 - 1, 0), kend = min(2 * K1, Lf.nz - 1);
+  float2 sa = make_float2(0.f, 0.f), sb = sa, sc = sa;
+  RowsRaw cur, nxt;
+  load(kbeg, cur);
+  for (int kf = kbeg; kf <= kend; ++kf) {
+    if (kf < kend) load(kf + 1, nxt);
+    const float2 S = reduce(cur);
+    if (kf < 2 * K0) {
+      sa = S;
+    } else if (kf == 2 * K0) {
+      sb = S;
+    } else {
+      const bool odd = kf & 1;
+      const int K = odd ? (kf - 1) >> 1 : (kf >> 1) - 1;
+      if (odd) sc = S;
+      if (!odd || K == Lc.nz - 1) {
+        const float2 sd = odd ? make_float2(0.f, 0.f) : S;
+        float2 v = make_float2(0.f, 0.f);
+        v = f2fma(K > 0 ? 0.25f : 0.f, sa, v);
+        v = f2fma(K == 0 ? 0.5f : 0.75f, sb, v);
+        v = f2fma(K == Lc.nz - 1 ? 0.5f : 0.75f, sc, v);
+        v = f2fma(K < Lc.nz - 1 ? 0.25f : 0.f, sd, v);
+        if (in) fb[rb_index(Lc, I, J, K)] = v;
+        sa = sc;
+        sb = sd;
+      }
+    }
+    cur = nxt;
+  }
+}
+
+// x_f += P e_c.  Thread = fine pair (2I, 2I + 1) of one fine row, CTA 32 x 8 fine rows x a chunk
+// of ZM_ZC fine planes, z-marching with the next fine pair and the next-but-one coarse plane's
+// rows in flight (register ring over the coarse planes).
+struct CoarseRaw {
+  float2 c[2], m[2], p[2];  // coarse rows of the fine row: I, I - 1 (lane 0), I + 1 (lane 31)
+};
+__global__ void __launch_bounds__(kT) prolong_pair_kernel(LevelViewT<float> Lf, LevelViewT<float> Lc, Batch bt,
+                                                          const float2* __restrict__ ec, float2* __restrict__ xf) {
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int nh = Lf.nx >> 1;  // pairs per fine row (= coarse nx)
+  const int tx = (nh + 31) / 32, ty = (Lf.ny + 7) / 8;
+  const int tile = cb % (tx * ty), chunk = cb / (tx * ty);
+  const int lane = threadIdx.x & 31;
+  const int I = (tile % tx) * 32 + lane, j = (tile / tx) * 8 + (threadIdx.x >> 5);
+  if (j >= Lf.ny) return;  // whole warp
+  const bool in = I < nh;
+  const int k0 = chunk * ZM_ZC, k1 = min(Lf.nz, k0 + ZM_ZC);
+  const float2* eb = ec + (int64_t)b * Lc.n;
+  float2* xb = xf + (int64_t)b * Lf.n;
+  // coarse rows of fine row j and their weights (Dirichlet ghost at the ends: 1/2 of J)
+  const int J = j >> 1;
+  int Jr[2];
+  float wr[2];
+  if ((j & 1) == 0) {
+    Jr[0] = J; wr[0] = J == 0 ? 0.5f : 0.75f; Jr[1] = J - 1; wr[1] = J > 0 ? 0.25f : 0.f;
+  } else {
+    Jr[0] = J; wr[0] = J == Lc.ny - 1 ? 0.5f : 0.75f; Jr[1] = J + 1; wr[1] = J < Lc.ny - 1 ? 0.25f : 0.f;
+  }
+  const float wxe0 = I == 0 ? 0.5f : 0.75f, wxe1 = I > 0 ? 0.25f : 0.f;            // fine 2I: I, I - 1
+  const float wxo0 = I == nh - 1 ? 0.5f : 0.75f, wxo1 = I < nh - 1 ? 0.25f : 0.f;  // fine 2I+1: I, I + 1
+  auto at = [&](int Ic, int Jc, int Kc) { return eb[rb_index(Lc, Ic, Jc, Kc)]; };
+  auto load = [&](int K, CoarseRaw& R) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      R.c[r] = R.m[r] = R.p[r] = make_float2(0.f, 0.f);
+      if (K < 0 || K >= Lc.nz || wr[r] == 0.f) continue;  // warp-uniform
+      if (in) R.c[r] = at(I, Jr[r], K);
+      if (lane == 0 && in && I > 0) R.m[r] = at(I - 1, Jr[r], K);
+      if (lane == 31 && I + 1 < nh) R.p[r] = at(I + 1, Jr[r], K);
+    }
+  };
+  // bilinear in-plane values (fine 2I, fine 2I + 1) of one coarse plane
+  auto interp = [&](const CoarseRaw& R, float2& pe, float2& po) {
+    pe = make_float2(0.f, 0.f);
+    po = pe;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      float2 m1 = shfl_f2(R.c[r], (lane + 31) & 31), p1 = shfl_f2(R.c[r], (lane + 1) & 31);
+      if (lane == 0) m1 = R.m[r];
+      if (lane == 31) p1 = R.p[r];
+      pe = f2fma(wr[r] * wxe0, R.c[r], f2fma(wr[r] * wxe1, m1, pe));
+      po = f2fma(wr[r] * wxo0, R.c[r], f2fma(wr[r] * wxo1, p1, po));
+    }
+  };
+  int K = k0 >> 1;
+  float2 sme, smo, sce, sco, spe, spo;
+  CoarseRaw raw;
+  load(K - 1, raw);
+  interp(raw, sme, smo);
+  load(K, raw);
+  interp(raw, sce, sco);
+  load(K + 1, raw);
+  interp(raw, spe, spo);
+  load(K + 2, raw);  // in flight: the next coarse plane to enter the ring
+  float2 e = make_float2(0.f, 0.f), o = e, en = e, on = e;
+  if (in) pair_load(Lf, xb, I, j, k0, e, o);
+  for (int k = k0; k < k1; ++k) {
+    if (in && k + 1 < k1) pair_load(Lf, xb, I, j, k + 1, en, on);
+    if ((k >> 1) != K) {
+      K = k >> 1;
+      sme = sce; smo = sco;
+      sce = spe; sco = spo;
+      interp(raw, spe, spo);
+      load(K + 2, raw);
+    }
+    float2 ve = make_float2(0.f, 0.f), vo = ve;
+    if ((k & 1) == 0) {
+      const float w0 = K == 0 ? 0.5f : 0.75f, w1 = K > 0 ? 0.25f : 0.f;
+      ve = f2fma(w1, sme, f2fma(w0, sce, ve));
+      vo = f2fma(w1, smo, f2fma(w0, sco, vo));
+    } else {
+      const float w0 = K == Lc.nz - 1 ? 0.5f : 0.75f, w1 = K < Lc.nz - 1 ? 0.25f : 0.f;
+      ve = f2fma(w1, spe, f2fma(w0, sce, ve));
+      vo = f2fma(w1, spo, f2fma(w0, sco, vo));
+    }
+    if (in) pair_store(Lf, xb, I, j, k, make_float2(e.x + ve.x, e.y + ve.y), make_float2(o.x + vo.x, o.y + vo.y));
+    e = en;
+    o = on;
+  }
+}
+
 // f_c = P^T r_f, z-marching over the coarse grid: each fine plane's in-plane (4 x 4) weighted
 // sum is formed once and added to the two coarse planes it belongs to (register ring).
 template <class R>
@@ -421,6 +662,11 @@ __global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, Level
   const int64_t fplane = (int64_t)Lf.nx * Lf.ny, cplane = (int64_t)Lc.nx * Lc.ny;
   auto inplane = [&](int kf) {
     V s = vzero<V>();
+    if (Lf.split) {
+      for (int p = 0; p < nyy; ++p)
+        for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(rb[rb_index(Lf, Fx[o], Fy[p], kf)], (R)(wy[p] * wx[o])));
+      return s;
+    }
     const V* pl = rb + kf * fplane;
     for (int p = 0; p < nyy; ++p) {
       const V* row = pl + (int64_t)Fy[p] * Lf.nx;
@@ -431,7 +677,7 @@ __global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, Level
   if (az == 1 || Lf.dim == 2) {
     for (int K = m.k0; K < m.k1; ++K) {
       const V v = inplane(K);
-      if (m.in) fb[K * cplane + m.ip] = v;
+      if (m.in) fb[rb_index(Lc, m.i, m.j, K)] = v;
     }
     return;
   }
@@ -447,7 +693,7 @@ __global__ void __launch_bounds__(kT) restrict_zm_kernel(LevelViewT<R> Lf, Level
     const R z2 = K == Lc.nz - 1 ? R(0.5) : R(0.75);
     const R z3 = K < Lc.nz - 1 ? R(0.25) : R(0);
     const V v = vadd(vadd(vscale(sa, z0), vscale(sb, z1)), vadd(vscale(sc, z2), vscale(sd, z3)));
-    if (m.in) fb[K * cplane + m.ip] = v;
+    if (m.in) fb[rb_index(Lc, m.i, m.j, K)] = v;
     sa = sc;
     sb = sd;
   }
@@ -476,6 +722,11 @@ __global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelV
   auto inplane = [&](int K) {
     V s = vzero<V>();
     if (K < 0 || K >= Lc.nz) return s;
+    if (Lc.split) {
+      for (int p = 0; p < nyy; ++p)
+        for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(eb[rb_index(Lc, Ix[o], Iy[p], K)], (R)(wy[p] * wx[o])));
+      return s;
+    }
     const V* pl = eb + K * cplane;
     for (int p = 0; p < nyy; ++p)
       for (int o = 0; o < nxx; ++o) s = vadd(s, vscale(pl[(int64_t)Iy[p] * Lc.nx + Ix[o]], (R)(wy[p] * wx[o])));
@@ -483,7 +734,7 @@ __global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelV
   };
   if (Lf.dim == 2 || az == 1) {
     for (int k = m.k0; k < m.k1; ++k) {
-      const int64_t a = k * plane + m.ip;
+      const int64_t a = rb_index(Lf, m.i, m.j, k);
       xb[a] = vadd(xb[a], inplane(Lf.dim == 2 ? 0 : k));
     }
     return;
@@ -492,11 +743,11 @@ __global__ void __launch_bounds__(kT) prolong_zm_kernel(LevelViewT<R> Lf, LevelV
   // K + 1 (k odd); at the ends the Dirichlet ghost makes it 1/2 of K (p1d_terms)
   int K = m.k0 >> 1;
   V sm = inplane(K - 1), sc = inplane(K), sp = inplane(K + 1);
-  V xn = xb[m.k0 * plane + m.ip];
+  V xn = xb[rb_index(Lf, m.i, m.j, m.k0)];
   for (int k = m.k0; k < m.k1; ++k) {
-    const int64_t a = k * plane + m.ip;
+    const int64_t a = rb_index(Lf, m.i, m.j, k);
     const V xc = xn;
-    if (k + 1 < m.k1) xn = xb[a + plane];
+    if (k + 1 < m.k1) xn = xb[rb_index(Lf, m.i, m.j, k + 1)];
     if ((k >> 1) != K) {
       K = k >> 1;
       sm = sc;
@@ -1070,6 +1321,175 @@ __global__ void __launch_bounds__(kTP, 2) mg_tma_kernel(const __grid_constant__ 
   }
 }
 
+// ---- colour-split (red-black ordered) TMA kernels -----------------------------------------
+// On levels with nx % 4 == 0 and nx >= 64 the multigrid vectors are stored colour-split: in
+// every row (j, k) the cells of colour 0 ((i + j + k) even) come first, ordered by i, then
+// those of colour 1; cell i sits at position i / 2 of its colour's half (rb_index).  Then
+//  * every cell of one colour in a row is one contiguous run, and so are its six neighbours
+//    (W / E at positions m - 1 + s / m + s of the other half, s = the row's parity offset;
+//    S / N / down / up at position m of the other half of the adjacent rows / planes), so a
+//    warp on 32 same-colour cells reads every operand as one 256-byte run: the natural-layout
+//    half sweep read stride-2 cells and stride-32-byte coefficient records, and was bound by
+//    shared-memory wavefronts (~64 per 64 cells), not by HBM;
+//  * a half sweep moves only half of each vector: it reads the other colour of x and its own
+//    colour of f and writes its own colour -- 1.5 complex64 per cell instead of 3 -- and the
+//    first sweep from zero reads no x at all.
+// The coefficients are stored the same way, planar (Level::packrb), so E = W(i + 1), N and T
+// are contiguous runs of the other half as well.
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Tile: 32 positions (one warp, 64 cells of a row) x RB_H rows, z-march over ZM_ZC planes.
+// Per plane slot: x (the other colour for a half sweep, both for the residual) over rows
+// y0-1 .. y0+RB_H and positions m0-2 .. m0+33, f over the tile (own colour, both with dot or
+// for the residual), coefficients of both colours over rows y0 .. y0+RB_H and positions
+// m0 .. m0+35.
+constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = 5;
+template <int MODE>
+struct RbSlot {
+  static constexpr int NX = MODE == 0 ? 1 : 2;  // colours of x in the slot
+  static constexpr uint32_t XB = sizeof(float2) * RB_XP * NX * (RB_H + 2);
+  static constexpr uint32_t FB = sizeof(float2) * RB_P * 2 * RB_H;  // room for both colours
+  static constexpr uint32_t CB = sizeof(float) * RB_CP * 2 * 4 * (RB_H + 1);
+  static constexpr uint32_t OFF_F = (XB + 127) / 128 * 128;
+  static constexpr uint32_t OFF_C = (OFF_F + FB + 127) / 128 * 128;
+  static constexpr uint32_t SLOT = (OFF_C + CB + 127) / 128 * 128;
+  static constexpr size_t SMEM = (size_t)SLOT * RB_D;
+};
+
+template <class VW>
+inline int rb_blocks(const VW& L) {
+  return ((L.nx / 2 + RB_P - 1) / RB_P) * ((L.ny + RB_H - 1) / RB_H) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+}
+
+// MODE 0: red-black half sweep of `color`, in place on the colour's half of x (zero_init: x = 0
+// on entry, so no x is read; dot: also the partials of f^T x over both colours after the
+// sweep).  MODE 1: r = f - A x on both colours.  mx / mf: 5-D maps {pos, colour, y, z, item}
+// of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.
+template <int MODE>
+__global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ CUtensorMap mx,
+                                                       const __grid_constant__ CUtensorMap mf,
+                                                       const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                       const double2* __restrict__ taus, float2* __restrict__ out,
+                                                       int color, int zero_init, double2* __restrict__ dot, int nblk) {
+  using S = RbSlot<MODE>;
+  extern __shared__ __align__(128) unsigned char rb_smem[];
+  __shared__ __align__(8) uint64_t full[RB_D], empty[RB_D];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int nh = L.nx >> 1;
+  const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  const ZRing<RB_D> ring{k0};
+  const bool fboth = MODE == 1 || dot != nullptr;  // f of both colours in the slot
+  if (tid == 0) {
+    for (int s = 0; s < RB_D; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  double2 acc = make_double2(0.0, 0.0);
+  if (wy == kT / 32) {  // producer warp
+    if (lane == 0) {
+      const bool ldx = MODE == 1 || !zero_init;
+      const uint32_t fb = fboth ? S::FB : S::FB / 2;
+      for (int p = k0 - 1; p <= k1; ++p) {
+        const int use = (p - k0 + 1) / RB_D, s = ring.slot(p);
+        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = rb_smem + (size_t)s * S::SLOT;
+        const bool lf = p >= k0 && p < k1, lc = p >= k0;
+        mbar_arrive_tx(&full[s], (ldx ? S::XB : 0u) + (lf ? fb : 0u) + (lc ? S::CB : 0u));
+        if (ldx) tma_load5(sp, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[s]);
+        if (lf) tma_load5(sp + S::OFF_F, &mf, m0, fboth ? 0 : color, y0, p, b, &full[s]);
+        if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[s]);
+      }
+    }
+  } else {
+    const int m = m0 + lane, j = y0 + wy;
+    const bool in = m < nh && j < L.ny;
+    const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+    float2* ob = out + (int64_t)b * L.n;
+    const int nf = fboth ? 2 : 1;
+    for (int k = k0; k < k1; ++k) {
+      mbar_wait(&full[ring.slot(k - 1)], ring.parity(k - 1));
+      mbar_wait(&full[ring.slot(k)], ring.parity(k));
+      mbar_wait(&full[ring.slot(k + 1)], ring.parity(k + 1));
+      const unsigned char* sm = rb_smem + (size_t)ring.slot(k - 1) * S::SLOT;
+      const unsigned char* s0 = rb_smem + (size_t)ring.slot(k) * S::SLOT;
+      const unsigned char* su = rb_smem + (size_t)ring.slot(k + 1) * S::SLOT;
+      // x[row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
+      auto X = [](const unsigned char* s, int r, int h, int q) {
+        return reinterpret_cast<const float2*>(s)[(r * S::NX + h) * RB_XP + q];
+      };
+      auto F = [&](int h) { return reinterpret_cast<const float2*>(s0 + S::OFF_F)[(wy * nf + h) * RB_P + lane]; };
+      // coefficient comp of colour h at [row rc = j - y0][position qc = pos - m0]
+      auto C = [](const unsigned char* s, int rc, int comp, int h, int qc) {
+        return reinterpret_cast<const float*>(s + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc];
+      };
+      if (in) {
+        // one colour-c cell at (row j, position m): i = 2m + s.  xh: the slot colour of the
+        // other colour's x (MODE 0: the only one, 0; MODE 1: c ^ 1)
+        auto update = [&](int c, int xh, float2 f, float2& xc_out) -> float2 {
+          const int s = (j + k + c) & 1, r = wy + 1, q = lane + 2;
+          const float tw = C(s0, wy, 0, c, lane), ts = C(s0, wy, 1, c, lane), tb = C(s0, wy, 2, c, lane);
+          const float mm = C(s0, wy, 3, c, lane);
+          const float te = C(s0, wy, 0, c ^ 1, lane + s), tn = C(s0, wy + 1, 1, c ^ 1, lane);
+          const float tt = C(su, wy, 2, c ^ 1, lane);
+          const float dk = tw + te + ts + tn + tb + tt;
+          float ox = 0.f, oy = 0.f;
+          if (MODE == 1 || !zero_init) {
+            const float2 w = X(s0, r, xh, q - 1 + s), e = X(s0, r, xh, q + s);
+            const float2 so = X(s0, r - 1, xh, q), no = X(s0, r + 1, xh, q);
+            const float2 dn = X(sm, r, xh, q), up = X(su, r, xh, q);
+            ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
+            oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
+          }
+          if (MODE == 0) {
+            xc_out = diag_solve_r<float, float2>(dk, mm, tr, ti, make_float2(f.x + ox, f.y + oy));
+            return xc_out;
+          }
+          const float2 xa = X(s0, r, c, q);
+          const float dr = dk + tr * mm, di = ti * mm;
+          return make_float2(f.x - (dr * xa.x - di * xa.y - ox), f.y - (dr * xa.y + di * xa.x - oy));
+        };
+        const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+        if (MODE == 0) {
+          float2 xn;
+          update(color, 0, F(fboth ? color : 0), xn);
+          ob[row + (int64_t)color * nh + m] = xn;
+          if (dot) {
+            const float2 fc = F(color), fo = F(color ^ 1), xo = X(s0, wy + 1, 0, lane + 2);
+            acc = cfma(make_double2(fc.x, fc.y), make_double2(xn.x, xn.y), acc);
+            acc = cfma(make_double2(fo.x, fo.y), make_double2(xo.x, xo.y), acc);
+          }
+        } else {
+          float2 unused;
+          ob[row + m] = update(0, 1, F(0), unused);
+          ob[row + nh + m] = update(1, 0, F(1), unused);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ring.slot(k - 1)]);  // this warp is done with plane k - 1
+    }
+  }
+  if (MODE == 0 && dot) {
+    acc = block_sum(acc);
+    if (threadIdx.x == 0) dot[(int64_t)b * nblk + cb] = acc;
+  }
+}
+
 // FP64 operator tiles: 32 x 8 cells, one per thread
 constexpr int TA_W = 32, TA_H = 8;
 constexpr int TA_XW = TA_W + 2, TA_XH = TA_H + 2;  // p: x0-1 .. x0+32, y0-1 .. y0+8
@@ -1163,6 +1583,8 @@ __global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant
 struct TzMaps {
   bool ok = false;
   CUtensorMap x, f, c;
+  bool rb = false;                // colour-split level: the mg_rb kernels and maps below
+  CUtensorMap rx0, rx1, rf1, rf2, rc;  // x (one / both colours), f (one / both), coefficients
 };
 
 // q = A p, partial p^T q
@@ -1186,13 +1608,14 @@ __global__ void __launch_bounds__(kT) apply_dot_kernel(LevelView L, Batch bt, co
 // into the next direction update, which reads p anyway.)
 __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
                                                        const double2* __restrict__ q, double2* __restrict__ r,
-                                                       VM* __restrict__ rmg, double* __restrict__ part, int nblk) {
+                                                       VM* __restrict__ rmg, double* __restrict__ part, int nblk,
+                                                       int snx, int sny) {
   ITEM_PROLOGUE(n);
   double s = 0.0;
   if (in) {
     const double2 ra = csub(r[b * n + a], cmul(alpha[b], q[b * n + a]));
     r[b * n + a] = ra;
-    rmg[b * n + a] = vfrom<VM>(ra);
+    rmg[b * n + rb_flat(a, snx, sny)] = vfrom<VM>(ra);
     s = cabs2(ra);
   }
   s = block_sum(s);
@@ -1204,10 +1627,10 @@ __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, cons
 __global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const double2* __restrict__ alpha,
                                                      const double2* __restrict__ beta, const VM* __restrict__ z,
                                                      double2* __restrict__ p, double2* __restrict__ u, int64_t us,
-                                                     int first) {
+                                                     int first, int snx, int sny) {
   ITEM_PROLOGUE(n);
   if (!in) return;
-  const double2 za = vto(z[b * n + a]);
+  const double2 za = vto(z[b * n + rb_flat(a, snx, sny)]);
   if (first) {
     p[b * n + a] = za;
     return;
@@ -1398,6 +1821,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   cudaStream_t st = ctx->stream;
   const int last = (int)p->levels.size() - 1;
   LevelViewT<R> L = mg_view<R>(p, l);
+  L.split = tz && tz[l].rb;
   const double vb = sizeof(V), rb = sizeof(R);
   const double cell_bytes = (double)L.n * Bc;
   const double coef = (double)L.n * rb * (DIM + 1);
@@ -1434,6 +1858,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     return X[l];
   }
   LevelViewT<R> Lc = mg_view<R>(p, l + 1);
+  Lc.split = tz && tz[l + 1].rb;
   const Level& lev = *p->levels[l];
   // red-black sweeps per pre/post smoothing (LT_MG_NU, default 2)
   static const int nu = [] {
@@ -1447,10 +1872,17 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   const bool tma = tz && tz[l].ok;
   const unsigned tgrid = (unsigned)tz_blocks(L) * (unsigned)Bc;
   const TzDims tdims{L.nx, L.ny, L.nz, L.n};
+  const bool rbk = tz && tz[l].rb;
+  const unsigned rgrid = (unsigned)rb_blocks(L) * (unsigned)Bc;
   auto half = [&](int color, int zero_init, double2* dot) {
-    // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled
-    launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", cell_bytes * (zero_init ? 2 : 3) * vb + coef, [&] {
-      if (tma)
+    // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled.
+    // Colour-split: a half sweep moves half of f and of x twice (1.5 c per cell, 1 from zero)
+    const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
+    launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", hb + coef, [&] {
+      if (rbk)
+        mg_rb_kernel<0><<<rgrid, kTP, RbSlot<0>::SMEM, st>>>(tz[l].rx0, dot ? tz[l].rf2 : tz[l].rf1, tz[l].rc, tdims, bt,
+                                                           taus, (float2*)X[l], color, zero_init, dot, rb_blocks(L));
+      else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
       else if (pairs)
@@ -1467,7 +1899,10 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     half(1, 0, nullptr);
   }
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
-    if (tma)
+    if (rbk)
+      mg_rb_kernel<1><<<rgrid, kTP, RbSlot<1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
+                                                         (float2*)Rr[l], 0, 0, nullptr, 0);
+    else if (tma)
       mg_tma_kernel<1><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
                                                  nullptr, 0);
     else if (pairs)
@@ -1477,13 +1912,31 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     else
       residual_kernel<R, DIM><<<(unsigned)L.ntiles * (unsigned)Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
   });
+  // pair transfers for aggregation 2 in every direction (3-D, FP32 V-cycle)
+  static const bool pair_on = std::getenv("LT_ZM_TRANSFER") == nullptr;
+  const bool ptr = pair_on && std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
+                   lev.agg[2] == 2 && (L.nx & 1) == 0;
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
+    if constexpr (std::is_same<R, float>::value) {
+      if (ptr) {
+        const unsigned g = (unsigned)(((Lc.nx + 31) / 32) * ((Lc.ny + TP_TY - 1) / TP_TY) * ((Lc.nz + TP_ZC - 1) / TP_ZC));
+        restrict_pair_kernel<<<g * Bc, 32 * TP_TY, 0, st>>>(L, Lc, bt, Rr[l], F[l + 1]);
+        return;
+      }
+    }
     restrict_zm_kernel<R><<<(unsigned)zm_blocks(Lc) * Bc, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt,
                                                                       Rr[l], F[l + 1]);
   });
   const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr, nullptr, nullptr, tz);
   // coarse correction, then the transpose of the pre-smoother (black, red, ...), in place
   launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+    if constexpr (std::is_same<R, float>::value) {
+      if (ptr) {
+        const unsigned g = (unsigned)(((L.nx / 2 + 31) / 32) * ((L.ny + 7) / 8) * ((L.nz + ZM_ZC - 1) / ZM_ZC));
+        prolong_pair_kernel<<<g * Bc, kT, 0, st>>>(L, Lc, bt, ec, X[l]);
+        return;
+      }
+    }
     prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
   });
   for (int s = 0; s < nu; ++s) {
@@ -1492,7 +1945,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     const bool last_sweep = s == nu - 1;
     half(0, 0, last_sweep && pairs ? dot_part : nullptr);
   }
-  if (dot_nblk) *dot_nblk = (tma || pairs) && dot_part ? zp_blocks(L) : 0;
+  if (dot_nblk) *dot_nblk = !dot_part ? 0 : rbk ? rb_blocks(L) : (tma || pairs) ? zp_blocks(L) : 0;
   return X[l];
 }
 
@@ -1561,6 +2014,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   // FP64 operator's maps on the finest level.  LT_NO_TMA=1 selects the register-pipelined
   // kernels instead.
   static const bool tma_on = std::getenv("LT_NO_TMA") == nullptr;
+  static const bool rb_on = std::getenv("LT_NO_RB") == nullptr;  // colour-split levels
   std::vector<TzMaps> tzm(nl);
   if (tma_on) {
     static bool attr = false;
@@ -1568,6 +2022,10 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<1>::SMEM));
       attr = true;
     }
   }
@@ -1586,6 +2044,24 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       tzm[l].f = tma_map_8b(F[l], 4, dims, str, bf);
       tzm[l].c = tma_map_8b(Lv.pack32.get(), 3, cd, cs, bc);
       tzm[l].ok = true;
+      if (rb_on && Lv.packrb.get() && nx % 4 == 0) {
+        // colour-split maps: vectors {pos, colour, y, z, item}, coefficients {pos, colour,
+        // comp, y, z} (Level::packrb)
+        const uint64_t vd[5] = {nx / 2, 2, ny, nz, (uint64_t)Bc};
+        const uint64_t vs[4] = {nx / 2 * 8, nx * 8, nx * ny * 8, nx * ny * nz * 8};
+        const uint32_t bx0[5] = {RB_XP, 1, RB_H + 2, 1, 1}, bx1[5] = {RB_XP, 2, RB_H + 2, 1, 1};
+        const uint32_t bf1[5] = {RB_P, 1, RB_H, 1, 1}, bf2[5] = {RB_P, 2, RB_H, 1, 1};
+        const uint64_t P = (uint64_t)Lv.rb_P;
+        const uint64_t kd[5] = {P, 2, 4, ny + 1, nz + 1};
+        const uint64_t ks[4] = {P * 4, 2 * P * 4, 8 * P * 4, 8 * P * 4 * (ny + 1)};
+        const uint32_t kb[5] = {RB_CP, 2, 4, RB_H + 1, 1};
+        tzm[l].rx0 = tma_map_8b(X[l], 5, vd, vs, bx0);
+        tzm[l].rx1 = tma_map_8b(X[l], 5, vd, vs, bx1);
+        tzm[l].rf1 = tma_map_8b(F[l], 5, vd, vs, bf1);
+        tzm[l].rf2 = tma_map_8b(F[l], 5, vd, vs, bf2);
+        tzm[l].rc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, kb);
+        tzm[l].rb = true;
+      }
     }
   }
   // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
@@ -1604,12 +2080,14 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     map_c64 = tma_map_8b(p->levels[0]->pack64.get(), 3, cd, cs, bc);
   }
   const unsigned grid = (unsigned)nblk * (unsigned)Bc;
+  // the finest level's multigrid vectors (rmg, z) are colour-split when its kernels are
+  const int snx = tzm[0].rb ? L0.nx : 0, sny = tzm[0].rb ? L0.ny : 0;
   const double nb = (double)n * Bc;
   const double coef = (double)n * 8.0 * (DIM + 1);
   const double vb = sizeof(V);
 
   launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
-    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), nblk);
+    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), nblk, snx, sny);
   });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), nblk, sc); });
   std::vector<double> bb(Bc), rr(Bc), best(Bc);
@@ -1647,7 +2125,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     if (dnb == 0) {
       dnb = nblk;
       launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
-        bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk);
+        bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk, snx, sny);
       });
     }
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(op, bt, partials.get(), dnb, sc); });
@@ -1655,7 +2133,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   // z = B r ; rho = r^T z ; p = z
   precondition(OP_RHO);
   launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
-    pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 1);
+    pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 1, snx, sny);
   });
   std::vector<int> pending(Bc, 0);  // items whose u still lacks this iteration's alpha p
   for (int it = 0; it < p->inner_maxit; ++it) {
@@ -1679,7 +2157,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     });
     (void)pdir;
     launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
-      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), nblk);
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), nblk, snx, sny);
     });
     for (int b = 0; b < Bc; ++b)
       if (!done[b]) pending[b] = 1;
@@ -1709,7 +2187,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     }
     precondition(OP_BETA);
     launch(ctx, "cocg_vec", nb * (64.0 + vb), [&] {
-      pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 0);
+      pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 0, snx, sny);
     });
     for (int b = 0; b < Bc; ++b)
       if (!done[b]) pending[b] = 0;

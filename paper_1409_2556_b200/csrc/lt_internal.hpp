@@ -105,6 +105,11 @@ struct lt_ctx_s {
 
 namespace lt {
 
+// LT_DEBUG_SYNC=1: synchronise after every launch and name the kernel class that failed
+inline bool debug_sync() {
+  static const bool on = std::getenv("LT_DEBUG_SYNC") != nullptr;
+  return on;
+}
 // Launch a kernel (callable issuing exactly one launch on ctx->stream) with accounting.
 template <class F>
 inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f) {
@@ -121,6 +126,10 @@ inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f
   }
   f();
   check_launch(name);
+  if (debug_sync()) {
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) throw Error(LT_ERR_CUDA, std::string("kernel ") + name + ": " + cudaGetErrorString(e));
+  }
 }
 
 // ---- host-side phase tracing (LT_TRACE=1): synchronising wall-clock scopes on stderr ----
@@ -184,6 +193,12 @@ struct Level {
   // (nz+1) (the high boundary faces in the extra row / column / plane), FP32 and FP64: the
   // operand tiles of the TMA-fed z-marching kernels
   DeviceBuffer pack32, pack64;
+  // FD levels with nx % 4 == 0 and nx >= 64: the same FP32 coefficients in the colour-split
+  // layout of the red-black TMA kernels (inner.cu), [k][j][comp W,S,B,M][colour][pos] with
+  // pos = i / 2, colour = (i + j + k) & 1, rb_P >= nx / 2 + 1 positions per colour (padded
+  // to a multiple of 4)
+  DeviceBuffer packrb;
+  int rb_P = 0;
   int agg[3] = {1, 1, 1};  // aggregation to the next coarser level (FD)
 };
 
@@ -202,6 +217,8 @@ struct LevelViewT {
   const R* Mx;  // P1 mass couplings (null for FD)
   const R* My;
   const R* Md;
+  // vectors of this level are stored colour-split (inner.cu: rb_index); set by the V-cycle
+  int split;
 };
 using LevelView = LevelViewT<double>;
 using LevelView32 = LevelViewT<float>;
@@ -253,6 +270,10 @@ void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, doub
 // Tiled TMA tensor map over 8-byte elements (no swizzle, out-of-bounds boxes read as zero);
 // dims / box innermost first, strides_bytes for dims 1.. (tma.cu)
 CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box);
+// the same over 4-byte (FP32) elements.  Every box must start 16-byte aligned in its
+// innermost dimension: an unaligned start faults ("illegal instruction") on B200.
+CUtensorMap tma_map_4b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                        const uint32_t* box);
 
 // device bytes a solve may still take: free + the pool's reserved-but-unused memory (ctx.cu)

@@ -417,6 +417,26 @@ __global__ void pack_coef_kernel(const double* __restrict__ Tx, const double* __
   out[t] = T4{(E)tw, (E)ts, (E)tb, (E)m};
 }
 
+// The FP32 coefficients in the colour-split layout (Level::packrb)
+__global__ void pack_rb_kernel(const double* __restrict__ Tx, const double* __restrict__ Ty,
+                               const double* __restrict__ Tz, const double* __restrict__ M, int nx, int ny, int nz,
+                               int P, float* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t cnt = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+  if (t >= cnt) return;
+  const int i = (int)(t % (nx + 1));
+  const int j = (int)((t / (nx + 1)) % (ny + 1));
+  const int k = (int)(t / ((int64_t)(nx + 1) * (ny + 1)));
+  const bool ci = i < nx, cj = j < ny, ck = k < nz;
+  const double v[4] = {(cj && ck) ? Tx[((int64_t)k * ny + j) * (nx + 1) + i] : 0.0,
+                       (ci && ck) ? Ty[((int64_t)k * (ny + 1) + j) * nx + i] : 0.0,
+                       (Tz && ci && cj) ? Tz[((int64_t)k * ny + j) * nx + i] : 0.0,
+                       (ci && cj && ck) ? M[((int64_t)k * ny + j) * nx + i] : 0.0};
+  const int h = (i + j + k) & 1, pos = i >> 1;
+  const int64_t row = (int64_t)k * (ny + 1) + j;
+  for (int c = 0; c < 4; ++c) out[((row * 4 + c) * 2 + h) * P + pos] = (float)v[c];
+}
+
 static void make_fp32_copies(lt_pencil p) {
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
@@ -585,6 +605,16 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
       pack_coef_kernel<float4><<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx, Lv.ny,
                                                                                Lv.nz, Lv.pack32.as<float4>());
     });
+    if (p->kind != LT_GRID_P1_TRI && Lv.nx % 4 == 0 && Lv.nx >= 64 && Lv.Tz) {
+      Lv.rb_P = ((Lv.nx / 2 + 1) + 3) / 4 * 4;
+      const size_t rb = sizeof(float) * (size_t)(Lv.nz + 1) * (Lv.ny + 1) * 8 * Lv.rb_P;
+      Lv.packrb.allocate(rb, st);
+      LT_CUDA(cudaMemsetAsync(Lv.packrb.get(), 0, rb, st));
+      launch(ctx, "assemble", 48.0 * cnt, [&] {
+        pack_rb_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx, Lv.ny, Lv.nz,
+                                                                       Lv.rb_P, Lv.packrb.as<float>());
+      });
+    }
     if (l == 0) {
       Lv.pack64.allocate(sizeof(double4) * cnt, st);
       launch(ctx, "assemble", 36.0 * cnt, [&] {

@@ -25,8 +25,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 }  // namespace
 
-CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                       const uint32_t* box) {
+static CUtensorMap tma_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                           const uint32_t* box, CUtensorMapDataType type) {
   auto fn = encode_fn();
   if (!fn) throw Error(LT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
   CUtensorMap m;
@@ -38,11 +38,21 @@ CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const u
     es[r] = 1;
     if (r + 1 < rank) gs[r] = strides_bytes[r];
   }
-  const CUresult res = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void*>(base), gd, gs, bx,
+  const CUresult res = fn(&m, type, (cuuint32_t)rank, const_cast<void*>(base), gd, gs, bx,
                           es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS) throw Error(LT_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)res));
   return m;
+}
+
+CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box) {
+  return tma_map(base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT64);
+}
+
+CUtensorMap tma_map_4b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box) {
+  return tma_map(base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
 }  // namespace lt
