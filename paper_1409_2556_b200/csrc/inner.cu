@@ -1345,20 +1345,24 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c
       : "memory");
 }
 
-// Tile: 32 positions (one warp, 64 cells of a row) x RB_H rows, z-march over ZM_ZC planes.
-// Per plane slot: x (the other colour for a half sweep, both for the residual) over rows
-// y0-1 .. y0+RB_H and positions m0-2 .. m0+33, f over the tile (own colour, both with dot or
-// for the residual), coefficients of both colours over rows y0 .. y0+RB_H and positions
+// Tile: 32 positions (one warp, 64 cells of a row) x RB_H rows, z-march over ZM_ZC planes,
+// for NI items at once (the items share the coefficient tiles and every coefficient-derived
+// register: a half sweep runs 2 items per CTA, the residual 1).  Per plane slot and item: x
+// (the other colour for a half sweep, both for the residual) over rows y0-1 .. y0+RB_H and
+// positions m0-2 .. m0+33, f over the tile (own colour; both with dot or for the residual);
+// once per slot the coefficients of both colours over rows y0 .. y0+RB_H, positions
 // m0 .. m0+35.
 constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = 5;
-template <int MODE>
+template <int MODE, int NI>
 struct RbSlot {
   static constexpr int NX = MODE == 0 ? 1 : 2;  // colours of x in the slot
-  static constexpr uint32_t XB = sizeof(float2) * RB_XP * NX * (RB_H + 2);
-  static constexpr uint32_t FB = sizeof(float2) * RB_P * 2 * RB_H;  // room for both colours
+  static constexpr uint32_t XB = sizeof(float2) * RB_XP * NX * (RB_H + 2);     // per item
+  static constexpr uint32_t XBA = (XB + 127) / 128 * 128;
+  // f per item: both colours when NI == 1 (residual, or a sweep forming f^T x), else its own
+  static constexpr uint32_t FB = sizeof(float2) * RB_P * (NI == 1 ? 2 : 1) * RB_H;
   static constexpr uint32_t CB = sizeof(float) * RB_CP * 2 * 4 * (RB_H + 1);
-  static constexpr uint32_t OFF_F = (XB + 127) / 128 * 128;
-  static constexpr uint32_t OFF_C = (OFF_F + FB + 127) / 128 * 128;
+  static constexpr uint32_t OFF_F = XBA * NI;
+  static constexpr uint32_t OFF_C = OFF_F + FB * NI;
   static constexpr uint32_t SLOT = (OFF_C + CB + 127) / 128 * 128;
   static constexpr size_t SMEM = (size_t)SLOT * RB_D;
 };
@@ -1368,21 +1372,47 @@ inline int rb_blocks(const VW& L) {
   return ((L.nx / 2 + RB_P - 1) / RB_P) * ((L.ny + RB_H - 1) / RB_H) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
 }
 
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // MODE 0: red-black half sweep of `color`, in place on the colour's half of x (zero_init: x = 0
 // on entry, so no x is read; dot: also the partials of f^T x over both colours after the
 // sweep).  MODE 1: r = f - A x on both colours.  mx / mf: 5-D maps {pos, colour, y, z, item}
-// of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.
-template <int MODE>
+// of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.  Blocks:
+// rb_blocks(L) per group of NI consecutive items (item group fastest).
+template <int MODE, int NI>
 __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ CUtensorMap mx,
                                                        const __grid_constant__ CUtensorMap mf,
                                                        const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                        const double2* __restrict__ taus, float2* __restrict__ out,
                                                        int color, int zero_init, double2* __restrict__ dot, int nblk) {
-  using S = RbSlot<MODE>;
+  using S = RbSlot<MODE, NI>;
   extern __shared__ __align__(128) unsigned char rb_smem[];
   __shared__ __align__(8) uint64_t full[RB_D], empty[RB_D];
-  LT_ITEM_BLOCK(bt.B, b, cb);
-  if (bt.done[b]) return;
+  const int ngroups = (bt.B + NI - 1) / NI;
+  const int grp = (int)(blockIdx.x % ngroups), cb = (int)(blockIdx.x / ngroups);
+  bool live[NI];
+  int nlive = 0;
+#pragma unroll
+  for (int t = 0; t < NI; ++t) {
+    const int b = grp * NI + t;
+    live[t] = b < bt.B && !bt.done[b];
+    nlive += live[t];
+  }
+  if (nlive == 0) return;
   const int nh = L.nx >> 1;
   const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
   const int ntile = tiles_x * tiles_y;
@@ -1390,103 +1420,155 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
   const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const ZRing<RB_D> ring{k0};
-  const bool fboth = MODE == 1 || dot != nullptr;  // f of both colours in the slot
+  const bool fboth = NI == 1 && (MODE == 1 || dot != nullptr);  // f of both colours in the slot
   if (tid == 0) {
-    for (int s = 0; s < RB_D; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kT / 32);
+    for (int q = 0; q < RB_D; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], kT / 32);
     }
     mbar_init_fence();
   }
   __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
   double2 acc = make_double2(0.0, 0.0);
   if (wy == kT / 32) {  // producer warp
     if (lane == 0) {
       const bool ldx = MODE == 1 || !zero_init;
-      const uint32_t fb = fboth ? S::FB : S::FB / 2;
+      const uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
+      uint32_t bytes_xf = 0;
+#pragma unroll
+      for (int t = 0; t < NI; ++t)
+        if (live[t]) bytes_xf += (ldx ? S::XB : 0u);
+      int q = 0, use = 0;
       for (int p = k0 - 1; p <= k1; ++p) {
-        const int use = (p - k0 + 1) / RB_D, s = ring.slot(p);
-        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-        unsigned char* sp = rb_smem + (size_t)s * S::SLOT;
+        if (use > 0) mbar_wait(&empty[q], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = rb_smem + (size_t)q * S::SLOT;
         const bool lf = p >= k0 && p < k1, lc = p >= k0;
-        mbar_arrive_tx(&full[s], (ldx ? S::XB : 0u) + (lf ? fb : 0u) + (lc ? S::CB : 0u));
-        if (ldx) tma_load5(sp, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[s]);
-        if (lf) tma_load5(sp + S::OFF_F, &mf, m0, fboth ? 0 : color, y0, p, b, &full[s]);
-        if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[s]);
+        uint32_t bytes = bytes_xf + (lc ? S::CB : 0u);
+        if (lf)
+#pragma unroll
+          for (int t = 0; t < NI; ++t) bytes += live[t] ? fb : 0u;
+        mbar_arrive_tx(&full[q], bytes);
+#pragma unroll
+        for (int t = 0; t < NI; ++t) {
+          if (!live[t]) continue;
+          const int b = grp * NI + t;
+          if (ldx) tma_load5(sp + t * S::XBA, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[q]);
+          if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, &full[q]);
+        }
+        if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[q]);
+        if (++q == RB_D) { q = 0; ++use; }
       }
     }
   } else {
     const int m = m0 + lane, j = y0 + wy;
     const bool in = m < nh && j < L.ny;
-    const float tr = (float)taus[b].x, ti = (float)taus[b].y;
-    float2* ob = out + (int64_t)b * L.n;
+    float tr[NI], ti[NI];
+#pragma unroll
+    for (int t = 0; t < NI; ++t) {
+      const int b = min(grp * NI + t, bt.B - 1);
+      tr[t] = (float)taus[b].x;
+      ti[t] = (float)taus[b].y;
+    }
     const int nf = fboth ? 2 : 1;
+    // ring: planes k - 1, k, k + 1 in slots qm, q0, qu; qu's phase parity pu
+    int qm = 0, q0 = 1, qu = 2;
+    uint32_t pu = 0;
+    mbar_wait_u32(full0 + 8 * qm, 0);
+    mbar_wait_u32(full0 + 8 * q0, 0);
+    const int r = wy + 1, xq = lane + 2;
     for (int k = k0; k < k1; ++k) {
-      mbar_wait(&full[ring.slot(k - 1)], ring.parity(k - 1));
-      mbar_wait(&full[ring.slot(k)], ring.parity(k));
-      mbar_wait(&full[ring.slot(k + 1)], ring.parity(k + 1));
-      const unsigned char* sm = rb_smem + (size_t)ring.slot(k - 1) * S::SLOT;
-      const unsigned char* s0 = rb_smem + (size_t)ring.slot(k) * S::SLOT;
-      const unsigned char* su = rb_smem + (size_t)ring.slot(k + 1) * S::SLOT;
-      // x[row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
-      auto X = [](const unsigned char* s, int r, int h, int q) {
-        return reinterpret_cast<const float2*>(s)[(r * S::NX + h) * RB_XP + q];
+      mbar_wait_u32(full0 + 8 * qu, pu);
+      const unsigned char* sm = rb_smem + (size_t)qm * S::SLOT;
+      const unsigned char* s0 = rb_smem + (size_t)q0 * S::SLOT;
+      const unsigned char* su = rb_smem + (size_t)qu * S::SLOT;
+      // x[item t][row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
+      auto X = [](const unsigned char* sl, int t, int rr, int h, int q) {
+        return reinterpret_cast<const float2*>(sl + t * S::XBA)[(rr * S::NX + h) * RB_XP + q];
       };
-      auto F = [&](int h) { return reinterpret_cast<const float2*>(s0 + S::OFF_F)[(wy * nf + h) * RB_P + lane]; };
+      auto F = [&](int t, int h) {
+        return reinterpret_cast<const float2*>(s0 + S::OFF_F + t * S::FB)[(wy * nf + h) * RB_P + lane];
+      };
       // coefficient comp of colour h at [row rc = j - y0][position qc = pos - m0]
-      auto C = [](const unsigned char* s, int rc, int comp, int h, int qc) {
-        return reinterpret_cast<const float*>(s + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc];
+      auto C = [](const unsigned char* sl, int rc, int comp, int h, int qc) {
+        return reinterpret_cast<const float*>(sl + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc];
       };
       if (in) {
-        // one colour-c cell at (row j, position m): i = 2m + s.  xh: the slot colour of the
-        // other colour's x (MODE 0: the only one, 0; MODE 1: c ^ 1)
-        auto update = [&](int c, int xh, float2 f, float2& xc_out) -> float2 {
-          const int s = (j + k + c) & 1, r = wy + 1, q = lane + 2;
-          const float tw = C(s0, wy, 0, c, lane), ts = C(s0, wy, 1, c, lane), tb = C(s0, wy, 2, c, lane);
-          const float mm = C(s0, wy, 3, c, lane);
-          const float te = C(s0, wy, 0, c ^ 1, lane + s), tn = C(s0, wy + 1, 1, c ^ 1, lane);
-          const float tt = C(su, wy, 2, c ^ 1, lane);
-          const float dk = tw + te + ts + tn + tb + tt;
-          float ox = 0.f, oy = 0.f;
-          if (MODE == 1 || !zero_init) {
-            const float2 w = X(s0, r, xh, q - 1 + s), e = X(s0, r, xh, q + s);
-            const float2 so = X(s0, r - 1, xh, q), no = X(s0, r + 1, xh, q);
-            const float2 dn = X(sm, r, xh, q), up = X(su, r, xh, q);
-            ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
-            oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
-          }
-          if (MODE == 0) {
-            xc_out = diag_solve_r<float, float2>(dk, mm, tr, ti, make_float2(f.x + ox, f.y + oy));
-            return xc_out;
-          }
-          const float2 xa = X(s0, r, c, q);
-          const float dr = dk + tr * mm, di = ti * mm;
-          return make_float2(f.x - (dr * xa.x - di * xa.y - ox), f.y - (dr * xa.y + di * xa.x - oy));
-        };
         const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+        // the colour-c cell at (row j, position m) is i = 2m + s; its coefficients (E, N, T from
+        // the other colour's W, S of row j + 1, B of plane k + 1)
+        auto coef = [&](int c, float& tw, float& te, float& ts, float& tn, float& tb, float& tt, float& mm) {
+          const int sft = (j + k + c) & 1;
+          tw = C(s0, wy, 0, c, lane);
+          ts = C(s0, wy, 1, c, lane);
+          tb = C(s0, wy, 2, c, lane);
+          mm = C(s0, wy, 3, c, lane);
+          te = C(s0, wy, 0, c ^ 1, lane + sft);
+          tn = C(s0, wy + 1, 1, c ^ 1, lane);
+          tt = C(su, wy, 2, c ^ 1, lane);
+          return sft;
+        };
+        // sum of T x over the six other-colour neighbours (xh: their colour in the slot)
+        auto offsum = [&](int t, int xh, int sft, float tw, float te, float ts, float tn, float tb, float tt) {
+          const float2 w = X(s0, t, r, xh, xq - 1 + sft), e = X(s0, t, r, xh, xq + sft);
+          const float2 so = X(s0, t, r - 1, xh, xq), no = X(s0, t, r + 1, xh, xq);
+          const float2 dn = X(sm, t, r, xh, xq), up = X(su, t, r, xh, xq);
+          return make_float2(tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x,
+                             tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y);
+        };
         if (MODE == 0) {
-          float2 xn;
-          update(color, 0, F(fboth ? color : 0), xn);
-          ob[row + (int64_t)color * nh + m] = xn;
-          if (dot) {
-            const float2 fc = F(color), fo = F(color ^ 1), xo = X(s0, wy + 1, 0, lane + 2);
-            acc = cfma(make_double2(fc.x, fc.y), make_double2(xn.x, xn.y), acc);
-            acc = cfma(make_double2(fo.x, fo.y), make_double2(xo.x, xo.y), acc);
+          float tw, te, ts, tn, tb, tt, mm;
+          const int sft = coef(color, tw, te, ts, tn, tb, tt, mm);
+          const float dk = tw + te + ts + tn + tb + tt;
+#pragma unroll
+          for (int t = 0; t < NI; ++t) {
+            if (!live[t]) continue;
+            float2 o = F(t, fboth ? color : 0);
+            if (!zero_init) {
+              const float2 os = offsum(t, 0, sft, tw, te, ts, tn, tb, tt);
+              o.x += os.x;
+              o.y += os.y;
+            }
+            const float dr = dk + tr[t] * mm, di = ti[t] * mm;
+            const float inv = __frcp_rn(dr * dr + di * di);
+            const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
+            const int b = grp * NI + t;
+            out[(int64_t)b * L.n + row + (int64_t)color * nh + m] = xn;
+            if (dot && t == 0) {  // (dot runs with NI = 1)
+              const float2 fc = F(t, color), fo = F(t, color ^ 1), xo = X(s0, t, r, 0, xq);
+              acc = cfma(make_double2(fc.x, fc.y), make_double2(xn.x, xn.y), acc);
+              acc = cfma(make_double2(fo.x, fo.y), make_double2(xo.x, xo.y), acc);
+            }
           }
         } else {
-          float2 unused;
-          ob[row + m] = update(0, 1, F(0), unused);
-          ob[row + nh + m] = update(1, 0, F(1), unused);
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float tw, te, ts, tn, tb, tt, mm;
+            const int sft = coef(c, tw, te, ts, tn, tb, tt, mm);
+            const float dk = tw + te + ts + tn + tb + tt;
+#pragma unroll
+            for (int t = 0; t < NI; ++t) {
+              if (!live[t]) continue;
+              const float2 os = offsum(t, c ^ 1, sft, tw, te, ts, tn, tb, tt);
+              const float2 xa = X(s0, t, r, c, xq), f = F(t, c);
+              const float dr = dk + tr[t] * mm, di = ti[t] * mm;
+              const int b = grp * NI + t;
+              out[(int64_t)b * L.n + row + (int64_t)c * nh + m] =
+                  make_float2(f.x - (dr * xa.x - di * xa.y - os.x), f.y - (dr * xa.y + di * xa.x - os.y));
+            }
+          }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[ring.slot(k - 1)]);  // this warp is done with plane k - 1
+      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // this warp is done with plane k - 1
+      qm = q0;
+      q0 = qu;
+      if (++qu == RB_D) { qu = 0; pu ^= 1u; }
     }
   }
   if (MODE == 0 && dot) {
     acc = block_sum(acc);
-    if (threadIdx.x == 0) dot[(int64_t)b * nblk + cb] = acc;
+    if (threadIdx.x == 0) dot[(int64_t)grp * nblk + cb] = acc;
   }
 }
 
@@ -1874,14 +1956,20 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   const TzDims tdims{L.nx, L.ny, L.nz, L.n};
   const bool rbk = tz && tz[l].rb;
   const unsigned rgrid = (unsigned)rb_blocks(L) * (unsigned)Bc;
+  const unsigned rgrid2 = (unsigned)rb_blocks(L) * (unsigned)((Bc + 1) / 2);
   auto half = [&](int color, int zero_init, double2* dot) {
     // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled.
     // Colour-split: a half sweep moves half of f and of x twice (1.5 c per cell, 1 from zero)
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
     launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", hb + coef, [&] {
       if (rbk)
-        mg_rb_kernel<0><<<rgrid, kTP, RbSlot<0>::SMEM, st>>>(tz[l].rx0, dot ? tz[l].rf2 : tz[l].rf1, tz[l].rc, tdims, bt,
-                                                           taus, (float2*)X[l], color, zero_init, dot, rb_blocks(L));
+        if (dot)  // one item per CTA: the partials are per item
+          mg_rb_kernel<0, 1><<<rgrid, kTP, RbSlot<0, 1>::SMEM, st>>>(tz[l].rx0, tz[l].rf2, tz[l].rc, tdims, bt, taus,
+                                                                    (float2*)X[l], color, zero_init, dot,
+                                                                    rb_blocks(L));
+        else
+          mg_rb_kernel<0, 2><<<rgrid2, kTP, RbSlot<0, 2>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
+                                                                     (float2*)X[l], color, zero_init, nullptr, 0);
       else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
@@ -1900,8 +1988,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   }
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
-      mg_rb_kernel<1><<<rgrid, kTP, RbSlot<1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
-                                                         (float2*)Rr[l], 0, 0, nullptr, 0);
+      mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
+                                                               (float2*)Rr[l], 0, 0, nullptr, 0);
     else if (tma)
       mg_tma_kernel<1><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
                                                  nullptr, 0);
@@ -2022,10 +2110,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)RbSlot<0>::SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)RbSlot<1>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0, 1>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0, 2>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<1, 1>::SMEM));
       attr = true;
     }
   }
