@@ -1572,18 +1572,25 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   }
 }
 
-// FP64 operator tiles: 32 x 8 cells, one per thread
+// FP64 operator tiles: 32 x 8 cells, one per thread (warp = one row of 32 cells).  The
+// coefficients come planar (Level::pack64: [k][j][W, S, B, M][i]), so every coefficient read
+// of a warp is one contiguous 256-byte run, and the in-row neighbours of p come from the
+// adjacent lanes: the interleaved {W, S, B, M} records made each coefficient read 8 shared
+// wavefronts and bound the kernel by shared memory at ~3.4 TB/s.
 constexpr int TA_W = 32, TA_H = 8;
 constexpr int TA_XW = TA_W + 2, TA_XH = TA_H + 2;  // p: x0-1 .. x0+32, y0-1 .. y0+8
-constexpr int TA_CW = TA_W + 1, TA_CH = TA_H + 1;  // packed coefficients x0 .. x0+32, y0 .. y0+8
-constexpr int TA_D = 4;
-constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;  // 5440
-constexpr uint32_t TA_CB = sizeof(double4) * TA_CW * TA_CH;  // 9504
-constexpr uint32_t TA_OFF_C = 5504, TA_SLOT = TA_OFF_C + 9600;
+constexpr int TA_CW = TA_W + 2, TA_CH = TA_H + 1;  // coefficients x0 .. x0+33 (x0+32 used), y0 .. y0+8
+#ifndef LT_TA_D
+#define LT_TA_D 6
+#endif
+constexpr int TA_D = LT_TA_D;  // ring depth: 3 live planes + 3 in flight
+constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;     // 5440
+constexpr uint32_t TA_CB = sizeof(double) * 4 * TA_CW * TA_CH;  // 9792
+constexpr uint32_t TA_OFF_C = 5504, TA_SLOT = TA_OFF_C + 9856;
 constexpr size_t TA_SMEM = (size_t)TA_SLOT * TA_D;
 
 // q = A(tau) p, partial p^T q (FP64)
-__global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
+__global__ void __launch_bounds__(kTP, TA_D <= 4 ? 3 : 2) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
                                                            const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                            const double2* __restrict__ taus, double2* __restrict__ q,
                                                            double2* __restrict__ part, int nblk) {
@@ -1597,7 +1604,6 @@ __global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant
   const int x0 = (tile % tiles_x) * TA_W, y0 = (tile / tiles_x) * TA_H;
   const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const ZRing<TA_D> ring{k0};
   if (tid == 0) {
     for (int s = 0; s < TA_D; ++s) {
       mbar_init(&full[s], 1);
@@ -1606,17 +1612,19 @@ __global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant
     mbar_init_fence();
   }
   __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
   double2 acc = make_double2(0.0, 0.0);
   if (wy == kT / 32) {  // producer warp
     if (lane == 0) {
+      int sl = 0, use = 0;
       for (int p = k0 - 1; p <= k1; ++p) {
-        const int use = (p - k0 + 1) / TA_D, s = ring.slot(p);
-        if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
-        unsigned char* sp = ta_smem + (size_t)s * TA_SLOT;
+        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = ta_smem + (size_t)sl * TA_SLOT;
         const bool lc = p >= k0;
-        mbar_arrive_tx(&full[s], TA_XB + (lc ? TA_CB : 0u));
-        tma_load4(sp, &mp, 2 * (x0 - 1), y0 - 1, p, b, &full[s]);
-        if (lc) tma_load3(sp + TA_OFF_C, &mc, 4 * x0, y0, p, &full[s]);
+        mbar_arrive_tx(&full[sl], TA_XB + (lc ? TA_CB : 0u));
+        tma_load4(sp, &mp, 2 * (x0 - 1), y0 - 1, p, b, &full[sl]);
+        if (lc) tma_load4(sp + TA_OFF_C, &mc, x0, 0, y0, p, &full[sl]);
+        if (++sl == TA_D) { sl = 0; ++use; }
       }
     }
   } else {
@@ -1625,36 +1633,49 @@ __global__ void __launch_bounds__(kTP, 3) apply_tma_kernel(const __grid_constant
     const double2 tau = taus[b];
     const int64_t plane = (int64_t)L.nx * L.ny;
     double2* qb = q + (int64_t)b * L.n;
+    int qm = 0, q0 = 1, qu = 2;
+    uint32_t pu = 0;
+    mbar_wait_u32(full0 + 8 * qm, 0);
+    mbar_wait_u32(full0 + 8 * q0, 0);
     for (int k = k0; k < k1; ++k) {
-      mbar_wait(&full[ring.slot(k - 1)], ring.parity(k - 1));
-      mbar_wait(&full[ring.slot(k)], ring.parity(k));
-      mbar_wait(&full[ring.slot(k + 1)], ring.parity(k + 1));
+      mbar_wait_u32(full0 + 8 * qu, pu);
+      const unsigned char* sm = ta_smem + (size_t)qm * TA_SLOT;
+      const unsigned char* s0 = ta_smem + (size_t)q0 * TA_SLOT;
+      const unsigned char* sp = ta_smem + (size_t)qu * TA_SLOT;
+      auto X = [](const unsigned char* sl, int yy, int xx) {
+        return reinterpret_cast<const double2*>(sl)[yy * TA_XW + xx];
+      };
+      auto C = [](const unsigned char* sl, int comp, int yy, int xx) {
+        return reinterpret_cast<const double*>(sl + TA_OFF_C)[(yy * 4 + comp) * TA_CW + xx];
+      };
+      // the row's centre values for every lane; in-row neighbours by shuffle
+      const double2 pc = X(s0, wy + 1, lane + 1);
+      double2 w, e;
+      w.x = __shfl_up_sync(0xffffffffu, pc.x, 1);
+      w.y = __shfl_up_sync(0xffffffffu, pc.y, 1);
+      e.x = __shfl_down_sync(0xffffffffu, pc.x, 1);
+      e.y = __shfl_down_sync(0xffffffffu, pc.y, 1);
+      if (lane == 0) w = X(s0, wy + 1, 0);
+      if (lane == 31) e = X(s0, wy + 1, TA_XW - 1);
       if (in) {
-        const unsigned char* sm = ta_smem + (size_t)ring.slot(k - 1) * TA_SLOT;
-        const unsigned char* s0 = ta_smem + (size_t)ring.slot(k) * TA_SLOT;
-        const unsigned char* sp = ta_smem + (size_t)ring.slot(k + 1) * TA_SLOT;
-        auto X = [](const unsigned char* s, int yy, int xx) {
-          return reinterpret_cast<const double2*>(s)[yy * TA_XW + xx];
-        };
-        auto Cf = [](const unsigned char* s, int yy, int xx) {
-          return reinterpret_cast<const double4*>(s + TA_OFF_C)[yy * TA_CW + xx];
-        };
-        const double4 cc = Cf(s0, wy, lane);
-        const double te = Cf(s0, wy, lane + 1).x, tn = Cf(s0, wy + 1, lane).y, tt = Cf(sp, wy, lane).z;
-        const double2 pc = X(s0, wy + 1, lane + 1);
-        const double2 w = X(s0, wy + 1, lane), e = X(s0, wy + 1, lane + 2);
+        const double tw = C(s0, 0, wy, lane), ts = C(s0, 1, wy, lane), tb = C(s0, 2, wy, lane);
+        const double mm = C(s0, 3, wy, lane);
+        const double te = C(s0, 0, wy, lane + 1), tn = C(s0, 1, wy + 1, lane), tt = C(sp, 2, wy, lane);
         const double2 so = X(s0, wy, lane + 1), no = X(s0, wy + 2, lane + 1);
         const double2 dn = X(sm, wy + 1, lane + 1), up = X(sp, wy + 1, lane + 1);
-        const double dk = cc.x + te + cc.y + tn + cc.z + tt;
-        const double ox = cc.x * w.x + te * e.x + cc.y * so.x + tn * no.x + cc.z * dn.x + tt * up.x;
-        const double oy = cc.x * w.y + te * e.y + cc.y * so.y + tn * no.y + cc.z * dn.y + tt * up.y;
-        const double dr = dk + tau.x * cc.w, di = tau.y * cc.w;
+        const double dk = tw + te + ts + tn + tb + tt;
+        const double ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
+        const double oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
+        const double dr = dk + tau.x * mm, di = tau.y * mm;
         const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
         qb[k * plane + (int64_t)j * L.nx + i] = qa;
         acc = cfma(pc, qa, acc);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[ring.slot(k - 1)]);
+      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);
+      qm = q0;
+      q0 = qu;
+      if (++qu == TA_D) { qu = 0; pu ^= 1u; }
     }
   }
   acc = block_sum(acc);
@@ -2156,18 +2177,21 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
   // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
   // reads and writes X[l]
-  const bool ta_ok = tma_on && p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32;
+  const bool ta_ok = tma_on && p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32 &&
+                     L0.nx % 2 == 0;
   CUtensorMap map_p{}, map_c64{};
   if (ta_ok) {
     const uint64_t nx = L0.nx, ny = L0.ny, nz = L0.nz;
     const uint64_t dims[4] = {2 * nx, ny, nz, (uint64_t)Bc};
     const uint64_t str[3] = {nx * 16, nx * ny * 16, nx * ny * nz * 16};
     const uint32_t bx[4] = {2 * TA_XW, TA_XH, 1, 1};
-    const uint64_t cd[3] = {4 * (nx + 1), ny + 1, nz + 1};
-    const uint64_t cs[2] = {(nx + 1) * 32, (nx + 1) * (ny + 1) * 32};
-    const uint32_t bc[3] = {4 * TA_CW, TA_CH, 1};
+    // planar coefficients [k][j][comp][i], rows of nx + 2 (Level::pack64)
+    const uint64_t P = nx + 2;
+    const uint64_t cd[4] = {P, 4, ny + 1, nz + 1};
+    const uint64_t cs[3] = {P * 8, 4 * P * 8, 4 * P * 8 * (ny + 1)};
+    const uint32_t bc[4] = {TA_CW, 4, TA_CH, 1};
     map_p = tma_map_8b(pp, 4, dims, str, bx);
-    map_c64 = tma_map_8b(p->levels[0]->pack64.get(), 3, cd, cs, bc);
+    map_c64 = tma_map_8b(p->levels[0]->pack64.get(), 4, cd, cs, bc);
   }
   const unsigned grid = (unsigned)nblk * (unsigned)Bc;
   // the finest level's multigrid vectors (rmg, z) are colour-split when its kernels are

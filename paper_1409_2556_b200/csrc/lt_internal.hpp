@@ -190,8 +190,9 @@ struct Level {
   DeviceBuffer storage32;
   DeviceBuffer elem;       // P1: per-element kappa then S on this level (coarsening input)
   // FD: per-cell packed {west face, south face, bottom face, mass} over (nx+1) x (ny+1) x
-  // (nz+1) (the high boundary faces in the extra row / column / plane), FP32 and FP64: the
-  // operand tiles of the TMA-fed z-marching kernels
+  // (nz+1) (the high boundary faces in the extra row / column / plane): pack32 (FP32
+  // records) for the natural-layout TMA kernels, pack64 (FP64, finest level, planar
+  // [k][j][comp][i] with rows of nx + 2) for the COCG operator
   DeviceBuffer pack32, pack64;
   // FD levels with nx % 4 == 0 and nx >= 64: the same FP32 coefficients in the colour-split
   // layout of the red-black TMA kernels (inner.cu), [k][j][comp W,S,B,M][colour][pos] with

@@ -417,6 +417,24 @@ __global__ void pack_coef_kernel(const double* __restrict__ Tx, const double* __
   out[t] = T4{(E)tw, (E)ts, (E)tb, (E)m};
 }
 
+// The FP64 coefficients of the finest level, planar: [k][j][W, S, B, M][i], rows of P >= nx + 1
+__global__ void pack_planar64_kernel(const double* __restrict__ Tx, const double* __restrict__ Ty,
+                                     const double* __restrict__ Tz, const double* __restrict__ M, int nx, int ny, int nz,
+                                     int P, double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t cnt = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
+  if (t >= cnt) return;
+  const int i = (int)(t % (nx + 1));
+  const int j = (int)((t / (nx + 1)) % (ny + 1));
+  const int k = (int)(t / ((int64_t)(nx + 1) * (ny + 1)));
+  const bool ci = i < nx, cj = j < ny, ck = k < nz;
+  const int64_t row = ((int64_t)k * (ny + 1) + j) * 4;
+  out[(row + 0) * P + i] = (cj && ck) ? Tx[((int64_t)k * ny + j) * (nx + 1) + i] : 0.0;
+  out[(row + 1) * P + i] = (ci && ck) ? Ty[((int64_t)k * (ny + 1) + j) * nx + i] : 0.0;
+  out[(row + 2) * P + i] = (Tz && ci && cj) ? Tz[((int64_t)k * ny + j) * nx + i] : 0.0;
+  out[(row + 3) * P + i] = (ci && cj && ck) ? M[((int64_t)k * ny + j) * nx + i] : 0.0;
+}
+
 // The FP32 coefficients in the colour-split layout (Level::packrb)
 __global__ void pack_rb_kernel(const double* __restrict__ Tx, const double* __restrict__ Ty,
                                const double* __restrict__ Tz, const double* __restrict__ M, int nx, int ny, int nz,
@@ -615,11 +633,14 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
                                                                        Lv.rb_P, Lv.packrb.as<float>());
       });
     }
-    if (l == 0) {
-      Lv.pack64.allocate(sizeof(double4) * cnt, st);
-      launch(ctx, "assemble", 36.0 * cnt, [&] {
-        pack_coef_kernel<double4><<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx,
-                                                                                  Lv.ny, Lv.nz, Lv.pack64.as<double4>());
+    if (l == 0 && Lv.nx % 2 == 0) {
+      const int P = Lv.nx + 2;
+      const size_t pb = sizeof(double) * (size_t)(Lv.nz + 1) * (Lv.ny + 1) * 4 * P;
+      Lv.pack64.allocate(pb, st);
+      LT_CUDA(cudaMemsetAsync(Lv.pack64.get(), 0, pb, st));
+      launch(ctx, "assemble", 40.0 * cnt, [&] {
+        pack_planar64_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx, Lv.ny,
+                                                                            Lv.nz, P, Lv.pack64.as<double>());
       });
     }
   }
