@@ -1577,20 +1577,24 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
 // of a warp is one contiguous 256-byte run, and the in-row neighbours of p come from the
 // adjacent lanes: the interleaved {W, S, B, M} records made each coefficient read 8 shared
 // wavefronts and bound the kernel by shared memory at ~3.4 TB/s.
-constexpr int TA_W = 32, TA_H = 8;
+#ifndef LT_TA_H
+#define LT_TA_H 8
+#endif
+constexpr int TA_W = 32, TA_H = LT_TA_H;  // one consumer warp per row
+constexpr int kTA = 32 * TA_H + 32;        // + the producer warp
 constexpr int TA_XW = TA_W + 2, TA_XH = TA_H + 2;  // p: x0-1 .. x0+32, y0-1 .. y0+8
 constexpr int TA_CW = TA_W + 2, TA_CH = TA_H + 1;  // coefficients x0 .. x0+33 (x0+32 used), y0 .. y0+8
 #ifndef LT_TA_D
 #define LT_TA_D 6
 #endif
 constexpr int TA_D = LT_TA_D;  // ring depth: 3 live planes + 3 in flight
-constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;     // 5440
+constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;     // 5440 (TA_H = 8)
 constexpr uint32_t TA_CB = sizeof(double) * 4 * TA_CW * TA_CH;  // 9792
-constexpr uint32_t TA_OFF_C = 5504, TA_SLOT = TA_OFF_C + 9856;
+constexpr uint32_t TA_OFF_C = (TA_XB + 127) / 128 * 128, TA_SLOT = (TA_OFF_C + TA_CB + 127) / 128 * 128;
 constexpr size_t TA_SMEM = (size_t)TA_SLOT * TA_D;
 
 // q = A(tau) p, partial p^T q (FP64)
-__global__ void __launch_bounds__(kTP, TA_D <= 4 ? 3 : 2) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
+__global__ void __launch_bounds__(kTA, TA_H > 8 ? 1 : (TA_D <= 4 ? 3 : 2)) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
                                                            const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                            const double2* __restrict__ taus, double2* __restrict__ q,
                                                            double2* __restrict__ part, int nblk) {
@@ -1607,14 +1611,14 @@ __global__ void __launch_bounds__(kTP, TA_D <= 4 ? 3 : 2) apply_tma_kernel(const
   if (tid == 0) {
     for (int s = 0; s < TA_D; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kT / 32);
+      mbar_init(&empty[s], TA_H);
     }
     mbar_init_fence();
   }
   __syncthreads();
   const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
   double2 acc = make_double2(0.0, 0.0);
-  if (wy == kT / 32) {  // producer warp
+  if (wy == TA_H) {  // producer warp
     if (lane == 0) {
       int sl = 0, use = 0;
       for (int p = k0 - 1; p <= k1; ++p) {
@@ -2252,10 +2256,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   std::vector<int> pending(Bc, 0);  // items whose u still lacks this iteration's alpha p
   for (int it = 0; it < p->inner_maxit; ++it) {
     const bool zm = DIM == 3 || p->kind != LT_GRID_P1_TRI;
-    const int nblk_apply = zm ? zm_blocks(L0) : L0.ntiles;
+    const int nblk_apply = ta_ok ? ((L0.nx + TA_W - 1) / TA_W) * ((L0.ny + TA_H - 1) / TA_H) *
+                                       ((L0.nz + ZM_ZC - 1) / ZM_ZC)
+                                 : zm ? zm_blocks(L0) : L0.ntiles;
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
       if (ta_ok)
-        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kTP, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
+        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kTA, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
                                                                          bt, d_taus, q, partials.as<double2>(),
                                                                          nblk_apply);
       else if (zm)
