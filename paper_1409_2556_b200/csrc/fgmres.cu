@@ -347,6 +347,12 @@ __global__ void small_solve(State S, int m, int force) {
 // partial ||r||^2 per (item, shift).  K u_j and M u_j are formed once per column and
 // accumulated as sum_j y_jq K u_j + (y_jq z_q) M u_j (y z staged in shared memory); the KC
 // per-shift partial norms are reduced together (one barrier per chunk, not one per shift).
+// Blocks: (x-y tile of the fine level, chunk of VR_Z planes) per item; each thread marches its
+// column through the chunk and accumulates its cells' |r|^2 per shift in registers, so the
+// per-shift block reductions run once per chunk instead of once per cell.
+constexpr int VR_Z = 16;
+inline int verify_blocks(const LevelView& L) { return L.tiles_x * L.tiles_y * ((L.nz + VR_Z - 1) / VR_Z); }
+
 template <int DIM>
 __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, int m, const double2* __restrict__ rhs,
                                                          const double2* const* __restrict__ Ucols,
@@ -357,7 +363,7 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
   __shared__ int flagged[256];
   __shared__ int nflag;
   __shared__ double2 ysm[MJ][KC], yzsm[MJ][KC];
-  __shared__ double red[NW][KC];
+  __shared__ double nsm[KC][kT];  // per-thread running |r|^2 per shift
   LT_ITEM_BLOCK(S.B, b, cb);
   if (threadIdx.x == 0) {
     int c = 0;
@@ -368,11 +374,13 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
   __syncthreads();
   if (nflag == 0) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tpp = L.tiles_x * L.tiles_y;
+  const int tile = (int)(cb % tpp), zc = (int)(cb / tpp);
+  const int kz0 = DIM == 3 ? zc * VR_Z : 0, kz1 = DIM == 3 ? min(L.nz, kz0 + VR_Z) : 1;
   int i, jj, kk;
-  int64_t a;
-  const bool in = tile_cell(L, (int)cb, i, jj, kk, a);
-  const double2 bv = in ? rhs[b * L.n + a] : make_double2(0.0, 0.0);
-  const double mval = in ? __ldg(L.M + a) : 0.0;
+  int64_t a0;
+  const bool in = tile_cell(L, tile, i, jj, kk, a0);  // (i, jj) of the column; plane 0
+  const int64_t plane = (int64_t)L.nx * L.ny;
   for (int c0 = 0; c0 < nflag; c0 += KC) {
     const int nc = min(KC, nflag - c0);
     const bool staged = m <= MJ;
@@ -391,49 +399,53 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
       }
     }
     __syncthreads();
-    double2 acc[KC];
 #pragma unroll
-    for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int q = 0; q < KC; ++q) nsm[q][threadIdx.x] = 0.0;
     if (in) {
-      for (int j = 0; j < m; ++j) {
-        const double2* ub = Ucols[j] + b * L.n;
-        double2 off;
-        double dk;
-        gather<DIM>(L, ub, a, i, jj, kk, off, dk);
-        const double2 ua = ub[a];
-        const double2 Ku = csub(cscale(ua, dk), off);
-        double2 Mu = cscale(ua, mval);
-        if (L.Mx) Mu = cadd(Mu, mass_off(L, ub, a, i, jj));
+      for (int k = kz0; k < kz1; ++k) {
+        const int64_t a = a0 + k * plane;
+        const double2 bv = rhs[b * L.n + a];
+        const double mval = __ldg(L.M + a);
+        double2 acc[KC];
 #pragma unroll
-        for (int q = 0; q < KC; ++q) {
-          if (q < nc) {
-            double2 y, yz;
-            if (staged) {
-              y = ysm[j][q];
-              yz = yzsm[j][q];
-            } else {
-              const int t = b * S.ns + flagged[c0 + q];
-              y = S.Y[(int64_t)t * S.maxit + j];
-              yz = cmul(y, S.shifts[t]);
+        for (int q = 0; q < KC; ++q) acc[q] = make_double2(0.0, 0.0);
+        for (int j = 0; j < m; ++j) {
+          const double2* ub = Ucols[j] + b * L.n;
+          double2 off;
+          double dk;
+          gather<DIM>(L, ub, a, i, jj, k, off, dk);
+          const double2 ua = ub[a];
+          const double2 Ku = csub(cscale(ua, dk), off);
+          double2 Mu = cscale(ua, mval);
+          if (L.Mx) Mu = cadd(Mu, mass_off(L, ub, a, i, jj));
+#pragma unroll
+          for (int q = 0; q < KC; ++q) {
+            if (q < nc) {
+              double2 y, yz;
+              if (staged) {
+                y = ysm[j][q];
+                yz = yzsm[j][q];
+              } else {
+                const int t = b * S.ns + flagged[c0 + q];
+                y = S.Y[(int64_t)t * S.maxit + j];
+                yz = cmul(y, S.shifts[t]);
+              }
+              acc[q] = cfma(y, Ku, cfma(yz, Mu, acc[q]));
             }
-            acc[q] = cfma(y, Ku, cfma(yz, Mu, acc[q]));
           }
         }
+#pragma unroll
+        for (int q = 0; q < KC; ++q)
+          if (q < nc) nsm[q][threadIdx.x] += cabs2(csub(bv, acc[q]));
       }
     }
-    // per-shift partial norms: warp sums, then one pass over the NW warp results
-#pragma unroll
-    for (int q = 0; q < KC; ++q) {
-      double nn = 0.0;
-      if (q < nc && in) nn = cabs2(csub(bv, acc[q]));
-      nn = warp_sum_d(nn);
-      if (lane == 0) red[w][q] = nn;
-    }
+    // per-shift partial norms: warp w reduces shifts w, w + NW over the block
     __syncthreads();
-    if (threadIdx.x < nc) {
+    for (int q = w; q < nc; q += NW) {
       double t = 0.0;
-      for (int v = 0; v < NW; ++v) t += red[v][threadIdx.x];
-      part[((int64_t)b * S.ns + flagged[c0 + threadIdx.x]) * S.nblk_tile + cb] = t;
+      for (int v = lane; v < kT; v += 32) t += nsm[q][v];
+      t = warp_sum_d(t);
+      if (lane == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = t;
     }
   }
 }
@@ -662,7 +674,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
 
   State S{};
   S.B = B; S.ns = ns; S.maxit = maxit; S.cap = cap; S.n = n; S.nblk = nblk;
-  S.nblk_tile = p->view(0).ntiles;
+  S.nblk_tile = verify_blocks(p->view(0));
   S.tol = prob.tol; S.variant = prob.variant; S.record_history = prob.record_history;
   S.active = active; S.beta = beta; S.shifts = dShifts.as<double2>(); S.taus = dTaus.as<double2>();
   S.H = dH.as<double2>(); S.conv = conv; S.iter = iter; S.est = est; S.true_res = true_res;

@@ -40,10 +40,11 @@ def test_stencil_apply_matches_csr(index, shape):
         assert rel(p.apply_adjoint(z, x[r]), ops.stiffness @ x[r] + np.conj(z) * (ops.mass @ x[r])) <= 1e-14
 
 
-# (100, 100), (64, 40, 24) and (96, 20, 18) run the TMA-fed multigrid kernels (rows of >= 64
-# cells; partial tiles in x, y and z), the others the register-pipelined ones
+# (100, 100) runs the natural-layout TMA kernels; (64, 40, 24), (96, 20, 18) and (128, 72, 12)
+# the colour-split ones (rows of >= 64 cells, nx % 4 == 0; partial tiles in x, y and z; on
+# two levels for (128, 72, 12)) with the pair transfers; the others the register-pipelined ones
 @pytest.mark.parametrize("index,shape", [(0, (100, 100)), (4, (16, 16, 16)), (3, (32, 32, 16)), (4, (64, 40, 24)),
-                                         (3, (96, 20, 18))])
+                                         (3, (96, 20, 18)), (4, (128, 72, 12))])
 def test_preconditioner_solve_matches_sparse_lu(index, shape):
     cfg, lk, ls, grid, ops = fd_case(index, shape)
     p = _pencil(cfg, lk, ls)
