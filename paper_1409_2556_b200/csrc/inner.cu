@@ -1572,6 +1572,183 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   }
 }
 
+// ---- fused residual + restriction (colour-split fine level, aggregation 2 x 2 x 2) -------
+// f_c = P^T (f - A x) without the fine residual ever reaching HBM.  A CTA owns the coarse
+// cells over its fine tile (32 positions = 32 coarse x, 8 rows = 4 coarse rows, ZM_ZC planes
+// = ZM_ZC / 2 coarse planes).  Per fine plane p it forms the residual of both colours on the
+// tile plus its one-cell ring (positions m0-1 .. m0+32, rows y0-1 .. y0+8: the x / y support of
+// the restriction), one warp per row, into a double-buffered plane of natural-order cell pairs;
+// after one barrier four warps reduce it in x and y for their coarse (I, J) and add it to the
+// z register ring of the pair restriction.  Each residual plane costs one barrier; the ring
+// cells are recomputed by the neighbouring CTAs (x and f are read with a 2-cell halo).
+constexpr int RR_NW = RB_H + 2;                                // consumer warps = residual rows
+constexpr int RR_XP = RB_P + 4, RR_XR = RB_H + 4;              // x: positions m0-2 .. m0+33, rows y0-2 .. y0+9
+constexpr int RR_FP = RB_P + 4, RR_FR = RB_H + 2;              // f: positions m0-2 .. m0+33, rows y0-1 .. y0+8
+constexpr int RR_CP = RB_P + 8, RR_CR = RB_H + 3;              // coef: positions m0-4 .. m0+35, rows y0-1 .. y0+9
+constexpr uint32_t RR_XB = sizeof(float2) * RR_XP * 2 * RR_XR;  // 6912
+constexpr uint32_t RR_FB = sizeof(float2) * RR_FP * 2 * RR_FR;  // 5760
+constexpr uint32_t RR_CB = sizeof(float) * RR_CP * 2 * 4 * RR_CR;  // 14080
+constexpr uint32_t RR_OFF_F = (RR_XB + 127) / 128 * 128, RR_OFF_C = (RR_OFF_F + RR_FB + 127) / 128 * 128;
+constexpr uint32_t RR_SLOT = (RR_OFF_C + RR_CB + 127) / 128 * 128;
+#ifndef LT_RR_D
+#define LT_RR_D 4
+#endif
+constexpr int RR_D = LT_RR_D;
+constexpr int RR_RP = RB_P + 2;                                  // residual pairs per row: m0-1 .. m0+32
+constexpr uint32_t RR_RB = sizeof(float4) * RR_RP * RR_NW;       // one residual plane
+constexpr size_t RR_SMEM = (size_t)RR_SLOT * RR_D + 2 * RR_RB;
+constexpr int kRR = 32 * RR_NW + 32;
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(kRR, 1) mg_resrestrict_kernel(const __grid_constant__ CUtensorMap mx,
+                                                               const __grid_constant__ CUtensorMap mf,
+                                                               const __grid_constant__ CUtensorMap mc, TzDims L,
+                                                               LevelViewT<float> Lc, Batch bt,
+                                                               const double2* __restrict__ taus, float2* __restrict__ fc) {
+  extern __shared__ __align__(128) unsigned char rr_smem[];
+  __shared__ __align__(8) uint64_t full[RR_D], empty[RR_D];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int nh = L.nx >> 1;
+  const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);  // k0 even
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  float4* Rbuf = reinterpret_cast<float4*>(rr_smem + (size_t)RR_SLOT * RR_D);  // [2][RR_NW][RR_RP]
+  if (tid == 0) {
+    for (int s = 0; s < RR_D; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], RR_NW);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  // residual planes k0-1 .. pl (pl = k1, or nz - 1 on the last chunk); loads: x for
+  // k0-2 .. pl+1 (ring index p - (k0 - 2)), f for the residual planes, coefficients k0-1 .. pl+1
+  const int pl = min(k1, L.nz - 1);
+  const int pb = k0 - 2, pe = pl + 1;
+  if (wy == RR_NW) {  // producer warp
+    if (lane == 0) {
+      int sl = 0, use = 0;
+      for (int p = pb; p <= pe; ++p) {
+        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = rr_smem + (size_t)sl * RR_SLOT;
+        const bool lf = p >= k0 - 1 && p <= pl, lc = p >= k0 - 1;
+        mbar_arrive_tx(&full[sl], RR_XB + (lf ? RR_FB : 0u) + (lc ? RR_CB : 0u));
+        tma_load5(sp, &mx, m0 - 2, 0, y0 - 2, p, b, &full[sl]);
+        if (lf) tma_load5(sp + RR_OFF_F, &mf, m0 - 2, 0, y0 - 1, p, b, &full[sl]);
+        if (lc) tma_load5(sp + RR_OFF_C, &mc, m0 - 4, 0, 0, y0 - 1, p, &full[sl]);
+        if (++sl == RR_D) { sl = 0; ++use; }
+      }
+    }
+    return;
+  }
+  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+  const int j = y0 - 1 + wy;  // this warp's residual row
+  // restriction threads: warps 0..3, coarse (I, J) = (m0 + lane, y0 / 2 + wy)
+  const int I = m0 + lane, J = (y0 >> 1) + wy;
+  const bool rthread = wy < RB_H / 2;
+  const bool own = rthread && I < Lc.nx && J < Lc.ny;
+  const float wxm = I > 0 ? 0.25f : 0.f, wx0 = I == 0 ? 0.5f : 0.75f;
+  const float wx1 = I == Lc.nx - 1 ? 0.5f : 0.75f, wxp = I < Lc.nx - 1 ? 0.25f : 0.f;
+  const float wyv[4] = {J > 0 ? 0.25f : 0.f, J == 0 ? 0.5f : 0.75f, J == Lc.ny - 1 ? 0.5f : 0.75f,
+                        J < Lc.ny - 1 ? 0.25f : 0.f};
+  float2* fcb = fc + (int64_t)b * Lc.n;
+  float2 sa = make_float2(0.f, 0.f), sb = sa, sc = sa;
+  // ring slots of planes p - 1, p, p + 1 (p = residual plane)
+  int qm = 0, q0 = 1, qu = 2;
+  uint32_t pu = 0;
+  mbar_wait_u32(full0 + 8 * qm, 0);
+  mbar_wait_u32(full0 + 8 * q0, 0);
+  int buf = 0;
+  for (int p = k0 - 1; p <= pl; ++p) {
+    mbar_wait_u32(full0 + 8 * qu, pu);
+    const unsigned char* sm = rr_smem + (size_t)qm * RR_SLOT;
+    const unsigned char* s0 = rr_smem + (size_t)q0 * RR_SLOT;
+    const unsigned char* su = rr_smem + (size_t)qu * RR_SLOT;
+    float4* R = Rbuf + buf * (RR_NW * RR_RP);
+    // ---- residual of row j, positions m0-1 .. m0+32 (two passes: lanes, then lanes 0, 1)
+    const bool pin = p >= 0 && p < L.nz && j >= 0 && j < L.ny;
+    for (int e = lane; e < RR_RP; e += 32) {
+      const int m = m0 - 1 + e;
+      float2 rc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      if (pin && m >= 0 && m < nh) {
+        const int rx = j - (y0 - 2), q = m - (m0 - 2), rf = j - (y0 - 1), qc = m - (m0 - 4);
+        auto X = [&](const unsigned char* sl, int rr, int h, int qq) {
+          return reinterpret_cast<const float2*>(sl)[(rr * 2 + h) * RR_XP + qq];
+        };
+        auto C = [&](const unsigned char* sl, int rr, int comp, int h, int qq) {
+          return reinterpret_cast<const float*>(sl + RR_OFF_C)[((rr * 4 + comp) * 2 + h) * RR_CP + qq];
+        };
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int s = (j + p + c) & 1, o = c ^ 1;
+          const float tw = C(s0, rf, 0, c, qc), ts = C(s0, rf, 1, c, qc), tb = C(s0, rf, 2, c, qc);
+          const float mm = C(s0, rf, 3, c, qc);
+          const float te = C(s0, rf, 0, o, qc + s), tn = C(s0, rf + 1, 1, o, qc), tt = C(su, rf, 2, o, qc);
+          const float2 w = X(s0, rx, o, q - 1 + s), ee = X(s0, rx, o, q + s);
+          const float2 so = X(s0, rx - 1, o, q), no = X(s0, rx + 1, o, q);
+          const float2 dn = X(sm, rx, o, q), up = X(su, rx, o, q);
+          const float ox = tw * w.x + te * ee.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
+          const float oy = tw * w.y + te * ee.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
+          const float2 xa = X(s0, rx, c, q);
+          const float2 f = reinterpret_cast<const float2*>(s0 + RR_OFF_F)[(rf * 2 + c) * RR_FP + q];
+          const float dk = tw + te + ts + tn + tb + tt;
+          const float dr = dk + tr * mm, di = ti * mm;
+          rc[s] = make_float2(f.x - (dr * xa.x - di * xa.y - ox), f.y - (dr * xa.y + di * xa.x - oy));
+        }
+      }
+      R[wy * RR_RP + e] = make_float4(rc[0].x, rc[0].y, rc[1].x, rc[1].y);  // (cell 2m, cell 2m + 1)
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // plane p - 1 is done
+    named_bar(1, 32 * RR_NW);
+    // ---- x / y reduction of plane p for (I, J), z ring
+    if (rthread) {
+      float2 S = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int rr = 2 * wy + r;  // local residual row of fine row 2J - 1 + r
+        const float4 c0 = R[rr * RR_RP + lane + 1], cmv = R[rr * RR_RP + lane], cpv = R[rr * RR_RP + lane + 2];
+        float2 xr = make_float2(0.f, 0.f);
+        xr = f2fma(wxm, make_float2(cmv.z, cmv.w), xr);
+        xr = f2fma(wx0, make_float2(c0.x, c0.y), xr);
+        xr = f2fma(wx1, make_float2(c0.z, c0.w), xr);
+        xr = f2fma(wxp, make_float2(cpv.x, cpv.y), xr);
+        S = f2fma(wyv[r], xr, S);
+      }
+      if (p < k0) {
+        sa = S;
+      } else if (p == k0) {
+        sb = S;
+      } else {
+        const bool odd = p & 1;
+        const int K = odd ? (p - 1) >> 1 : (p >> 1) - 1;
+        if (odd) sc = S;
+        if (!odd || K == Lc.nz - 1) {
+          const float2 sd = odd ? make_float2(0.f, 0.f) : S;
+          float2 v = make_float2(0.f, 0.f);
+          v = f2fma(K > 0 ? 0.25f : 0.f, sa, v);
+          v = f2fma(K == 0 ? 0.5f : 0.75f, sb, v);
+          v = f2fma(K == Lc.nz - 1 ? 0.5f : 0.75f, sc, v);
+          v = f2fma(K < Lc.nz - 1 ? 0.25f : 0.f, sd, v);
+          if (own && K < Lc.nz) fcb[rb_index(Lc, I, J, K)] = v;
+          sa = sc;
+          sb = sd;
+        }
+      }
+    }
+    buf ^= 1;
+    qm = q0;
+    q0 = qu;
+    if (++qu == RR_D) { qu = 0; pu ^= 1u; }
+  }
+}
+
 // FP64 operator tiles: 32 x 8 cells, one per thread (warp = one row of 32 cells).  The
 // coefficients come planar (Level::pack64: [k][j][W, S, B, M][i]), so every coefficient read
 // of a warp is one contiguous 256-byte run, and the in-row neighbours of p come from the
@@ -1692,6 +1869,8 @@ struct TzMaps {
   CUtensorMap x, f, c;
   bool rb = false;                // colour-split level: the mg_rb kernels and maps below
   CUtensorMap rx0, rx1, rf1, rf2, rc;  // x (one / both colours), f (one / both), coefficients
+  bool rr = false;                // ... and the fused residual + restriction (agg 2 x 2 x 2)
+  CUtensorMap rrx, rrf, rrc;
 };
 
 // q = A p, partial p^T q
@@ -2011,6 +2190,15 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     half(0, 0, nullptr);
     half(1, 0, nullptr);
   }
+  const bool rrk = rbk && tz[l].rr && std::is_same<R, float>::value && DIM == 3;
+  if (rrk) {
+    // r = f - A x restricted on the fly: x and f read once, only the coarse f written
+    launch(ctx, "mg_residual", cell_bytes * 2.125 * vb + coef, [&] {
+      if constexpr (std::is_same<R, float>::value)
+        mg_resrestrict_kernel<<<rgrid, kRR, RR_SMEM, st>>>(tz[l].rrx, tz[l].rrf, tz[l].rrc, tdims, Lc, bt, taus,
+                                                          (float2*)F[l + 1]);
+    });
+  } else
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
       mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
@@ -2029,6 +2217,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   static const bool pair_on = std::getenv("LT_ZM_TRANSFER") == nullptr;
   const bool ptr = pair_on && std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
                    lev.agg[2] == 2 && (L.nx & 1) == 0;
+  if (!rrk)
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
       if (ptr) {
@@ -2141,6 +2330,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
                                    (int)RbSlot<0, 2>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_resrestrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
       attr = true;
     }
   }
@@ -2176,6 +2366,16 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         tzm[l].rf2 = tma_map_8b(F[l], 5, vd, vs, bf2);
         tzm[l].rc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, kb);
         tzm[l].rb = true;
+        // opt-in (LT_RESRESTRICT=1): bit-identical to residual + restriction, but at one CTA per SM
+        // it is latency-bound (40.8 vs 31.9 ms per configs[4] inner solve)
+        if (Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2 && std::getenv("LT_RESRESTRICT") != nullptr) {
+          const uint32_t rbx[5] = {RR_XP, 2, RR_XR, 1, 1}, rbf[5] = {RR_FP, 2, RR_FR, 1, 1};
+          const uint32_t rbc[5] = {RR_CP, 2, 4, RR_CR, 1};
+          tzm[l].rrx = tma_map_8b(X[l], 5, vd, vs, rbx);
+          tzm[l].rrf = tma_map_8b(F[l], 5, vd, vs, rbf);
+          tzm[l].rrc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, rbc);
+          tzm[l].rr = true;
+        }
       }
     }
   }
