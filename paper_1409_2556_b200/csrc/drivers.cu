@@ -457,7 +457,8 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
         const int s = combo % JW_SMAX, s2 = (combo / JW_SMAX) % 2, c = combo / (2 * JW_SMAX);
         const int k = kp + s2;
         const bool live = s < n_src && k < ns;
-        const double2 wk = live ? w[k] : make_double2(0.0, 0.0);
+        // w == nullptr: the source fields already carry w_k (expand), wz then holds z_k or 1
+        const double2 wk = live ? (w ? w[k] : make_double2(1.0, 0.0)) : make_double2(0.0, 0.0);
         const double2* R = rw + min(s, B - 1);
         const double2 pa = R[chunk(jw_chunk<DIM>(s2, c, 0))];
         const int mt = s >> 3, lrow = (s & 7) * 4;
@@ -473,14 +474,14 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
           if ((p - 1) % 4 != part) continue;
           const double2 d = live ? cscale(csub(pa, R[chunk(jw_chunk<DIM>(s2, c, p))]), wt[c * NPC + p]) : make_double2(0.0, 0.0);
           a0 = cadd(a0, d);
-          put(p, cmul(wk, make_double2(-d.x, -d.y)));
+          put(p, w ? cmul(wk, make_double2(-d.x, -d.y)) : make_double2(-d.x, -d.y));
         }
 #pragma unroll
         for (int o = 1; o < 4; o <<= 1) {
           a0.x += __shfl_xor_sync(0xffffffffu, a0.x, o);
           a0.y += __shfl_xor_sync(0xffffffffu, a0.y, o);
         }
-        if (part == 0) put(0, cmul(wk, a0));
+        if (part == 0) put(0, w ? cmul(wk, a0) : a0);
         if (part == 1) {  // storativity block: K = s2 2 + comp in step KS
           const double2 As = live ? cmul(wz[k], cscale(pa, wt[c * NPC])) : make_double2(0.0, 0.0);
           Ac[KS * 32 + lrow + s2 * 2] = As.x;
@@ -1079,14 +1080,19 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   std::vector<double2> scale((size_t)B * ns, make_double2(1.0, 0.0));
   for (int s = 0; s < n_src; ++s)
     for (int k = 0; k < ns; ++k) scale[(size_t)s * ns + k] = d2(ex.rates[s] / nodes[k]);
-  DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
-  LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
-  DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n, st);
   // FD with <= 16 sources and <= 64 receivers: tensor-core Jacobian on cell-major fields
   // (LT_JAC_V2=1 selects the CUDA-core kernel)
   static const bool mma_on = std::getenv("LT_JAC_V2") == nullptr;
   const bool tensor_jac = mma_on && p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
                           (p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B)) <= 227 * 1024;
+  // tensor path: the quadrature weight w_k rides on the source fields (phi'_{s,k} = w_k phi_{s,k}),
+  // which takes one complex product per A element out of the kernel's arrow transform
+  if (tensor_jac)
+    for (int s = 0; s < n_src; ++s)
+      for (int k = 0; k < ns; ++k) scale[(size_t)s * ns + k] = cmul(scale[(size_t)s * ns + k], d2(weights[k]));
+  DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
+  LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
+  DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n, st);
   {
     TraceScope tr(ctx, "  expand", B);
     expand_solutions(p, res, dscale.as<double2>(), fields.as<double2>(), tensor_jac);
@@ -1095,8 +1101,10 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
 
   std::vector<double2> w(ns), wz(ns);
   for (int k = 0; k < ns; ++k) {
-    w[k] = d2(weights[k]);
-    wz[k] = d2(ex.storativity_z_factor ? weights[k] * nodes[k] : weights[k]);
+    // tensor path: w_k is already in the source fields (w = 1 for the predictions, wz = z_k or 1)
+    w[k] = tensor_jac ? make_double2(1.0, 0.0) : d2(weights[k]);
+    const cd zf = ex.storativity_z_factor ? nodes[k] : cd(1.0, 0.0);
+    wz[k] = d2(tensor_jac ? zf : weights[k] * zf);
   }
   DeviceBuffer dw(sizeof(double2) * 2 * ns, st);
   LT_CUDA(cudaMemcpyAsync(dw.get(), w.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
@@ -1163,7 +1171,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
       const CUtensorMap mB = tma_map_8b(fields.get(), 5, dims, strd, boxB);
       launch(ctx, "jacobian", bytes, [&] {
         fn<<<grid, JW_THREADS, smem, st>>>(mA, mB, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
-                                           face_scale, n_src, n_rec, ns, dw.as<double2>(), dw.as<double2>() + ns, J,
+                                           face_scale, n_src, n_rec, ns, nullptr, dw.as<double2>() + ns, J,
                                            ex.include_storativity ? J + n : nullptr, n_param, ntiles, jw_dbg);
       });
       if (mem != LT_MEM_DEVICE)
