@@ -1389,8 +1389,9 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
 }
 
 // MODE 0: red-black half sweep of `color`, in place on the colour's half of x (zero_init: x = 0
-// on entry, so no x is read; dot: also the partials of f^T x over both colours after the
-// sweep).  MODE 1: r = f - A x on both colours.  mx / mf: 5-D maps {pos, colour, y, z, item}
+// on entry, so no x is read; dot: also the partials of f^T x over the colour's cells, written
+// to dot[((item * 2 + color) * nblk + block] -- the last black and the last red sweep of the
+// post-smoother together form f^T x).  MODE 1: r = f - A x on both colours.  mx / mf: 5-D maps {pos, colour, y, z, item}
 // of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.  Blocks:
 // rb_blocks(L) per group of NI consecutive items (item group fastest).
 template <int MODE, int NI>
@@ -1420,7 +1421,7 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
   const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const bool fboth = NI == 1 && (MODE == 1 || dot != nullptr);  // f of both colours in the slot
+  const bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
   if (tid == 0) {
     for (int q = 0; q < RB_D; ++q) {
       mbar_init(&full[q], 1);
@@ -1430,7 +1431,9 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   }
   __syncthreads();
   const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
-  double2 acc = make_double2(0.0, 0.0);
+  double2 acc[NI];
+#pragma unroll
+  for (int t = 0; t < NI; ++t) acc[t] = make_double2(0.0, 0.0);
   if (wy == kT / 32) {  // producer warp
     if (lane == 0) {
       const bool ldx = MODE == 1 || !zero_init;
@@ -1523,7 +1526,8 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
 #pragma unroll
           for (int t = 0; t < NI; ++t) {
             if (!live[t]) continue;
-            float2 o = F(t, fboth ? color : 0);
+            const float2 fcol = F(t, fboth ? color : 0);
+            float2 o = fcol;
             if (!zero_init) {
               const float2 os = offsum(t, 0, sft, tw, te, ts, tn, tb, tt);
               o.x += os.x;
@@ -1534,11 +1538,7 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
             const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
             const int b = grp * NI + t;
             out[(int64_t)b * L.n + row + (int64_t)color * nh + m] = xn;
-            if (dot && t == 0) {  // (dot runs with NI = 1)
-              const float2 fc = F(t, color), fo = F(t, color ^ 1), xo = X(s0, t, r, 0, xq);
-              acc = cfma(make_double2(fc.x, fc.y), make_double2(xn.x, xn.y), acc);
-              acc = cfma(make_double2(fo.x, fo.y), make_double2(xo.x, xo.y), acc);
-            }
+            if (dot) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
           }
         } else {
 #pragma unroll
@@ -1567,8 +1567,13 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
     }
   }
   if (MODE == 0 && dot) {
-    acc = block_sum(acc);
-    if (threadIdx.x == 0) dot[(int64_t)grp * nblk + cb] = acc;
+#pragma unroll
+    for (int t = 0; t < NI; ++t) {
+      const double2 v = block_sum(acc[t]);
+      const int b = grp * NI + t;
+      if (threadIdx.x == 0 && b < bt.B) dot[((int64_t)b * 2 + color) * nblk + cb] = v;
+      __syncthreads();  // block_sum's shared scratch is reused by the next item
+    }
   }
 }
 
@@ -2167,13 +2172,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
     launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", hb + coef, [&] {
       if (rbk)
-        if (dot)  // one item per CTA: the partials are per item
-          mg_rb_kernel<0, 1><<<rgrid, kTP, RbSlot<0, 1>::SMEM, st>>>(tz[l].rx0, tz[l].rf2, tz[l].rc, tdims, bt, taus,
-                                                                    (float2*)X[l], color, zero_init, dot,
-                                                                    rb_blocks(L));
-        else
-          mg_rb_kernel<0, 2><<<rgrid2, kTP, RbSlot<0, 2>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
-                                                                     (float2*)X[l], color, zero_init, nullptr, 0);
+        mg_rb_kernel<0, 2><<<rgrid2, kTP, RbSlot<0, 2>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
+                                                                   (float2*)X[l], color, zero_init, dot, rb_blocks(L));
       else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
@@ -2242,12 +2242,14 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
   });
   for (int s = 0; s < nu; ++s) {
-    half(1, 0, nullptr);
-    // the last half sweep also forms the partial sums of f^T x when asked (and possible)
+    // the last half sweeps also form the partial sums of f^T x when asked (and possible):
+    // colour-split, each of the last black and red sweeps over its own colour; else the last
+    // (red) sweep over both
     const bool last_sweep = s == nu - 1;
+    half(1, 0, last_sweep && rbk ? dot_part : nullptr);
     half(0, 0, last_sweep && pairs ? dot_part : nullptr);
   }
-  if (dot_nblk) *dot_nblk = !dot_part ? 0 : rbk ? rb_blocks(L) : (tma || pairs) ? zp_blocks(L) : 0;
+  if (dot_nblk) *dot_nblk = !dot_part ? 0 : rbk ? 2 * rb_blocks(L) : (tma || pairs) ? zp_blocks(L) : 0;
   return X[l];
 }
 
@@ -2324,8 +2326,6 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)RbSlot<0, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<0, 2>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
