@@ -1577,6 +1577,106 @@ __global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ C
   }
 }
 
+// ---- TMA-fed restriction from a colour-split fine level (aggregation 2 x 2 x 2) ----------
+// f_c = P^T r_f.  CTA = 32 x 4 coarse columns (warp = coarse row J, lane = coarse I) x RT_ZC
+// coarse planes; a producer warp streams each fine plane's tile (rows 2J0-1 .. 2J0+8, the
+// positions I0-2 .. I0+33 of both colours) into a ring; the x / y reduction reads shared
+// memory directly (cell 2I of a row sits at position I of colour (j + k) & 1, cell 2I + 1 at
+// position I of the other colour, 2I - 1 / 2I + 2 at positions I - 1 / I + 1), and the z
+// direction is the register ring of the pair restriction.  Every fine value is read from HBM
+// once; the register-pipelined pair kernel was latency-bound at ~1.8 TB/s.
+constexpr int RT_ZC = 16, RT_D = 6, RT_P = 36, RT_R = 10;
+constexpr uint32_t RT_SLOT = sizeof(float2) * RT_P * 2 * RT_R;  // 5760
+constexpr size_t RT_SMEM = (size_t)RT_SLOT * RT_D;
+constexpr int kRT = 32 * 4 + 32;
+
+__global__ void __launch_bounds__(kRT) restrict_tma_kernel(const __grid_constant__ CUtensorMap mr, TzDims L,
+                                                          LevelViewT<float> Lc, Batch bt, float2* __restrict__ fc) {
+  extern __shared__ __align__(128) unsigned char rt_smem[];
+  __shared__ __align__(8) uint64_t full[RT_D], empty[RT_D];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int tx = (Lc.nx + 31) / 32, ty = (Lc.ny + 3) / 4;
+  const int tile = cb % (tx * ty), chunk = cb / (tx * ty);
+  const int I0 = (tile % tx) * 32, J0 = (tile / tx) * 4;
+  const int K0 = chunk * RT_ZC, K1 = min(Lc.nz, K0 + RT_ZC);
+  const int kbeg = max(2 * K0 - 1, 0), kend = min(2 * K1, L.nz - 1);  // fine planes
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  if (tid == 0) {
+    for (int q = 0; q < RT_D; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 4);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  if (wy == 4) {  // producer warp
+    if (lane == 0) {
+      int sl = 0, use = 0;
+      for (int p = kbeg; p <= kend; ++p) {
+        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
+        mbar_arrive_tx(&full[sl], RT_SLOT);
+        tma_load5(rt_smem + (size_t)sl * RT_SLOT, &mr, I0 - 2, 0, 2 * J0 - 1, p, b, &full[sl]);
+        if (++sl == RT_D) { sl = 0; ++use; }
+      }
+    }
+    return;
+  }
+  const int I = I0 + lane, J = J0 + wy;
+  const bool own = I < Lc.nx && J < Lc.ny;
+  const float wxm = I > 0 ? 0.25f : 0.f, wx0 = I == 0 ? 0.5f : 0.75f;
+  const float wx1 = I == Lc.nx - 1 ? 0.5f : 0.75f, wxp = I < Lc.nx - 1 ? 0.25f : 0.f;
+  const float wyv[4] = {J > 0 ? 0.25f : 0.f, J == 0 ? 0.5f : 0.75f, J == Lc.ny - 1 ? 0.5f : 0.75f,
+                        J < Lc.ny - 1 ? 0.25f : 0.f};
+  float2* fcb = fc + (int64_t)b * Lc.n;
+  float2 sa = make_float2(0.f, 0.f), sb = sa, sc = sa;
+  int sl = 0;
+  uint32_t par = 0;
+  for (int p = kbeg; p <= kend; ++p) {
+    mbar_wait_u32(full0 + 8 * sl, par);
+    const float2* T = reinterpret_cast<const float2*>(rt_smem + (size_t)sl * RT_SLOT);  // [row][colour][pos]
+    float2 S = make_float2(0.f, 0.f);
+    const int q = lane + 2;  // position I in the tile
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int rr = 2 * wy + r, jf = 2 * J - 1 + r;
+      const int s = (jf + p) & 1;  // colour of the row's even cells
+      const float2* E = T + (rr * 2 + s) * RT_P;
+      const float2* O = T + (rr * 2 + (s ^ 1)) * RT_P;
+      float2 xr = make_float2(0.f, 0.f);
+      xr = f2fma(wxm, O[q - 1], xr);
+      xr = f2fma(wx0, E[q], xr);
+      xr = f2fma(wx1, O[q], xr);
+      xr = f2fma(wxp, E[q + 1], xr);
+      S = f2fma(wyv[r], xr, S);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(empty0 + 8 * sl);
+    if (++sl == RT_D) { sl = 0; par ^= 1u; }
+    if (p < 2 * K0) {
+      sa = S;
+    } else if (p == 2 * K0) {
+      sb = S;
+    } else {
+      const bool odd = p & 1;
+      const int K = odd ? (p - 1) >> 1 : (p >> 1) - 1;
+      if (odd) sc = S;
+      if (!odd || K == Lc.nz - 1) {
+        const float2 sd = odd ? make_float2(0.f, 0.f) : S;
+        float2 v = make_float2(0.f, 0.f);
+        v = f2fma(K > 0 ? 0.25f : 0.f, sa, v);
+        v = f2fma(K == 0 ? 0.5f : 0.75f, sb, v);
+        v = f2fma(K == Lc.nz - 1 ? 0.5f : 0.75f, sc, v);
+        v = f2fma(K < Lc.nz - 1 ? 0.25f : 0.f, sd, v);
+        if (own) fcb[rb_index(Lc, I, J, K)] = v;
+        sa = sc;
+        sb = sd;
+      }
+    }
+  }
+}
+
 // ---- fused residual + restriction (colour-split fine level, aggregation 2 x 2 x 2) -------
 // f_c = P^T (f - A x) without the fine residual ever reaching HBM.  A CTA owns the coarse
 // cells over its fine tile (32 positions = 32 coarse x, 8 rows = 4 coarse rows, ZM_ZC planes
@@ -1876,6 +1976,7 @@ struct TzMaps {
   CUtensorMap rx0, rx1, rf1, rf2, rc;  // x (one / both colours), f (one / both), coefficients
   bool rr = false;                // ... and the fused residual + restriction (agg 2 x 2 x 2)
   CUtensorMap rrx, rrf, rrc;
+  CUtensorMap rt;                 // the residual's tiles for restrict_tma_kernel
 };
 
 // q = A p, partial p^T q
@@ -2215,11 +2316,17 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   });
   // pair transfers for aggregation 2 in every direction (3-D, FP32 V-cycle)
   static const bool pair_on = std::getenv("LT_ZM_TRANSFER") == nullptr;
+  static const bool rt_on = std::getenv("LT_PAIR_RESTRICT") == nullptr;  // TMA restriction from colour-split levels
   const bool ptr = pair_on && std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
                    lev.agg[2] == 2 && (L.nx & 1) == 0;
   if (!rrk)
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
+      if (ptr && rbk && rt_on) {
+        const unsigned g = (unsigned)(((Lc.nx + 31) / 32) * ((Lc.ny + 3) / 4) * ((Lc.nz + RT_ZC - 1) / RT_ZC));
+        restrict_tma_kernel<<<g * Bc, kRT, RT_SMEM, st>>>(tz[l].rt, tdims, Lc, bt, (float2*)F[l + 1]);
+        return;
+      }
       if (ptr) {
         const unsigned g = (unsigned)(((Lc.nx + 31) / 32) * ((Lc.ny + TP_TY - 1) / TP_TY) * ((Lc.nz + TP_ZC - 1) / TP_ZC));
         restrict_pair_kernel<<<g * Bc, 32 * TP_TY, 0, st>>>(L, Lc, bt, Rr[l], F[l + 1]);
@@ -2331,6 +2438,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_resrestrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM));
       attr = true;
     }
   }
@@ -2366,6 +2474,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         tzm[l].rf2 = tma_map_8b(F[l], 5, vd, vs, bf2);
         tzm[l].rc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, kb);
         tzm[l].rb = true;
+        const uint32_t brt[5] = {RT_P, 2, RT_R, 1, 1};
+        tzm[l].rt = tma_map_8b(Rr[l], 5, vd, vs, brt);
         // opt-in (LT_RESRESTRICT=1): bit-identical to residual + restriction, but at one CTA per SM
         // it is latency-bound (40.8 vs 31.9 ms per configs[4] inner solve)
         if (Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2 && std::getenv("LT_RESRESTRICT") != nullptr) {
