@@ -1677,6 +1677,158 @@ __global__ void __launch_bounds__(kRT) restrict_tma_kernel(const __grid_constant
   }
 }
 
+// ---- TMA-fed prolongation onto a colour-split fine level (aggregation 2 x 2 x 2) ---------
+// x_f += P e_c.  CTA = 32 fine pairs (positions I0 .. I0+31 = coarse I) x 8 fine rows x ZM_ZC
+// fine planes; producer lane 0 streams the fine x tiles (both colours), lane 1 the coarse e
+// tiles (coarse rows j0/2-1 .. j0/2+4, coarse x I0-2 .. I0+33: natural, or positions
+// I0/2-2 .. I0/2+17 of both colours when the coarse level is colour-split too) into two
+// rings; the bilinear in-plane values of each coarse plane are formed once (register ring over
+// the coarse planes, as in prolong_pair_kernel) from shared memory.
+constexpr int PT_D = 6, PT_CD = 5;                         // fine / coarse ring depths
+constexpr int PT_CR = 6, PT_CXN = 36, PT_CXS = 20;         // coarse rows; x extent natural / split positions
+constexpr uint32_t PT_FSLOT = sizeof(float2) * 32 * 2 * 8;  // 4096
+template <bool CSPLIT>
+struct PtGeom {
+  static constexpr uint32_t CSLOT = CSPLIT ? sizeof(float2) * PT_CXS * 2 * PT_CR : sizeof(float2) * PT_CXN * PT_CR;
+  static constexpr uint32_t CSLOT_A = (CSLOT + 127) / 128 * 128;
+  static constexpr size_t SMEM = (size_t)PT_FSLOT * PT_D + (size_t)CSLOT_A * PT_CD;
+};
+
+template <bool CSPLIT>
+__global__ void __launch_bounds__(kTP) prolong_tma_kernel(const __grid_constant__ CUtensorMap mxf,
+                                                         const __grid_constant__ CUtensorMap mec, TzDims L,
+                                                         LevelViewT<float> Lc, Batch bt, float2* __restrict__ xf) {
+  using G = PtGeom<CSPLIT>;
+  extern __shared__ __align__(128) unsigned char pt_smem[];
+  __shared__ __align__(8) uint64_t ffull[PT_D], fempty[PT_D], cfull[PT_CD], cempty[PT_CD];
+  LT_ITEM_BLOCK(bt.B, b, cb);
+  if (bt.done[b]) return;
+  const int nh = L.nx >> 1;  // fine pairs per row (= coarse nx)
+  const int tx = (nh + 31) / 32, ty = (L.ny + 7) / 8;
+  const int tile = cb % (tx * ty), chunk = cb / (tx * ty);
+  const int I0 = (tile % tx) * 32, j0 = (tile / tx) * 8;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int Kb = (k0 >> 1) - 1, Ke = ((k1 - 1) >> 1) + 1;  // coarse planes used (out of range: zero tiles)
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  unsigned char* fring = pt_smem;
+  unsigned char* cring = pt_smem + (size_t)PT_FSLOT * PT_D;
+  if (tid == 0) {
+    for (int q = 0; q < PT_D; ++q) { mbar_init(&ffull[q], 1); mbar_init(&fempty[q], 8); }
+    for (int q = 0; q < PT_CD; ++q) { mbar_init(&cfull[q], 1); mbar_init(&cempty[q], 8); }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (wy == 8) {  // producer warp: lane 0 fine planes, lane 1 coarse planes
+    if (lane == 0) {
+      int sl = 0, use = 0;
+      for (int k = k0; k < k1; ++k) {
+        if (use > 0) mbar_wait(&fempty[sl], (uint32_t)((use - 1) & 1));
+        mbar_arrive_tx(&ffull[sl], PT_FSLOT);
+        tma_load5(fring + (size_t)sl * PT_FSLOT, &mxf, I0, 0, j0, k, b, &ffull[sl]);
+        if (++sl == PT_D) { sl = 0; ++use; }
+      }
+    } else if (lane == 1) {
+      int sl = 0, use = 0;
+      for (int K = Kb; K <= Ke; ++K) {
+        if (use > 0) mbar_wait(&cempty[sl], (uint32_t)((use - 1) & 1));
+        mbar_arrive_tx(&cfull[sl], G::CSLOT);
+        unsigned char* dst = cring + (size_t)sl * G::CSLOT_A;
+        if (CSPLIT) tma_load5(dst, &mec, (I0 >> 1) - 2, 0, (j0 >> 1) - 1, K, b, &cfull[sl]);
+        else tma_load4(dst, &mec, I0 - 2, (j0 >> 1) - 1, K, b, &cfull[sl]);
+        if (++sl == PT_CD) { sl = 0; ++use; }
+      }
+    }
+    return;
+  }
+  const int I = I0 + lane, j = j0 + wy;
+  const bool in = I < nh && j < L.ny;
+  const uint32_t ff0 = smem_u32(ffull), fe0 = smem_u32(fempty), cf0 = smem_u32(cfull), ce0 = smem_u32(cempty);
+  // coarse rows of fine row j and their weights (Dirichlet ghost at the ends: 1/2 of J)
+  const int J = j >> 1;
+  int Jr[2];
+  float wr[2];
+  if ((j & 1) == 0) {
+    Jr[0] = J; wr[0] = J == 0 ? 0.5f : 0.75f; Jr[1] = J - 1; wr[1] = J > 0 ? 0.25f : 0.f;
+  } else {
+    Jr[0] = J; wr[0] = J == Lc.ny - 1 ? 0.5f : 0.75f; Jr[1] = J + 1; wr[1] = J < Lc.ny - 1 ? 0.25f : 0.f;
+  }
+  const float wxe0 = I == 0 ? 0.5f : 0.75f, wxe1 = I > 0 ? 0.25f : 0.f;            // fine 2I: I, I - 1
+  const float wxo0 = I == nh - 1 ? 0.5f : 0.75f, wxo1 = I < nh - 1 ? 0.25f : 0.f;  // fine 2I+1: I, I + 1
+  // coarse ring: plane K in slot (K - Kb) % PT_CD
+  int cnext = Kb;  // next coarse plane to wait for
+  auto interp = [&](int K, float2& pe, float2& po) {
+    pe = make_float2(0.f, 0.f);
+    po = pe;
+    const int q = (K - Kb) % PT_CD;
+    const float2* C = reinterpret_cast<const float2*>(cring + (size_t)q * G::CSLOT_A);
+    auto E = [&](int Jc, int Ic) {
+      const int rr = Jc - ((j0 >> 1) - 1);
+      if (CSPLIT) return C[(rr * 2 + ((Ic + Jc + K) & 1)) * PT_CXS + (Ic >> 1) - ((I0 >> 1) - 2)];
+      return C[rr * PT_CXN + Ic - (I0 - 2)];
+    };
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float2 c = E(Jr[r], I), m1 = E(Jr[r], I - 1), p1 = E(Jr[r], I + 1);
+      pe = f2fma(wr[r] * wxe0, c, f2fma(wr[r] * wxe1, m1, pe));
+      po = f2fma(wr[r] * wxo0, c, f2fma(wr[r] * wxo1, p1, po));
+    }
+  };
+  auto wait_coarse = [&](int K) {  // planes up to K are resident
+    while (cnext <= K) {
+      const int u = cnext - Kb;
+      mbar_wait_u32(cf0 + 8 * (u % PT_CD), (uint32_t)((u / PT_CD) & 1));
+      ++cnext;
+    }
+  };
+  auto release_coarse = [&](int K) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(ce0 + 8 * ((K - Kb) % PT_CD));
+  };
+  int K = k0 >> 1;
+  float2 sme, smo, sce, sco, spe, spo;
+  wait_coarse(K + 1);
+  interp(K - 1, sme, smo);
+  interp(K, sce, sco);
+  interp(K + 1, spe, spo);
+  release_coarse(K - 1);
+  int fs = 0;
+  uint32_t fp = 0;
+  float2* xb = xf + (int64_t)b * L.n;
+  for (int k = k0; k < k1; ++k) {
+    if ((k >> 1) != K) {
+      K = k >> 1;
+      sme = sce; smo = sco;
+      sce = spe; sco = spo;
+      wait_coarse(K + 1);
+      interp(K + 1, spe, spo);
+      release_coarse(K - 1);
+    }
+    float2 ve = make_float2(0.f, 0.f), vo = ve;
+    if ((k & 1) == 0) {
+      const float w0 = K == 0 ? 0.5f : 0.75f, w1 = K > 0 ? 0.25f : 0.f;
+      ve = f2fma(w1, sme, f2fma(w0, sce, ve));
+      vo = f2fma(w1, smo, f2fma(w0, sco, vo));
+    } else {
+      const float w0 = K == Lc.nz - 1 ? 0.5f : 0.75f, w1 = K < Lc.nz - 1 ? 0.25f : 0.f;
+      ve = f2fma(w1, spe, f2fma(w0, sce, ve));
+      vo = f2fma(w1, spo, f2fma(w0, sco, vo));
+    }
+    mbar_wait_u32(ff0 + 8 * fs, fp);
+    const float2* T = reinterpret_cast<const float2*>(fring + (size_t)fs * PT_FSLOT);  // [row][colour][pos]
+    const int s = (j + k) & 1;  // colour of the row's even cells
+    if (in) {
+      const float2 e = T[(wy * 2 + s) * 32 + lane], o = T[(wy * 2 + (s ^ 1)) * 32 + lane];
+      const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+      xb[row + (int64_t)s * nh + I] = make_float2(e.x + ve.x, e.y + ve.y);
+      xb[row + (int64_t)(s ^ 1) * nh + I] = make_float2(o.x + vo.x, o.y + vo.y);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(fe0 + 8 * fs);
+    if (++fs == PT_D) { fs = 0; fp ^= 1u; }
+  }
+  // the coarse planes still held: release so the producer is never left waiting (it is done)
+}
+
 // ---- fused residual + restriction (colour-split fine level, aggregation 2 x 2 x 2) -------
 // f_c = P^T (f - A x) without the fine residual ever reaching HBM.  A CTA owns the coarse
 // cells over its fine tile (32 positions = 32 coarse x, 8 rows = 4 coarse rows, ZM_ZC planes
@@ -1977,6 +2129,8 @@ struct TzMaps {
   bool rr = false;                // ... and the fused residual + restriction (agg 2 x 2 x 2)
   CUtensorMap rrx, rrf, rrc;
   CUtensorMap rt;                 // the residual's tiles for restrict_tma_kernel
+  bool pt = false, pt_csplit = false;  // prolong_tma_kernel onto this level (coarse level split?)
+  CUtensorMap ptf, ptc;           // fine x tiles, coarse e tiles
 };
 
 // q = A p, partial p^T q
@@ -2340,6 +2494,16 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   // coarse correction, then the transpose of the pre-smoother (black, red, ...), in place
   launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
+      if (ptr && rbk && tz[l].pt) {
+        const unsigned g = (unsigned)(((L.nx / 2 + 31) / 32) * ((L.ny + 7) / 8) * ((L.nz + ZM_ZC - 1) / ZM_ZC));
+        if (tz[l].pt_csplit)
+          prolong_tma_kernel<true><<<g * Bc, kTP, PtGeom<true>::SMEM, st>>>(tz[l].ptf, tz[l].ptc, tdims, Lc, bt,
+                                                                           (float2*)X[l]);
+        else
+          prolong_tma_kernel<false><<<g * Bc, kTP, PtGeom<false>::SMEM, st>>>(tz[l].ptf, tz[l].ptc, tdims, Lc, bt,
+                                                                             (float2*)X[l]);
+        return;
+      }
       if (ptr) {
         const unsigned g = (unsigned)(((L.nx / 2 + 31) / 32) * ((L.ny + 7) / 8) * ((L.nz + ZM_ZC - 1) / ZM_ZC));
         prolong_pair_kernel<<<g * Bc, kT, 0, st>>>(L, Lc, bt, ec, X[l]);
@@ -2439,6 +2603,10 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
                                    (int)RbSlot<1, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_resrestrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
       LT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)PtGeom<true>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)PtGeom<false>::SMEM));
       attr = true;
     }
   }
@@ -2488,6 +2656,32 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         }
       }
     }
+  }
+  // prolongation onto colour-split levels with aggregation 2 x 2 x 2: fine x and coarse e maps
+  for (int l = 0; l + 1 < nl && tma_on; ++l) {
+    const Level& Lv = *p->levels[l];
+    if (!tzm[l].rb || std::getenv("LT_PAIR_PROLONG") || !(Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2))
+      continue;
+    const Level& Lc = *p->levels[l + 1];
+    const uint64_t nx = Lv.nx, ny = Lv.ny, nz = Lv.nz;
+    const uint64_t vd[5] = {nx / 2, 2, ny, nz, (uint64_t)Bc};
+    const uint64_t vs[4] = {nx / 2 * 8, nx * 8, nx * ny * 8, nx * ny * nz * 8};
+    const uint32_t bf[5] = {32, 2, 8, 1, 1};
+    tzm[l].ptf = tma_map_8b(X[l], 5, vd, vs, bf);
+    const uint64_t cx = Lc.nx, cy = Lc.ny, cz = Lc.nz;
+    tzm[l].pt_csplit = tzm[l + 1].rb;
+    if (tzm[l + 1].rb) {
+      const uint64_t cd[5] = {cx / 2, 2, cy, cz, (uint64_t)Bc};
+      const uint64_t cs[4] = {cx / 2 * 8, cx * 8, cx * cy * 8, cx * cy * cz * 8};
+      const uint32_t bc[5] = {PT_CXS, 2, PT_CR, 1, 1};
+      tzm[l].ptc = tma_map_8b(X[l + 1], 5, cd, cs, bc);
+    } else {
+      const uint64_t cd[4] = {cx, cy, cz, (uint64_t)Bc};
+      const uint64_t cs[3] = {cx * 8, cx * cy * 8, cx * cy * cz * 8};
+      const uint32_t bc[4] = {PT_CXN, PT_CR, 1, 1};
+      tzm[l].ptc = tma_map_8b(X[l + 1], 4, cd, cs, bc);
+    }
+    tzm[l].pt = true;
   }
   // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
   // reads and writes X[l]

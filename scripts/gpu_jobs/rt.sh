@@ -1,5 +1,5 @@
 for s in 64 96 128; do
-  LT_PAIR_RESTRICT=1 timeout 300 python scripts/probe_vcycle.py a_$s $s 1 2>&1 | tail -1
+  LT_PAIR_PROLONG=1 timeout 300 python scripts/probe_vcycle.py a_$s $s 1 2>&1 | tail -1
   LT_DEBUG_SYNC=1 timeout 300 python scripts/probe_vcycle.py c_$s $s 1 2>&1 | tail -1
 done
 python - <<'P'
