@@ -844,11 +844,19 @@ __global__ void __launch_bounds__(kT) apply_dot_zm_kernel(LevelView L, Batch bt,
 // one-cell kernel idles half its lanes and was issue-bound), the pair moves as one 16-byte
 // access, and the in-row neighbours come from the adjacent lanes by shuffle (a warp is one
 // row of 64 cells).  CTA = 32 pairs x 8 rows x a chunk of ZM_ZC planes.
+// The chunk of planes per CTA shrinks on the small levels (ZM_ZC on nz >= 64, else nz / 8, at
+// least 2): they are latency-bound, and with 32-plane chunks a 32^3 level had 4 CTAs per item.
 constexpr int ZP_TX = 32;
+__host__ __device__ __forceinline__ int zp_chunk(int nz) { return nz >= 64 ? ZM_ZC : (nz >= 16 ? nz / 8 : 2); }
+
+// Rows of <= 32 cells: a warp covers two rows (16 pairs each), so no lane idles; the tile is
+// then 32 x 16 cells.
+__host__ __device__ __forceinline__ int zp_rows(int nx) { return nx <= ZP_TX ? 2 : 1; }
 
 template <class VW>
 inline int zp_blocks(const VW& L) {
-  return ((L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX)) * ((L.ny + ZM_TY - 1) / ZM_TY) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+  const int zc = zp_chunk(L.nz), ty = ZM_TY * zp_rows(L.nx);
+  return ((L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX)) * ((L.ny + ty - 1) / ty) * ((L.nz + zc - 1) / zc);
 }
 
 template <class V>
@@ -892,22 +900,28 @@ __device__ __forceinline__ V pick(const Pair<V>& p, int o) {
 
 struct ZpMap {
   int i0, j, k0, k1, lane;
+  bool first, last;  // first / last pair of the warp's row segment (x-neighbours from memory)
   bool in;
   int64_t ip;
 };
 
 template <class VW>
 __device__ __forceinline__ ZpMap zp_map(const VW& L, int cb) {
-  const int tiles_x = (L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX), tiles_y = (L.ny + ZM_TY - 1) / ZM_TY;
+  const int rows = zp_rows(L.nx), seg = 32 / rows;  // row segments per warp, pairs per segment
+  const int tiles_x = (L.nx + 2 * ZP_TX - 1) / (2 * ZP_TX), tiles_y = (L.ny + ZM_TY * rows - 1) / (ZM_TY * rows);
   const int ntile = tiles_x * tiles_y;
   const int tile = cb % ntile, chunk = cb / ntile;
   ZpMap m;
   m.lane = threadIdx.x & 31;
-  m.i0 = (tile % tiles_x) * 2 * ZP_TX + 2 * m.lane;
-  m.j = (tile / tiles_x) * ZM_TY + (threadIdx.x >> 5);
+  const int rl = m.lane % seg;
+  m.first = rl == 0;
+  m.last = rl == seg - 1;
+  m.i0 = (tile % tiles_x) * 2 * ZP_TX + 2 * rl;
+  m.j = (tile / tiles_x) * ZM_TY * rows + (threadIdx.x >> 5) * rows + m.lane / seg;
   m.in = m.i0 < L.nx && m.j < L.ny;
-  m.k0 = chunk * ZM_ZC;
-  m.k1 = min(L.nz, m.k0 + ZM_ZC);
+  const int zc = zp_chunk(L.nz);
+  m.k0 = chunk * zc;
+  m.k1 = min(L.nz, m.k0 + zc);
   m.ip = (int64_t)m.j * L.nx + m.i0;
   return m;
 }
@@ -965,8 +979,8 @@ __global__ void __launch_bounds__(kT, 3) rbpair_zm_kernel(LevelViewT<R> L, Batch
     if (!zero_init) {
       if (m.j > 0) o.ns = ld_pair(xb + a - L.nx);
       if (m.j < L.ny - 1) o.nn = ld_pair(xb + a + L.nx);
-      if (off == 0 && m.lane == 0 && m.i0 > 0) o.xw = xb[a - 1];
-      if (off == 1 && m.lane == 31 && m.i0 + 2 < L.nx) o.xe = xb[a + 2];
+      if (off == 0 && m.first && m.i0 > 0) o.xw = xb[a - 1];
+      if (off == 1 && m.last && m.i0 + 2 < L.nx) o.xe = xb[a + 2];
     }
   };
   Ops cur, nxt;
@@ -980,8 +994,8 @@ __global__ void __launch_bounds__(kT, 3) rbpair_zm_kernel(LevelViewT<R> L, Batch
     // in-row neighbours of the colour cell from the adjacent lanes (every lane shuffles)
     const V up = shfl_up1(xc.c), dn = shfl_down1(xc.a);
     if (m.in) {
-      const V west = off ? xc.a : (m.lane > 0 ? up : cur.xw);
-      const V east = off ? (m.lane < 31 ? dn : cur.xe) : xc.c;
+      const V west = off ? xc.a : (!m.first ? up : cur.xw);
+      const V east = off ? (!m.last ? dn : cur.xe) : xc.c;
       const R dk = cur.tw + cur.te + cur.ts + cur.tn + cur.tb + cur.tt;
       V o = pick(cur.fv, off);
       o = vadd(o, vadd(vadd(vscale(west, cur.tw), vscale(east, cur.te)),
@@ -1058,8 +1072,8 @@ __global__ void __launch_bounds__(kT, 3) residual_pair_zm_kernel(LevelViewT<R> L
     o.fv = ld_pair(fb + a);
     o.ns = m.j > 0 ? ld_pair(xb + a - L.nx) : pz;
     o.nn = m.j < L.ny - 1 ? ld_pair(xb + a + L.nx) : pz;
-    o.xw = (m.lane == 0 && m.i0 > 0) ? xb[a - 1] : vzero<V>();
-    o.xe = (m.lane == 31 && m.i0 + 2 < L.nx) ? xb[a + 2] : vzero<V>();
+    o.xw = (m.first && m.i0 > 0) ? xb[a - 1] : vzero<V>();
+    o.xe = (m.last && m.i0 + 2 < L.nx) ? xb[a + 2] : vzero<V>();
   };
   Ops cur, nxt;
   if (m.in) load_ops(m.k0, cur);
@@ -1069,8 +1083,8 @@ __global__ void __launch_bounds__(kT, 3) residual_pair_zm_kernel(LevelViewT<R> L
     if (m.in && k + 1 < m.k1) load_ops(k + 1, nxt);
     const V up = shfl_up1(xc.c), dn = shfl_down1(xc.a);
     if (m.in) {
-      const V west = m.lane > 0 ? up : cur.xw;
-      const V east = m.lane < 31 ? dn : cur.xe;
+      const V west = !m.first ? up : cur.xw;
+      const V east = !m.last ? dn : cur.xe;
       PV out;
       {  // cell i0: neighbours west, xc.c
         const R dk = cur.tx0 + cur.tx1 + cur.ts.x + cur.tn.x + cur.tb.x + cur.tt.x;
