@@ -243,20 +243,22 @@ __global__ void __launch_bounds__(kT, 2) jacobian_kernel(LevelView L, const doub
 // = real GEMMs over K = (shift, point, re/im) whose B operand is the raw receiver field (no
 // difference pass for the receivers).  A persistent CTA walks tasks = (tile of 2 cells of a
 // row, pair of shifts), warp-specialised:
-//   producer warp 8 : bulk-copies each task's raw fields (all items at the tile's 12 points,
+//   copy warp 16   : bulk-copies each task's raw fields (all items at the tile's 12 points,
 //                     one contiguous B x 16-byte run per (shift, point) of the cell-major field
-//                     array) into a 4-deep ring, 3 tasks ahead;
+//                     array) into a 4-deep ring, gated only by the ring's empty barriers (a
+//                     dedicated warp: issuing from a transform warp tied each refill to that
+//                     warp's transform of the next task, ~30% of the kernel's time);
 //   producer warps 8-15: the arrow transform of the 16 sources into mma A fragments
-//                     (double-buffered; 4 lanes per (cell, shift, source), faces split);
+//                     (3 buffers; 4 lanes per (cell, shift, source), faces split);
 //   consumer warps 0-7: warp = (cell, 16 receivers): 2 x 2 accumulator tiles per block.
 // mbarriers hand the stages over; J is written after a tile's last shift pair.
 // Requires n_src <= 16 and n_rec <= 64.
 constexpr int JW_TC = 2;  // cells per tile
 constexpr int JW_SMAX = 16, JW_RMAX = 64;
-constexpr int JW_NRAW = 4, JW_AHEAD = 3;
+constexpr int JW_NRAW = 4;
 constexpr int JW_CONS = 8, JW_PROD = 8;
-constexpr int JW_NA = 2;  // A-fragment buffers
-constexpr int JW_THREADS = 32 * (JW_CONS + JW_PROD);
+constexpr int JW_NA = 3;  // A-fragment buffers
+constexpr int JW_THREADS = 32 * (JW_CONS + JW_PROD + 1);  // + the copy warp
 
 template <int DIM>
 struct JwGeom {
@@ -391,24 +393,26 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
   }
   __syncthreads();
 
-  if (wc >= JW_CONS) {
+  if (wc == JW_CONS + JW_PROD) {
+    // ------------------------------- copy warp -------------------------------------------
+    // task t's two boxes into slot t % JW_NRAW once every consumer and producer warp has
+    // released the slot's previous task (t - JW_NRAW)
+    if (lane == 0) {
+      for (int t = 0; t < T; ++t) {
+        const int slot = t % JW_NRAW;
+        if (t >= JW_NRAW) jw_wait(&raw_empty[slot], (uint32_t)(((t - JW_NRAW) / JW_NRAW) & 1));
+        const TileXY g = tile_at(t);
+        const int kp = (t % npair) * 2;
+        double2* dst = raw + slot * SLOT;
+        const uint32_t ca = (uint32_t)B * 16u;
+        jw_expect(&raw_full[slot], 24u * ca + (DIM == 3 ? 12u * ca : 0u));
+        tma5(dst, &mA, 0, g.i0 - 1, g.j - 1, g.kz, kp, &raw_full[slot]);
+        if (DIM == 3) tma5(dst + OFFB, &mB, 0, g.i0, g.j, g.kz - 1, kp, &raw_full[slot]);
+      }
+    }
+  } else if (wc >= JW_CONS) {
     // ------------------------------- producers -------------------------------------------
-    const int pw = wc - JW_CONS;  // 0 issues the copies
     const int ptid = tid - 32 * JW_CONS;
-    // task t's two boxes into slot t % JW_NRAW (one thread)
-    auto issue = [&](int t) {
-      if (lane != 0) return;
-      const TileXY g = tile_at(t);
-      const int kp = (t % npair) * 2;
-      const int slot = t % JW_NRAW;
-      double2* dst = raw + slot * SLOT;
-      const uint32_t ca = (uint32_t)B * 16u;
-      jw_expect(&raw_full[slot], 24u * ca + (DIM == 3 ? 12u * ca : 0u));
-      tma5(dst, &mA, 0, g.i0 - 1, g.j - 1, g.kz, kp, &raw_full[slot]);
-      if (DIM == 3) tma5(dst + OFFB, &mB, 0, g.i0, g.j, g.kz - 1, kp, &raw_full[slot]);
-    };
-    if (pw == 0)
-      for (int t = 0; t < min(T, JW_AHEAD); ++t) issue(t);
     // face / storativity weights of tile u into wts[u & 1] (loads issued a tile ahead of use)
     auto weights = [&](int u) {
       if ((dbg & 8) || ptid >= JW_TC * NPC || u * npair >= T) return;
@@ -493,11 +497,6 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
         jw_arrive(&a_full[t % JW_NA]);
         jw_arrive(&raw_empty[t % JW_NRAW]);
       }
-      // refill: task t + AHEAD goes into the slot task t - 1 used, once everyone is done with it
-      if (pw == 0 && t + JW_AHEAD < T) {
-        if (t >= 1) jw_wait(&raw_empty[(t - 1) % JW_NRAW], (uint32_t)(((t - 1) / JW_NRAW) & 1));
-        issue(t + JW_AHEAD);
-      }
     }
   } else {
     // ------------------------------- consumers -------------------------------------------
@@ -570,6 +569,256 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
                 if (both) ps[1] = 2.0 * accS[1][mt][h];
               }
             }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---- Jacobian on the FP64 tensor cores, 4-cell tiles -----------------------------------------
+// The same GEMM formulation as jacobian_mma_kernel (arrow transform of the sources, raw receiver
+// fields as the B operand), with a task = (4 consecutive cells of a row, pair of shifts):
+//  * the halo costs 44 chunks per 8 (cell, shift) units (centre row i0-1..i0+4, rows j-1 / j+1
+//    and planes kz-1 / kz+1 over i0..i0+3: five TMA boxes, no corner cells) instead of 36 per 4:
+//    5.5x instead of 9x the field bytes from L2 per cell and shift;
+//  * every lane ends a tile holding the 4 cells of each of its (s, r) entries and writes them as
+//    one 32-byte store (STG.256) -- full L2 sectors, where 2-cell tiles wrote half sectors
+//    (ncu: 16 of 32 bytes per sector used), half the store transactions;
+//  * a dedicated copy warp keeps the 3-deep ring full, gated only by its empty barriers.
+// Warps: 0-7 consumers (8 receivers x 4 cells x 16 sources each), 8-11 producers (arrow
+// transform, one lane per (cell, shift, source)), 12 the copy warp (13 warps: <= 4 per SM
+// sub-partition, so 128 registers per thread).  Needs nx % 4 == 0,
+// n_src <= 16, n_rec <= 64 and 32-byte aligned J rows (checked by the caller).
+constexpr int J4_TC = 4;
+constexpr int J4_NRAW = 3, J4_NA = 2;
+constexpr int J4_CONS = 8, J4_PROD = 4;
+constexpr int J4_THREADS = 32 * (J4_CONS + J4_PROD + 1);
+
+// slot regions (complex offsets, each 128-byte aligned): C = centre row, 6 cells x 2 shifts;
+// then 4-cell x 2-shift boxes S (row j-1), N (row j+1), D (plane kz-1), U (plane kz+1)
+__host__ __device__ inline int j4_rnd(int cplx) { return ((cplx * 16 + 127) / 128) * 8; }
+__host__ __device__ inline int j4_offC() { return 0; }
+__host__ __device__ inline int j4_offF(int B, int f) { return j4_rnd(12 * B) + f * j4_rnd(8 * B); }  // f: 0 S 1 N 2 D 3 U
+template <int DIM>
+__host__ __device__ inline int j4_slot(int B) { return j4_offF(B, DIM == 3 ? 4 : 2); }
+
+template <int DIM>
+size_t j4_smem(int B) {
+  constexpr int NPC = 2 * DIM + 1, KS = NPC;
+  return sizeof(double2) * J4_NRAW * (size_t)j4_slot<DIM>(B)      // raw ring
+         + sizeof(double) * J4_NA * J4_TC * 2 * (KS + 1) * 32     // A fragments [buf][cell][mt][ks][lane]
+         + sizeof(double) * 2 * J4_TC * NPC;                       // weights [tile parity][cell][point]
+}
+
+// complex offset in a slot of cell c's point p (0 centre, 1 W, 2 E, 3 S, 4 N, 5 D, 6 U), shift s2
+__device__ __forceinline__ int j4_at(int B, int s2, int c, int p) {
+  switch (p) {
+    case 0: return (s2 * 6 + c + 1) * B;
+    case 1: return (s2 * 6 + c) * B;
+    case 2: return (s2 * 6 + c + 2) * B;
+    default: return j4_offF(B, p - 3) + (s2 * 4 + c) * B;
+  }
+}
+
+__device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
+    const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mF, LevelView L,
+    const double* __restrict__ kappa, const double* __restrict__ stor, double hd, double face_scale, int n_src,
+    int n_rec, int ns, const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj,
+    int ntiles) {
+  constexpr int NPC = 2 * DIM + 1, KS = NPC;
+  constexpr int AF = J4_TC * 2 * (KS + 1) * 32;  // doubles per A-fragment buffer
+  extern __shared__ __align__(128) unsigned char jsm[];
+  __shared__ __align__(8) uint64_t raw_full[J4_NRAW], raw_empty[J4_NRAW], a_full[J4_NA], a_empty[J4_NA];
+  const int B = n_src + n_rec;
+  const int SLOT = j4_slot<DIM>(B);
+  double2* raw = reinterpret_cast<double2*>(jsm);
+  double* Af = reinterpret_cast<double*>(raw + J4_NRAW * SLOT);
+  double* wts = Af + J4_NA * AF;
+  const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
+  const int tiles_x = L.nx / J4_TC;
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  if ((int)blockIdx.x >= ntiles) return;
+  const int npair = (ns + 1) / 2;
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int T = my_tiles * npair;
+  struct TileXY {
+    int i0, j, kz;
+  };
+  // x segments fastest, then YB rows, then planes, then blocks of YB rows: the tiles in flight
+  // at any time share their y and z neighbours through L2
+  const int YB = (L.ny % 4 == 0) ? 4 : ((L.ny % 2 == 0) ? 2 : 1);
+  auto tile_at = [&](int t) {
+    const int tile = (int)blockIdx.x + (t / npair) * (int)gridDim.x;
+    const int tx = tile % tiles_x, r = tile / tiles_x;
+    const int yi = r % YB, r2 = r / YB;
+    const int kz = r2 % L.nz, yb = r2 / L.nz;
+    return TileXY{tx * J4_TC, yb * YB + yi, kz};
+  };
+  if (tid == 0) {
+    for (int q = 0; q < J4_NRAW; ++q) {
+      jw_init(&raw_full[q], 1);
+      jw_init(&raw_empty[q], J4_CONS + J4_PROD);
+    }
+    for (int q = 0; q < J4_NA; ++q) {
+      jw_init(&a_full[q], J4_PROD);
+      jw_init(&a_empty[q], J4_CONS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (wc == J4_CONS + J4_PROD) {
+    // ------------------------------- copy warp -------------------------------------------
+    if (lane == 0) {
+      const uint32_t ca = (uint32_t)B * 16u;
+      for (int t = 0; t < T; ++t) {
+        const int slot = t % J4_NRAW;
+        if (t >= J4_NRAW) jw_wait(&raw_empty[slot], (uint32_t)(((t - J4_NRAW) / J4_NRAW) & 1));
+        const TileXY g = tile_at(t);
+        const int kp = (t % npair) * 2;
+        double2* dst = raw + slot * SLOT;
+        jw_expect(&raw_full[slot], (12u + (DIM == 3 ? 32u : 16u)) * ca);
+        tma5(dst + j4_offC(), &mC, 0, g.i0 - 1, g.j, g.kz, kp, &raw_full[slot]);
+        tma5(dst + j4_offF(B, 0), &mF, 0, g.i0, g.j - 1, g.kz, kp, &raw_full[slot]);
+        tma5(dst + j4_offF(B, 1), &mF, 0, g.i0, g.j + 1, g.kz, kp, &raw_full[slot]);
+        if (DIM == 3) {
+          tma5(dst + j4_offF(B, 2), &mF, 0, g.i0, g.j, g.kz - 1, kp, &raw_full[slot]);
+          tma5(dst + j4_offF(B, 3), &mF, 0, g.i0, g.j, g.kz + 1, kp, &raw_full[slot]);
+        }
+      }
+    }
+  } else if (wc >= J4_CONS) {
+    // ------------------------------- producers -------------------------------------------
+    const int ptid = tid - 32 * J4_CONS;
+    // face / storativity weights of tile u into wts[u & 1]
+    auto weights = [&](int u) {
+      if (ptid >= J4_TC * NPC || u * npair >= T) return;
+      const TileXY g = tile_at(u * npair);
+      const int c = ptid / NPC, p = ptid % NPC;
+      const int i = g.i0 + c;
+      const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + i;
+      double wv;
+      if (p == 0) {
+        wv = stor[a] * hd;
+      } else {
+        const int f = p - 1, d = f >> 1, hi = f & 1;
+        const int coord = d == 0 ? i : (d == 1 ? g.j : g.kz);
+        const int ext = d == 0 ? L.nx : (d == 1 ? L.ny : L.nz);
+        const int64_t stride = d == 0 ? 1 : (d == 1 ? (int64_t)L.nx : plane);
+        const double ka = kappa[a];
+        if (hi ? coord == ext - 1 : coord == 0) {
+          wv = 2.0 * ka * face_scale;  // dT/dln k_a = T = 2 k_a h^(d-2); ghost value 0
+        } else {
+          const double kb = kappa[hi ? a + stride : a - stride];
+          const double Tf = 2.0 * ka * kb / (ka + kb) * face_scale;
+          wv = Tf * kb / (ka + kb);
+        }
+      }
+      wts[(u & 1) * J4_TC * NPC + c * NPC + p] = wv;
+    };
+    weights(0);
+    // one lane per (cell, shift of the pair, source)
+    const int combo = ptid;
+    const int s = combo % JW_SMAX, s2 = (combo / JW_SMAX) % 2, c = combo / (2 * JW_SMAX);
+    const int mt = s >> 3, lrow = (s & 7) * 4;
+    for (int t = 0; t < T; ++t) {
+      const int kp = (t % npair) * 2;
+      const double* wt = wts + ((t / npair) & 1) * J4_TC * NPC;
+      if (t % npair == 0) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * J4_PROD) : "memory");
+        weights(t / npair + 1);
+      }
+      jw_wait(&raw_full[t % J4_NRAW], (uint32_t)((t / J4_NRAW) & 1));
+      if (t >= J4_NA) jw_wait(&a_empty[t % J4_NA], (uint32_t)(((t - J4_NA) / J4_NA) & 1));
+      {
+        const double2* rw = raw + (t % J4_NRAW) * SLOT;
+        double* Ac = Af + (t % J4_NA) * AF + (c * 2 + mt) * (KS + 1) * 32;
+        const int k = kp + s2;
+        const bool live = s < n_src && k < ns;
+        const double2* R = rw + min(s, B - 1);
+        const double2 pa = R[j4_at(B, s2, c, 0)];
+        auto put = [&](int p, double2 v) {  // A'[s][K], K = (s2 NPC + p) 2 + comp (re, -im)
+          const int K0 = (s2 * NPC + p) * 2;
+          Ac[(K0 >> 2) * 32 + lrow + (K0 & 3)] = v.x;
+          Ac[((K0 + 1) >> 2) * 32 + lrow + ((K0 + 1) & 3)] = -v.y;
+        };
+        double2 a0 = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int p = 1; p < NPC; ++p) {
+          const double2 d = live ? cscale(csub(pa, R[j4_at(B, s2, c, p)]), wt[c * NPC + p]) : make_double2(0.0, 0.0);
+          a0 = cadd(a0, d);
+          put(p, make_double2(-d.x, -d.y));
+        }
+        put(0, a0);
+        {  // storativity block: K = s2 2 + comp in step KS
+          const double2 As = live ? cmul(wz[k], cscale(pa, wt[c * NPC])) : make_double2(0.0, 0.0);
+          Ac[KS * 32 + lrow + s2 * 2] = As.x;
+          Ac[KS * 32 + lrow + s2 * 2 + 1] = -As.y;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jw_arrive(&a_full[t % J4_NA]);
+        jw_arrive(&raw_empty[t % J4_NRAW]);
+      }
+    }
+  } else {
+    // ------------------------------- consumers -------------------------------------------
+    const int kq = lane & 3, rl = lane >> 2;
+    const int rcol = n_src + min(wc * 8 + rl, n_rec - 1);
+    double accK[J4_TC][2][2], accS[J4_TC][2][2];  // [cell][m tile][2]
+    for (int t = 0; t < T; ++t) {
+      if (t % npair == 0) {
+#pragma unroll
+        for (int c = 0; c < J4_TC; ++c)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) accK[c][mt][0] = accK[c][mt][1] = accS[c][mt][0] = accS[c][mt][1] = 0.0;
+      }
+      jw_wait(&raw_full[t % J4_NRAW], (uint32_t)((t / J4_NRAW) & 1));
+      jw_wait(&a_full[t % J4_NA], (uint32_t)((t / J4_NA) & 1));
+      const double* rw = reinterpret_cast<const double*>(raw + (t % J4_NRAW) * SLOT) + 2 * rcol;
+      const double* Ab = Af + (t % J4_NA) * AF;
+#pragma unroll
+      for (int c = 0; c < J4_TC; ++c) {
+        const double* Ac = Ab + c * 2 * (KS + 1) * 32;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int K = ks * 4 + kq, comp = K & 1, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
+          const double bv = rw[2 * j4_at(B, s2, c, p) + comp];
+          dmma(accK[c][0], Ac[ks * 32 + lane], bv);
+          dmma(accK[c][1], Ac[(KS + 1) * 32 + ks * 32 + lane], bv);
+        }
+        {  // storativity: K = s2 2 + comp at the centre point
+          const double bv = rw[2 * j4_at(B, kq >> 1, c, 0) + (kq & 1)];
+          dmma(accS[c][0], Ac[KS * 32 + lane], bv);
+          dmma(accS[c][1], Ac[(KS + 1) * 32 + KS * 32 + lane], bv);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        jw_arrive(&a_empty[t % J4_NA]);
+        jw_arrive(&raw_empty[t % J4_NRAW]);
+      }
+      if (t % npair == npair - 1) {
+        const TileXY g = tile_at(t);
+        const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + g.i0;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int s = mt * 8 + (lane >> 2);
+          if (s >= n_src) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = wc * 8 + (lane & 3) * 2 + h;
+            if (r >= n_rec) continue;
+            const int64_t o = ((int64_t)s * n_rec + r) * ldj + a;
+            stg256(Jk + o, 2.0 * accK[0][mt][h], 2.0 * accK[1][mt][h], 2.0 * accK[2][mt][h], 2.0 * accK[3][mt][h]);
+            if (Js) stg256(Js + o, 2.0 * accS[0][mt][h], 2.0 * accS[1][mt][h], 2.0 * accS[2][mt][h], 2.0 * accS[3][mt][h]);
           }
         }
       }
@@ -1154,7 +1403,32 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     const double face_scale = p->dim == 3 ? h : 1.0;
     const double hd = p->dim == 3 ? h * h * h : h * h;
     const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
-    if (tensor_jac) {
+    // 4-cell tiles with 32-byte J stores where rows allow it (LT_JAC_MMA2=1 keeps 2-cell tiles)
+    static const bool mma4_on = std::getenv("LT_JAC_MMA2") == nullptr;
+    const bool tile4 = tensor_jac && mma4_on && p->view(0).nx % J4_TC == 0 && n_param % 4 == 0 && n % 4 == 0 &&
+                       (reinterpret_cast<uintptr_t>(J) & 31) == 0 &&
+                       (p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B)) <= 227 * 1024;
+    if (tile4) {
+      LevelView L = p->view(0);
+      const int ntiles = (L.nx / J4_TC) * L.ny * L.nz;
+      const int grid = std::min(ntiles, ctx->num_sms);
+      const size_t smem = p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B);
+      auto fn = p->dim == 3 ? jacobian_mma4_kernel<3> : jacobian_mma4_kernel<2>;
+      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
+      const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
+                                (uint64_t)n * B * 16};
+      const uint32_t boxC[5] = {2 * (uint32_t)B, 6, 1, 1, 2}, boxF[5] = {2 * (uint32_t)B, 4, 1, 1, 2};
+      const CUtensorMap mC = tma_map_8b(fields.get(), 5, dims, strd, boxC);
+      const CUtensorMap mF = tma_map_8b(fields.get(), 5, dims, strd, boxF);
+      launch(ctx, "jacobian", bytes, [&] {
+        fn<<<grid, J4_THREADS, smem, st>>>(mC, mF, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
+                                           face_scale, n_src, n_rec, ns, dw.as<double2>() + ns, J,
+                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles);
+      });
+      if (mem != LT_MEM_DEVICE)
+        LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
+    } else if (tensor_jac) {
       static const int jw_dbg = std::getenv("LT_JW_DBG") ? std::atoi(std::getenv("LT_JW_DBG")) : 0;
       LevelView L = p->view(0);
       const int ntiles = ((L.nx + JW_TC - 1) / JW_TC) * L.ny * L.nz;

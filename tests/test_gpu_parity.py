@@ -201,6 +201,19 @@ def test_jacobian_3d_reduced():
     assert row <= 1e-8 and entry <= 1e-8 and s_err <= 1e-8, (row, entry, s_err)
 
 
+@pytest.mark.parametrize("shape,n_src,n_rec", [((16, 16, 16), 16, 64), ((14, 14, 14), 5, 7)])
+def test_jacobian_3d_tiles(shape, n_src, n_rec):
+    """The tensor-core Jacobian's tile paths: 4-cell tiles with the full 16 x 64 item set
+    (every consumer warp and both source m-tiles live), and the 2-cell fallback (nx % 4 != 0)."""
+    cfg, lk, ls, grid, ops = fd_case(4, shape, n_src=n_src, n_rec=n_rec, n_times=1)
+    ex, oex = _experiment(cfg, grid, True)
+    got = L.ThtForwardModel(ex, ls).jacobian(lk)
+    ref = ojac.ThtForwardModel(oex, ls).jacobian(lk)
+    assert np.max(np.abs(got.predictions - ref.predictions) / np.abs(ref.predictions)) <= 1e-8
+    row, entry, s_err = jacobian_errors(got.jacobian, ref.jacobian, grid.n_cells, True)
+    assert row <= 1e-8 and entry <= 1e-8 and s_err <= 1e-8, (row, entry, s_err)
+
+
 def test_predict_matches_jacobian_predictions():
     cfg, lk, ls, grid, ops = fd_case(2, (32, 32), n_src=2, n_rec=3, n_times=2)
     ex, _ = _experiment(cfg, grid, False)
