@@ -607,7 +607,7 @@ template <int DIM>
 size_t j4_smem(int B) {
   constexpr int NPC = 2 * DIM + 1, KS = NPC;
   return sizeof(double2) * J4_NRAW * (size_t)j4_slot<DIM>(B)      // raw ring
-         + sizeof(double) * J4_NA * J4_TC * 2 * (KS + 1) * 32     // A fragments [buf][cell][mt][ks][lane]
+         + sizeof(double) * J4_NA * J4_TC * 2 * ((KS + 1) * 32 + 1) // A fragments [buf][cell][mt][ks][lane] (+pad)
          + sizeof(double) * 2 * J4_TC * NPC;                       // weights [tile parity][cell][point]
 }
 
@@ -621,8 +621,16 @@ __device__ __forceinline__ int j4_at(int B, int s2, int c, int p) {
   }
 }
 
-__device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d) {
+// 32-byte store with an L2 evict-first policy: J (34 GB per 128^3 slice) streams through L2
+// without evicting the field planes the neighbouring tiles still read
+__device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d, uint64_t pol) {
+#ifdef J4_NO_EVICT
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+#else
+  asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d), "l"(pol)
+               : "memory");
+#endif
 }
 
 template <int DIM>
@@ -632,7 +640,12 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     int n_rec, int ns, const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj,
     int ntiles) {
   constexpr int NPC = 2 * DIM + 1, KS = NPC;
-  constexpr int AF = J4_TC * 2 * (KS + 1) * 32;  // doubles per A-fragment buffer
+#ifdef J4_NO_PAD
+  constexpr int MTS = (KS + 1) * 32;
+#else
+  constexpr int MTS = (KS + 1) * 32 + 1;  // doubles per (cell, m tile) fragment block (+1: bank spread)
+#endif
+  constexpr int AF = J4_TC * 2 * MTS;      // doubles per A-fragment buffer
   extern __shared__ __align__(128) unsigned char jsm[];
   __shared__ __align__(8) uint64_t raw_full[J4_NRAW], raw_empty[J4_NRAW], a_full[J4_NA], a_empty[J4_NA];
   const int B = n_src + n_rec;
@@ -731,6 +744,8 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
       const int kp = (t % npair) * 2;
       const double* wt = wts + ((t / npair) & 1) * J4_TC * NPC;
       if (t % npair == 0) {
+        // tile u's weights (stored a tile ago) are visible after this barrier; tile u + 1's go
+        // into the other half (its previous user, tile u - 1, is finished)
         asm volatile("bar.sync 1, %0;" ::"n"(32 * J4_PROD) : "memory");
         weights(t / npair + 1);
       }
@@ -738,7 +753,7 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
       if (t >= J4_NA) jw_wait(&a_empty[t % J4_NA], (uint32_t)(((t - J4_NA) / J4_NA) & 1));
       {
         const double2* rw = raw + (t % J4_NRAW) * SLOT;
-        double* Ac = Af + (t % J4_NA) * AF + (c * 2 + mt) * (KS + 1) * 32;
+        double* Ac = Af + (t % J4_NA) * AF + (c * 2 + mt) * MTS;
         const int k = kp + s2;
         const bool live = s < n_src && k < ns;
         const double2* R = rw + min(s, B - 1);
@@ -772,6 +787,16 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     // ------------------------------- consumers -------------------------------------------
     const int kq = lane & 3, rl = lane >> 2;
     const int rcol = n_src + min(wc * 8 + rl, n_rec - 1);
+    // lane-constant B-operand offsets (doubles from the slot base) of every K step, cell 0;
+    // cell c adds c B complex in every region.  Step KS is the storativity block (centre point).
+    int offk[KS + 1];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int K = ks * 4 + kq, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
+      offk[ks] = 2 * j4_at(B, s2, 0, p) + 2 * rcol + (K & 1);
+    }
+    offk[KS] = 2 * j4_at(B, kq >> 1, 0, 0) + 2 * rcol + (kq & 1);
+    const int cstep = 2 * B;
     double accK[J4_TC][2][2], accS[J4_TC][2][2];  // [cell][m tile][2]
     for (int t = 0; t < T; ++t) {
       if (t % npair == 0) {
@@ -782,22 +807,27 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
       }
       jw_wait(&raw_full[t % J4_NRAW], (uint32_t)((t / J4_NRAW) & 1));
       jw_wait(&a_full[t % J4_NA], (uint32_t)((t / J4_NA) & 1));
-      const double* rw = reinterpret_cast<const double*>(raw + (t % J4_NRAW) * SLOT) + 2 * rcol;
-      const double* Ab = Af + (t % J4_NA) * AF;
+      const double* rw = reinterpret_cast<const double*>(raw + (t % J4_NRAW) * SLOT);
+      const double* Al = Af + (t % J4_NA) * AF + lane;
+      // K steps outer, cells inner: 8 independent accumulator chains per step
 #pragma unroll
-      for (int c = 0; c < J4_TC; ++c) {
-        const double* Ac = Ab + c * 2 * (KS + 1) * 32;
+      for (int ks = 0; ks <= KS; ++ks) {
+        double bv[J4_TC], a0[J4_TC], a1[J4_TC];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int K = ks * 4 + kq, comp = K & 1, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
-          const double bv = rw[2 * j4_at(B, s2, c, p) + comp];
-          dmma(accK[c][0], Ac[ks * 32 + lane], bv);
-          dmma(accK[c][1], Ac[(KS + 1) * 32 + ks * 32 + lane], bv);
+        for (int c = 0; c < J4_TC; ++c) {
+          bv[c] = rw[offk[ks] + c * cstep];
+          a0[c] = Al[c * 2 * MTS + ks * 32];
+          a1[c] = Al[c * 2 * MTS + MTS + ks * 32];
         }
-        {  // storativity: K = s2 2 + comp at the centre point
-          const double bv = rw[2 * j4_at(B, kq >> 1, c, 0) + (kq & 1)];
-          dmma(accS[c][0], Ac[KS * 32 + lane], bv);
-          dmma(accS[c][1], Ac[(KS + 1) * 32 + KS * 32 + lane], bv);
+#pragma unroll
+        for (int c = 0; c < J4_TC; ++c) {
+          if (ks < KS) {
+            dmma(accK[c][0], a0[c], bv[c]);
+            dmma(accK[c][1], a1[c], bv[c]);
+          } else {
+            dmma(accS[c][0], a0[c], bv[c]);
+            dmma(accS[c][1], a1[c], bv[c]);
+          }
         }
       }
       __syncwarp();
@@ -808,6 +838,8 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
       if (t % npair == npair - 1) {
         const TileXY g = tile_at(t);
         const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + g.i0;
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
           const int s = mt * 8 + (lane >> 2);
@@ -817,8 +849,10 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
             const int r = wc * 8 + (lane & 3) * 2 + h;
             if (r >= n_rec) continue;
             const int64_t o = ((int64_t)s * n_rec + r) * ldj + a;
-            stg256(Jk + o, 2.0 * accK[0][mt][h], 2.0 * accK[1][mt][h], 2.0 * accK[2][mt][h], 2.0 * accK[3][mt][h]);
-            if (Js) stg256(Js + o, 2.0 * accS[0][mt][h], 2.0 * accS[1][mt][h], 2.0 * accS[2][mt][h], 2.0 * accS[3][mt][h]);
+            stg256(Jk + o, 2.0 * accK[0][mt][h], 2.0 * accK[1][mt][h], 2.0 * accK[2][mt][h], 2.0 * accK[3][mt][h], pol);
+            if (Js)
+              stg256(Js + o, 2.0 * accS[0][mt][h], 2.0 * accS[1][mt][h], 2.0 * accS[2][mt][h], 2.0 * accS[3][mt][h],
+                     pol);
           }
         }
       }
