@@ -591,7 +591,10 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
 // sub-partition, so 128 registers per thread).  Needs nx % 4 == 0,
 // n_src <= 16, n_rec <= 64 and 32-byte aligned J rows (checked by the caller).
 constexpr int J4_TC = 4;
-constexpr int J4_NRAW = 3, J4_NA = 2;
+#ifndef J4_NA_BUFS
+#define J4_NA_BUFS 3
+#endif
+constexpr int J4_NRAW = 3, J4_NA = J4_NA_BUFS;
 constexpr int J4_CONS = 8, J4_PROD = 4;
 constexpr int J4_THREADS = 32 * (J4_CONS + J4_PROD + 1);
 
