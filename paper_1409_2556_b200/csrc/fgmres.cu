@@ -590,6 +590,52 @@ __global__ void __launch_bounds__(256) expand_cm_kernel(int64_t n, int B, int ns
   }
 }
 
+// Cell-major expansion, v2: the (scaled, column-masked) coefficients of all items and shifts,
+// ys[(k mmax + j) B + b] = scale_bk y_bk[j] (0 for j >= m_bk), are staged once per block in
+// shared memory; thread <-> (cell, item) pairs in item-fastest order, so for every shift a
+// warp writes one contiguous 512-byte run of out[(k n + a) B + b] (the block's CT x B pairs
+// are one contiguous run per shift) and reads its coefficients conflict-free.  No per-shift
+// barriers (the v1 kernel transposed every shift through shared memory, 2 barriers each).
+__global__ void expand_coeffs(int B, int ns, int maxit, int mmax, const double2* __restrict__ Y,
+                              const int* __restrict__ m_used, const double2* __restrict__ scale,
+                              double2* __restrict__ ys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns * mmax * B) return;
+  const int b = i % B, j = (i / B) % mmax, k = i / (B * mmax);
+  const int bk = b * ns + k;
+  double2 v = make_double2(0.0, 0.0);
+  if (j < m_used[bk]) v = Y[(int64_t)bk * maxit + j];
+  if (scale) v = cmul(scale[bk], v);
+  ys[i] = v;
+}
+
+template <int MAXM>
+__global__ void __launch_bounds__(256) expand_cm2_kernel(int64_t n, int B, int ns, int mmax, int CT,
+                                                         const double2* const* __restrict__ Ucols,
+                                                         const double2* __restrict__ ysg, double2* __restrict__ out) {
+  extern __shared__ double2 ys[];  // [k][j][b]
+  for (int i = threadIdx.x; i < ns * mmax * B; i += blockDim.x) ys[i] = ysg[i];
+  __syncthreads();
+  const int64_t a0 = (int64_t)blockIdx.x * CT;
+  const int npairs = (int)(n - a0 < (int64_t)CT ? n - a0 : (int64_t)CT) * B;
+  for (int idx = threadIdx.x; idx < npairs; idx += blockDim.x) {
+    const int c = idx / B, b = idx - c * B;
+    const int64_t a = a0 + c;
+    double2 u[MAXM];
+#pragma unroll
+    for (int j = 0; j < MAXM; ++j) u[j] = j < mmax ? Ucols[j][(int64_t)b * n + a] : make_double2(0.0, 0.0);
+    double2* o = out + a0 * B + idx;
+    for (int k = 0; k < ns; ++k) {
+      const double2* yk = ys + (k * mmax) * B + b;
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int j = 0; j < MAXM; ++j)
+        if (j < mmax) acc = cfma(yk[j * B], u[j], acc);
+      o[(int64_t)k * n * B] = acc;
+    }
+  }
+}
+
 }  // namespace
 
 void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
@@ -920,6 +966,25 @@ void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_
   LT_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(void*) * cols.size(), cudaMemcpyHostToDevice, st));
   LT_CUDA(cudaMemcpyAsync(dmu.get(), res.m_used.data(), sizeof(int) * res.m_used.size(), cudaMemcpyHostToDevice, st));
   const int nblk = (int)blocks_for(n, kT);
+  int mmax = 0;
+  for (int v : res.m_used) mmax = std::max(mmax, v);
+  constexpr int kCT = 32;
+  const size_t ys_bytes = sizeof(double2) * (size_t)ns * std::max(mmax, 1) * B;
+  static const bool cm2_on = std::getenv("LT_EXPAND_V1") == nullptr;
+  if (cell_major && cm2_on && mmax >= 1 && mmax <= 8 && mmax <= ncols && ys_bytes <= 110 * 1024) {
+    DeviceBuffer ys(ys_bytes, st);
+    const int ny = ns * mmax * B;
+    expand_coeffs<<<(unsigned)((ny + 255) / 256), 256, 0, st>>>(B, ns, res.maxit, mmax, res.Y.as<double2>(),
+                                                                 dmu.as<int>(), scale_dev, ys.as<double2>());
+    auto fn = mmax <= 4 ? expand_cm2_kernel<4> : expand_cm2_kernel<8>;
+    LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ys_bytes));
+    launch(ctx, "expand", (double)n * B * 16.0 * (mmax + ns), [&] {
+      fn<<<(unsigned)((n + kCT - 1) / kCT), 256, ys_bytes, st>>>(n, B, ns, mmax, kCT, dcols.as<const double2*>(),
+                                                                  ys.as<double2>(), x_out);
+    });
+    LT_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   launch(ctx, "expand", (double)n * B * 16.0 * (ncols + ns), [&] {
     if (cell_major)
       expand_cm_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((B + 7) / 8)), 256, 0, st>>>(

@@ -1366,7 +1366,13 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c
 // positions m0-2 .. m0+33, f over the tile (own colour; both with dot or for the residual);
 // once per slot the coefficients of both colours over rows y0 .. y0+RB_H, positions
 // m0 .. m0+35.
-constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = 5;
+#ifndef RB_DEPTH
+#define RB_DEPTH 5
+#endif
+#ifndef RB_MINB
+#define RB_MINB 2
+#endif
+constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = RB_DEPTH;
 template <int MODE, int NI>
 struct RbSlot {
   static constexpr int NX = MODE == 0 ? 1 : 2;  // colours of x in the slot
@@ -1409,7 +1415,7 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
 // of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.  Blocks:
 // rb_blocks(L) per group of NI consecutive items (item group fastest).
 template <int MODE, int NI>
-__global__ void __launch_bounds__(kTP, 2) mg_rb_kernel(const __grid_constant__ CUtensorMap mx,
+__global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_constant__ CUtensorMap mx,
                                                        const __grid_constant__ CUtensorMap mf,
                                                        const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                        const double2* __restrict__ taus, float2* __restrict__ out,

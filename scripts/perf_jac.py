@@ -29,6 +29,6 @@ for r in range(reps):
     capi.check(lib.lt_jacobian_slice(p._h, C.byref(exc), 0, capi.LT_MEM_HOST, capi.dptr(J), capi.dptr(pred)))
     ctx.set_profiling(False)
 prof = ctx.profile()
-for k, (ms, cnt, by) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:8]:
+for k, (ms, cnt, by) in sorted(prof.items(), key=lambda kv: -kv[1][0])[:14]:
     print(f"  {k:16s} {ms:9.2f} ms {cnt:6d}")
 print("J row0 norm", float(np.linalg.norm(J[0])))
