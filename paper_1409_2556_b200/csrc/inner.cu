@@ -2140,6 +2140,127 @@ __global__ void __launch_bounds__(kTA, TA_H > 8 ? 1 : (TA_D <= 4 ? 3 : 2)) apply
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
 }
 
+// The same operator on two items per CTA: the coefficient tiles (9.8 KB per plane, 64% of a
+// one-item slot) are brought in once for both items and every coefficient-derived register is
+// shared, as in the colour-split sweeps.  5-deep ring (2 CTAs per SM).
+constexpr int TA2_D = 5;
+constexpr uint32_t TA2_XBA = (TA_XB + 127) / 128 * 128;
+constexpr uint32_t TA2_OFF_C = 2 * TA2_XBA, TA2_SLOT = (TA2_OFF_C + TA_CB + 127) / 128 * 128;
+constexpr size_t TA2_SMEM = (size_t)TA2_SLOT * TA2_D;
+
+__global__ void __launch_bounds__(kTA, 2) apply_tma2_kernel(const __grid_constant__ CUtensorMap mp,
+                                                           const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
+                                                           const double2* __restrict__ taus, double2* __restrict__ q,
+                                                           double2* __restrict__ part, int nblk) {
+  extern __shared__ __align__(128) unsigned char ta_smem[];
+  __shared__ __align__(8) uint64_t full[TA2_D], empty[TA2_D];
+  const int Bp = (bt.B + 1) / 2;
+  LT_ITEM_BLOCK(Bp, bp, cb);
+  const int b0 = 2 * bp;
+  const bool has1 = b0 + 1 < bt.B;
+  const bool live0 = !bt.done[b0], live1 = has1 && !bt.done[b0 + 1];
+  if (!live0 && !live1) return;
+  const int tiles_x = (L.nx + TA_W - 1) / TA_W, tiles_y = (L.ny + TA_H - 1) / TA_H;
+  const int ntile = tiles_x * tiles_y;
+  const int tile = cb % ntile, chunk = cb / ntile;
+  const int x0 = (tile % tiles_x) * TA_W, y0 = (tile / tiles_x) * TA_H;
+  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < TA2_D; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], TA_H);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+  double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
+  if (wy == TA_H) {  // producer warp
+    if (lane == 0) {
+      int sl = 0, use = 0;
+      for (int p = k0 - 1; p <= k1; ++p) {
+        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
+        unsigned char* sp = ta_smem + (size_t)sl * TA2_SLOT;
+        const bool lc = p >= k0;
+        mbar_arrive_tx(&full[sl], TA_XB * (has1 ? 2u : 1u) + (lc ? TA_CB : 0u));
+        tma_load4(sp, &mp, 2 * (x0 - 1), y0 - 1, p, b0, &full[sl]);
+        if (has1) tma_load4(sp + TA2_XBA, &mp, 2 * (x0 - 1), y0 - 1, p, b0 + 1, &full[sl]);
+        if (lc) tma_load4(sp + TA2_OFF_C, &mc, x0, 0, y0, p, &full[sl]);
+        if (++sl == TA2_D) { sl = 0; ++use; }
+      }
+    }
+  } else {
+    const int i = x0 + lane, j = y0 + wy;
+    const bool in = i < L.nx && j < L.ny;
+    const double2 tau0 = taus[b0], tau1 = has1 ? taus[b0 + 1] : tau0;
+    const int64_t plane = (int64_t)L.nx * L.ny;
+    double2* qb0 = q + (int64_t)b0 * L.n;
+    double2* qb1 = q + (int64_t)(b0 + 1) * L.n;
+    int qm = 0, q0 = 1, qu = 2;
+    uint32_t pu = 0;
+    mbar_wait_u32(full0 + 8 * qm, 0);
+    mbar_wait_u32(full0 + 8 * q0, 0);
+    for (int k = k0; k < k1; ++k) {
+      mbar_wait_u32(full0 + 8 * qu, pu);
+      const unsigned char* sm = ta_smem + (size_t)qm * TA2_SLOT;
+      const unsigned char* s0 = ta_smem + (size_t)q0 * TA2_SLOT;
+      const unsigned char* sp = ta_smem + (size_t)qu * TA2_SLOT;
+      auto X = [](const unsigned char* sl, int it, int yy, int xx) {
+        return reinterpret_cast<const double2*>(sl + it * TA2_XBA)[yy * TA_XW + xx];
+      };
+      auto C = [](const unsigned char* sl, int comp, int yy, int xx) {
+        return reinterpret_cast<const double*>(sl + TA2_OFF_C)[(yy * 4 + comp) * TA_CW + xx];
+      };
+      const double tw = C(s0, 0, wy, lane), ts = C(s0, 1, wy, lane), tb = C(s0, 2, wy, lane);
+      const double mm = C(s0, 3, wy, lane);
+      const double te = C(s0, 0, wy, lane + 1), tn = C(s0, 1, wy + 1, lane), tt = C(sp, 2, wy, lane);
+      const double dk = tw + te + ts + tn + tb + tt;
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        if (it == 1 && !has1) break;  // uniform
+        const double2 pc = X(s0, it, wy + 1, lane + 1);
+        double2 w, e;
+        w.x = __shfl_up_sync(0xffffffffu, pc.x, 1);
+        w.y = __shfl_up_sync(0xffffffffu, pc.y, 1);
+        e.x = __shfl_down_sync(0xffffffffu, pc.x, 1);
+        e.y = __shfl_down_sync(0xffffffffu, pc.y, 1);
+        if (lane == 0) w = X(s0, it, wy + 1, 0);
+        if (lane == 31) e = X(s0, it, wy + 1, TA_XW - 1);
+        if (in) {
+          const double2 so = X(s0, it, wy, lane + 1), no = X(s0, it, wy + 2, lane + 1);
+          const double2 dn = X(sm, it, wy + 1, lane + 1), up = X(sp, it, wy + 1, lane + 1);
+          const double ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
+          const double oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
+          const double2 tau = it == 0 ? tau0 : tau1;
+          const double dr = dk + tau.x * mm, di = tau.y * mm;
+          const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
+          const int64_t o = k * plane + (int64_t)j * L.nx + i;
+          if (it == 0) {
+            if (live0) qb0[o] = qa;
+            acc0 = cfma(pc, qa, acc0);
+          } else {
+            if (live1) qb1[o] = qa;
+            acc1 = cfma(pc, qa, acc1);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);
+      qm = q0;
+      q0 = qu;
+      if (++qu == TA2_D) { qu = 0; pu ^= 1u; }
+    }
+  }
+  acc0 = block_sum(acc0);
+  if (threadIdx.x == 0 && live0) part[(int64_t)b0 * nblk + cb] = acc0;
+  if (has1) {
+    __syncthreads();
+    acc1 = block_sum(acc1);
+    if (threadIdx.x == 0 && live1) part[(int64_t)(b0 + 1) * nblk + cb] = acc1;
+  }
+}
+
 // per-level tensor maps of one inner solve (ok = the level runs the TMA kernels)
 struct TzMaps {
   bool ok = false;
@@ -2624,6 +2745,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(apply_tma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA2_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<0, 2>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2790,8 +2912,12 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     const int nblk_apply = ta_ok ? ((L0.nx + TA_W - 1) / TA_W) * ((L0.ny + TA_H - 1) / TA_H) *
                                        ((L0.nz + ZM_ZC - 1) / ZM_ZC)
                                  : zm ? zm_blocks(L0) : L0.ntiles;
+    static const bool ta2_on = std::getenv("LT_APPLY_NI1") == nullptr;
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
-      if (ta_ok)
+      if (ta_ok && ta2_on)
+        apply_tma2_kernel<<<(unsigned)nblk_apply * ((Bc + 1) / 2), kTA, TA2_SMEM, st>>>(
+            map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n}, bt, d_taus, q, partials.as<double2>(), nblk_apply);
+      else if (ta_ok)
         apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kTA, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
                                                                          bt, d_taus, q, partials.as<double2>(),
                                                                          nblk_apply);
