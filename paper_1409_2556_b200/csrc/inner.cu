@@ -1372,6 +1372,9 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c
 #ifndef RB_MINB
 #define RB_MINB 2
 #endif
+#ifndef RB_NI
+#define RB_NI 2  // items per CTA of the colour-split half sweeps
+#endif
 constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = RB_DEPTH;
 template <int MODE, int NI>
 struct RbSlot {
@@ -1384,7 +1387,8 @@ struct RbSlot {
   static constexpr uint32_t OFF_F = XBA * NI;
   static constexpr uint32_t OFF_C = OFF_F + FB * NI;
   static constexpr uint32_t SLOT = (OFF_C + CB + 127) / 128 * 128;
-  static constexpr size_t SMEM = (size_t)SLOT * RB_D;
+  static constexpr int D = NI >= 4 ? 4 : RB_D;  // ring depth (4 items: 4 deep, 2 CTAs per SM)
+  static constexpr size_t SMEM = (size_t)SLOT * D;
 };
 
 template <class VW>
@@ -1422,7 +1426,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
                                                        int color, int zero_init, double2* __restrict__ dot, int nblk) {
   using S = RbSlot<MODE, NI>;
   extern __shared__ __align__(128) unsigned char rb_smem[];
-  __shared__ __align__(8) uint64_t full[RB_D], empty[RB_D];
+  __shared__ __align__(8) uint64_t full[S::D], empty[S::D];
   const int ngroups = (bt.B + NI - 1) / NI;
   const int grp = (int)(blockIdx.x % ngroups), cb = (int)(blockIdx.x / ngroups);
   bool live[NI];
@@ -1443,7 +1447,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
   const bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
   if (tid == 0) {
-    for (int q = 0; q < RB_D; ++q) {
+    for (int q = 0; q < S::D; ++q) {
       mbar_init(&full[q], 1);
       mbar_init(&empty[q], kT / 32);
     }
@@ -1480,7 +1484,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
           if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, &full[q]);
         }
         if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[q]);
-        if (++q == RB_D) { q = 0; ++use; }
+        if (++q == S::D) { q = 0; ++use; }
       }
     }
   } else {
@@ -1583,7 +1587,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
       if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // this warp is done with plane k - 1
       qm = q0;
       q0 = qu;
-      if (++qu == RB_D) { qu = 0; pu ^= 1u; }
+      if (++qu == S::D) { qu = 0; pu ^= 1u; }
     }
   }
   if (MODE == 0 && dot) {
@@ -2568,14 +2572,14 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   const TzDims tdims{L.nx, L.ny, L.nz, L.n};
   const bool rbk = tz && tz[l].rb;
   const unsigned rgrid = (unsigned)rb_blocks(L) * (unsigned)Bc;
-  const unsigned rgrid2 = (unsigned)rb_blocks(L) * (unsigned)((Bc + 1) / 2);
+  const unsigned rgrid2 = (unsigned)rb_blocks(L) * (unsigned)((Bc + RB_NI - 1) / RB_NI);
   auto half = [&](int color, int zero_init, double2* dot) {
     // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled.
     // Colour-split: a half sweep moves half of f and of x twice (1.5 c per cell, 1 from zero)
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
     launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", hb + coef, [&] {
       if (rbk)
-        mg_rb_kernel<0, 2><<<rgrid2, kTP, RbSlot<0, 2>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
+        mg_rb_kernel<0, RB_NI><<<rgrid2, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
                                                                    (float2*)X[l], color, zero_init, dot, rb_blocks(L));
       else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
@@ -2746,8 +2750,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA2_SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)RbSlot<0, 2>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0, RB_NI>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_resrestrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
