@@ -13,6 +13,7 @@
 #pragma once
 
 #include <complex>
+#include <cstdint>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -126,6 +127,20 @@ inline Complex qhat_step(double q0, Complex z) {
   lt_complex out;
   detail::check(lt_qhat_step(q0, detail::c(z), &out));
   return {out.re, out.im};
+}
+
+// ---- fields (sample_field_on_mesh, fields.hpp:41-44): structured-grid GRF on the device ----
+// log-field realisation, x fastest, covariance variance * exp(-|r / l|) (one l per axis)
+inline std::vector<double> sample_field_grid(const Context& ctx, const std::vector<int>& shape, double h,
+                                             double variance, const std::vector<double>& corr_lengths,
+                                             double mean_log, std::uint64_t seed) {
+  if (shape.size() != corr_lengths.size()) throw std::invalid_argument("sample_field_grid: one length per axis");
+  std::size_t n = 1;
+  for (int v : shape) n *= static_cast<std::size_t>(v > 0 ? v : 0);
+  std::vector<double> out(n);
+  detail::check(lt_sample_field_grid(ctx.handle(), static_cast<int>(shape.size()), shape.data(), h, variance,
+                                     corr_lengths.data(), mean_log, seed, nullptr, LT_MEM_HOST, out.data()));
+  return out;
 }
 
 // ---- shifted solver (shifted_solver.hpp:21-132) ---------------------------------------

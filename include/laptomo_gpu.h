@@ -250,6 +250,18 @@ lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out,
 /* ThtForwardModel::predict (jacobian.cpp:158-187): n_meas predictions. */
 lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_out);
 
+/* ---- fields (sample_field / sample_field_on_mesh, fields.hpp:27-44, fields.cpp:84-123) --
+ * The reference draws mean + C zeta with C C^T = Q, Q the dense exponential covariance over
+ * the element centres (Cholesky).  On a structured grid this draws the same Gaussian law by
+ * circulant embedding on a torus twice the grid (cuFFT): covariance variance *
+ * exp(-|(dx/l0, dy/l1, dz/l2)|) between cell centres (isotropic: equal lengths), grid spacing
+ * h, shape[dim] cells, out = n cells (x fastest; host or device per `mem`).  noise == NULL:
+ * complex standard normals from Philox(seed); else prod(2 shape) complex standard normals
+ * (x fastest over the doubled grid, same `mem`), the deterministic path. */
+lt_status lt_sample_field_grid(lt_ctx ctx, int dim, const int* shape, double h, double variance,
+                               const double* corr_lengths, double mean, uint64_t seed,
+                               const lt_complex* noise, int mem, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ SIGNATURES = {
     "lt_talbot_default_params": (None, [C.POINTER(LtTalbotParams)]),
     "lt_talbot_build": (I, [I, D, C.POINTER(LtTalbotParams), PD, PC, PC, PC]),
     "lt_qhat_step": (I, [D, LtComplex, PC]),
+    "lt_sample_field_grid": (I, [P, I, PI, D, D, PD, D, C.c_uint64, PC, I, PD]),
     "lt_select_preconditioner_shifts": (I, [PC, I, PC, PI, PI, PI]),
     "lt_pencil_create_grid": (I, [P, C.POINTER(LtGrid), PD, PD, I, C.POINTER(P)]),
     "lt_pencil_destroy": (I, [P]),

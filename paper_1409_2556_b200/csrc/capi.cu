@@ -244,6 +244,15 @@ lt_status lt_talbot_build(int n_quad, double time, const lt_talbot_params* param
   });
 }
 
+lt_status lt_sample_field_grid(lt_ctx ctx, int dim, const int* shape, double h, double variance,
+                               const double* corr_lengths, double mean, uint64_t seed, const lt_complex* noise,
+                               int mem, double* out) {
+  return guard([&] {
+    lt::sample_field_grid(ctx, dim, shape, h, variance, corr_lengths, mean, seed,
+                          reinterpret_cast<const double2*>(noise), mem, out);
+  });
+}
+
 lt_status lt_qhat_step(double q0, lt_complex z, lt_complex* out) {
   return guard([&] {
     LT_REQUIRE(!(z.re == 0.0 && z.im == 0.0), "qhat_step: z must be nonzero");

@@ -1,6 +1,10 @@
 #pragma once
 #include <vector>
 
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
 #include "laptomo_gpu.h"
 
 namespace lt {
@@ -13,5 +17,8 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
              lt_time_diag* diag_out, double* shift_residuals);
 
 void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double* jac_out, double* pred_out);
+
+void sample_field_grid(lt_ctx ctx, int dim, const int* shape, double h, double variance, const double* corr,
+                       double mean, uint64_t seed, const double2* noise, int mem, double* out);
 
 }  // namespace lt

@@ -20,10 +20,13 @@ import numpy as np
 
 
 def grf_exponential(shape: Sequence[int], h: float, variance: float,
-                    corr_lengths: Sequence[float], mean: float, seed: int) -> np.ndarray:
+                    corr_lengths: Sequence[float], mean: float, seed: int,
+                    noise: Optional[np.ndarray] = None) -> np.ndarray:
     """Stationary GRF with covariance var * exp(-|r / l|) (anisotropic l),
     sampled on cell centres by circulant embedding on a torus twice the grid.
-    Returns an array in C order with x fastest: shape reversed(shape)."""
+    Returns an array in C order with x fastest: shape reversed(shape).
+    `noise` (complex, indexed (x, y[, z]) over the doubled grid) replaces the PCG64 normals
+    (the device generator lt_sample_field_grid is checked against this with shared noise)."""
     dim = len(shape)
     ext = [2 * n for n in shape]
     axes = []
@@ -36,8 +39,11 @@ def grf_exponential(shape: Sequence[int], h: float, variance: float,
     cov = variance * np.exp(-r)
     lam = np.fft.fftn(cov).real
     lam = np.maximum(lam, 0.0)  # clip the (tiny) negative embedding modes
-    rng = np.random.Generator(np.random.PCG64(seed))
-    xi = rng.standard_normal(ext) + 1j * rng.standard_normal(ext)
+    if noise is None:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        xi = rng.standard_normal(ext) + 1j * rng.standard_normal(ext)
+    else:
+        xi = np.asarray(noise, dtype=np.complex128).reshape(ext)
     total = float(np.prod(ext))
     field_c = np.fft.ifftn(np.sqrt(lam) * xi) * math.sqrt(total)
     sample = field_c.real[tuple(slice(0, n) for n in shape)]

@@ -174,6 +174,31 @@ def qhat_step(q0: float, z: complex) -> complex:
     return complex(out.re, out.im)
 
 
+# ---- fields ------------------------------------------------------------------------------
+def sample_field_grid(ctx: "Context", shape: Sequence[int], h: float, variance: float,
+                      corr_lengths: Sequence[float], mean: float, seed: int = 0,
+                      noise: Optional[np.ndarray] = None) -> np.ndarray:
+    """sample_field_on_mesh (fields.hpp:41-44, fields.cpp:84-123) on a structured grid, by
+    circulant embedding on the device (lt_sample_field_grid): a GRF with covariance
+    variance * exp(-|r / l|) on the cell centres, flat, x fastest.  `noise` (complex, shape
+    2 * shape reversed, i.e. x fastest over the doubled grid) replaces the Philox normals."""
+    dim = len(shape)
+    sh = (C.c_int * dim)(*[int(v) for v in shape])
+    cl = np.ascontiguousarray(np.asarray(corr_lengths, dtype=np.float64))
+    if cl.size != dim:
+        raise ValueError("sample_field_grid: one correlation length per axis")
+    out = np.empty(int(np.prod(shape)), dtype=np.float64)
+    nz = None
+    if noise is not None:
+        nz = np.ascontiguousarray(noise, dtype=np.complex128).ravel()
+        if nz.size != int(np.prod([2 * v for v in shape])):
+            raise ValueError("sample_field_grid: noise must hold prod(2 * shape) values")
+    check(lib().lt_sample_field_grid(ctx._h, dim, sh, float(h), float(variance), dptr(cl), float(mean),
+                                     int(seed), cptr(nz) if nz is not None else None, capi.LT_MEM_HOST,
+                                     dptr(out)))
+    return out
+
+
 # ---- schedule ----------------------------------------------------------------------------
 @dataclass
 class PreconditionerSchedule:
