@@ -1391,9 +1391,17 @@ struct RbSlot {
   static constexpr size_t SMEM = (size_t)SLOT * D;
 };
 
+// planes per CTA: ZM_ZC on the finest levels; shorter chunks below (64^3 x 80 items with 32-plane
+// chunks is 640 CTAs = 2.2 waves of 296 resident CTAs, a 16%-full last wave)
+#ifndef RB_ZC_SMALL
+#define RB_ZC_SMALL 16
+#endif
+__host__ __device__ __forceinline__ int rb_zc(int nz) { return nz >= 128 ? ZM_ZC : RB_ZC_SMALL; }
+
 template <class VW>
 inline int rb_blocks(const VW& L) {
-  return ((L.nx / 2 + RB_P - 1) / RB_P) * ((L.ny + RB_H - 1) / RB_H) * ((L.nz + ZM_ZC - 1) / ZM_ZC);
+  const int zc = rb_zc(L.nz);
+  return ((L.nx / 2 + RB_P - 1) / RB_P) * ((L.ny + RB_H - 1) / RB_H) * ((L.nz + zc - 1) / zc);
 }
 
 __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
@@ -1443,7 +1451,8 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   const int ntile = tiles_x * tiles_y;
   const int tile = cb % ntile, chunk = cb / ntile;
   const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
-  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
+  const int zc = rb_zc(L.nz);
+  const int k0 = chunk * zc, k1 = min(L.nz, k0 + zc);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
   const bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
   if (tid == 0) {
