@@ -14,6 +14,7 @@ from oracle import forward as ofw
 from oracle import jacobian as ojac
 from oracle import shifted_solver as oss
 from oracle import talbot as otal
+from paper_1409_2556_b200 import inputs
 from paper_1409_2556_b200 import laptomo as L
 
 from .helpers import fd_case, jacobian_errors, rel
@@ -221,3 +222,28 @@ def test_predict_matches_jacobian_predictions():
     pred = model.predict(lk)
     jr = model.jacobian(lk)
     assert rel(pred, jr.predictions) <= 1e-9
+
+
+@pytest.mark.parametrize("index", [1, 2, 3, 4])
+def test_full_size_self_checks(index):
+    """BASELINE configs[1..4] at their full sizes (512^2 .. 128^3), where the oracle cannot run: size-independent
+    properties of the discrete model.  (1) Scaling both kappa and S by e^eps scales (K + zM) and
+    hence every shifted solution by e^-eps, so each Jacobian row sums to minus its prediction
+    (kappa block + S block; the oracle satisfies it to 8e-12 at 12^3).  (2) Reciprocity: swapping
+    the source and receiver points leaves the predictions unchanged (K, M symmetric, the same
+    point weights for both)."""
+    cfg = inputs.config(index)
+    lk, ls = cfg.fields()
+    g = L.Grid(tuple(cfg.shape), cfg.h)
+    src, rec, times = cfg.sources[:2], cfg.receivers[:2], cfg.times[:1]
+    solver = L.SolverConfig(kind=cfg.solver_kind)
+    ex = L.ThtExperiment(g, src, [1e-4] * 2, rec, times, cfg.n_quad, solver=solver, include_storativity=True)
+    model = L.ThtForwardModel(ex, ls)
+    jr = model.jacobian(lk)
+    assert jr.jacobian.shape == (4, 2 * g.n_cells)
+    row_sum = jr.jacobian.sum(axis=1)
+    assert np.max(np.abs(row_sum + jr.predictions)) <= 1e-8 * np.max(np.abs(jr.predictions))
+    ex_swapped = L.ThtExperiment(g, rec, [1e-4] * 2, src, times, cfg.n_quad, solver=solver)
+    pred_swapped = L.ThtForwardModel(ex_swapped, ls).predict(lk).reshape(2, 2)
+    pred = jr.predictions.reshape(2, 2)
+    assert np.max(np.abs(pred - pred_swapped.T)) <= 1e-8 * np.max(np.abs(pred))
