@@ -591,6 +591,12 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
 // sub-partition, so 128 registers per thread).  Needs nx % 4 == 0,
 // n_src <= 16, n_rec <= 64 and 32-byte aligned J rows (checked by the caller).
 constexpr int J4_TC = 4;
+// faces-only K (B operand psi_f - psi_a formed by the consumers; no centre column): 1/8 fewer
+// DMMA steps per shift pair (47.4 vs 49.6 ms per 128^3 slice); J4_NO_FACES restores the
+// centre column of the arrow transform
+#ifndef J4_NO_FACES
+#define J4_FACES 1
+#endif
 #ifndef J4_NA_BUFS
 #define J4_NA_BUFS 3
 #endif
@@ -642,7 +648,13 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     const double* __restrict__ kappa, const double* __restrict__ stor, double hd, double face_scale, int n_src,
     int n_rec, int ns, const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj,
     int ntiles) {
-  constexpr int NPC = 2 * DIM + 1, KS = NPC;
+  constexpr int NPC = 2 * DIM + 1;
+#ifdef J4_FACES
+  // faces only: B operand psi_f - psi_a formed by the consumers, K per shift pair 4 NF
+  constexpr int NF = NPC - 1, KS = NF;
+#else
+  constexpr int KS = NPC;
+#endif
 #ifdef J4_NO_PAD
   constexpr int MTS = (KS + 1) * 32;
 #else
@@ -762,7 +774,11 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
         const double2* R = rw + min(s, B - 1);
         const double2 pa = R[j4_at(B, s2, c, 0)];
         auto put = [&](int p, double2 v) {  // A'[s][K], K = (s2 NPC + p) 2 + comp (re, -im)
+#ifdef J4_FACES
+          const int K0 = (s2 * NF + p - 1) * 2;
+#else
           const int K0 = (s2 * NPC + p) * 2;
+#endif
           Ac[(K0 >> 2) * 32 + lrow + (K0 & 3)] = v.x;
           Ac[((K0 + 1) >> 2) * 32 + lrow + ((K0 + 1) & 3)] = -v.y;
         };
@@ -773,7 +789,9 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
           a0 = cadd(a0, d);
           put(p, make_double2(-d.x, -d.y));
         }
+#ifndef J4_FACES
         put(0, a0);
+#endif
         {  // storativity block: K = s2 2 + comp in step KS
           const double2 As = live ? cmul(wz[k], cscale(pa, wt[c * NPC])) : make_double2(0.0, 0.0);
           Ac[KS * 32 + lrow + s2 * 2] = As.x;
@@ -795,9 +813,16 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     int offk[KS + 1];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
+#ifdef J4_FACES
+      const int K = ks * 4 + kq, s2 = K / (2 * NF), p = 1 + (K >> 1) % NF;
+#else
       const int K = ks * 4 + kq, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
+#endif
       offk[ks] = 2 * j4_at(B, s2, 0, p) + 2 * rcol + (K & 1);
     }
+#ifdef J4_FACES
+    const int offc0 = 2 * j4_at(B, 0, 0, 0) + 2 * rcol + (kq & 1), offc1 = 2 * j4_at(B, 1, 0, 0) + 2 * rcol + (kq & 1);
+#endif
     offk[KS] = 2 * j4_at(B, kq >> 1, 0, 0) + 2 * rcol + (kq & 1);
     const int cstep = 2 * B;
     double accK[J4_TC][2][2], accS[J4_TC][2][2];  // [cell][m tile][2]
@@ -819,6 +844,9 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
 #pragma unroll
         for (int c = 0; c < J4_TC; ++c) {
           bv[c] = rw[offk[ks] + c * cstep];
+#ifdef J4_FACES
+          if (ks < KS) bv[c] -= rw[((ks * 4) / (2 * NF) == 0 ? offc0 : offc1) + c * cstep];
+#endif
           a0[c] = Al[c * 2 * MTS + ks * 32];
           a1[c] = Al[c * 2 * MTS + MTS + ks * 32];
         }
