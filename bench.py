@@ -357,9 +357,10 @@ def main():
             traffic = None
     if dname == "jacobian":
         # FP64 tensor-core GEMM: flops per launch (one time slice) = 2 n_src n_rec K n, with
-        # K = n_h shifts x ((2d+1) stencil points x (re, im) + (re, im) for the S block)
+        # K = n_h shifts x (2d faces x (re, im) + (re, im) for the S block)  (faces-only K,
+        # drivers.cu: jacobian_mma4_kernel)
         d = len(cfg.shape)
-        flops = 2.0 * n_src * n_rec * (cfg.n_quad // 2) * (2 * (2 * d + 1) + 2) * n
+        flops = 2.0 * n_src * n_rec * (cfg.n_quad // 2) * (2 * (2 * d) + 2) * n
         ach_tf = flops / (dms / dcnt * 1e-3) / 1e12 if dms > 0 else 0.0
         roofline = {"bound": "tensor", "kernel": dname, "achieved": ach_tf, "peak": FP64_DMMA_TFLOPS,
                     "unit": "TFLOP/s", "frac": ach_tf / FP64_DMMA_TFLOPS, "traffic": traffic,
