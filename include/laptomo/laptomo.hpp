@@ -12,6 +12,7 @@
 // per-cell log fields (assembled on the device) instead of assembled sparse (K, M).
 #pragma once
 
+#include <algorithm>
 #include <complex>
 #include <cstdint>
 #include <memory>
@@ -282,7 +283,9 @@ inline ShiftedSolveResult solve_shifted_flexible(const ShiftedPencil& pencil, co
   r.solutions.assign((size_t)n * ns, Complex(0.0));
   std::vector<lt_shift_status> st(ns > 0 ? ns : 1);
   int iters = 0;
-  const int maxit = options.maxit > 0 ? options.maxit : 10 * ns;
+  // the C API writes min(n, maxit) entries per shift (capi.cu), maxit defaulting to 10 n_shifts
+  const long maxit_req = options.maxit > 0 ? options.maxit : 10L * ns;
+  const int maxit = (int)std::min<long>(n, maxit_req);
   std::vector<double> hist((size_t)(ns > 0 ? ns : 1) * (maxit > 0 ? maxit : 1));
   detail::check(lt_solve_shifted(pencil.handle(), detail::c(b.data()), 1, detail::c(shifts.data()), ns,
                                  detail::c(schedule.taus.data()), (int)schedule.taus.size(), schedule.pattern.data(),

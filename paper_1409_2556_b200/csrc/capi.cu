@@ -101,6 +101,24 @@ __global__ void conj_kernel(const double2* in, double2* out, int64_t n) {
   if (a < n) out[a] = lt::cconj(in[a]);
 }
 
+// A shift-and-invert solve (the reference's exact LU) that ended above the inner solve's
+// stagnation floor (1e4 x its tolerance) fails with LT_ERR_NOT_CONVERGED; lt_last_unconverged
+// lists the offending right-hand sides (or shifts).
+void check_inner(lt_pencil p, const std::vector<double>& rel, int shift = -1) {
+  std::vector<int> bad;
+  double worst = 0.0;
+  for (size_t b = 0; b < rel.size(); ++b)
+    if (!(rel[b] <= 1e4 * p->inner_tol)) {
+      bad.push_back(shift >= 0 ? shift : (int)b);
+      worst = std::max(worst, rel[b]);
+    }
+  if (bad.empty()) return;
+  lt::g_last_unconverged = bad;
+  throw lt::Error(LT_ERR_NOT_CONVERGED, "shift-and-invert solve: relative residual " + std::to_string(worst) +
+                                            " above " + std::to_string(1e4 * p->inner_tol) + " after " +
+                                            std::to_string(p->inner_maxit) + " iterations");
+}
+
 // adjoint: (K + tau M)^{-H} v = conj((K + tau M)^{-1} conj(v)) since K, M are real symmetric,
 // so the adjoint solve reuses the factorisation of tau (factorization.hpp:25).
 void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, int n_rhs, int mem, bool adjoint) {
@@ -122,7 +140,9 @@ void solve_common(lt_pencil p, double2 tau, const lt_complex* v, lt_complex* u, 
     });
     vsrc = vc.as<double2>();
   }
-  lt::inner_solve(p, n_rhs, taus.data(), vsrc, p->n, uout.ptr, p->n);
+  std::vector<double> rel(n_rhs, 0.0);
+  lt::inner_solve(p, n_rhs, taus.data(), vsrc, p->n, uout.ptr, p->n, nullptr, rel.data());
+  check_inner(p, rel);
   if (adjoint)
     lt::launch(p->ctx, "conj", 32.0 * count, [&] {
       conj_kernel<<<lt::blocks_for((int64_t)count, 256), 256, 0, st>>>(uout.ptr, uout.ptr, (int64_t)count);
@@ -466,10 +486,27 @@ lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs, c
     Staged bin = stage_in(b, (size_t)n * n_rhs, mem, st);
     const size_t count = (size_t)n * n_shifts * n_rhs;
     Staged xo = stage_out(x_out, count, mem, st);
+    std::vector<int> bad;
+    double worst = 0.0;
     for (int k = 0; k < n_shifts; ++k) {
       std::vector<double2> t(n_rhs, make_double2(shifts[k].re, shifts[k].im));
-      lt::inner_solve(p, n_rhs, t.data(), bin.ptr, n, xo.ptr + (size_t)k * n, (int64_t)n * n_shifts);
+      std::vector<double> rel(n_rhs, 0.0);
+      lt::inner_solve(p, n_rhs, t.data(), bin.ptr, n, xo.ptr + (size_t)k * n, (int64_t)n * n_shifts, nullptr,
+                      rel.data());
+      for (double r : rel)
+        if (!(r <= 1e4 * p->inner_tol)) {
+          if (bad.empty() || bad.back() != k) bad.push_back(k);
+          worst = std::max(worst, r);
+        }
     }
+    finish_out(x_out, xo, count, mem, st);
+    if (!bad.empty()) {
+      lt::g_last_unconverged = bad;
+      throw lt::Error(LT_ERR_NOT_CONVERGED, "solve_shifted_direct: " + std::to_string(bad.size()) +
+                                                " shifts above the shift-and-invert floor (worst relative residual " +
+                                                std::to_string(worst) + ")");
+    }
+    return;
     finish_out(x_out, xo, count, mem, st);
   });
 }

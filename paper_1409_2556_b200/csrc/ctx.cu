@@ -49,6 +49,20 @@ void lt_ctx_s::resolve_profile() {
   pending.clear();
 }
 
+FlagSlot* lt_ctx_s::flag_ring_dev() {
+  if (!flag_host) {
+    void* hp = nullptr;
+    LT_CUDA(cudaHostAlloc(&hp, sizeof(FlagSlot) * kFlagRing, cudaHostAllocMapped));
+    flag_host = static_cast<FlagSlot*>(hp);
+    for (int i = 0; i < kFlagRing; ++i) flag_host[i] = FlagSlot{0.0, -1, 0};
+    void* dp = nullptr;
+    LT_CUDA(cudaHostGetDevicePointer(&dp, hp, 0));
+    flag_dev = static_cast<FlagSlot*>(dp);
+    for (int i = 0; i < kFlagRing; ++i) LT_CUDA(cudaEventCreateWithFlags(&flag_ev[i], cudaEventDisableTiming));
+  }
+  return flag_dev;
+}
+
 namespace lt {
 double available_device_bytes(lt_ctx ctx) {
   // device free memory + what the stream-ordered pool holds reserved but unused + the block
@@ -96,6 +110,10 @@ void ctx_destroy(lt_ctx ctx) {
     cudaEventDestroy(pe.stop);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->flag_host) {
+    for (auto e : ctx->flag_ev) cudaEventDestroy(e);
+    cudaFreeHost(ctx->flag_host);
+  }
   cache_release_stream(ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamDestroy(ctx->stream);

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
     const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB, LevelView L,
     const double* __restrict__ kappa, const double* __restrict__ stor, double hd, double face_scale, int n_src, int n_rec,
     int ns, const double2* __restrict__ w,
-    const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj, int ntiles, int dbg) {
+    const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj, int ntiles) {
   using G = JwGeom<DIM>;
   constexpr int NPC = G::NPC, NCH = G::NCH, KS = G::KS;
   constexpr int AF = JW_TC * 2 * (KS + 1) * 32;  // doubles per A-fragment buffer
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
     const int ptid = tid - 32 * JW_CONS;
     // face / storativity weights of tile u into wts[u & 1] (loads issued a tile ahead of use)
     auto weights = [&](int u) {
-      if ((dbg & 8) || ptid >= JW_TC * NPC || u * npair >= T) return;
+      if (ptid >= JW_TC * NPC || u * npair >= T) return;
       const TileXY g = tile_at(u * npair);
       const int c = ptid / NPC, p = ptid % NPC;
       const int i = g.i0 + c;
@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
       jw_wait(&raw_full[t % JW_NRAW], (uint32_t)((t / JW_NRAW) & 1));
       if (t >= JW_NA) jw_wait(&a_empty[t % JW_NA], (uint32_t)(((t - JW_NA) / JW_NA) & 1));
       // arrow transform: 4 lanes per (cell, shift of the pair, source), faces p - 1 = part mod 4
-      if (!(dbg & 2)) {
+      {
         const double2* rw = raw + (t % JW_NRAW) * SLOT;
         double* Ab = Af + (t % JW_NA) * AF;
         const int combo = ptid >> 2, part = ptid & 3;
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
       jw_wait(&a_full[t % JW_NA], (uint32_t)((t / JW_NA) & 1));
       const double2* rw = raw + (t % JW_NRAW) * SLOT;
       const double* Ab = Af + (t % JW_NA) * AF;
-      if (!(dbg & 1)) {
+      {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const double* Ac = Ab + c * 2 * (KS + 1) * 32;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
         jw_arrive(&a_empty[t % JW_NA]);
         jw_arrive(&raw_empty[t % JW_NRAW]);
       }
-      if (!(dbg & 4) && t % npair == npair - 1) {
+      if (t % npair == npair - 1) {
         const int64_t a = ((int64_t)g.kz * L.ny + g.j) * L.nx + g.i0;
         const bool both = g.i0 + 1 < L.nx;
 #pragma unroll
@@ -592,15 +592,9 @@ __global__ void __launch_bounds__(JW_THREADS, 1) jacobian_mma_kernel(
 // n_src <= 16, n_rec <= 64 and 32-byte aligned J rows (checked by the caller).
 constexpr int J4_TC = 4;
 // faces-only K (B operand psi_f - psi_a formed by the consumers; no centre column): 1/8 fewer
-// DMMA steps per shift pair (47.4 vs 49.6 ms per 128^3 slice); J4_NO_FACES restores the
-// centre column of the arrow transform
-#ifndef J4_NO_FACES
-#define J4_FACES 1
-#endif
-#ifndef J4_NA_BUFS
-#define J4_NA_BUFS 3
-#endif
-constexpr int J4_NRAW = 3, J4_NA = J4_NA_BUFS;
+// DMMA steps per shift pair than the arrow transform with its centre column (47.4 vs 49.6 ms per
+// 128^3 slice)
+constexpr int J4_NRAW = 3, J4_NA = 3;
 constexpr int J4_CONS = 8, J4_PROD = 4;
 constexpr int J4_THREADS = 32 * (J4_CONS + J4_PROD + 1);
 
@@ -614,7 +608,7 @@ __host__ __device__ inline int j4_slot(int B) { return j4_offF(B, DIM == 3 ? 4 :
 
 template <int DIM>
 size_t j4_smem(int B) {
-  constexpr int NPC = 2 * DIM + 1, KS = NPC;
+  constexpr int NPC = 2 * DIM + 1, KS = NPC - 1;  // faces-only K steps (+1: the storativity step)
   return sizeof(double2) * J4_NRAW * (size_t)j4_slot<DIM>(B)      // raw ring
          + sizeof(double) * J4_NA * J4_TC * 2 * ((KS + 1) * 32 + 1) // A fragments [buf][cell][mt][ks][lane] (+pad)
          + sizeof(double) * 2 * J4_TC * NPC;                       // weights [tile parity][cell][point]
@@ -633,13 +627,9 @@ __device__ __forceinline__ int j4_at(int B, int s2, int c, int p) {
 // 32-byte store with an L2 evict-first policy: J (34 GB per 128^3 slice) streams through L2
 // without evicting the field planes the neighbouring tiles still read
 __device__ __forceinline__ void stg256(double* p, double a, double b, double c, double d, uint64_t pol) {
-#ifdef J4_NO_EVICT
-  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
-#else
   asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "d"(a), "d"(b), "d"(c),
                "d"(d), "l"(pol)
                : "memory");
-#endif
 }
 
 template <int DIM>
@@ -649,17 +639,9 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     int n_rec, int ns, const double2* __restrict__ wz, double* __restrict__ Jk, double* __restrict__ Js, int64_t ldj,
     int ntiles) {
   constexpr int NPC = 2 * DIM + 1;
-#ifdef J4_FACES
   // faces only: B operand psi_f - psi_a formed by the consumers, K per shift pair 4 NF
   constexpr int NF = NPC - 1, KS = NF;
-#else
-  constexpr int KS = NPC;
-#endif
-#ifdef J4_NO_PAD
-  constexpr int MTS = (KS + 1) * 32;
-#else
   constexpr int MTS = (KS + 1) * 32 + 1;  // doubles per (cell, m tile) fragment block (+1: bank spread)
-#endif
   constexpr int AF = J4_TC * 2 * MTS;      // doubles per A-fragment buffer
   extern __shared__ __align__(128) unsigned char jsm[];
   __shared__ __align__(8) uint64_t raw_full[J4_NRAW], raw_empty[J4_NRAW], a_full[J4_NA], a_empty[J4_NA];
@@ -774,11 +756,7 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
         const double2* R = rw + min(s, B - 1);
         const double2 pa = R[j4_at(B, s2, c, 0)];
         auto put = [&](int p, double2 v) {  // A'[s][K], K = (s2 NPC + p) 2 + comp (re, -im)
-#ifdef J4_FACES
           const int K0 = (s2 * NF + p - 1) * 2;
-#else
-          const int K0 = (s2 * NPC + p) * 2;
-#endif
           Ac[(K0 >> 2) * 32 + lrow + (K0 & 3)] = v.x;
           Ac[((K0 + 1) >> 2) * 32 + lrow + ((K0 + 1) & 3)] = -v.y;
         };
@@ -789,9 +767,6 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
           a0 = cadd(a0, d);
           put(p, make_double2(-d.x, -d.y));
         }
-#ifndef J4_FACES
-        put(0, a0);
-#endif
         {  // storativity block: K = s2 2 + comp in step KS
           const double2 As = live ? cmul(wz[k], cscale(pa, wt[c * NPC])) : make_double2(0.0, 0.0);
           Ac[KS * 32 + lrow + s2 * 2] = As.x;
@@ -813,16 +788,10 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
     int offk[KS + 1];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-#ifdef J4_FACES
       const int K = ks * 4 + kq, s2 = K / (2 * NF), p = 1 + (K >> 1) % NF;
-#else
-      const int K = ks * 4 + kq, s2 = K / (2 * NPC), p = (K >> 1) % NPC;
-#endif
       offk[ks] = 2 * j4_at(B, s2, 0, p) + 2 * rcol + (K & 1);
     }
-#ifdef J4_FACES
     const int offc0 = 2 * j4_at(B, 0, 0, 0) + 2 * rcol + (kq & 1), offc1 = 2 * j4_at(B, 1, 0, 0) + 2 * rcol + (kq & 1);
-#endif
     offk[KS] = 2 * j4_at(B, kq >> 1, 0, 0) + 2 * rcol + (kq & 1);
     const int cstep = 2 * B;
     double accK[J4_TC][2][2], accS[J4_TC][2][2];  // [cell][m tile][2]
@@ -844,9 +813,7 @@ __global__ void __launch_bounds__(J4_THREADS, 1) jacobian_mma4_kernel(
 #pragma unroll
         for (int c = 0; c < J4_TC; ++c) {
           bv[c] = rw[offk[ks] + c * cstep];
-#ifdef J4_FACES
           if (ks < KS) bv[c] -= rw[((ks * 4) / (2 * NF) == 0 ? offc0 : offc1) + c * cstep];
-#endif
           a0[c] = Al[c * 2 * MTS + ks * 32];
           a1[c] = Al[c * 2 * MTS + MTS + ks * 32];
         }
@@ -1047,9 +1014,11 @@ int effective_maxit(int64_t n, int maxit, int ns) {
   return maxit > 0 ? (int)std::min<int64_t>(n, maxit) : (int)std::min<int64_t>(n, 10 * (int64_t)ns);
 }
 
-// Direct mode (solve_shifted_direct): one exact shift-and-invert solve per shift, stored as a
-// basis whose coefficient vectors select column k.
-void direct_solve(lt_pencil p, int B, const double2* b_dev, const std::vector<cd>& shifts_all, int ns,
+// Direct mode (solve_shifted_direct, cpp:324-332): one shift-and-invert solve per shift, stored
+// as a basis whose coefficient vectors select column k.  The reference's LU is exact; here each
+// solve's final relative residual is reported as the shift's true residual, and a shift whose
+// solve ended above `tol` is unconverged (the driver then raises ConvergenceError).
+void direct_solve(lt_pencil p, int B, const double2* b_dev, const std::vector<cd>& shifts_all, int ns, double tol,
                   OuterResult& res) {
   cudaStream_t st = p->ctx->stream;
   const int64_t n = p->n;
@@ -1058,7 +1027,7 @@ void direct_solve(lt_pencil p, int B, const double2* b_dev, const std::vector<cd
   res.maxit = ns;
   res.cap = ns;
   res.iterations.assign(B, 0);
-  res.status.assign((size_t)B * ns, lt_shift_status{1, 0, 0.0, 0.0});
+  res.status.assign((size_t)B * ns, lt_shift_status{1, 1, 0.0, 0.0});
   res.m_used.assign((size_t)B * ns, 0);
   res.U.clear();
   std::vector<double2> Y((size_t)B * ns * ns, make_double2(0, 0));
@@ -1066,8 +1035,10 @@ void direct_solve(lt_pencil p, int B, const double2* b_dev, const std::vector<cd
     res.U.emplace_back(sizeof(double2) * (size_t)B * n, st);
     std::vector<double2> taus(B);
     for (int b = 0; b < B; ++b) taus[b] = d2(shifts_all[(size_t)b * ns + k]);
-    inner_solve(p, B, taus.data(), b_dev, n, res.U.back().as<double2>(), n);
+    std::vector<double> rel(B, 0.0);
+    inner_solve(p, B, taus.data(), b_dev, n, res.U.back().as<double2>(), n, nullptr, rel.data());
     for (int b = 0; b < B; ++b) {
+      res.status[(size_t)b * ns + k] = lt_shift_status{rel[b] <= tol, 1, rel[b], rel[b]};
       Y[((size_t)b * ns + k) * ns + k] = make_double2(1.0, 0.0);
       res.m_used[(size_t)b * ns + k] = k + 1;
     }
@@ -1083,7 +1054,7 @@ void solve_families(lt_pencil p, const lt_solver_config& cfg, int B, const doubl
   if (cfg.kind == LT_SOLVER_DIRECT) {
     std::vector<cd> all;
     for (auto& s : shifts) all.insert(all.end(), s.begin(), s.end());
-    direct_solve(p, B, b_dev, all, ns, res);
+    direct_solve(p, B, b_dev, all, ns, cfg.tol, res);
     return;
   }
   OuterProblem prob;
@@ -1394,10 +1365,9 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   std::vector<double2> scale((size_t)B * ns, make_double2(1.0, 0.0));
   for (int s = 0; s < n_src; ++s)
     for (int k = 0; k < ns; ++k) scale[(size_t)s * ns + k] = d2(ex.rates[s] / nodes[k]);
-  // FD with <= 16 sources and <= 64 receivers: tensor-core Jacobian on cell-major fields
-  // (LT_JAC_V2=1 selects the CUDA-core kernel)
-  static const bool mma_on = std::getenv("LT_JAC_V2") == nullptr;
-  const bool tensor_jac = mma_on && p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
+  // FD with <= 16 sources and <= 64 receivers: tensor-core Jacobian on cell-major fields (the
+  // CUDA-core kernel otherwise)
+  const bool tensor_jac = p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
                           (p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B)) <= 227 * 1024;
   // tensor path: the quadrature weight w_k rides on the source fields (phi'_{s,k} = w_k phi_{s,k}),
   // which takes one complex product per A element out of the kernel's arrow transform
@@ -1468,9 +1438,8 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     const double face_scale = p->dim == 3 ? h : 1.0;
     const double hd = p->dim == 3 ? h * h * h : h * h;
     const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
-    // 4-cell tiles with 32-byte J stores where rows allow it (LT_JAC_MMA2=1 keeps 2-cell tiles)
-    static const bool mma4_on = std::getenv("LT_JAC_MMA2") == nullptr;
-    const bool tile4 = tensor_jac && mma4_on && p->view(0).nx % J4_TC == 0 && n_param % 4 == 0 && n % 4 == 0 &&
+    // 4-cell tiles with 32-byte J stores where rows allow it (2-cell tiles otherwise)
+    const bool tile4 = tensor_jac && p->view(0).nx % J4_TC == 0 && n_param % 4 == 0 && n % 4 == 0 &&
                        (reinterpret_cast<uintptr_t>(J) & 31) == 0 &&
                        (p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B)) <= 227 * 1024;
     if (tile4) {
@@ -1494,7 +1463,6 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
       if (mem != LT_MEM_DEVICE)
         LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
     } else if (tensor_jac) {
-      static const int jw_dbg = std::getenv("LT_JW_DBG") ? std::atoi(std::getenv("LT_JW_DBG")) : 0;
       LevelView L = p->view(0);
       const int ntiles = ((L.nx + JW_TC - 1) / JW_TC) * L.ny * L.nz;
       const int grid = std::min(ntiles, ctx->num_sms);
@@ -1511,7 +1479,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
       launch(ctx, "jacobian", bytes, [&] {
         fn<<<grid, JW_THREADS, smem, st>>>(mA, mB, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
                                            face_scale, n_src, n_rec, ns, nullptr, dw.as<double2>() + ns, J,
-                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles, jw_dbg);
+                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles);
       });
       if (mem != LT_MEM_DEVICE)
         LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));

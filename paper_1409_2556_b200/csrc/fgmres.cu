@@ -69,7 +69,7 @@ struct State {
   double tol;
   int variant;
   int record_history;
-  const int* active;     // B: item still iterating
+  int* active;           // B: item still iterating
   const double* beta;    // B
   const double2* shifts; // B*ns
   const double2* taus;   // B*maxit (tau applied at iteration j)
@@ -365,14 +365,6 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
   __shared__ double2 ysm[MJ][KC], yzsm[MJ][KC];
   __shared__ double nsm[KC][kT];  // per-thread running |r|^2 per shift
   LT_ITEM_BLOCK(S.B, b, cb);
-  if (threadIdx.x == 0) {
-    int c = 0;
-    for (int k = 0; k < S.ns && c < 256; ++k)
-      if (S.flag[b * S.ns + k]) flagged[c++] = k;
-    nflag = c;
-  }
-  __syncthreads();
-  if (nflag == 0) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int tpp = L.tiles_x * L.tiles_y;
   const int tile = (int)(cb % tpp), zc = (int)(cb / tpp);
@@ -381,6 +373,17 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
   int64_t a0;
   const bool in = tile_cell(L, tile, i, jj, kk, a0);  // (i, jj) of the column; plane 0
   const int64_t plane = (int64_t)L.nx * L.ny;
+  // the flagged shifts of this item, in windows of 256 shift indices
+  for (int base = 0; base < S.ns; base += 256) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int k = base; k < S.ns && k < base + 256; ++k)
+      if (S.flag[b * S.ns + k]) flagged[c++] = k;
+    nflag = c;
+  }
+  __syncthreads();
+  if (nflag == 0) continue;  // uniform
   for (int c0 = 0; c0 < nflag; c0 += KC) {
     const int nc = min(KC, nflag - c0);
     const bool staged = m <= MJ;
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
       if (lane == 0) part[((int64_t)b * S.ns + flagged[c0 + q]) * S.nblk_tile + cb] = t;
     }
   }
+  }  // window
 }
 
 // per (item, shift) flagged: true_rel; freeze or back off.  best_effort: record only.
@@ -478,12 +482,42 @@ __global__ void __launch_bounds__(kT) verify_finalize(State S, int m, const doub
   }
 }
 
-__global__ void count_unconverged(State S, int m) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= S.B) return;
-  int c = 0;
-  for (int k = 0; k < S.ns; ++k) c += !S.conv[b * S.ns + k];
-  S.n_unconv[b] = c;
+// After the freeze checks of iteration m: unconverged shifts per item; an item whose shifts
+// all froze, or that broke down, stops iterating (cpp:250-262).
+__global__ void outer_control(State S, int m, int* __restrict__ iterations) {
+  for (int b = threadIdx.x; b < S.B; b += blockDim.x) {
+    if (!S.active[b]) continue;
+    int c = 0;
+    for (int k = 0; k < S.ns; ++k) c += !S.conv[b * S.ns + k];
+    S.n_unconv[b] = c;
+    iterations[b] = m;
+    if (c == 0 || S.breakdown[b]) S.active[b] = 0;
+  }
+}
+
+// dense batch <-> item positions: to = 0: out[q] = in[idx[q]]; to = 1: out[idx[q]] = in[q]
+__global__ void __launch_bounds__(kT) pack_items(int64_t n, const int* __restrict__ idx, const double2* __restrict__ in,
+                                                 double2* __restrict__ out, int to) {
+  const int q = blockIdx.y;
+  const int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int64_t src = (to ? q : idx[q]) * n + a, dst = (to ? idx[q] : q) * n + a;
+  out[dst] = in[src];
+}
+
+// beta = ||b|| known: beta == 0 items are done, every shift converged with zero estimate and
+// residual (cpp:147-156); the others iterate.
+__global__ void outer_init(State S) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= S.B * S.ns) return;
+  const int b = t / S.ns;
+  const bool zero = !(S.beta[b] > 0.0);
+  if (t % S.ns == 0) S.active[b] = !zero;
+  if (zero) {
+    S.conv[t] = 1;
+    S.est[t] = 0.0;
+    S.true_res[t] = 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(kT) norm_kernel(int64_t n, int B, const double2* __restrict__ x, double* __restrict__ part,
@@ -738,48 +772,20 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
   launch(ctx, "fgmres_small", 0.0, [&] { reduce_beta<<<B, kT, 0, st>>>(B, nblk, partials.as<double>(), beta); });
   add_v();
   launch(ctx, "fgmres_vec", nb * 32.0, [&] { scale_to<<<grid, kT, 0, st>>>(n, B, prob.b, beta, Vc[0].as<double2>()); });
-  std::vector<double> h_beta(B);
-  LT_CUDA(cudaMemcpyAsync(h_beta.data(), beta, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  launch(ctx, "fgmres_small", 0.0, [&] { outer_init<<<blocks_for(n_bs, 128), 128, 0, st>>>(S); });
+
+  // Per outer iteration the host reads the active flags once (one small copy, after the
+  // iteration's last kernel): the next inner solve runs on the active items only, packed into a
+  // dense batch, so the two-items-per-CTA kernels never pair a live item with a finished one.
+  // The inner COCG loop itself is device-resident (inner.cu).
+  DeviceBuffer dIter(sizeof(int) * B, st);
+  LT_CUDA(cudaMemsetAsync(dIter.get(), 0, sizeof(int) * B, st));
+  int* d_iterations = dIter.as<int>();
+  std::vector<int> h_active(B, 0);
+  LT_CUDA(cudaMemcpyAsync(h_active.data(), active, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
   LT_CUDA(cudaStreamSynchronize(st));
-
-  std::vector<int> h_active(B, 1);
-  {
-    // beta == 0: every shift converged with zero estimate / residual (cpp:147-156)
-    std::vector<int> conv0(n_bs, 0);
-    std::vector<double> est0(n_bs, 0.0);
-    bool any = false;
-    for (int b = 0; b < B; ++b)
-      if (!(h_beta[b] > 0.0)) {
-        h_active[b] = 0;
-        any = true;
-        for (int k = 0; k < ns; ++k) conv0[(size_t)b * ns + k] = 1;
-      }
-    if (any) {
-      for (int b = 0; b < B; ++b)
-        if (!h_active[b])
-          for (int k = 0; k < ns; ++k) {
-            res.status[(size_t)b * ns + k] = lt_shift_status{1, 0, 0.0, 0.0};
-          }
-      LT_CUDA(cudaMemcpyAsync(conv, conv0.data(), sizeof(int) * n_bs, cudaMemcpyHostToDevice, st));
-      std::vector<double> zero(n_bs, 0.0);
-      for (int b = 0; b < B; ++b)
-        if (h_active[b])
-          for (int k = 0; k < ns; ++k) { zero[(size_t)b * ns + k] = INFINITY; }
-      LT_CUDA(cudaMemcpyAsync(est, zero.data(), sizeof(double) * n_bs, cudaMemcpyHostToDevice, st));
-      for (int b = 0; b < B; ++b)
-        if (h_active[b])
-          for (int k = 0; k < ns; ++k) zero[(size_t)b * ns + k] = NAN;
-        else
-          for (int k = 0; k < ns; ++k) zero[(size_t)b * ns + k] = 0.0;
-      LT_CUDA(cudaMemcpyAsync(true_res, zero.data(), sizeof(double) * n_bs, cudaMemcpyHostToDevice, st));
-    }
-  }
-  LT_CUDA(cudaMemcpyAsync(active, h_active.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
-
-  std::vector<int> h_brk(B, 0), h_unconv(B, 0);
   std::vector<double2> taus_j(B);
-  DeviceBuffer gather_v, gather_u;
-  int m_global = 0;
+  DeviceBuffer gather_v, gather_u, gather_idx;
   for (int j = 0; j < maxit; ++j) {
     int n_active = 0;
     for (int b = 0; b < B; ++b) n_active += h_active[b];
@@ -801,24 +807,25 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
       for (int b = 0; b < B; ++b) taus_j[b] = prob.tau_table[b][j];
       inner_solve(p, B, taus_j.data(), Vj, n, Uj, n);
     } else {
+      // pack the active items' v_j, solve, scatter u_j back (one launch each way)
+      std::vector<int> idx;
+      for (int b = 0; b < B; ++b)
+        if (h_active[b]) {
+          taus_j[idx.size()] = prob.tau_table[b][j];
+          idx.push_back(b);
+        }
       gather_v.ensure(sizeof(double2) * (size_t)n_active * n, st);
       gather_u.ensure(sizeof(double2) * (size_t)n_active * n, st);
-      int q = 0;
-      for (int b = 0; b < B; ++b) {
-        if (!h_active[b]) continue;
-        taus_j[q] = prob.tau_table[b][j];
-        LT_CUDA(cudaMemcpyAsync(gather_v.as<double2>() + (size_t)q * n, Vj + (size_t)b * n, sizeof(double2) * n,
-                                cudaMemcpyDeviceToDevice, st));
-        ++q;
-      }
+      gather_idx.ensure(sizeof(int) * B, st);
+      LT_CUDA(cudaMemcpyAsync(gather_idx.get(), idx.data(), sizeof(int) * n_active, cudaMemcpyHostToDevice, st));
+      const dim3 g2((unsigned)nblk, (unsigned)n_active);
+      launch(ctx, "fgmres_vec", (double)n * n_active * 32.0, [&] {
+        pack_items<<<g2, kT, 0, st>>>(n, gather_idx.as<int>(), Vj, gather_v.as<double2>(), 0);
+      });
       inner_solve(p, n_active, taus_j.data(), gather_v.as<double2>(), n, gather_u.as<double2>(), n);
-      q = 0;
-      for (int b = 0; b < B; ++b) {
-        if (!h_active[b]) continue;
-        LT_CUDA(cudaMemcpyAsync(Uj + (size_t)b * n, gather_u.as<double2>() + (size_t)q * n, sizeof(double2) * n,
-                                cudaMemcpyDeviceToDevice, st));
-        ++q;
-      }
+      launch(ctx, "fgmres_vec", (double)n * n_active * 32.0, [&] {
+        pack_items<<<g2, kT, 0, st>>>(n, gather_idx.as<int>(), gather_u.as<double2>(), Uj, 1);
+      });
     }
     // 2. s = M u_j into V_{j+1}; Gram-Schmidt with conditional re-orthogonalisation
     add_v();
@@ -859,19 +866,21 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
         verify_residual<2><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
     });
     launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 0); });
-    launch(ctx, "fgmres_small", 0.0, [&] { count_unconverged<<<blocks_for(B, 128), 128, 0, st>>>(S, m); });
-    LT_CUDA(cudaMemcpyAsync(h_unconv.data(), n_unconv, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaMemcpyAsync(h_brk.data(), brk, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+    launch(ctx, "fgmres_small", 0.0, [&] {
+      outer_control<<<1, 256, 0, st>>>(S, m, d_iterations);
+    });
+    LT_CUDA(cudaMemcpyAsync(h_active.data(), active, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
     LT_CUDA(cudaStreamSynchronize(st));
-    m_global = m;
-    bool changed = false;
-    for (int b = 0; b < B; ++b) {
-      if (!h_active[b]) continue;
-      res.iterations[b] = m;
-      if (h_unconv[b] == 0 || h_brk[b]) { h_active[b] = 0; changed = true; }
-    }
-    if (changed) LT_CUDA(cudaMemcpyAsync(active, h_active.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
   }
+  std::vector<double> h_beta(B);
+  std::vector<int> h_brk(B, 0), h_unconv(B, 0);
+  LT_CUDA(cudaMemcpyAsync(h_beta.data(), beta, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(res.iterations.data(), d_iterations, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_unconv.data(), n_unconv, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaMemcpyAsync(h_brk.data(), brk, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  int m_global = 0;
+  for (int b = 0; b < B; ++b) m_global = std::max(m_global, res.iterations[b]);
   res.cap = maxit;
 
   // best-effort iterates for unconverged shifts (cpp:270-285), at each item's own m
@@ -970,8 +979,9 @@ void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_
   for (int v : res.m_used) mmax = std::max(mmax, v);
   constexpr int kCT = 32;
   const size_t ys_bytes = sizeof(double2) * (size_t)ns * std::max(mmax, 1) * B;
-  static const bool cm2_on = std::getenv("LT_EXPAND_V1") == nullptr;
-  if (cell_major && cm2_on && mmax >= 1 && mmax <= 8 && mmax <= ncols && ys_bytes <= 110 * 1024) {
+  // cell-major v2 (coefficients staged in shared memory) up to 8 basis columns; the v1 kernel
+  // (per-shift shared-memory transpose) for longer bases
+  if (cell_major && mmax >= 1 && mmax <= 8 && mmax <= ncols && ys_bytes <= 110 * 1024) {
     DeviceBuffer ys(ys_bytes, st);
     const int ny = ns * mmax * B;
     expand_coeffs<<<(unsigned)((ny + 255) / 256), 256, 0, st>>>(B, ns, res.maxit, mmax, res.Y.as<double2>(),

@@ -60,6 +60,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 template <>
+__device__ __forceinline__ int warp_sum(int v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffff, v, o);
+  return v;
+}
+template <>
 __device__ __forceinline__ double2 warp_sum(double2 v) {
   for (int o = 16; o > 0; o >>= 1) {
     v.x += __shfl_down_sync(0xffffffff, v.x, o);
@@ -103,6 +108,13 @@ struct Batch {
   int i, j, k;                              \
   int64_t a;                                \
   const bool in = tile_cell(LV, cb, i, j, k, a);
+
+// Grid-stride COCG vector kernels: G = gridDim.x / B blocks per item (a few per SM in total,
+// chunk_vec_blocks), so a launch over finished items costs G blocks per item, not n / 256.
+#define ITEM_GRID_PROLOGUE                                        \
+  LT_ITEM_BLOCK(bt.B, b, cb)                                      \
+  if (bt.done[b]) return;                                         \
+  const int64_t stride_ = (int64_t)(gridDim.x / bt.B) * blockDim.x;
 
 #define ITEM_PROLOGUE(n)                                          \
   LT_ITEM_BLOCK(bt.B, b, cb)                                      \
@@ -225,14 +237,14 @@ __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, cons
                                                        double2* __restrict__ r, VM* __restrict__ rmg,
                                                        double2* __restrict__ u, int64_t us, double* __restrict__ part,
                                                        int nblk, int snx, int sny) {
-  ITEM_PROLOGUE(n);
+  ITEM_GRID_PROLOGUE
   double s = 0.0;
-  if (in) {
+  for (int64_t a = cb * (int64_t)blockDim.x + threadIdx.x; a < n; a += stride_) {
     const double2 x = v[b * vs + a];
     r[b * n + a] = x;
     rmg[b * n + rb_flat(a, snx, sny)] = vfrom<VM>(x);
     u[b * us + a] = make_double2(0.0, 0.0);
-    s = cabs2(x);
+    s += cabs2(x);
   }
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
@@ -242,9 +254,10 @@ __global__ void __launch_bounds__(kT) copy_norm_kernel(int64_t n, Batch bt, cons
 __global__ void __launch_bounds__(kT) bdot_kernel(int64_t n, Batch bt, const double2* __restrict__ x,
                                                   const VM* __restrict__ y, double2* __restrict__ part, int nblk,
                                                   int snx, int sny) {
-  ITEM_PROLOGUE(n);
+  ITEM_GRID_PROLOGUE
   double2 s = make_double2(0.0, 0.0);
-  if (in) s = cmul(x[b * n + a], vto(y[b * n + rb_flat(a, snx, sny)]));
+  for (int64_t a = cb * (int64_t)blockDim.x + threadIdx.x; a < n; a += stride_)
+    s = cfma(x[b * n + a], vto(y[b * n + rb_flat(a, snx, sny)]), s);
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
 }
@@ -1862,296 +1875,18 @@ __global__ void __launch_bounds__(kTP) prolong_tma_kernel(const __grid_constant_
   // the coarse planes still held: release so the producer is never left waiting (it is done)
 }
 
-// ---- fused residual + restriction (colour-split fine level, aggregation 2 x 2 x 2) -------
-// f_c = P^T (f - A x) without the fine residual ever reaching HBM.  A CTA owns the coarse
-// cells over its fine tile (32 positions = 32 coarse x, 8 rows = 4 coarse rows, ZM_ZC planes
-// = ZM_ZC / 2 coarse planes).  Per fine plane p it forms the residual of both colours on the
-// tile plus its one-cell ring (positions m0-1 .. m0+32, rows y0-1 .. y0+8: the x / y support of
-// the restriction), one warp per row, into a double-buffered plane of natural-order cell pairs;
-// after one barrier four warps reduce it in x and y for their coarse (I, J) and add it to the
-// z register ring of the pair restriction.  Each residual plane costs one barrier; the ring
-// cells are recomputed by the neighbouring CTAs (x and f are read with a 2-cell halo).
-constexpr int RR_NW = RB_H + 2;                                // consumer warps = residual rows
-constexpr int RR_XP = RB_P + 4, RR_XR = RB_H + 4;              // x: positions m0-2 .. m0+33, rows y0-2 .. y0+9
-constexpr int RR_FP = RB_P + 4, RR_FR = RB_H + 2;              // f: positions m0-2 .. m0+33, rows y0-1 .. y0+8
-constexpr int RR_CP = RB_P + 8, RR_CR = RB_H + 3;              // coef: positions m0-4 .. m0+35, rows y0-1 .. y0+9
-constexpr uint32_t RR_XB = sizeof(float2) * RR_XP * 2 * RR_XR;  // 6912
-constexpr uint32_t RR_FB = sizeof(float2) * RR_FP * 2 * RR_FR;  // 5760
-constexpr uint32_t RR_CB = sizeof(float) * RR_CP * 2 * 4 * RR_CR;  // 14080
-constexpr uint32_t RR_OFF_F = (RR_XB + 127) / 128 * 128, RR_OFF_C = (RR_OFF_F + RR_FB + 127) / 128 * 128;
-constexpr uint32_t RR_SLOT = (RR_OFF_C + RR_CB + 127) / 128 * 128;
-#ifndef LT_RR_D
-#define LT_RR_D 4
-#endif
-constexpr int RR_D = LT_RR_D;
-constexpr int RR_RP = RB_P + 2;                                  // residual pairs per row: m0-1 .. m0+32
-constexpr uint32_t RR_RB = sizeof(float4) * RR_RP * RR_NW;       // one residual plane
-constexpr size_t RR_SMEM = (size_t)RR_SLOT * RR_D + 2 * RR_RB;
-constexpr int kRR = 32 * RR_NW + 32;
-
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-__global__ void __launch_bounds__(kRR, 1) mg_resrestrict_kernel(const __grid_constant__ CUtensorMap mx,
-                                                               const __grid_constant__ CUtensorMap mf,
-                                                               const __grid_constant__ CUtensorMap mc, TzDims L,
-                                                               LevelViewT<float> Lc, Batch bt,
-                                                               const double2* __restrict__ taus, float2* __restrict__ fc) {
-  extern __shared__ __align__(128) unsigned char rr_smem[];
-  __shared__ __align__(8) uint64_t full[RR_D], empty[RR_D];
-  LT_ITEM_BLOCK(bt.B, b, cb);
-  if (bt.done[b]) return;
-  const int nh = L.nx >> 1;
-  const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
-  const int ntile = tiles_x * tiles_y;
-  const int tile = cb % ntile, chunk = cb / ntile;
-  const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
-  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);  // k0 even
-  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  float4* Rbuf = reinterpret_cast<float4*>(rr_smem + (size_t)RR_SLOT * RR_D);  // [2][RR_NW][RR_RP]
-  if (tid == 0) {
-    for (int s = 0; s < RR_D; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], RR_NW);
-    }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
-  // residual planes k0-1 .. pl (pl = k1, or nz - 1 on the last chunk); loads: x for
-  // k0-2 .. pl+1 (ring index p - (k0 - 2)), f for the residual planes, coefficients k0-1 .. pl+1
-  const int pl = min(k1, L.nz - 1);
-  const int pb = k0 - 2, pe = pl + 1;
-  if (wy == RR_NW) {  // producer warp
-    if (lane == 0) {
-      int sl = 0, use = 0;
-      for (int p = pb; p <= pe; ++p) {
-        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
-        unsigned char* sp = rr_smem + (size_t)sl * RR_SLOT;
-        const bool lf = p >= k0 - 1 && p <= pl, lc = p >= k0 - 1;
-        mbar_arrive_tx(&full[sl], RR_XB + (lf ? RR_FB : 0u) + (lc ? RR_CB : 0u));
-        tma_load5(sp, &mx, m0 - 2, 0, y0 - 2, p, b, &full[sl]);
-        if (lf) tma_load5(sp + RR_OFF_F, &mf, m0 - 2, 0, y0 - 1, p, b, &full[sl]);
-        if (lc) tma_load5(sp + RR_OFF_C, &mc, m0 - 4, 0, 0, y0 - 1, p, &full[sl]);
-        if (++sl == RR_D) { sl = 0; ++use; }
-      }
-    }
-    return;
-  }
-  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
-  const int j = y0 - 1 + wy;  // this warp's residual row
-  // restriction threads: warps 0..3, coarse (I, J) = (m0 + lane, y0 / 2 + wy)
-  const int I = m0 + lane, J = (y0 >> 1) + wy;
-  const bool rthread = wy < RB_H / 2;
-  const bool own = rthread && I < Lc.nx && J < Lc.ny;
-  const float wxm = I > 0 ? 0.25f : 0.f, wx0 = I == 0 ? 0.5f : 0.75f;
-  const float wx1 = I == Lc.nx - 1 ? 0.5f : 0.75f, wxp = I < Lc.nx - 1 ? 0.25f : 0.f;
-  const float wyv[4] = {J > 0 ? 0.25f : 0.f, J == 0 ? 0.5f : 0.75f, J == Lc.ny - 1 ? 0.5f : 0.75f,
-                        J < Lc.ny - 1 ? 0.25f : 0.f};
-  float2* fcb = fc + (int64_t)b * Lc.n;
-  float2 sa = make_float2(0.f, 0.f), sb = sa, sc = sa;
-  // ring slots of planes p - 1, p, p + 1 (p = residual plane)
-  int qm = 0, q0 = 1, qu = 2;
-  uint32_t pu = 0;
-  mbar_wait_u32(full0 + 8 * qm, 0);
-  mbar_wait_u32(full0 + 8 * q0, 0);
-  int buf = 0;
-  for (int p = k0 - 1; p <= pl; ++p) {
-    mbar_wait_u32(full0 + 8 * qu, pu);
-    const unsigned char* sm = rr_smem + (size_t)qm * RR_SLOT;
-    const unsigned char* s0 = rr_smem + (size_t)q0 * RR_SLOT;
-    const unsigned char* su = rr_smem + (size_t)qu * RR_SLOT;
-    float4* R = Rbuf + buf * (RR_NW * RR_RP);
-    // ---- residual of row j, positions m0-1 .. m0+32 (two passes: lanes, then lanes 0, 1)
-    const bool pin = p >= 0 && p < L.nz && j >= 0 && j < L.ny;
-    for (int e = lane; e < RR_RP; e += 32) {
-      const int m = m0 - 1 + e;
-      float2 rc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      if (pin && m >= 0 && m < nh) {
-        const int rx = j - (y0 - 2), q = m - (m0 - 2), rf = j - (y0 - 1), qc = m - (m0 - 4);
-        auto X = [&](const unsigned char* sl, int rr, int h, int qq) {
-          return reinterpret_cast<const float2*>(sl)[(rr * 2 + h) * RR_XP + qq];
-        };
-        auto C = [&](const unsigned char* sl, int rr, int comp, int h, int qq) {
-          return reinterpret_cast<const float*>(sl + RR_OFF_C)[((rr * 4 + comp) * 2 + h) * RR_CP + qq];
-        };
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int s = (j + p + c) & 1, o = c ^ 1;
-          const float tw = C(s0, rf, 0, c, qc), ts = C(s0, rf, 1, c, qc), tb = C(s0, rf, 2, c, qc);
-          const float mm = C(s0, rf, 3, c, qc);
-          const float te = C(s0, rf, 0, o, qc + s), tn = C(s0, rf + 1, 1, o, qc), tt = C(su, rf, 2, o, qc);
-          const float2 w = X(s0, rx, o, q - 1 + s), ee = X(s0, rx, o, q + s);
-          const float2 so = X(s0, rx - 1, o, q), no = X(s0, rx + 1, o, q);
-          const float2 dn = X(sm, rx, o, q), up = X(su, rx, o, q);
-          const float ox = tw * w.x + te * ee.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
-          const float oy = tw * w.y + te * ee.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
-          const float2 xa = X(s0, rx, c, q);
-          const float2 f = reinterpret_cast<const float2*>(s0 + RR_OFF_F)[(rf * 2 + c) * RR_FP + q];
-          const float dk = tw + te + ts + tn + tb + tt;
-          const float dr = dk + tr * mm, di = ti * mm;
-          rc[s] = make_float2(f.x - (dr * xa.x - di * xa.y - ox), f.y - (dr * xa.y + di * xa.x - oy));
-        }
-      }
-      R[wy * RR_RP + e] = make_float4(rc[0].x, rc[0].y, rc[1].x, rc[1].y);  // (cell 2m, cell 2m + 1)
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // plane p - 1 is done
-    named_bar(1, 32 * RR_NW);
-    // ---- x / y reduction of plane p for (I, J), z ring
-    if (rthread) {
-      float2 S = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int rr = 2 * wy + r;  // local residual row of fine row 2J - 1 + r
-        const float4 c0 = R[rr * RR_RP + lane + 1], cmv = R[rr * RR_RP + lane], cpv = R[rr * RR_RP + lane + 2];
-        float2 xr = make_float2(0.f, 0.f);
-        xr = f2fma(wxm, make_float2(cmv.z, cmv.w), xr);
-        xr = f2fma(wx0, make_float2(c0.x, c0.y), xr);
-        xr = f2fma(wx1, make_float2(c0.z, c0.w), xr);
-        xr = f2fma(wxp, make_float2(cpv.x, cpv.y), xr);
-        S = f2fma(wyv[r], xr, S);
-      }
-      if (p < k0) {
-        sa = S;
-      } else if (p == k0) {
-        sb = S;
-      } else {
-        const bool odd = p & 1;
-        const int K = odd ? (p - 1) >> 1 : (p >> 1) - 1;
-        if (odd) sc = S;
-        if (!odd || K == Lc.nz - 1) {
-          const float2 sd = odd ? make_float2(0.f, 0.f) : S;
-          float2 v = make_float2(0.f, 0.f);
-          v = f2fma(K > 0 ? 0.25f : 0.f, sa, v);
-          v = f2fma(K == 0 ? 0.5f : 0.75f, sb, v);
-          v = f2fma(K == Lc.nz - 1 ? 0.5f : 0.75f, sc, v);
-          v = f2fma(K < Lc.nz - 1 ? 0.25f : 0.f, sd, v);
-          if (own && K < Lc.nz) fcb[rb_index(Lc, I, J, K)] = v;
-          sa = sc;
-          sb = sd;
-        }
-      }
-    }
-    buf ^= 1;
-    qm = q0;
-    q0 = qu;
-    if (++qu == RR_D) { qu = 0; pu ^= 1u; }
-  }
-}
-
 // FP64 operator tiles: 32 x 8 cells, one per thread (warp = one row of 32 cells).  The
 // coefficients come planar (Level::pack64: [k][j][W, S, B, M][i]), so every coefficient read
 // of a warp is one contiguous 256-byte run, and the in-row neighbours of p come from the
 // adjacent lanes: the interleaved {W, S, B, M} records made each coefficient read 8 shared
 // wavefronts and bound the kernel by shared memory at ~3.4 TB/s.
-#ifndef LT_TA_H
-#define LT_TA_H 8
-#endif
-constexpr int TA_W = 32, TA_H = LT_TA_H;  // one consumer warp per row
+constexpr int TA_W = 32, TA_H = 8;  // one consumer warp per row
 constexpr int kTA = 32 * TA_H + 32;        // + the producer warp
 constexpr int TA_XW = TA_W + 2, TA_XH = TA_H + 2;  // p: x0-1 .. x0+32, y0-1 .. y0+8
 constexpr int TA_CW = TA_W + 2, TA_CH = TA_H + 1;  // coefficients x0 .. x0+33 (x0+32 used), y0 .. y0+8
-#ifndef LT_TA_D
-#define LT_TA_D 6
-#endif
-constexpr int TA_D = LT_TA_D;  // ring depth: 3 live planes + 3 in flight
 constexpr uint32_t TA_XB = sizeof(double2) * TA_XW * TA_XH;     // 5440 (TA_H = 8)
 constexpr uint32_t TA_CB = sizeof(double) * 4 * TA_CW * TA_CH;  // 9792
 constexpr uint32_t TA_OFF_C = (TA_XB + 127) / 128 * 128, TA_SLOT = (TA_OFF_C + TA_CB + 127) / 128 * 128;
-constexpr size_t TA_SMEM = (size_t)TA_SLOT * TA_D;
-
-// q = A(tau) p, partial p^T q (FP64)
-__global__ void __launch_bounds__(kTA, TA_H > 8 ? 1 : (TA_D <= 4 ? 3 : 2)) apply_tma_kernel(const __grid_constant__ CUtensorMap mp,
-                                                           const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
-                                                           const double2* __restrict__ taus, double2* __restrict__ q,
-                                                           double2* __restrict__ part, int nblk) {
-  extern __shared__ __align__(128) unsigned char ta_smem[];
-  __shared__ __align__(8) uint64_t full[TA_D], empty[TA_D];
-  LT_ITEM_BLOCK(bt.B, b, cb);
-  if (bt.done[b]) return;
-  const int tiles_x = (L.nx + TA_W - 1) / TA_W, tiles_y = (L.ny + TA_H - 1) / TA_H;
-  const int ntile = tiles_x * tiles_y;
-  const int tile = cb % ntile, chunk = cb / ntile;
-  const int x0 = (tile % tiles_x) * TA_W, y0 = (tile / tiles_x) * TA_H;
-  const int k0 = chunk * ZM_ZC, k1 = min(L.nz, k0 + ZM_ZC);
-  const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < TA_D; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], TA_H);
-    }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
-  double2 acc = make_double2(0.0, 0.0);
-  if (wy == TA_H) {  // producer warp
-    if (lane == 0) {
-      int sl = 0, use = 0;
-      for (int p = k0 - 1; p <= k1; ++p) {
-        if (use > 0) mbar_wait(&empty[sl], (uint32_t)((use - 1) & 1));
-        unsigned char* sp = ta_smem + (size_t)sl * TA_SLOT;
-        const bool lc = p >= k0;
-        mbar_arrive_tx(&full[sl], TA_XB + (lc ? TA_CB : 0u));
-        tma_load4(sp, &mp, 2 * (x0 - 1), y0 - 1, p, b, &full[sl]);
-        if (lc) tma_load4(sp + TA_OFF_C, &mc, x0, 0, y0, p, &full[sl]);
-        if (++sl == TA_D) { sl = 0; ++use; }
-      }
-    }
-  } else {
-    const int i = x0 + lane, j = y0 + wy;
-    const bool in = i < L.nx && j < L.ny;
-    const double2 tau = taus[b];
-    const int64_t plane = (int64_t)L.nx * L.ny;
-    double2* qb = q + (int64_t)b * L.n;
-    int qm = 0, q0 = 1, qu = 2;
-    uint32_t pu = 0;
-    mbar_wait_u32(full0 + 8 * qm, 0);
-    mbar_wait_u32(full0 + 8 * q0, 0);
-    for (int k = k0; k < k1; ++k) {
-      mbar_wait_u32(full0 + 8 * qu, pu);
-      const unsigned char* sm = ta_smem + (size_t)qm * TA_SLOT;
-      const unsigned char* s0 = ta_smem + (size_t)q0 * TA_SLOT;
-      const unsigned char* sp = ta_smem + (size_t)qu * TA_SLOT;
-      auto X = [](const unsigned char* sl, int yy, int xx) {
-        return reinterpret_cast<const double2*>(sl)[yy * TA_XW + xx];
-      };
-      auto C = [](const unsigned char* sl, int comp, int yy, int xx) {
-        return reinterpret_cast<const double*>(sl + TA_OFF_C)[(yy * 4 + comp) * TA_CW + xx];
-      };
-      // the row's centre values for every lane; in-row neighbours by shuffle
-      const double2 pc = X(s0, wy + 1, lane + 1);
-      double2 w, e;
-      w.x = __shfl_up_sync(0xffffffffu, pc.x, 1);
-      w.y = __shfl_up_sync(0xffffffffu, pc.y, 1);
-      e.x = __shfl_down_sync(0xffffffffu, pc.x, 1);
-      e.y = __shfl_down_sync(0xffffffffu, pc.y, 1);
-      if (lane == 0) w = X(s0, wy + 1, 0);
-      if (lane == 31) e = X(s0, wy + 1, TA_XW - 1);
-      if (in) {
-        const double tw = C(s0, 0, wy, lane), ts = C(s0, 1, wy, lane), tb = C(s0, 2, wy, lane);
-        const double mm = C(s0, 3, wy, lane);
-        const double te = C(s0, 0, wy, lane + 1), tn = C(s0, 1, wy + 1, lane), tt = C(sp, 2, wy, lane);
-        const double2 so = X(s0, wy, lane + 1), no = X(s0, wy + 2, lane + 1);
-        const double2 dn = X(sm, wy + 1, lane + 1), up = X(sp, wy + 1, lane + 1);
-        const double dk = tw + te + ts + tn + tb + tt;
-        const double ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
-        const double oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
-        const double dr = dk + tau.x * mm, di = tau.y * mm;
-        const double2 qa = make_double2(dr * pc.x - di * pc.y - ox, dr * pc.y + di * pc.x - oy);
-        qb[k * plane + (int64_t)j * L.nx + i] = qa;
-        acc = cfma(pc, qa, acc);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);
-      qm = q0;
-      q0 = qu;
-      if (++qu == TA_D) { qu = 0; pu ^= 1u; }
-    }
-  }
-  acc = block_sum(acc);
-  if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = acc;
-}
 
 // The same operator on two items per CTA: the coefficient tiles (9.8 KB per plane, 64% of a
 // one-item slot) are brought in once for both items and every coefficient-derived register is
@@ -2280,8 +2015,6 @@ struct TzMaps {
   CUtensorMap x, f, c;
   bool rb = false;                // colour-split level: the mg_rb kernels and maps below
   CUtensorMap rx0, rx1, rf1, rf2, rc;  // x (one / both colours), f (one / both), coefficients
-  bool rr = false;                // ... and the fused residual + restriction (agg 2 x 2 x 2)
-  CUtensorMap rrx, rrf, rrc;
   CUtensorMap rt;                 // the residual's tiles for restrict_tma_kernel
   bool pt = false, pt_csplit = false;  // prolong_tma_kernel onto this level (coarse level split?)
   CUtensorMap ptf, ptc;           // fine x tiles, coarse e tiles
@@ -2310,13 +2043,14 @@ __global__ void __launch_bounds__(kT) axpy_norm_kernel(int64_t n, Batch bt, cons
                                                        const double2* __restrict__ q, double2* __restrict__ r,
                                                        VM* __restrict__ rmg, double* __restrict__ part, int nblk,
                                                        int snx, int sny) {
-  ITEM_PROLOGUE(n);
+  ITEM_GRID_PROLOGUE
+  const double2 al = alpha[b];
   double s = 0.0;
-  if (in) {
-    const double2 ra = csub(r[b * n + a], cmul(alpha[b], q[b * n + a]));
+  for (int64_t a = cb * (int64_t)blockDim.x + threadIdx.x; a < n; a += stride_) {
+    const double2 ra = csub(r[b * n + a], cmul(al, q[b * n + a]));
     r[b * n + a] = ra;
     rmg[b * n + rb_flat(a, snx, sny)] = vfrom<VM>(ra);
-    s = cabs2(ra);
+    s += cabs2(ra);
   }
   s = block_sum(s);
   if (threadIdx.x == 0) part[(int64_t)b * nblk + cb] = s;
@@ -2328,17 +2062,19 @@ __global__ void __launch_bounds__(kT) pupdate_kernel(int64_t n, Batch bt, const 
                                                      const double2* __restrict__ beta, const VM* __restrict__ z,
                                                      double2* __restrict__ p, double2* __restrict__ u, int64_t us,
                                                      int first, int snx, int sny) {
-  ITEM_PROLOGUE(n);
-  if (!in) return;
-  const double2 za = vto(z[b * n + rb_flat(a, snx, sny)]);
-  if (first) {
-    p[b * n + a] = za;
-    return;
+  ITEM_GRID_PROLOGUE
+  const double2 al = alpha[b], be = beta[b];
+  for (int64_t a = cb * (int64_t)blockDim.x + threadIdx.x; a < n; a += stride_) {
+    const double2 za = vto(z[b * n + rb_flat(a, snx, sny)]);
+    if (first) {
+      p[b * n + a] = za;
+      continue;
+    }
+    const double2 pa = p[b * n + a];
+    double2* ua = u + b * us + a;
+    *ua = cfma(al, pa, *ua);
+    p[b * n + a] = cfma(be, pa, za);
   }
-  const double2 pa = p[b * n + a];
-  double2* ua = u + b * us + a;
-  *ua = cfma(alpha[b], pa, *ua);
-  p[b * n + a] = cfma(beta[b], pa, za);
 }
 
 // u += alpha p for the items whose last update is still pending (mask)
@@ -2560,17 +2296,11 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   LevelViewT<R> Lc = mg_view<R>(p, l + 1);
   Lc.split = tz && tz[l + 1].rb;
   const Level& lev = *p->levels[l];
-  // red-black sweeps per pre/post smoothing (LT_MG_NU, default 2)
   // red-black sweeps per pre/post smoothing, by level: 2 on the finest, 4 on the next, 8 on
-  // the coarser ones (LT_MG_NU0 / LT_MG_NU1 / LT_MG_NU override).  Convergence is set by the
-  // coarse levels' smoothing, while their sweeps are cheap: at configs[4] (80 items) this
-  // takes the inner solve from 17 to 12 COCG iterations, 194 -> 163 ms; more finest-level
-  // sweeps do not reduce the count, fewer raise it
-  auto env_nu = [](const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::max(1, std::atoi(e)) : dflt;
-  };
-  static const int nu0 = env_nu("LT_MG_NU0", 2), nu1 = env_nu("LT_MG_NU1", 4), nu_c = env_nu("LT_MG_NU", 8);
+  // the coarser ones.  Convergence is set by the coarse levels' smoothing, while their sweeps
+  // are cheap: at configs[4] (80 items) this takes the inner solve from 17 to 12 COCG
+  // iterations, 194 -> 163 ms; more finest-level sweeps do not reduce the count, fewer raise it
+  constexpr int nu0 = 2, nu1 = 4, nu_c = 8;
   const int nu = l == 0 ? nu0 : l == 1 ? nu1 : nu_c;
   // half sweeps on cell pairs when the rows have even length, else one cell per thread
   const bool pairs = (L.nx & 1) == 0;
@@ -2606,15 +2336,6 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     half(0, 0, nullptr);
     half(1, 0, nullptr);
   }
-  const bool rrk = rbk && tz[l].rr && std::is_same<R, float>::value && DIM == 3;
-  if (rrk) {
-    // r = f - A x restricted on the fly: x and f read once, only the coarse f written
-    launch(ctx, "mg_residual", cell_bytes * 2.125 * vb + coef, [&] {
-      if constexpr (std::is_same<R, float>::value)
-        mg_resrestrict_kernel<<<rgrid, kRR, RR_SMEM, st>>>(tz[l].rrx, tz[l].rrf, tz[l].rrc, tdims, Lc, bt, taus,
-                                                          (float2*)F[l + 1]);
-    });
-  } else
   launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
       mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
@@ -2630,14 +2351,11 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
       residual_kernel<R, DIM><<<(unsigned)L.ntiles * (unsigned)Bc, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
   });
   // pair transfers for aggregation 2 in every direction (3-D, FP32 V-cycle)
-  static const bool pair_on = std::getenv("LT_ZM_TRANSFER") == nullptr;
-  static const bool rt_on = std::getenv("LT_PAIR_RESTRICT") == nullptr;  // TMA restriction from colour-split levels
-  const bool ptr = pair_on && std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
+  const bool ptr = std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
                    lev.agg[2] == 2 && (L.nx & 1) == 0;
-  if (!rrk)
   launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
-      if (ptr && rbk && rt_on) {
+      if (ptr && rbk) {
         const unsigned g = (unsigned)(((Lc.nx + 31) / 32) * ((Lc.ny + 3) / 4) * ((Lc.nz + RT_ZC - 1) / RT_ZC));
         restrict_tma_kernel<<<g * Bc, kRT, RT_SMEM, st>>>(tz[l].rt, tdims, Lc, bt, (float2*)F[l + 1]);
         return;
@@ -2685,9 +2403,82 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   return X[l];
 }
 
+// Device-resident COCG control (one block): items masked out by the caller start done.
+__global__ void cocg_mask_kernel(int B, const int* __restrict__ active, int* __restrict__ done) {
+  for (int b = threadIdx.x; b < B; b += blockDim.x) done[b] = active ? !active[b] : 0;
+}
+
+// After ||v||^2: items with a zero right-hand side are done with u = 0; stagnation state.
+__global__ void cocg_init_kernel(int B, int* __restrict__ done, int* __restrict__ zero, const double* __restrict__ bb,
+                                 double* __restrict__ rr, double* __restrict__ best, int* __restrict__ stall,
+                                 int* __restrict__ pending, int* __restrict__ counts) {
+  int cnt = 0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int z = !done[b] && !(bb[b] > 0.0);
+    zero[b] = z;
+    if (z) { done[b] = 1; rr[b] = 0.0; }
+    best[b] = bb[b];
+    stall[b] = 0;
+    pending[b] = 0;
+    cnt += !done[b];
+  }
+  cnt = block_sum(cnt);
+  if (counts && threadIdx.x == 0) counts[0] = cnt;
+}
+
+// block-wide max, valid in thread 0
+__device__ __forceinline__ double block_max(double v) {
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffff, v, o));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = lane < (int)((blockDim.x + 31) >> 5) ? sh[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffff, v, o));
+  }
+  return v;
+}
+
+// Per iteration, after ||r||^2: converged at ||r|| <= tol ||v||; stagnated at the rounding
+// floor (within 1e4 of the tolerance and no halving of the residual in 6 iterations; far from
+// the floor COCG's residual is non-monotone on the indefinite pencils Re tau < 0 gives, so
+// plateaus there are not stagnation).  An item stopping here still owes its deferred u += alpha p
+// (pending).  The count of items still iterating and the worst remaining ratio to the tolerance
+// go to the host through mapped pinned memory, slot (*counter)++ % ring, which the host reads an
+// iteration later (no pipeline drain); counts (profiling only) keeps the whole count sequence
+// for the byte accounting.
+__global__ void cocg_control_kernel(int B, int* __restrict__ done, const double* __restrict__ rr,
+                                    const double* __restrict__ bb, double* __restrict__ best, int* __restrict__ stall,
+                                    int* __restrict__ pending, double tol2, int* __restrict__ counter,
+                                    volatile FlagSlot* __restrict__ host_ring, int ring, int* __restrict__ counts) {
+  int cnt = 0;
+  double worst = 0.0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (done[b]) continue;
+    const double r = rr[b], lim = tol2 * bb[b];
+    bool stop = r <= lim;
+    if (!stop) {
+      if (r < 0.25 * best[b]) { best[b] = r; stall[b] = 0; }
+      else if (r <= 1e8 * lim && ++stall[b] >= 6) stop = true;
+    }
+    if (stop) { done[b] = 1; pending[b] = 1; }
+    else { ++cnt; worst = fmax(worst, r / lim); }
+  }
+  cnt = block_sum(cnt);
+  worst = block_max(worst);
+  if (threadIdx.x == 0) {
+    const int s = *counter;
+    *counter = s + 1;
+    host_ring[s % ring].worst = worst;
+    host_ring[s % ring].active = cnt;
+    if (counts) counts[s + 1] = cnt;
+  }
+}
+
 template <int DIM>
 void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v, int64_t vs, double2* u,
-                 int64_t us) {
+                 int64_t us, const int* active, double* rel_out) {
   using R = MgReal;
   using V = VM;
   lt_ctx ctx = p->ctx;
@@ -2707,9 +2498,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
   const int64_t inv_ld = fp64 ? 2 * nc : nc, inv_off = fp64 ? nc : 0;
 
-  // small per-item state: taus, inverse pointers, done flags, scalars
-  const size_t small_bytes = sizeof(double2) * Bc * 4 + sizeof(double) * Bc * 2 + sizeof(void*) * Bc +
-                             sizeof(int) * Bc + 64;
+  // small per-item state: taus, scalars, inverse pointers, control flags
+  const size_t small_bytes = sizeof(double2) * Bc * 4 + sizeof(double) * Bc * 3 + sizeof(void*) * Bc +
+                             sizeof(int) * (Bc * 5 + 1) + 64;
   DeviceBuffer small(small_bytes, st);
   char* sp = small.as<char>();
   double2* d_taus = reinterpret_cast<double2*>(sp);
@@ -2718,11 +2509,16 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   double2* d_beta = d_alpha + Bc;
   double* d_bb = reinterpret_cast<double*>(d_beta + Bc);
   double* d_rr = d_bb + Bc;
-  const V** d_inv = reinterpret_cast<const V**>(d_rr + Bc);
+  double* d_best = d_rr + Bc;
+  const V** d_inv = reinterpret_cast<const V**>(d_best + Bc);
   int* d_done = reinterpret_cast<int*>(d_inv + Bc);
+  int* d_zero = d_done + Bc;
+  int* d_stall = d_zero + Bc;
+  int* d_pending = d_stall + Bc;
+  int* d_counter = d_pending + Bc;
   LT_CUDA(cudaMemcpyAsync(d_taus, taus_host, sizeof(double2) * Bc, cudaMemcpyHostToDevice, st));
   LT_CUDA(cudaMemcpyAsync(d_inv, inv_host.data(), sizeof(void*) * Bc, cudaMemcpyHostToDevice, st));
-  LT_CUDA(cudaMemsetAsync(d_done, 0, sizeof(int) * Bc, st));
+  LT_CUDA(cudaMemsetAsync(d_counter, 0, sizeof(int), st));
   Scalars sc{d_bb, d_rr, d_rho, d_alpha, d_beta};
   Batch bt{Bc, d_done};
 
@@ -2747,23 +2543,19 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   V* rmg = F[0];  // the multigrid copy of the COCG residual
 
   // TMA tensor maps (FD levels with even rows of >= 64 cells; FP32 V-cycle only) and the
-  // FP64 operator's maps on the finest level.  LT_NO_TMA=1 selects the register-pipelined
-  // kernels instead.
-  static const bool tma_on = std::getenv("LT_NO_TMA") == nullptr;
-  static const bool rb_on = std::getenv("LT_NO_RB") == nullptr;  // colour-split levels
+  // FP64 operator's maps on the finest level; the other levels run the register-pipelined
+  // z-march kernels
   std::vector<TzMaps> tzm(nl);
-  if (tma_on) {
+  {
     static bool attr = false;
     if (!attr) {
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
-      LT_CUDA(cudaFuncSetAttribute(apply_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA2_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<0, RB_NI>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_resrestrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RR_SMEM));
       LT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM));
       LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)PtGeom<true>::SMEM));
@@ -2772,7 +2564,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       attr = true;
     }
   }
-  if (tma_on && p->kind != LT_GRID_P1_TRI && sizeof(R) == 4) {
+  if (p->kind != LT_GRID_P1_TRI && sizeof(R) == 4) {
     for (int l = 0; l < nl - 1; ++l) {
       const Level& Lv = *p->levels[l];
       if (Lv.nx % 2 != 0 || Lv.nx < 64) continue;
@@ -2787,7 +2579,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       tzm[l].f = tma_map_8b(F[l], 4, dims, str, bf);
       tzm[l].c = tma_map_8b(Lv.pack32.get(), 3, cd, cs, bc);
       tzm[l].ok = true;
-      if (rb_on && Lv.packrb.get() && nx % 4 == 0) {
+      if (Lv.packrb.get() && nx % 4 == 0) {
         // colour-split maps: vectors {pos, colour, y, z, item}, coefficients {pos, colour,
         // comp, y, z} (Level::packrb)
         const uint64_t vd[5] = {nx / 2, 2, ny, nz, (uint64_t)Bc};
@@ -2806,23 +2598,13 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         tzm[l].rb = true;
         const uint32_t brt[5] = {RT_P, 2, RT_R, 1, 1};
         tzm[l].rt = tma_map_8b(Rr[l], 5, vd, vs, brt);
-        // opt-in (LT_RESRESTRICT=1): bit-identical to residual + restriction, but at one CTA per SM
-        // it is latency-bound (40.8 vs 31.9 ms per configs[4] inner solve)
-        if (Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2 && std::getenv("LT_RESRESTRICT") != nullptr) {
-          const uint32_t rbx[5] = {RR_XP, 2, RR_XR, 1, 1}, rbf[5] = {RR_FP, 2, RR_FR, 1, 1};
-          const uint32_t rbc[5] = {RR_CP, 2, 4, RR_CR, 1};
-          tzm[l].rrx = tma_map_8b(X[l], 5, vd, vs, rbx);
-          tzm[l].rrf = tma_map_8b(F[l], 5, vd, vs, rbf);
-          tzm[l].rrc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, rbc);
-          tzm[l].rr = true;
-        }
       }
     }
   }
   // prolongation onto colour-split levels with aggregation 2 x 2 x 2: fine x and coarse e maps
-  for (int l = 0; l + 1 < nl && tma_on; ++l) {
+  for (int l = 0; l + 1 < nl; ++l) {
     const Level& Lv = *p->levels[l];
-    if (!tzm[l].rb || std::getenv("LT_PAIR_PROLONG") || !(Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2))
+    if (!tzm[l].rb || !(Lv.agg[0] == 2 && Lv.agg[1] == 2 && Lv.agg[2] == 2))
       continue;
     const Level& Lc = *p->levels[l + 1];
     const uint64_t nx = Lv.nx, ny = Lv.ny, nz = Lv.nz;
@@ -2847,7 +2629,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
   // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
   // reads and writes X[l]
-  const bool ta_ok = tma_on && p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32 &&
+  const bool ta_ok = p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32 &&
                      L0.nx % 2 == 0;
   CUtensorMap map_p{}, map_c64{};
   if (ta_ok) {
@@ -2863,41 +2645,40 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     map_p = tma_map_8b(pp, 4, dims, str, bx);
     map_c64 = tma_map_8b(p->levels[0]->pack64.get(), 4, cd, cs, bc);
   }
-  const unsigned grid = (unsigned)nblk * (unsigned)Bc;
+  // COCG vector kernels: vblk grid-stride blocks per item (about LT_VBLK_SM per SM over the batch)
+#ifndef LT_VBLK_SM
+#define LT_VBLK_SM 64
+#endif
+  const int vblk = (int)std::min<int64_t>(nblk, std::max<int64_t>(4, ((int64_t)LT_VBLK_SM * ctx->num_sms + Bc - 1) / Bc));
+  const unsigned grid = (unsigned)vblk * (unsigned)Bc;
   // the finest level's multigrid vectors (rmg, z) are colour-split when its kernels are
   const int snx = tzm[0].rb ? L0.nx : 0, sny = tzm[0].rb ? L0.ny : 0;
   const double nb = (double)n * Bc;
   const double coef = (double)n * 8.0 * (DIM + 1);
   const double vb = sizeof(V);
+  const unsigned cblk = (unsigned)std::min(1024, (Bc + 31) / 32 * 32);
 
+  // r = v, u = 0, ||v||^2; items masked out by the caller and zero right-hand sides are done
+  launch(ctx, "cocg_scalar", 0.0, [&] { cocg_mask_kernel<<<1, cblk, 0, st>>>(Bc, active, d_done); });
   launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
-    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), nblk, snx, sny);
+    copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), vblk, snx, sny);
   });
-  launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), nblk, sc); });
-  std::vector<double> bb(Bc), rr(Bc), best(Bc);
-  LT_CUDA(cudaMemcpyAsync(bb.data(), d_bb, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
-  std::vector<int> done(Bc, 0), zero(Bc, 0), stall(Bc, 0);
-  bool any_zero = false;
-  for (int b = 0; b < Bc; ++b)
-    if (!(bb[b] > 0.0)) { done[b] = 1; zero[b] = 1; any_zero = true; }
-  if (any_zero) {
-    DeviceBuffer dz(sizeof(int) * Bc, st);
-    LT_CUDA(cudaMemcpyAsync(dz.get(), zero.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
-    launch(ctx, "cocg_vec", nb * 16.0, [&] {
-      zero_kernel<<<dim3(blocks_for(n, kT), Bc), kT, 0, st>>>(n, dz.as<int>(), u, us, Bc);
-    });
-    LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
-  }
-  int active = 0;
-  for (int b = 0; b < Bc; ++b) active += !done[b];
-  if (active == 0) return;
+  launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), vblk, sc); });
+  // profiling: the number of items still active at every step (bytes of the launches of a
+  // step are charged for those items only)
+  DeviceBuffer counts;
+  const bool prof = ctx->profiling;
+  if (prof) counts.allocate(sizeof(int) * (size_t)(p->inner_maxit + 2), st);
+  int* d_counts = prof ? counts.as<int>() : nullptr;
+  launch(ctx, "cocg_scalar", 0.0, [&] {
+    cocg_init_kernel<<<1, cblk, 0, st>>>(Bc, d_done, d_zero, d_bb, d_rr, d_best, d_stall, d_pending, d_counts);
+  });
+  const size_t pend0 = ctx->pending.size();
+  if (prof) ctx->profile_tag = 0;
+  launch(ctx, "cocg_vec", nb * 16.0, [&] {
+    zero_kernel<<<dim3(std::min<unsigned>(blocks_for(n, kT), 2 * ctx->num_sms), Bc), kT, 0, st>>>(n, d_zero, u, us, Bc);
+  });
 
-  const double tol2 = p->inner_tol * p->inner_tol;
-  int iters_seen = 0;
-  double sync_ms = 0.0;
-  const auto wall0 = std::chrono::steady_clock::now();
-  for (int b = 0; b < Bc; ++b) best[b] = bb[b];
   // FD: rho = r^T z is fused into the V-cycle's last sweep (partials of f^T x on the finest
   // level, f the multigrid copy of r); P1 keeps the separate dot kernel
   const bool fused = p->kind != LT_GRID_P1_TRI;
@@ -2907,9 +2688,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     z = vcycle<R, DIM>(p, 0, Bc, bt, d_taus, d_inv, inv_ld, inv_off, X, F, Rr, fused ? partials.as<double2>() : nullptr,
                        &dnb, tzm.data());
     if (dnb == 0) {
-      dnb = nblk;
+      dnb = vblk;
       launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
-        bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), nblk, snx, sny);
+        bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), vblk, snx, sny);
       });
     }
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(op, bt, partials.get(), dnb, sc); });
@@ -2919,21 +2700,18 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
     pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 1, snx, sny);
   });
-  std::vector<int> pending(Bc, 0);  // items whose u still lacks this iteration's alpha p
-  for (int it = 0; it < p->inner_maxit; ++it) {
-    const bool zm = DIM == 3 || p->kind != LT_GRID_P1_TRI;
-    const int nblk_apply = ta_ok ? ((L0.nx + TA_W - 1) / TA_W) * ((L0.ny + TA_H - 1) / TA_H) *
-                                       ((L0.nz + ZM_ZC - 1) / ZM_ZC)
-                                 : zm ? zm_blocks(L0) : L0.ntiles;
-    static const bool ta2_on = std::getenv("LT_APPLY_NI1") == nullptr;
+
+  const bool zm = DIM == 3 || p->kind != LT_GRID_P1_TRI;
+  const int nblk_apply = ta_ok ? ((L0.nx + TA_W - 1) / TA_W) * ((L0.ny + TA_H - 1) / TA_H) * ((L0.nz + ZM_ZC - 1) / ZM_ZC)
+                               : zm ? zm_blocks(L0) : L0.ntiles;
+  const double tol2 = p->inner_tol * p->inner_tol;
+  FlagSlot* host_ring = ctx->flag_ring_dev();
+  // one COCG iteration; u += alpha p is deferred into the direction update (pupdate)
+  auto body = [&] {
     launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
-      if (ta_ok && ta2_on)
+      if (ta_ok)
         apply_tma2_kernel<<<(unsigned)nblk_apply * ((Bc + 1) / 2), kTA, TA2_SMEM, st>>>(
             map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n}, bt, d_taus, q, partials.as<double2>(), nblk_apply);
-      else if (ta_ok)
-        apply_tma_kernel<<<(unsigned)nblk_apply * Bc, kTA, TA_SMEM, st>>>(map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n},
-                                                                         bt, d_taus, q, partials.as<double2>(),
-                                                                         nblk_apply);
       else if (zm)
         apply_dot_zm_kernel<<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q, partials.as<double2>(),
                                                                       nblk_apply);
@@ -2941,71 +2719,108 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         apply_dot_kernel<DIM><<<(unsigned)nblk_apply * Bc, kT, 0, st>>>(L0, bt, d_taus, pp, q,
                                                                         partials.as<double2>(), nblk_apply);
     });
-    const double2* pdir = pp;
     launch(ctx, "cocg_scalar", 0.0, [&] {
       scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk_apply, sc);
     });
-    (void)pdir;
     launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
-      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), nblk, snx, sny);
+      axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), vblk, snx, sny);
     });
-    for (int b = 0; b < Bc; ++b)
-      if (!done[b]) pending[b] = 1;
-    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), nblk, sc); });
-    LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
-    {
-      const auto s0 = std::chrono::steady_clock::now();
-      LT_CUDA(cudaStreamSynchronize(st));
-      if (inner_trace())
-        sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
-    }
-    bool changed = false;
-    for (int b = 0; b < Bc; ++b) {
-      if (done[b]) continue;
-      if (rr[b] <= tol2 * bb[b]) { done[b] = 1; changed = true; continue; }
-      // stagnation at the rounding floor: within 1e4 of the tolerance and no halving of the
-      // residual in 6 iterations.  (Far from the floor COCG's residual is non-monotone on the
-      // indefinite pencils Re tau < 0 gives -- plateaus there are not stagnation.)
-      if (rr[b] < 0.25 * best[b]) { best[b] = rr[b]; stall[b] = 0; }
-      else if (rr[b] <= 1e8 * tol2 * bb[b] && ++stall[b] >= 6) { done[b] = 1; changed = true; }
-    }
-    if (changed) {
-      active = 0;
-      for (int b = 0; b < Bc; ++b) active += !done[b];
-      if (active == 0) break;
-      LT_CUDA(cudaMemcpyAsync(d_done, done.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
-    }
+    launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), vblk, sc); });
+    launch(ctx, "cocg_scalar", 0.0, [&] {
+      cocg_control_kernel<<<1, cblk, 0, st>>>(Bc, d_done, d_rr, d_bb, d_best, d_stall, d_pending, tol2, d_counter,
+                                              host_ring, kFlagRing, d_counts);
+    });
+    if (prof) ++ctx->profile_tag;
     precondition(OP_BETA);
     launch(ctx, "cocg_vec", nb * (64.0 + vb), [&] {
       pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 0, snx, sny);
     });
-    for (int b = 0; b < Bc; ++b)
-      if (!done[b]) pending[b] = 0;
-    if (inner_trace()) iters_seen = it + 1;
+  };
+
+  // The host never drains the stream inside the loop: it issues iteration `it`, then waits
+  // for iteration it - kFlagLag (already followed by queued work) and stops once that one
+  // reported no active item.  The iteration issued after it is a no-op (every kernel skips
+  // done items).  Without profiling the iteration body is one CUDA graph launch.
+  const bool graph = !ctx->profiling && !debug_sync();
+  cudaGraphExec_t exec = nullptr;
+  int64_t body_launches = 0;
+  if (graph) {
+    const int64_t l0 = ctx->launches;
+    cudaGraph_t g = nullptr;
+    LT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    body();
+    LT_CUDA(cudaStreamEndCapture(st, &g));
+    body_launches = ctx->launches - l0;
+    ctx->launches = l0;
+    exec = p->graph_exec(g);
+    LT_CUDA(cudaGraphDestroy(g));
+  }
+  // Near the end the host predicts the last iteration from the worst item's contraction and
+  // waits for that iteration itself instead of issuing a speculative no-op one.
+  volatile FlagSlot* ring = ctx->flag_ring_host();
+  double w_prev = -1.0, w_last = -1.0;  // worst ratios of the last two iterations read
+  auto read = [&](int k) -> bool {     // false: no item left after iteration k
+    const int s = k % kFlagRing;
+    LT_CUDA(cudaEventSynchronize(ctx->flag_ev[s]));
+    if (ring[s].active == 0) return false;
+    w_prev = w_last;
+    w_last = ring[s].worst;
+    return true;
+  };
+  int issued = 0;
+  for (int it = 0; it < p->inner_maxit; ++it) {
+    if (prof) ctx->profile_tag = it;
+    if (graph) {
+      LT_CUDA(cudaGraphLaunch(exec, st));
+      ctx->launches += body_launches;
+    } else {
+      body();
+    }
+    LT_CUDA(cudaEventRecord(ctx->flag_ev[it % kFlagRing], st));
+    issued = it + 1;
+    if (it < kFlagLag) continue;
+    if (!read(it - kFlagLag)) break;
+    // predicted ratio after iteration it: the last one times the last contraction
+    const bool last = w_prev > 0.0 && w_last < w_prev && w_last * (w_last / w_prev) <= 1.0;
+    if (last && !read(it)) break;
+  }
+  if (prof) {
+    // charge every tagged launch of this chunk for the items active at its step
+    std::vector<int> cnt(issued + 1, Bc);
+    LT_CUDA(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(int) * (size_t)(issued + 1), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    for (size_t e = pend0; e < ctx->pending.size(); ++e) {
+      auto& pe = ctx->pending[e];
+      if (pe.tag >= 0 && pe.tag < (int)cnt.size()) pe.bytes *= (double)cnt[pe.tag] / Bc;
+      pe.tag = -1;
+    }
+    ctx->profile_tag = -1;
   }
   // the last deferred solution update of the items that stopped after an r update
-  bool any_pending = false;
-  for (int b = 0; b < Bc; ++b) any_pending |= pending[b] != 0;
-  if (any_pending) {
-    DeviceBuffer dm(sizeof(int) * Bc, st);
-    LT_CUDA(cudaMemcpyAsync(dm.get(), pending.data(), sizeof(int) * Bc, cudaMemcpyHostToDevice, st));
-    launch(ctx, "cocg_vec", nb * 48.0, [&] {
-      uupdate_kernel<<<dim3(blocks_for(n, kT), Bc), kT, 0, st>>>(n, dm.as<int>(), d_alpha, pp, u, us);
-    });
+  launch(ctx, "cocg_vec", nb * 48.0, [&] {
+    uupdate_kernel<<<dim3(std::min<unsigned>(blocks_for(n, kT), 2 * ctx->num_sms), Bc), kT, 0, st>>>(
+        n, d_pending, d_alpha, pp, u, us);
+  });
+  if (rel_out || inner_trace()) {
+    std::vector<double> rr(Bc), bb(Bc);
+    std::vector<int> done(Bc);
+    LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaMemcpyAsync(bb.data(), d_bb, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < Bc; ++b) {
+      const double rel = bb[b] > 0.0 ? std::sqrt(rr[b] / bb[b]) : 0.0;
+      if (rel_out) rel_out[b] = rel;
+      if (inner_trace() >= 2)
+        std::fprintf(stderr, "[inner] tau=(%.4g,%.4g) rel=%.3e\n", taus_host[b].x, taus_host[b].y, rel);
+    }
+    if (inner_trace()) std::fprintf(stderr, "[inner] chunk B=%d iterations issued=%d\n", Bc, issued);
   }
-  LT_CUDA(cudaStreamSynchronize(st));
-  if (inner_trace())
-    std::fprintf(stderr, "[inner] chunk B=%d iters=%d wall=%.3f ms sync-wait=%.3f ms\n", Bc, iters_seen + 1,
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count(), sync_ms);
-  if (inner_trace() >= 2)
-    for (int b = 0; b < Bc; ++b)
-      std::fprintf(stderr, "[inner] tau=(%.4g,%.4g) it<=%d rel=%.3e %s\n", taus_host[b].x, taus_host[b].y,
-                   iters_seen + 1, std::sqrt(rr[b] / bb[b]), rr[b] <= tol2 * bb[b] ? "ok" : "STAGNATED");
 }
 
 }  // namespace
 
-void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us) {
+void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us,
+                 const int* active, double* rel_out) {
   // Chunk so that the Krylov + multigrid workspace stays bounded.
   const int64_t n = p->n;
   const double avail = available_device_bytes(p->ctx);
@@ -3015,8 +2830,10 @@ void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v,
     std::fprintf(stderr, "[inner] B=%d chunk=%d available=%.1fGB\n", B, chunk, avail / 1e9);
   for (int b0 = 0; b0 < B; b0 += chunk) {
     const int bc = std::min(chunk, B - b0);
-    if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);
-    else inner_chunk<2>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us);
+    const int* act = active ? active + b0 : nullptr;
+    double* rel = rel_out ? rel_out + b0 : nullptr;
+    if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us, act, rel);
+    else inner_chunk<2>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us, act, rel);
   }
 }
 

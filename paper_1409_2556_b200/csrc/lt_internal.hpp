@@ -82,9 +82,20 @@ struct PendingEvent {
   std::string name;
   cudaEvent_t start, stop;
   double bytes;
+  int tag;  // >= 0: bytes still to be scaled by the active-item fraction of step `tag` (inner.cu)
 };
 
 }  // namespace lt
+
+// Host-visible convergence state of the device-resident COCG loop (inner.cu): a ring of
+// kFlagRing slots in mapped pinned memory written by the control kernel, each slot paired with
+// an event; the host reads slot it - kFlagLag while iteration it is still queued.
+constexpr int kFlagRing = 4, kFlagLag = 1;
+struct FlagSlot {
+  double worst;  // max over the items still iterating of ||r||^2 / (tol^2 ||v||^2)
+  int active;    // items still iterating
+  int pad;
+};
 
 struct lt_ctx_s {
   int device = 0;
@@ -97,6 +108,16 @@ struct lt_ctx_s {
   int num_sms = 148;
   int sample_every = 1;                              // time 1 in N launches of each class
   std::map<const char*, int64_t> class_counter;      // keyed by the (literal) class name
+  // >= 0 inside a device-resident loop: launches record this tag, and their algorithmic bytes
+  // (written for every item of the batch) are scaled once the loop knows how many items were
+  // still active at that step
+  int profile_tag = -1;
+
+  FlagSlot* flag_host = nullptr;  // mapped pinned ring (kFlagRing slots)
+  FlagSlot* flag_dev = nullptr;   // its device alias
+  cudaEvent_t flag_ev[kFlagRing] = {};
+  FlagSlot* flag_ring_dev();      // allocates the ring and its events on first use
+  volatile FlagSlot* flag_ring_host() { return flag_host; }
 
   void resolve_profile();    // waits for all pending events
   void resolve_completed();  // accumulates the already-completed prefix of pending events
@@ -119,9 +140,9 @@ inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f
     cudaEventRecord(a, ctx->stream);
     f();
     cudaEventRecord(b, ctx->stream);
-    ctx->pending.push_back({name, a, b, algorithmic_bytes});
+    ctx->pending.push_back({name, a, b, algorithmic_bytes, ctx->profile_tag});
     check_launch(name);
-    if (ctx->pending.size() >= 1024) ctx->resolve_completed();  // non-blocking, recycles events
+    if (ctx->pending.size() >= 1024 && ctx->profile_tag < 0) ctx->resolve_completed();  // non-blocking
     return;
   }
   f();
@@ -253,6 +274,12 @@ struct lt_pencil_s {
   double inner_tol = 1e-12;
   int inner_maxit = 200;
   lt::KeptBasis kept;
+  cudaGraphExec_t inner_exec = nullptr;  // the inner COCG iteration body (updated per chunk)
+  cudaGraphExec_t graph_exec(cudaGraph_t g);  // instantiates or updates inner_exec to g
+  lt_pencil_s() = default;
+  lt_pencil_s(const lt_pencil_s&) = delete;
+  lt_pencil_s& operator=(const lt_pencil_s&) = delete;
+  ~lt_pencil_s();
 
   lt::LevelView view(int l) const;
   lt::LevelView32 view32(int l) const;
@@ -280,8 +307,11 @@ CUtensorMap tma_map_4b(const void* base, int rank, const uint64_t* dims, const u
 // device bytes a solve may still take: free + the pool's reserved-but-unused memory (ctx.cu)
 double available_device_bytes(lt_ctx ctx);
 
+// active (device, B ints) may be null: items with active[b] == 0 are skipped (u untouched);
+// rel_out (host, B) may be null: each item's final relative residual ||v - A u|| / ||v||
+// (recursive COCG residual).
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs,
-                 double2* u, int64_t us);
+                 double2* u, int64_t us, const int* active = nullptr, double* rel_out = nullptr);
 
 // fgmres.cu
 struct OuterProblem {

@@ -652,6 +652,22 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
 lt::LevelView lt_pencil_s::view(int l) const { return lt::lt_pencil_view(this, l); }
 lt::LevelView32 lt_pencil_s::view32(int l) const { return lt::lt_pencil_view32(this, l); }
 
+cudaGraphExec_t lt_pencil_s::graph_exec(cudaGraph_t g) {
+  if (inner_exec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(inner_exec, g, &info) == cudaSuccess) return inner_exec;
+    cudaGetLastError();
+    cudaGraphExecDestroy(inner_exec);
+    inner_exec = nullptr;
+  }
+  LT_CUDA(cudaGraphInstantiate(&inner_exec, g, 0));
+  return inner_exec;
+}
+
+lt_pencil_s::~lt_pencil_s() {
+  if (inner_exec) cudaGraphExecDestroy(inner_exec);
+}
+
 const lt::CoarseFactor& lt_pencil_s::factor(double2 tau) {
   for (auto& f : factors)
     if (f->tau.x == tau.x && f->tau.y == tau.y) return *f;

@@ -163,3 +163,34 @@ def config(index: int) -> ThtConfig:
             [1e-4] * 16, list(np.logspace(2, 6, 4)), 32, "flexible", True,
             description="BASELINE configs[4] (headline)")
     raise ValueError(f"unknown config {index}")
+
+
+def reduced(index: int, shape: Tuple[int, ...], n_src: Optional[int] = None,
+            receivers: Optional[Sequence[int]] = None, n_times: Optional[int] = None) -> ThtConfig:
+    """Config `index`'s statistics on a smaller box for the oracle parity fixtures.
+
+    The spacing is h = 1 / shape[0] (unit extent along x, like every config), the other extents
+    are shape[d] * h, the fields are drawn on the new grid with the same GRF statistics and
+    seeds, and the source / receiver points are mapped linearly into the box (p_d * new extent /
+    old extent), so the lattices keep their layout.  `receivers` selects receiver indices."""
+    base = config(index)
+    old_ext = [n * base.h for n in base.shape]
+    h = 1.0 / shape[0]
+    new_ext = [n * h for n in shape]
+    scale = [new_ext[d] / old_ext[d] for d in range(len(shape))]
+
+    def move(p):
+        return tuple(float(p[d]) * scale[d] for d in range(len(shape)))
+
+    out = ThtConfig(**{**base.__dict__})
+    out.shape = tuple(shape)
+    out.h = h
+    out.name = f"{base.name}@box{'x'.join(map(str, shape))}"
+    src = base.sources if n_src is None else base.sources[:n_src]
+    out.sources = [move(p) for p in src]
+    out.rates = base.rates[:len(src)]
+    rec = base.receivers if receivers is None else [base.receivers[i] for i in receivers]
+    out.receivers = [move(p) for p in rec]
+    if n_times is not None:
+        out.times = base.times[:n_times]
+    return out

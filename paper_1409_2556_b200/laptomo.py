@@ -611,6 +611,31 @@ def _forward(pencil: ShiftedPencil, problem: ForwardProblem, solver: SolverConfi
     return sol
 
 
+def solve_forward_sources(pencil: ShiftedPencil, sources, rates, times, n_quad: int, receivers,
+                          solver: SolverConfig = SolverConfig(), pooled: bool = False,
+                          contour: TalbotParams = TalbotParams()):
+    """solve_forward (forward.cpp:75-118) for n_src pumping sources that share the times, contour
+    and solver, batched in lockstep on the device (one lt_forward call): drawdown at the
+    receiver points, (n_src, n_rec, n_times), and the per-time diagnostics.  `sources` are
+    points (the multilinear weights are formed by the library, lt_pencil_point_weights)."""
+    n = pencil.rows()
+    src_w = np.ascontiguousarray(np.stack([pencil.point_weights(q) for q in sources]).astype(np.float64))
+    rates = np.ascontiguousarray(np.asarray(rates, dtype=np.float64))
+    times = np.ascontiguousarray(np.asarray(times, dtype=np.float64))
+    rec = np.ascontiguousarray(np.asarray(receivers, dtype=np.float64))
+    n_src, n_rec = src_w.shape[0], rec.shape[0]
+    assert src_w.shape[1] == n and rates.size == n_src
+    dd = np.zeros(n_src * n_rec * times.size)
+    diag = (capi.LtTimeDiag * times.size)()
+    cp = contour.c()
+    sc = solver.c()
+    check(lib().lt_forward(pencil.handle, dptr(src_w), dptr(rates), n_src, None, dptr(times), int(times.size),
+                           int(n_quad), C.byref(cp), C.byref(sc), int(pooled), capi.LT_MEM_HOST, None, dptr(rec),
+                           n_rec, dptr(dd), diag, None))
+    diags = [TimeDiagnostics(int(diag[t].iterations), bool(diag[t].all_converged)) for t in range(times.size)]
+    return dd.reshape(n_src, n_rec, times.size), diags
+
+
 def solve_forward(pencil: ShiftedPencil, problem: ForwardProblem, solver: SolverConfig = SolverConfig()):
     """forward.cpp:75-118."""
     return _forward(pencil, problem, solver, False)
