@@ -8,8 +8,10 @@
 //   matrices are column-major (n rows), like the Eigen objects they replace.  With Eigen
 //   available, the Eigen overloads at the end accept/return Eigen types.
 //
-// Difference at the boundary: a pencil is built from a structured cell-centred grid and
-// per-cell log fields (assembled on the device) instead of assembled sparse (K, M).
+// Difference at the boundary: the device operator is matrix-free on a structured grid, so a
+// pencil is built either from a grid and per-cell (per-element) log fields, assembled on the
+// device, or from an assembled sparse pair (K, M) declared on its grid (ShiftedPencil(ctx,
+// grid, K, M): the FD cell-centred operator or the reference's own P1 pair from assemble()).
 #pragma once
 
 #include <algorithm>
@@ -181,11 +183,42 @@ struct ShiftStatus {
   std::vector<double> history;
 };
 
+/// Arnoldi data of the flexible iteration after m steps (shifted_solver.hpp:63-74):
+///   (K + z M) U_m = V_{m+1} Hbar_m(z; T_m),  Hbar_m(z; T_m) = [I; 0] + Hbar_m (z I - T_m).
+struct FlexibleBasisState {
+  std::vector<Complex> V;     // n x (m+1), column-major, orthonormal
+  std::vector<Complex> U;     // n x m, preconditioned basis
+  std::vector<Complex> Hbar;  // (m+1) x m, column-major
+  std::vector<Complex> taus;  // applied tau_j, j = 1..m
+  double beta = 0.0;          // ||b||
+  int m = 0;
+  int steps() const { return m; }
+  /// Hbar_m(z; T_m) for a probe shift, (m+1) x m column-major.
+  std::vector<Complex> shifted_hessenberg(Complex z) const {
+    std::vector<Complex> hz(Hbar);
+    for (int l = 0; l < m; ++l) {
+      for (int i = 0; i <= m; ++i) hz[(size_t)l * (m + 1) + i] *= (z - taus[l]);
+      hz[(size_t)l * (m + 1) + l] += 1.0;
+    }
+    return hz;
+  }
+};
+
+/// residual_estimate (shifted_solver.cpp:334-343): the FOM residual norm |eta_k|.
+inline double residual_estimate(const FlexibleBasisState& state, Complex z, const std::vector<Complex>& y_fom) {
+  double out = 0.0;
+  detail::check(lt_residual_estimate(detail::c(state.Hbar.data()), detail::c(state.taus.data()), state.m, detail::c(z),
+                                     detail::c(y_fom.data()), (int)y_fom.size(), &out));
+  return out;
+}
+
 struct ShiftedSolveResult {
   std::vector<Complex> solutions;  // n x n_shifts, column-major
   int iterations = 0;
   bool all_converged = false;
   std::vector<ShiftStatus> shifts;
+  bool has_basis = false;          // std::optional<FlexibleBasisState> basis (keep_basis)
+  FlexibleBasisState basis;
   std::vector<int> unconverged() const {
     std::vector<int> out;
     for (int k = 0; k < (int)shifts.size(); ++k)
@@ -194,12 +227,31 @@ struct ShiftedSolveResult {
   }
 };
 
-/// Cell-centred grid (x fastest): dims 2 or 3.
+/// Cell-centred grid (x fastest): dims 2 or 3.  p1_mesh(n, L) declares the reference's P1
+/// mesh build_mesh(n, L) instead (mesh.cpp:14-52).
 struct Grid {
   int dim = 2;
   int shape[3] = {1, 1, 1};
   double h = 1.0;
-  lt_grid c() const { return lt_grid{LT_GRID_FD_CELL, dim, {shape[0], shape[1], shape[2]}, h}; }
+  int kind = LT_GRID_FD_CELL;
+  lt_grid c() const { return lt_grid{kind, dim, {shape[0], shape[1], shape[2]}, h}; }
+  static Grid p1_mesh(int n_per_side, double side_length) {
+    Grid g;
+    g.kind = LT_GRID_P1_TRI;
+    g.shape[0] = g.shape[1] = n_per_side;
+    g.h = side_length / (n_per_side - 1);
+    return g;
+  }
+};
+
+/// An assembled sparse matrix in compressed rows (SparseReal of the reference; K and M being
+/// symmetric, the compressed columns of Eigen's default SparseMatrix<double> work as well).
+struct SparseMatrix {
+  long n = 0;
+  std::vector<std::int64_t> outer;  // n + 1
+  std::vector<std::int64_t> inner;  // nnz
+  std::vector<double> values;       // nnz
+  lt_sparse c() const { return lt_sparse{outer.data(), inner.data(), values.data(), 8}; }
 };
 
 class ShiftedPencil;
@@ -223,6 +275,13 @@ class ShiftedPencil {
                 const std::vector<double>& log_storativity) {
     const lt_grid g = grid.c();
     detail::check(lt_pencil_create_grid(ctx.handle(), &g, log_kappa.data(), log_storativity.data(), LT_MEM_HOST, &h_));
+  }
+  /// ShiftedPencil(const SparseReal& K, const SparseReal& M) (shifted_solver.hpp:90) on `grid`.
+  ShiftedPencil(const Context& ctx, const Grid& grid, const SparseMatrix& K, const SparseMatrix& M) {
+    if (K.n != M.n) throw std::invalid_argument("ShiftedPencil: K and M dimensions disagree");
+    const lt_grid g = grid.c();
+    const lt_sparse k = K.c(), m = M.c();
+    detail::check(lt_pencil_create_csr(ctx.handle(), &g, K.n, &k, &m, &h_));
   }
   ~ShiftedPencil() { if (h_) lt_pencil_destroy(h_); }
   ShiftedPencil(const ShiftedPencil&) = delete;
@@ -278,7 +337,7 @@ inline ShiftedSolveResult solve_shifted_flexible(const ShiftedPencil& pencil, co
   const long n = pencil.rows();
   const int ns = (int)shifts.size();
   lt_solve_options o{options.variant == KrylovVariant::Fom ? LT_VARIANT_FOM : LT_VARIANT_GMRES, options.tol,
-                     options.maxit, 0, options.record_history ? 1 : 0};
+                     options.maxit, options.keep_basis ? 1 : 0, options.record_history ? 1 : 0};
   ShiftedSolveResult r;
   r.solutions.assign((size_t)n * ns, Complex(0.0));
   std::vector<lt_shift_status> st(ns > 0 ? ns : 1);
@@ -303,13 +362,46 @@ inline ShiftedSolveResult solve_shifted_flexible(const ShiftedPencil& pencil, co
     r.all_converged = r.all_converged && s.converged;
     r.shifts.push_back(std::move(s));
   }
+  if (options.keep_basis) {
+    FlexibleBasisState& bs = r.basis;
+    detail::check(lt_last_basis(pencil.handle(), 0, &bs.m, &bs.beta, nullptr, nullptr, nullptr, nullptr));
+    const int m = bs.m;
+    bs.V.assign((size_t)n * (m + 1), Complex(0.0));
+    bs.U.assign((size_t)n * (m > 0 ? m : 1), Complex(0.0));
+    bs.Hbar.assign((size_t)(m + 1) * (m > 0 ? m : 1), Complex(0.0));
+    bs.taus.assign(m > 0 ? m : 1, Complex(0.0));
+    detail::check(lt_last_basis(pencil.handle(), 0, nullptr, nullptr, detail::c(bs.V.data()), detail::c(bs.U.data()),
+                                detail::c(bs.Hbar.data()), detail::c(bs.taus.data())));
+    bs.U.resize((size_t)n * m);
+    bs.Hbar.resize((size_t)(m + 1) * m);
+    bs.taus.resize(m);
+    r.has_basis = true;
+  }
   return r;
+}
+
+/// The (K, M) overloads (shifted_solver.hpp:114-128): a temporary pencil on `grid`.
+inline ShiftedSolveResult solve_shifted_flexible(const Context& ctx, const Grid& grid, const SparseMatrix& K,
+                                                 const SparseMatrix& M, const std::vector<Complex>& b,
+                                                 const std::vector<Complex>& shifts,
+                                                 const PreconditionerSchedule& schedule,
+                                                 const ShiftedSolveOptions& options = {}) {
+  ShiftedPencil p(ctx, grid, K, M);
+  return solve_shifted_flexible(p, b, shifts, schedule, options);
 }
 
 inline ShiftedSolveResult solve_shifted_single(const ShiftedPencil& pencil, const std::vector<Complex>& b,
                                                const std::vector<Complex>& shifts, Complex tau,
                                                const ShiftedSolveOptions& options = {}) {
   return solve_shifted_flexible(pencil, b, shifts, single_tau_schedule(tau), options);
+}
+
+inline ShiftedSolveResult solve_shifted_single(const Context& ctx, const Grid& grid, const SparseMatrix& K,
+                                               const SparseMatrix& M, const std::vector<Complex>& b,
+                                               const std::vector<Complex>& shifts, Complex tau,
+                                               const ShiftedSolveOptions& options = {}) {
+  ShiftedPencil p(ctx, grid, K, M);
+  return solve_shifted_flexible(p, b, shifts, single_tau_schedule(tau), options);
 }
 
 inline std::vector<Complex> solve_shifted_direct(const ShiftedPencil& pencil, const std::vector<Complex>& b,

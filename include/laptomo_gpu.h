@@ -113,9 +113,33 @@ typedef struct {
  * ShiftedPencil(K, M) (assembly.cpp:69-113, shifted_solver.cpp:106-107). */
 lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* log_kappa,
                                 const double* log_storativity, int mem, lt_pencil* out);
+/* A compressed sparse matrix, 0-based: outer[n + 1] offsets, inner[nnz] indices, values[nnz].
+ * Compressed rows (CSR) or, K and M being symmetric, compressed columns (the layout of Eigen's
+ * default column-major SparseMatrix<double>); index_bytes = 4 (Eigen's int StorageIndex) or 8. */
+typedef struct {
+  const void* outer;
+  const void* inner;
+  const double* values;
+  int index_bytes;
+} lt_sparse;
+
+/* ShiftedPencil(const SparseReal& K, const SparseReal& M) (shifted_solver.hpp:90,
+ * shifted_solver.cpp:106-107) for an assembled pair on a declared structured grid: K, M host
+ * matrices of n rows.  The device operator is matrix-free, so the pair is checked against the
+ * grid's stencil and converted to its coefficients:
+ *   LT_GRID_FD_CELL  K the 5-/7-point cell-centred operator, M diagonal (n = cells);
+ *   LT_GRID_P1_TRI   the reference's assemble() pair on build_mesh(shape[0], L) interior nodes
+ *                    (assembly.cpp:69-113; K's NE/SW hypotenuse entries zero), n = (shape[0]-2)^2.
+ * Entries off the stencil, an asymmetric pair or a negative boundary coupling give
+ * LT_ERR_INVALID_ARGUMENT.  The pencil then solves and applies exactly like a grid pencil (same
+ * multigrid shift-and-invert, coarsened from the given operator); it carries no parameter
+ * fields, so lt_jacobian / lt_predict need lt_pencil_create_grid. */
+lt_status lt_pencil_create_csr(lt_ctx ctx, const lt_grid* grid, int64_t n, const lt_sparse* K,
+                               const lt_sparse* M, lt_pencil* out);
 lt_status lt_pencil_destroy(lt_pencil p);
 int64_t lt_pencil_rows(lt_pencil p);
-/* Number of per-parameter cells of the log fields: cells (FD) or elements (P1). */
+/* Number of per-parameter cells of the log fields: cells (FD) or elements (P1); 0 for a
+ * pencil created from (K, M). */
 int64_t lt_pencil_parameters(lt_pencil p);
 int lt_pencil_levels(lt_pencil p);
 
@@ -181,7 +205,15 @@ lt_status lt_solve_shifted(lt_pencil p, const lt_complex* b, int n_rhs, const lt
 lt_status lt_last_basis(lt_pencil p, int rhs, int* steps_out, double* beta_out, lt_complex* V,
                         lt_complex* U, lt_complex* Hbar, lt_complex* taus);
 
-/* solve_shifted_direct (shifted_solver.cpp:324-332): one exact shift-and-invert per shift. */
+/* residual_estimate (shifted_solver.cpp:334-343): |h_{m+1,m} (z - tau_m) y_m|, the FOM residual
+ * norm, on a FlexibleBasisState as lt_last_basis returns it (Hbar (m+1) x m column-major, taus m)
+ * for FOM coefficients y_fom of length y_len (must equal m >= 1).  Host arithmetic. */
+lt_status lt_residual_estimate(const lt_complex* Hbar, const lt_complex* taus, int m, lt_complex z,
+                               const lt_complex* y_fom, int y_len, double* out);
+
+/* solve_shifted_direct (shifted_solver.cpp:324-332): one shift-and-invert solve per shift.
+ * LT_ERR_NOT_CONVERGED (shift indices via lt_last_unconverged) if a solve ended above the
+ * inner solve's floor (1e4 x its tolerance); x_out is written either way. */
 lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs,
                                   const lt_complex* shifts, int n_shifts, int mem,
                                   lt_complex* x_out);

@@ -58,6 +58,11 @@ class LtSolverConfig(C.Structure):
     _fields_ = [("kind", C.c_int), ("variant", C.c_int), ("tol", C.c_double), ("maxit", C.c_int)]
 
 
+class LtSparse(C.Structure):
+    _fields_ = [("outer", C.c_void_p), ("inner", C.c_void_p), ("values", C.POINTER(C.c_double)),
+                ("index_bytes", C.c_int)]
+
+
 class LtTimeDiag(C.Structure):
     _fields_ = [("iterations", C.c_int), ("all_converged", C.c_int)]
 
@@ -99,6 +104,7 @@ SIGNATURES = {
     "lt_sample_field_grid": (I, [P, I, PI, D, D, PD, D, C.c_uint64, PC, I, PD]),
     "lt_select_preconditioner_shifts": (I, [PC, I, PC, PI, PI, PI]),
     "lt_pencil_create_grid": (I, [P, C.POINTER(LtGrid), PD, PD, I, C.POINTER(P)]),
+    "lt_pencil_create_csr": (I, [P, C.POINTER(LtGrid), I64, C.POINTER(LtSparse), C.POINTER(LtSparse), C.POINTER(P)]),
     "lt_pencil_destroy": (I, [P]),
     "lt_pencil_rows": (I64, [P]),
     "lt_pencil_parameters": (I64, [P]),
@@ -117,6 +123,7 @@ SIGNATURES = {
                              C.POINTER(LtShiftStatus), PI, PD]),
     "lt_last_basis": (I, [P, I, PI, PD, PC, PC, PC, PC]),
     "lt_solve_shifted_direct": (I, [P, PC, I, PC, I, I, PC]),
+    "lt_residual_estimate": (I, [PC, PC, I, LtComplex, PC, I, PD]),
     "lt_solver_default_config": (None, [C.POINTER(LtSolverConfig)]),
     "lt_forward": (I, [P, PD, PD, I, PD, PD, I, I, C.POINTER(LtTalbotParams), C.POINTER(LtSolverConfig), I, I,
                        PD, PD, I, PD, C.POINTER(LtTimeDiag), PD]),

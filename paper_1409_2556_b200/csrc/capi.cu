@@ -329,6 +329,43 @@ lt_status lt_pencil_create_grid(lt_ctx ctx, const lt_grid* grid, const double* l
   });
 }
 
+lt_status lt_pencil_create_csr(lt_ctx ctx, const lt_grid* grid, int64_t n, const lt_sparse* K, const lt_sparse* M,
+                               lt_pencil* out) {
+  return guard([&] {
+    LT_REQUIRE(ctx && grid && K && M && out, "ShiftedPencil(K, M): null argument");
+    LT_REQUIRE(K->outer && K->inner && K->values && M->outer && M->inner && M->values,
+               "ShiftedPencil(K, M): null matrix array");
+    LT_REQUIRE((K->index_bytes == 4 || K->index_bytes == 8) && (M->index_bytes == 4 || M->index_bytes == 8),
+               "ShiftedPencil(K, M): index_bytes must be 4 or 8");
+    LT_REQUIRE(n >= 1, "ShiftedPencil(K, M): empty matrices");
+    LT_REQUIRE(grid->h > 0.0, "ShiftedPencil(K, M): grid spacing must be positive");
+    if (grid->kind == LT_GRID_P1_TRI) {
+      LT_REQUIRE(grid->dim == 2 && grid->shape[0] >= 3, "ShiftedPencil(K, M): the P1 mesh is 2-D with n_per_side >= 3");
+    } else {
+      LT_REQUIRE(grid->kind == LT_GRID_FD_CELL && (grid->dim == 2 || grid->dim == 3),
+                 "ShiftedPencil(K, M): unsupported grid");
+      for (int d = 0; d < grid->dim; ++d) LT_REQUIRE(grid->shape[d] >= 1, "ShiftedPencil(K, M): empty grid");
+    }
+    set_device(ctx);
+    auto* p = new lt_pencil_s();
+    p->ctx = ctx;
+    p->grid = *grid;
+    p->kind = grid->kind;
+    if (grid->dim == 2) p->grid.shape[2] = 1;
+    if (grid->kind == LT_GRID_P1_TRI) p->grid.shape[1] = grid->shape[0];
+    p->dim = grid->dim;
+    p->n = n;
+    p->from_csr = true;
+    try {
+      lt::pencil_build_csr(p, K, M);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
 lt_status lt_pencil_destroy(lt_pencil p) {
   return guard([&] {
     if (!p) return;
@@ -343,6 +380,7 @@ int64_t lt_pencil_rows(lt_pencil p) { return p ? p->n : -1; }
 
 int64_t lt_pencil_parameters(lt_pencil p) {
   if (!p) return -1;
+  if (p->from_csr) return 0;
   if (p->kind == LT_GRID_P1_TRI) {
     const int64_t nc = p->grid.shape[0] - 1;
     return 2 * nc * nc;
@@ -475,6 +513,18 @@ lt_status lt_last_basis(lt_pencil p, int rhs, int* steps_out, double* beta_out, 
   });
 }
 
+lt_status lt_residual_estimate(const lt_complex* Hbar, const lt_complex* taus, int m, lt_complex z, const lt_complex* y_fom,
+                               int y_len, double* out) {
+  return guard([&] {
+    LT_REQUIRE(out != nullptr, "residual_estimate: null output");
+    if (m < 1 || y_len != m || !Hbar || !taus || !y_fom)
+      throw lt::Error(LT_ERR_INVALID_ARGUMENT, "residual_estimate: FOM coefficients of length m required");
+    const std::complex<double> h_next(Hbar[(size_t)(m - 1) * (m + 1) + m].re, Hbar[(size_t)(m - 1) * (m + 1) + m].im);
+    const std::complex<double> tau_m(taus[m - 1].re, taus[m - 1].im), zz(z.re, z.im), y(y_fom[m - 1].re, y_fom[m - 1].im);
+    *out = std::abs(h_next * (zz - tau_m) * y);
+  });
+}
+
 lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs, const lt_complex* shifts, int n_shifts,
                                   int mem, lt_complex* x_out) {
   return guard([&] {
@@ -556,6 +606,8 @@ lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out, do
   return guard([&] {
     check_pencil(p);
     LT_REQUIRE(exp, "null experiment");
+    LT_REQUIRE(!(jac_out && p->from_csr),
+               "ThtForwardModel::jacobian: the pencil was created from (K, M) and carries no parameter fields");
     set_device(p->ctx);
     const int64_t n_param = exp->include_storativity ? 2 * lt_pencil_parameters(p) : lt_pencil_parameters(p);
     const int pairs = exp->n_src * exp->n_rec;

@@ -1302,6 +1302,8 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   const int n_src = ex.n_src, n_rec = ex.n_rec;
   LT_REQUIRE(n_src >= 1 && n_rec >= 1 && ex.n_times >= 1, "ThtForwardModel: experiment must be nonempty");
   LT_REQUIRE(t >= 0 && t < ex.n_times, "jacobian_slice: time index out of range");
+  LT_REQUIRE(!(jac_out && p->from_csr),
+             "ThtForwardModel::jacobian: the pencil was created from (K, M) and carries no parameter fields");
   LT_REQUIRE(ex.n_quad >= 4 && ex.n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
   LT_REQUIRE(ex.times[t] > 0.0, "build_contour: time must be positive");
   TraceScope trace_all(ctx, "jacobian_slice", t);

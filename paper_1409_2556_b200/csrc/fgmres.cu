@@ -832,7 +832,9 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
     LT_CUDA(cudaMemcpyAsync(dVcols + j + 1, &vptr[j + 1], sizeof(void*), cudaMemcpyHostToDevice, st));
     double2* s = const_cast<double2*>(vptr[j + 1]);
     partials.ensure(sizeof(double2) * (size_t)B * (j + 2) * nblk, st);
-    launch(ctx, "fgmres_orth", nb * (16.0 * (j + 3)) + n * 8.0, [&] {
+    // bytes are charged for the items still iterating (the others' blocks exit at once)
+    const double nba = (double)n * n_active;
+    launch(ctx, "fgmres_orth:mass_multidot", nba * (16.0 * (j + 3)) + n * 8.0, [&] {
       if (p->dim == 3)
         mass_multidot<3><<<grid, kT, 0, st>>>(L0, S, j, Uj, s, dVcols, partials.as<double2>());
       else
@@ -841,25 +843,25 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
     launch(ctx, "fgmres_small", 0.0, [&] {
       reduce_dots<<<B * (j + 2), kT, 0, st>>>(S, j, partials.as<double2>(), 0, hcoef.as<double2>());
     });
-    launch(ctx, "fgmres_orth", nb * (16.0 * (j + 3)), [&] {
+    launch(ctx, "fgmres_orth:gs_update", nba * (16.0 * (j + 3)), [&] {
       gs_update<<<grid, kT, 0, st>>>(S, j, 0, s, dVcols, hcoef.as<double2>(), partials.as<double>());
     });
     launch(ctx, "fgmres_small", 0.0, [&] { reduce_norm<<<B, kT, 0, st>>>(S, j, 0, partials.as<double>()); });
     // re-orthogonalisation pass (items whose norm dropped by more than 1/sqrt(2))
-    launch(ctx, "fgmres_orth", 0.0, [&] { multidot<<<grid, kT, 0, st>>>(S, j, s, dVcols, partials.as<double2>()); });
+    launch(ctx, "fgmres_orth:multidot", 0.0, [&] { multidot<<<grid, kT, 0, st>>>(S, j, s, dVcols, partials.as<double2>()); });
     launch(ctx, "fgmres_small", 0.0, [&] {
       reduce_dots<<<B * (j + 2), kT, 0, st>>>(S, j, partials.as<double2>(), 1, hcoef.as<double2>());
     });
-    launch(ctx, "fgmres_orth", 0.0, [&] {
+    launch(ctx, "fgmres_orth:gs_update", 0.0, [&] {
       gs_update<<<grid, kT, 0, st>>>(S, j, 1, s, dVcols, hcoef.as<double2>(), partials.as<double>());
     });
     launch(ctx, "fgmres_small", 0.0, [&] { reduce_norm<<<B, kT, 0, st>>>(S, j, 1, partials.as<double>()); });
-    launch(ctx, "fgmres_vec", nb * 32.0, [&] { normalize<<<grid, kT, 0, st>>>(S, s); });
+    launch(ctx, "fgmres_vec", nba * 32.0, [&] { normalize<<<grid, kT, 0, st>>>(S, s); });
     const int m = j + 1;
     // 3. per-shift small solves, verification, freeze
     launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 0); });
     partials.ensure(sizeof(double) * n_bs * std::max(nblk, S.nblk_tile), st);
-    launch(ctx, "fgmres_verify", nb * (16.0 * (m + 1)) + n * 8.0 * (p->dim + 1), [&] {
+    launch(ctx, "fgmres_verify:verify_residual", nba * (16.0 * (m + 1)) + n * 8.0 * (p->dim + 1), [&] {
       if (p->dim == 3)
         verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
       else
@@ -899,7 +901,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
       LT_CUDA(cudaMemcpyAsync(active, act.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
       launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 1); });
       // restrict flags to the items of this m
-      launch(ctx, "fgmres_verify", 0.0, [&] {
+      launch(ctx, "fgmres_verify:verify_residual", 0.0, [&] {
         if (p->dim == 3)
           verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
         else

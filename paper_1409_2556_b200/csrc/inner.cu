@@ -2253,6 +2253,20 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
                                 const TzMaps* tz) {
   if (dot_nblk) *dot_nblk = 0;
   using V = typename CT<R>::V;
+  // per-level kernel names (class:level) for the profile
+  static const char* const kSmooth[] = {"mg_smooth:l0", "mg_smooth_coarse:l1", "mg_smooth_coarse:l2",
+                                        "mg_smooth_coarse:l3", "mg_smooth_coarse:l4", "mg_smooth_coarse:l5",
+                                        "mg_smooth_coarse:l6", "mg_smooth_coarse:l7", "mg_smooth_coarse:l8"};
+  static const char* const kResid[] = {"mg_residual:l0", "mg_residual:l1", "mg_residual:l2", "mg_residual:l3",
+                                       "mg_residual:l4", "mg_residual:l5", "mg_residual:l6", "mg_residual:l7",
+                                       "mg_residual:l8"};
+  static const char* const kRestr[] = {"mg_restrict:l0", "mg_restrict:l1", "mg_restrict:l2", "mg_restrict:l3",
+                                       "mg_restrict:l4", "mg_restrict:l5", "mg_restrict:l6", "mg_restrict:l7",
+                                       "mg_restrict:l8"};
+  static const char* const kProl[] = {"mg_prolong:l0", "mg_prolong:l1", "mg_prolong:l2", "mg_prolong:l3",
+                                      "mg_prolong:l4", "mg_prolong:l5", "mg_prolong:l6", "mg_prolong:l7",
+                                      "mg_prolong:l8"};
+  const int ln = l < 8 ? l : 8;
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int last = (int)p->levels.size() - 1;
@@ -2267,28 +2281,28 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     const unsigned grid = (unsigned)L.ntiles * (unsigned)Bc;
     const double cb6 = coef + (double)L.n * rb * 3;  // + the three mass-coupling arrays
     for (int c = 0; c < 3; ++c)
-      launch(ctx, "mg_smooth", cell_bytes * 3 * vb + cb6, [&] {
+      launch(ctx, kSmooth[ln], cell_bytes * 3 * vb + cb6, [&] {
         p1_gs_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], c, c == 0);
       });
-    launch(ctx, "mg_residual", cell_bytes * 3 * vb + cb6, [&] {
+    launch(ctx, kResid[ln], cell_bytes * 3 * vb + cb6, [&] {
       p1_residual_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], Rr[l]);
     });
-    launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
+    launch(ctx, kRestr[ln], cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
       p1_restrict_kernel<R><<<(unsigned)Lc.ntiles * Bc, kT, 0, st>>>(L, Lc, bt, Rr[l], F[l + 1]);
     });
     const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr, nullptr, nullptr, tz);
-    launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+    launch(ctx, kProl[ln], cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
       p1_prolong_kernel<R><<<grid, kT, 0, st>>>(L, Lc, bt, ec, X[l]);
     });
     for (int c = 2; c >= 0; --c)
-      launch(ctx, "mg_smooth", cell_bytes * 3 * vb + cb6, [&] {
+      launch(ctx, kSmooth[ln], cell_bytes * 3 * vb + cb6, [&] {
         p1_gs_kernel<R><<<grid, kT, 0, st>>>(L, bt, taus, F[l], X[l], c, 0);
       });
     return X[l];
   }
   if (l == last) {
     dim3 g(blocks_for(L.n, kT / 32), Bc);
-    launch(ctx, "mg_coarse_solve", cell_bytes * 2 * vb, [&] {
+    launch(ctx, "mg_coarse_solve:dense", cell_bytes * 2 * vb, [&] {
       coarse_solve_kernel<V><<<g, kT, 0, st>>>((int)L.n, bt, inv, inv_ld, inv_off, F[l], X[l]);
     });
     return X[l];
@@ -2316,7 +2330,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     // finest-level sweeps are their own class (the roofline kernel); coarser levels pooled.
     // Colour-split: a half sweep moves half of f and of x twice (1.5 c per cell, 1 from zero)
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
-    launch(ctx, l == 0 ? "mg_smooth" : "mg_smooth_coarse", hb + coef, [&] {
+    launch(ctx, kSmooth[ln], hb + coef, [&] {
       if (rbk)
         mg_rb_kernel<0, RB_NI><<<rgrid2, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
                                                                    (float2*)X[l], color, zero_init, dot, rb_blocks(L));
@@ -2336,7 +2350,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     half(0, 0, nullptr);
     half(1, 0, nullptr);
   }
-  launch(ctx, "mg_residual", cell_bytes * 3 * vb + coef, [&] {
+  launch(ctx, kResid[ln], cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
       mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
                                                                (float2*)Rr[l], 0, 0, nullptr, 0);
@@ -2353,7 +2367,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   // pair transfers for aggregation 2 in every direction (3-D, FP32 V-cycle)
   const bool ptr = std::is_same<R, float>::value && DIM == 3 && lev.agg[0] == 2 && lev.agg[1] == 2 &&
                    lev.agg[2] == 2 && (L.nx & 1) == 0;
-  launch(ctx, "mg_restrict", cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
+  launch(ctx, kRestr[ln], cell_bytes * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
       if (ptr && rbk) {
         const unsigned g = (unsigned)(((Lc.nx + 31) / 32) * ((Lc.ny + 3) / 4) * ((Lc.nz + RT_ZC - 1) / RT_ZC));
@@ -2371,7 +2385,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   });
   const V* ec = vcycle<R, DIM>(p, l + 1, Bc, bt, taus, inv, inv_ld, inv_off, X, F, Rr, nullptr, nullptr, tz);
   // coarse correction, then the transpose of the pre-smoother (black, red, ...), in place
-  launch(ctx, "mg_prolong", cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
+  launch(ctx, kProl[ln], cell_bytes * 2 * vb + (double)Lc.n * Bc * vb, [&] {
     if constexpr (std::is_same<R, float>::value) {
       if (ptr && rbk && tz[l].pt) {
         const unsigned g = (unsigned)(((L.nx / 2 + 31) / 32) * ((L.ny + 7) / 8) * ((L.nz + ZM_ZC - 1) / ZM_ZC));
@@ -2660,7 +2674,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
 
   // r = v, u = 0, ||v||^2; items masked out by the caller and zero right-hand sides are done
   launch(ctx, "cocg_scalar", 0.0, [&] { cocg_mask_kernel<<<1, cblk, 0, st>>>(Bc, active, d_done); });
-  launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
+  launch(ctx, "cocg_vec:copy_norm", nb * (48.0 + vb), [&] {
     copy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, v, vs, r, rmg, u, us, (double*)partials.get(), vblk, snx, sny);
   });
   launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_BB, bt, partials.get(), vblk, sc); });
@@ -2675,7 +2689,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   });
   const size_t pend0 = ctx->pending.size();
   if (prof) ctx->profile_tag = 0;
-  launch(ctx, "cocg_vec", nb * 16.0, [&] {
+  launch(ctx, "cocg_vec:zero", nb * 16.0, [&] {
     zero_kernel<<<dim3(std::min<unsigned>(blocks_for(n, kT), 2 * ctx->num_sms), Bc), kT, 0, st>>>(n, d_zero, u, us, Bc);
   });
 
@@ -2689,7 +2703,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
                        &dnb, tzm.data());
     if (dnb == 0) {
       dnb = vblk;
-      launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+      launch(ctx, "cocg_vec:bdot", nb * (16.0 + vb), [&] {
         bdot_kernel<<<grid, kT, 0, st>>>(n, bt, r, z, partials.as<double2>(), vblk, snx, sny);
       });
     }
@@ -2697,7 +2711,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   };
   // z = B r ; rho = r^T z ; p = z
   precondition(OP_RHO);
-  launch(ctx, "cocg_vec", nb * (16.0 + vb), [&] {
+  launch(ctx, "cocg_vec:pupdate", nb * (16.0 + vb), [&] {
     pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 1, snx, sny);
   });
 
@@ -2708,7 +2722,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   FlagSlot* host_ring = ctx->flag_ring_dev();
   // one COCG iteration; u += alpha p is deferred into the direction update (pupdate)
   auto body = [&] {
-    launch(ctx, "cocg_apply", nb * 32.0 + coef, [&] {
+    launch(ctx, "cocg_apply:operator", nb * 32.0 + coef, [&] {
       if (ta_ok)
         apply_tma2_kernel<<<(unsigned)nblk_apply * ((Bc + 1) / 2), kTA, TA2_SMEM, st>>>(
             map_p, map_c64, TzDims{L0.nx, L0.ny, L0.nz, L0.n}, bt, d_taus, q, partials.as<double2>(), nblk_apply);
@@ -2722,7 +2736,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     launch(ctx, "cocg_scalar", 0.0, [&] {
       scalar_kernel<<<Bc, kT, 0, st>>>(OP_ALPHA, bt, partials.get(), nblk_apply, sc);
     });
-    launch(ctx, "cocg_vec", nb * (48.0 + vb), [&] {
+    launch(ctx, "cocg_vec:axpy_norm", nb * (48.0 + vb), [&] {
       axpy_norm_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, q, r, rmg, (double*)partials.get(), vblk, snx, sny);
     });
     launch(ctx, "cocg_scalar", 0.0, [&] { scalar_kernel<<<Bc, kT, 0, st>>>(OP_RR, bt, partials.get(), vblk, sc); });
@@ -2732,7 +2746,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     });
     if (prof) ++ctx->profile_tag;
     precondition(OP_BETA);
-    launch(ctx, "cocg_vec", nb * (64.0 + vb), [&] {
+    launch(ctx, "cocg_vec:pupdate", nb * (64.0 + vb), [&] {
       pupdate_kernel<<<grid, kT, 0, st>>>(n, bt, d_alpha, d_beta, z, pp, u, us, 0, snx, sny);
     });
   };
@@ -2797,7 +2811,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     ctx->profile_tag = -1;
   }
   // the last deferred solution update of the items that stopped after an r update
-  launch(ctx, "cocg_vec", nb * 48.0, [&] {
+  launch(ctx, "cocg_vec:uupdate", nb * 48.0, [&] {
     uupdate_kernel<<<dim3(std::min<unsigned>(blocks_for(n, kT), 2 * ctx->num_sms), Bc), kT, 0, st>>>(
         n, d_pending, d_alpha, pp, u, us);
   });

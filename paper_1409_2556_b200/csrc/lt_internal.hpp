@@ -271,6 +271,7 @@ struct lt_pencil_s {
   std::vector<std::unique_ptr<lt::CoarseFactor>> factors;  // keyed by exact tau
   lt::DeviceBuffer kappa;         // per cell (fine), for Jacobian
   lt::DeviceBuffer storativity;   // per cell (fine)
+  bool from_csr = false;          // built by lt_pencil_create_csr: no parameter fields
   double inner_tol = 1e-12;
   int inner_maxit = 200;
   lt::KeptBasis kept;
@@ -290,6 +291,7 @@ namespace lt {
 
 // pencil.cu
 void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int mem);
+void pencil_build_csr(lt_pencil p, const lt_sparse* K, const lt_sparse* M);
 void apply_batch(lt_pencil p, int level, const double2* taus_dev, const double2* x, int64_t xs,
                  double2* y, int64_t ys, int B, bool mass_only, const char* name);
 void point_weights(const lt_pencil_s* p, const double* point, int64_t* idx, double* w, int* count);

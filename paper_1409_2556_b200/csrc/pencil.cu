@@ -528,6 +528,8 @@ static void pencil_build_p1(lt_pencil p, const double* log_kappa, const double* 
   LT_CUDA(cudaStreamSynchronize(st));
 }
 
+static void build_hierarchy_fd(lt_pencil p);
+
 void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int mem) {
   if (p->kind == LT_GRID_P1_TRI) {
     pencil_build_p1(p, log_kappa, log_s, mem);
@@ -573,7 +575,15 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
   launch(ctx, "assemble", 16.0 * n, [&] { scale_kernel<<<blocks_for(n, kThreads), kThreads, 0, st>>>(sto, F->M, n, hd); });
   p->levels.clear();
   p->levels.push_back(std::move(fine));
+  build_hierarchy_fd(p);
+}
 
+// FD: the multigrid hierarchy below the (assembled) finest level, the FP32 copies and the
+// packed operand arrays of the TMA kernels.
+static void build_hierarchy_fd(lt_pencil p) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int dim = p->dim;
   // Hierarchy: halve every even dimension >= 4 until <= kMaxCoarse cells remain.
   while (p->levels.back()->n > kMaxCoarse) {
     Level& Fl = *p->levels.back();
@@ -645,6 +655,228 @@ void pencil_build(lt_pencil p, const double* log_kappa, const double* log_s, int
     }
   }
   LT_CUDA(cudaStreamSynchronize(st));
+}
+
+// ---- pencils from assembled sparse (K, M) (ShiftedPencil(K, M), shifted_solver.cpp:106-107) --
+// The device operator is matrix-free on a structured grid, so the CSR pair is checked against
+// the stencil of the grid it is declared on and converted to that stencil's coefficients:
+//   FD_CELL: K = the 5-/7-point cell-centred operator (off-diagonals -T_f, diagonal = sum of the
+//            cell's faces, the boundary faces taking what the interior ones leave), M diagonal;
+//   P1_TRI:  the reference's P1 pair on build_mesh's interior nodes (assembly.cpp:69-113):
+//            K on the E/W/N/S edges (the NE/SW hypotenuse entries zero), M on those plus NE/SW.
+// Entries off the stencil, asymmetric pairs or a negative boundary remainder are rejected
+// (std::invalid_argument).  The fine-level operator is the given one (to rounding in the
+// diagonal, which the kernels form as the sum of the faces); the preconditioner hierarchy is
+// coarsened from it (FD: face sums; P1: element fields estimated from the node diagonals).
+namespace {
+
+struct CsrView {
+  int64_t n;
+  const lt_sparse* s;
+  int64_t outer(int64_t r) const {
+    return s->index_bytes == 4 ? (int64_t) static_cast<const int32_t*>(s->outer)[r] : static_cast<const int64_t*>(s->outer)[r];
+  }
+  int64_t inner(int64_t e) const {
+    return s->index_bytes == 4 ? (int64_t) static_cast<const int32_t*>(s->inner)[e] : static_cast<const int64_t*>(s->inner)[e];
+  }
+};
+
+void csr_fail(const char* what, int64_t r, int64_t col) {
+  throw Error(LT_ERR_INVALID_ARGUMENT, std::string("ShiftedPencil(K, M): ") + what + " (row " + std::to_string(r) +
+                                           ", column " + std::to_string(col) + ")");
+}
+
+// set a symmetric coupling once from either triangle; the second sighting must agree
+void set_pair(std::vector<double>& arr, std::vector<char>& seen, int64_t idx, double v, int64_t r, int64_t col) {
+  if (!seen[idx]) {
+    arr[idx] = v;
+    seen[idx] = 1;
+  } else if (std::fabs(arr[idx] - v) > 1e-12 * std::max(std::fabs(arr[idx]), std::fabs(v))) {
+    csr_fail("matrix is not symmetric", r, col);
+  }
+}
+
+// face / boundary remainder split: rem over nb boundary faces (FD) or edges (P1)
+void split_boundary(double rem, double diag, int nb, int64_t r, double* faces[], int nf) {
+  const double tiny = 1e-12 * std::fabs(diag);
+  if (nb == 0) {
+    if (std::fabs(rem) > tiny) csr_fail("row sum of K is not zero on an interior unknown", r, r);
+    return;
+  }
+  if (rem < -tiny) csr_fail("negative boundary coupling in K", r, r);
+  for (int f = 0; f < nf; ++f) *faces[f] = std::max(rem, 0.0) / nb;
+}
+
+}  // namespace
+
+void pencil_build_csr(lt_pencil p, const lt_sparse* K, const lt_sparse* M) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const CsrView k{p->n, K}, m{p->n, M};
+  const int64_t n = p->n;
+  if (p->kind == LT_GRID_FD_CELL) {
+    const int nx = p->grid.shape[0], ny = p->grid.shape[1], nz = p->dim == 3 ? p->grid.shape[2] : 1;
+    LT_REQUIRE((int64_t)nx * ny * nz == n, "ShiftedPencil(K, M): rows do not match the grid's cell count");
+    const int64_t nfx = (int64_t)(nx + 1) * ny * nz, nfy = (int64_t)nx * (ny + 1) * nz,
+                  nfz = p->dim == 3 ? (int64_t)nx * ny * (nz + 1) : 0;
+    std::vector<double> Tx(nfx, 0.0), Ty(nfy, 0.0), Tz(nfz, 0.0), Md(n, 0.0);
+    std::vector<char> sx(nfx, 0), sy(nfy, 0), sz(nfz, 0);
+    std::vector<double> diag(n, 0.0);
+    const int64_t plane = (int64_t)nx * ny;
+    for (int64_t r = 0; r < n; ++r) {
+      const int i = (int)(r % nx), j = (int)((r / nx) % ny), kk = (int)(r / plane);
+      for (int64_t e = k.outer(r); e < k.outer(r + 1); ++e) {
+        const int64_t col = k.inner(e);
+        const double v = K->values[e];
+        if (col < 0 || col >= n) csr_fail("column index out of range", r, col);
+        const int64_t d = col - r;
+        if (d == 0) { diag[r] += v; continue; }
+        if (d == 1 && i + 1 < nx) set_pair(Tx, sx, ((int64_t)kk * ny + j) * (nx + 1) + i + 1, -v, r, col);
+        else if (d == -1 && i > 0) set_pair(Tx, sx, ((int64_t)kk * ny + j) * (nx + 1) + i, -v, r, col);
+        else if (d == nx && j + 1 < ny) set_pair(Ty, sy, ((int64_t)kk * (ny + 1) + j + 1) * nx + i, -v, r, col);
+        else if (d == -nx && j > 0) set_pair(Ty, sy, ((int64_t)kk * (ny + 1) + j) * nx + i, -v, r, col);
+        else if (p->dim == 3 && d == plane && kk + 1 < nz) set_pair(Tz, sz, ((int64_t)(kk + 1) * ny + j) * nx + i, -v, r, col);
+        else if (p->dim == 3 && d == -plane && kk > 0) set_pair(Tz, sz, ((int64_t)kk * ny + j) * nx + i, -v, r, col);
+        else if (v != 0.0) csr_fail("K entry outside the grid's finite-difference stencil", r, col);
+      }
+      for (int64_t e = m.outer(r); e < m.outer(r + 1); ++e) {
+        const int64_t col = m.inner(e);
+        if (col == r) Md[r] += M->values[e];
+        else if (M->values[e] != 0.0) csr_fail("M is not diagonal (the cell-centred mass is)", r, col);
+      }
+    }
+    for (int64_t r = 0; r < n; ++r) {
+      const int i = (int)(r % nx), j = (int)((r / nx) % ny), kk = (int)(r / plane);
+      double* w = &Tx[((int64_t)kk * ny + j) * (nx + 1) + i];
+      double* e = w + 1;
+      double* s = &Ty[((int64_t)kk * (ny + 1) + j) * nx + i];
+      double* nn = s + nx;
+      double* b = p->dim == 3 ? &Tz[((int64_t)kk * ny + j) * nx + i] : nullptr;
+      double* t = p->dim == 3 ? b + plane : nullptr;
+      double rem = diag[r];
+      double* bnd[6];
+      int nb = 0;
+      auto face = [&](double* f, bool boundary) {
+        if (boundary) bnd[nb++] = f;
+        else rem -= *f;
+      };
+      face(w, i == 0);
+      face(e, i == nx - 1);
+      face(s, j == 0);
+      face(nn, j == ny - 1);
+      if (p->dim == 3) {
+        face(b, kk == 0);
+        face(t, kk == nz - 1);
+      }
+      split_boundary(rem, diag[r], nb, r, bnd, nb);
+    }
+    auto fine = std::make_unique<Level>();
+    fine->nx = nx;
+    fine->ny = ny;
+    fine->nz = nz;
+    alloc_level(*fine, p->dim, st);
+    LT_CUDA(cudaMemcpyAsync(fine->Tx, Tx.data(), sizeof(double) * nfx, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(fine->Ty, Ty.data(), sizeof(double) * nfy, cudaMemcpyHostToDevice, st));
+    if (nfz) LT_CUDA(cudaMemcpyAsync(fine->Tz, Tz.data(), sizeof(double) * nfz, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(fine->M, Md.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaStreamSynchronize(st));  // the host arrays go out of scope
+    p->levels.clear();
+    p->levels.push_back(std::move(fine));
+    build_hierarchy_fd(p);
+    return;
+  }
+  // P1_TRI: interior node grid nx x nx, unknown a = j nx + i; Tx[(j)(nx+1) + i] = edge (i-1, i)
+  const int nps = p->grid.shape[0], nx = nps - 2;
+  LT_REQUIRE((int64_t)nx * nx == n, "ShiftedPencil(K, M): rows do not match build_mesh's interior nodes");
+  const double h = p->grid.h, h2 = h * h;
+  const int64_t nfx = (int64_t)(nx + 1) * nx, nfy = (int64_t)nx * (nx + 1);
+  std::vector<double> Tx(nfx, 0.0), Ty(nfy, 0.0), Mx(nfx, 0.0), My(nfy, 0.0), Mn(n, 0.0), Mdg(n, 0.0), diag(n, 0.0);
+  std::vector<char> sx(nfx, 0), sy(nfy, 0), smx(nfx, 0), smy(nfy, 0), smd(n, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    const int i = (int)(r % nx), j = (int)(r / nx);
+    for (int64_t e = k.outer(r); e < k.outer(r + 1); ++e) {
+      const int64_t col = k.inner(e);
+      const double v = K->values[e];
+      if (col < 0 || col >= n) csr_fail("column index out of range", r, col);
+      const int64_t d = col - r;
+      if (d == 0) diag[r] += v;
+      else if (d == 1 && i + 1 < nx) set_pair(Tx, sx, (int64_t)j * (nx + 1) + i + 1, -v, r, col);
+      else if (d == -1 && i > 0) set_pair(Tx, sx, (int64_t)j * (nx + 1) + i, -v, r, col);
+      else if (d == nx && j + 1 < nx) set_pair(Ty, sy, (int64_t)(j + 1) * nx + i, -v, r, col);
+      else if (d == -nx && j > 0) set_pair(Ty, sy, (int64_t)j * nx + i, -v, r, col);
+      else if (v != 0.0) csr_fail("K entry outside the P1 edge stencil of build_mesh", r, col);
+    }
+    for (int64_t e = m.outer(r); e < m.outer(r + 1); ++e) {
+      const int64_t col = m.inner(e);
+      const double v = M->values[e];
+      if (col < 0 || col >= n) csr_fail("column index out of range", r, col);
+      const int64_t d = col - r;
+      if (d == 0) Mn[r] += v;
+      else if (d == 1 && i + 1 < nx) set_pair(Mx, smx, (int64_t)j * (nx + 1) + i + 1, v, r, col);
+      else if (d == -1 && i > 0) set_pair(Mx, smx, (int64_t)j * (nx + 1) + i, v, r, col);
+      else if (d == nx && j + 1 < nx) set_pair(My, smy, (int64_t)(j + 1) * nx + i, v, r, col);
+      else if (d == -nx && j > 0) set_pair(My, smy, (int64_t)j * nx + i, v, r, col);
+      else if (d == nx + 1 && i + 1 < nx && j + 1 < nx) set_pair(Mdg, smd, r, v, r, col);
+      else if (d == -(nx + 1) && i > 0 && j > 0) set_pair(Mdg, smd, r - nx - 1, v, r, col);
+      else if (v != 0.0) csr_fail("M entry outside the P1 stencil of build_mesh", r, col);
+    }
+  }
+  for (int64_t r = 0; r < n; ++r) {
+    const int i = (int)(r % nx), j = (int)(r / nx);
+    double* w = &Tx[(int64_t)j * (nx + 1) + i];
+    double* e = w + 1;
+    double* s = &Ty[(int64_t)j * nx + i];
+    double* nn = s + nx;
+    double rem = diag[r];
+    double* bnd[4];
+    int nb = 0;
+    auto edge = [&](double* f, bool boundary) {
+      if (boundary) bnd[nb++] = f;
+      else rem -= *f;
+    };
+    edge(w, i == 0);
+    edge(e, i == nx - 1);
+    edge(s, j == 0);
+    edge(nn, j == nx - 1);
+    split_boundary(rem, diag[r], nb, r, bnd, nb);
+  }
+  // element fields for the coarse levels: kappa_T from the mean of its interior vertices'
+  // K_aa / 4, S_T from their 2 M_aa / h^2 (exact for uniform fields)
+  const int nc = nps - 1;
+  const int64_t nelem = 2 * (int64_t)nc * nc;
+  std::vector<double> lk(nelem), ls(nelem);
+  auto node = [&](int I, int J, double& kv, double& sv, int& cnt) {
+    if (I <= 0 || J <= 0 || I >= nps - 1 || J >= nps - 1) return;
+    const int64_t a = (int64_t)(J - 1) * nx + (I - 1);
+    kv += diag[a] / 4.0;
+    sv += 2.0 * Mn[a] / h2;
+    ++cnt;
+  };
+  for (int cj = 0; cj < nc; ++cj)
+    for (int ci = 0; ci < nc; ++ci)
+      for (int up = 0; up < 2; ++up) {
+        double kv = 0.0, sv = 0.0;
+        int cnt = 0;
+        node(ci, cj, kv, sv, cnt);
+        node(ci + 1, cj + 1, kv, sv, cnt);
+        if (up) node(ci, cj + 1, kv, sv, cnt);
+        else node(ci + 1, cj, kv, sv, cnt);
+        const int64_t el = 2 * ((int64_t)cj * nc + ci) + up;
+        lk[el] = std::log(std::max(kv / std::max(cnt, 1), 1e-300));
+        ls[el] = std::log(std::max(sv / std::max(cnt, 1), 1e-300));
+      }
+  pencil_build_p1(p, lk.data(), ls.data(), LT_MEM_HOST);
+  // the finest level is the given operator
+  Level& F = *p->levels[0];
+  LT_CUDA(cudaMemcpyAsync(F.Tx, Tx.data(), sizeof(double) * nfx, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(F.Ty, Ty.data(), sizeof(double) * nfy, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(F.M, Mn.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(F.Mx, Mx.data(), sizeof(double) * nfx, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(F.My, My.data(), sizeof(double) * nfy, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(F.Md, Mdg.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  make_fp32_copies(p);
+  LT_CUDA(cudaStreamSynchronize(st));
+  (void)h2;
 }
 
 }  // namespace lt

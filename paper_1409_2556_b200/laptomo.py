@@ -327,12 +327,46 @@ class ShiftedPencil:
         check(lib().lt_pencil_create_grid(self.ctx.handle, C.byref(g), dptr(lk), dptr(ls), capi.LT_MEM_HOST,
                                           C.byref(self._h)))
 
+    @classmethod
+    def from_csr(cls, grid, stiffness, mass, ctx: Optional[Context] = None) -> "ShiftedPencil":
+        """ShiftedPencil(K, M) (shifted_solver.hpp:90): an assembled sparse pair (SciPy sparse,
+        any format) declared on `grid` (Grid for the FD operator, Mesh2D for the reference's P1
+        pair on build_mesh's interior nodes); checked against that stencil on the host and
+        converted to it (lt_pencil_create_csr)."""
+        import scipy.sparse as sp
+        self = cls.__new__(cls)
+        self.ctx = ctx or default_context()
+        self.grid = grid
+        K = sp.csr_matrix(stiffness)
+        M = sp.csr_matrix(mass)
+        n = K.shape[0]
+        if K.shape != (n, n) or M.shape != (n, n):
+            raise ValueError("ShiftedPencil(K, M): square matrices of equal size required")
+        keep = []
+
+        def sparse(A):
+            outer = np.ascontiguousarray(A.indptr.astype(np.int64))
+            inner = np.ascontiguousarray(A.indices.astype(np.int64))
+            vals = np.ascontiguousarray(A.data.astype(np.float64))
+            keep.extend([outer, inner, vals])
+            return capi.LtSparse(outer.ctypes.data, inner.ctypes.data, dptr(vals), 8)
+
+        ks, ms = sparse(K), sparse(M)
+        self._h = C.c_void_p()
+        g = grid.c()
+        check(lib().lt_pencil_create_csr(self.ctx.handle, C.byref(g), int(n), C.byref(ks), C.byref(ms),
+                                         C.byref(self._h)))
+        return self
+
     @property
     def handle(self):
         return self._h
 
     def rows(self) -> int:
         return int(lib().lt_pencil_rows(self._h))
+
+    def parameters(self) -> int:
+        return int(lib().lt_pencil_parameters(self._h))
 
     def levels(self) -> int:
         return int(lib().lt_pencil_levels(self._h))
@@ -526,11 +560,15 @@ def solve_shifted_direct(pencil: ShiftedPencil, b, shifts):
 
 
 def residual_estimate(state: FlexibleBasisState, z, y_fom) -> float:
-    """shifted_solver.cpp:334-343."""
+    """shifted_solver.cpp:334-343 (lt_residual_estimate)."""
     m = state.steps()
-    if m < 1 or len(y_fom) != m:
-        raise ValueError("residual_estimate: FOM coefficients of length m required")
-    return abs(state.Hbar[m, m - 1] * (z - state.taus[m - 1]) * y_fom[m - 1])
+    H = np.ascontiguousarray(state.Hbar.T.astype(np.complex128))  # column-major (m+1) x m
+    T = np.ascontiguousarray(np.asarray(state.taus, dtype=np.complex128))
+    y = np.ascontiguousarray(np.asarray(y_fom, dtype=np.complex128).ravel())
+    out = np.zeros(1)
+    check(lib().lt_residual_estimate(cptr(H) if H.size else None, cptr(T) if T.size else None, int(m), lc(z),
+                                     cptr(y) if y.size else None, int(y.size), dptr(out)))
+    return float(out[0])
 
 
 # ---- forward -----------------------------------------------------------------------------
