@@ -282,6 +282,40 @@ lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out,
 /* ThtForwardModel::predict (jacobian.cpp:158-187): n_meas predictions. */
 lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_out);
 
+/* ---- split build of one Jacobian time slice across ranks -------------
+ * The rows of jacobian.cpp:205-246 are independent, and each needs phi_s and psi_r on the same
+ * cells: one rank per GPU solves a contiguous range of the slice's items (sources, then
+ * receivers: the lockstep batch of lt_jacobian_slice) and keeps their bases; the caller moves
+ * every z-slab's basis rows (the slab's planes plus one halo plane on each interior side) to
+ * the slab's owner in one all-to-all (NCCL over NVLink; paper_1409_2556_b200/split_build.py);
+ * each rank then assembles the J columns of its slab.  J rows need no reduction.
+ * Planes are z-planes (3-D) or rows (2-D) of the FD grid pencil.                           */
+typedef struct lt_split_s* lt_split;
+/* Solves items [item0, item1) of time slice `time_index` (ConvergenceError like
+ * lt_jacobian_slice). */
+lt_status lt_split_solve(lt_pencil p, const lt_experiment* exp, int time_index, int item0, int item1,
+                         lt_split* out);
+/* m: basis columns of this part (the all-to-all pads every part to the max over ranks). */
+int lt_split_columns(lt_split s);
+/* Y[(b ns + k) m_pad + j] (zero for j >= m_used), m_used[b ns + k] for this part's items
+ * (host arrays; ns = n_quad / 2). */
+lt_status lt_split_coefficients(lt_split s, int m_pad, lt_complex* Y, int* m_used);
+/* Basis rows of planes [plane0, plane1): dst[(j (item1-item0) + b) cells + a'], j < m_pad
+ * (zero columns past this part's m), cells = (plane1-plane0) x plane size; host or device. */
+lt_status lt_split_export(lt_split s, int plane0, int plane1, int m_pad, lt_complex* dst, int mem);
+/* Predictions (jacobian.cpp:241-244) of this part's sources at every receiver: (s, r) row-major
+ * over the part's sources (none if the part holds only receivers). */
+lt_status lt_split_predictions(lt_split s, double* predictions_out);
+lt_status lt_split_destroy(lt_split s);
+/* The J columns of slab [plane0, plane1) from every item's basis rows over the slab and its
+ * halo planes (planes plane0 - (plane0 > 0) .. plane1 + (plane1 < planes)):
+ *   U_slab[(j B + b) view_cells + a'], B = n_src + n_rec, j < m;  Y, m_used as
+ *   lt_split_coefficients over all B items (host);
+ *   jac_out rows (s n_rec + r), kappa block then storativity block, n_slab columns each. */
+lt_status lt_jacobian_assemble_slab(lt_pencil p, const lt_experiment* exp, int time_index, int plane0,
+                                    int plane1, const lt_complex* U_slab, int m, const lt_complex* Y,
+                                    const int* m_used, int mem, double* jac_out);
+
 /* ---- fields (sample_field / sample_field_on_mesh, fields.hpp:27-44, fields.cpp:84-123) --
  * The reference draws mean + C zeta with C C^T = Q, Q the dense exponential covariance over
  * the element centres (Cholesky).  On a structured grid this draws the same Gaussian law by

@@ -131,6 +131,13 @@ SIGNATURES = {
     "lt_jacobian_slice": (I, [P, C.POINTER(LtExperiment), I, I, PD, PD]),
     "lt_jacobian": (I, [P, C.POINTER(LtExperiment), PD, PD]),
     "lt_predict": (I, [P, C.POINTER(LtExperiment), PD]),
+    "lt_split_solve": (I, [P, C.POINTER(LtExperiment), I, I, I, C.POINTER(P)]),
+    "lt_split_columns": (I, [P]),
+    "lt_split_coefficients": (I, [P, I, PC, PI]),
+    "lt_split_export": (I, [P, I, I, I, P, I]),
+    "lt_split_predictions": (I, [P, PD]),
+    "lt_split_destroy": (I, [P]),
+    "lt_jacobian_assemble_slab": (I, [P, C.POINTER(LtExperiment), I, I, I, P, I, PC, PI, I, P]),
 }
 
 _lib = None

@@ -643,4 +643,85 @@ lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_
   });
 }
 
+lt_status lt_split_solve(lt_pencil p, const lt_experiment* exp, int time_index, int item0, int item1, lt_split* out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(exp && out, "lt_split_solve: null argument");
+    LT_REQUIRE(exp->n_src >= 1 && exp->n_rec >= 1 && exp->n_times >= 1, "ThtForwardModel: experiment must be nonempty");
+    set_device(p->ctx);
+    auto* s = new lt_split_s();
+    s->p = p;
+    s->t = time_index;
+    s->item0 = item0;
+    s->item1 = item1;
+    const int d = p->dim;
+    s->sources.assign(exp->sources, exp->sources + (size_t)exp->n_src * d);
+    s->receivers.assign(exp->receivers, exp->receivers + (size_t)exp->n_rec * d);
+    s->rates.assign(exp->rates, exp->rates + exp->n_src);
+    s->times.assign(exp->times, exp->times + exp->n_times);
+    s->ex = *exp;
+    s->ex.sources = s->sources.data();
+    s->ex.receivers = s->receivers.data();
+    s->ex.rates = s->rates.data();
+    s->ex.times = s->times.data();
+    try {
+      lt::split_solve(s);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int lt_split_columns(lt_split s) { return s ? (int)s->res.U.size() : -1; }
+
+lt_status lt_split_coefficients(lt_split s, int m_pad, lt_complex* Y, int* m_used) {
+  return guard([&] {
+    LT_REQUIRE(s && Y && m_used, "lt_split_coefficients: null argument");
+    set_device(s->p->ctx);
+    lt::split_coefficients(s, reinterpret_cast<double2*>(Y), m_used, m_pad);
+  });
+}
+
+lt_status lt_split_export(lt_split s, int plane0, int plane1, int m_pad, lt_complex* dst, int mem) {
+  return guard([&] {
+    LT_REQUIRE(s && dst, "lt_split_export: null argument");
+    set_device(s->p->ctx);
+    lt::split_export(s, plane0, plane1, m_pad, reinterpret_cast<double2*>(dst), mem);
+  });
+}
+
+lt_status lt_split_predictions(lt_split s, double* predictions_out) {
+  return guard([&] {
+    LT_REQUIRE(s && predictions_out, "lt_split_predictions: null argument");
+    set_device(s->p->ctx);
+    lt::split_predictions(s, predictions_out);
+  });
+}
+
+lt_status lt_split_destroy(lt_split s) {
+  return guard([&] {
+    if (!s) return;
+    set_device(s->p->ctx);
+    cudaStreamSynchronize(s->p->ctx->stream);
+    delete s;
+  });
+}
+
+lt_status lt_jacobian_assemble_slab(lt_pencil p, const lt_experiment* exp, int time_index, int plane0, int plane1,
+                                    const lt_complex* U_slab, int m, const lt_complex* Y, const int* m_used, int mem,
+                                    double* jac_out) {
+  return guard([&] {
+    check_pencil(p);
+    LT_REQUIRE(exp && U_slab && Y && m_used && jac_out, "lt_jacobian_assemble_slab: null argument");
+    LT_REQUIRE(exp->n_src >= 1 && exp->n_rec >= 1 && exp->n_times >= 1, "ThtForwardModel: experiment must be nonempty");
+    set_device(p->ctx);
+    const int nplanes = p->dim == 3 ? p->grid.shape[2] : p->grid.shape[1];
+    const int lo = plane0 > 0 ? 1 : 0, hi = plane1 < nplanes ? 1 : 0;
+    lt::jacobian_assemble_slab(p, *exp, time_index, plane0, plane1, lo, hi, reinterpret_cast<const double2*>(U_slab), m,
+                               reinterpret_cast<const double2*>(Y), m_used, mem, jac_out);
+  });
+}
+
 }  // extern "C"

@@ -1295,6 +1295,163 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
     for (int t = 0; t < n_times; ++t) diag_out[t] = diags[t];
 }
 
+// FD with <= 16 sources and <= 64 receivers: the tensor-core Jacobian on cell-major fields
+bool use_tensor_jacobian(lt_pencil p, int n_src, int n_rec) {
+  const int B = n_src + n_rec;
+  return p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
+         (p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B)) <= 227 * 1024;
+}
+
+// The forward (sources, b_s) and adjoint (receivers, -e_r) shifted families of items
+// [item0, item1) of one time slice (jacobian.cpp:205-227; items = sources then receivers) as one
+// lockstep FGMRES-Sh batch; raises ConvergenceError like solve_family_or_throw (cpp:19-43).
+void solve_slice_items(lt_pencil p, const lt_experiment& ex, const std::vector<cd>& nodes, int item0, int item1,
+                       OuterResult& res) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int n_src = ex.n_src, n_rec = ex.n_rec, ns = ex.n_quad / 2;
+  const int64_t n = p->n;
+  PointSet src = make_points(p, ex.sources, n_src);
+  PointSet rec = make_points(p, ex.receivers, n_rec);
+  const int BT = n_src + n_rec;
+  LT_REQUIRE(item0 >= 0 && item0 < item1 && item1 <= BT, "jacobian: bad item range");
+  // rhs: sources b_s, receivers -e_r  (jacobian.cpp:216, 227, solve_adjoint_fields cpp:49)
+  // sparse point weights of all items (sources +w, receivers -w), scattered on the device
+  std::vector<int64_t> pidx((size_t)BT * 8, 0);
+  std::vector<double> pw((size_t)BT * 8, 0.0);
+  std::vector<int> pcnt(BT, 0);
+  for (int s = 0; s < n_src; ++s) {
+    pcnt[s] = src.cnt[s];
+    for (int q = 0; q < src.cnt[s]; ++q) { pidx[s * 8 + q] = src.idx[s * 8 + q]; pw[s * 8 + q] = src.w[s * 8 + q]; }
+  }
+  for (int r = 0; r < n_rec; ++r) {
+    pcnt[n_src + r] = rec.cnt[r];
+    for (int q = 0; q < rec.cnt[r]; ++q) {
+      pidx[(n_src + r) * 8 + q] = rec.idx[r * 8 + q];
+      pw[(n_src + r) * 8 + q] = -rec.w[r * 8 + q];
+    }
+  }
+  // this part's items only
+  const int B = item1 - item0;
+  pidx.erase(pidx.begin(), pidx.begin() + (size_t)item0 * 8);
+  pw.erase(pw.begin(), pw.begin() + (size_t)item0 * 8);
+  pcnt.erase(pcnt.begin(), pcnt.begin() + item0);
+  DeviceBuffer rhs(sizeof(double2) * (size_t)B * n, st);
+  {
+    DeviceBuffer didx(sizeof(int64_t) * pidx.size(), st), dwt(sizeof(double) * pw.size(), st), dcnt(sizeof(int) * B, st);
+    LT_CUDA(cudaMemcpyAsync(didx.get(), pidx.data(), sizeof(int64_t) * pidx.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dwt.get(), pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemcpyAsync(dcnt.get(), pcnt.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
+    LT_CUDA(cudaMemsetAsync(rhs.get(), 0, rhs.bytes(), st));
+    launch(ctx, "rhs", 0.0, [&] {
+      scatter_points<<<blocks_for((int64_t)B * 8, 128), 128, 0, st>>>(n, B, didx.as<int64_t>(), dwt.as<double>(),
+                                                                      dcnt.as<int>(), rhs.as<double2>());
+    });
+  }
+  std::vector<std::vector<cd>> shifts(B, nodes);
+  {
+    TraceScope tr(ctx, "  solve_families", B);
+    solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
+  }
+  // forward failures first (jacobian.cpp:214-218), then adjoint
+  {
+    OuterResult* r = &res;
+    for (int b = 0; b < B; ++b) {
+      std::vector<int> bad;
+      for (int k = 0; k < ns; ++k)
+        if (!r->status[(size_t)b * ns + k].converged) bad.push_back(k);
+      if (!bad.empty()) {
+        g_last_unconverged = bad;
+        throw Error(LT_ERR_NOT_CONVERGED, std::string(item0 + b < n_src ? "forward solve" : "adjoint solve") + ": " +
+                                              std::to_string(bad.size()) + " of " + std::to_string(ns) +
+                                              " shifts unconverged after " + std::to_string(r->iterations[b]) + " iterations");
+      }
+    }
+  }
+}
+
+// FD Jacobian rows of every (source, receiver) pair over the cells of the view Lv (the whole
+// fine grid, or a z-slab with its halo planes for the split build): J[(s n_rec + r) ldj + a]
+// (kappa block) and J[... + s_off + a] (storativity block, include_s), fields over the view's
+// cells, cell-major for the tensor-core kernels (tensor_jac) else RHS-major; dw = the w_k then
+// wz_k factors (n_shifts each).  kappa / stor are the view's per-cell fields.
+void fd_jacobian_kernels(lt_pencil p, const LevelView& Lv, const double* kappa, const double* stor,
+                         const double2* fields, int n_src, int n_rec, int ns, const double2* dw, bool tensor_jac,
+                         bool include_s, double* J, int64_t ldj, int64_t s_off) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const int B = n_src + n_rec;
+  const double h = p->grid.h;
+  const double face_scale = p->dim == 3 ? h : 1.0;
+  const double hd = p->dim == 3 ? h * h * h : h * h;
+  const double bytes = (double)Lv.n * (16.0 * ns * B + 8.0 * n_src * n_rec * (include_s ? 2 : 1));
+  // 4-cell tiles with 32-byte J stores where rows allow it (2-cell tiles otherwise)
+  const bool tile4 = tensor_jac && Lv.nx % J4_TC == 0 && ldj % 4 == 0 && s_off % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(J) & 31) == 0 &&
+                     (p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B)) <= 227 * 1024;
+  if (tile4) {
+    const LevelView& L = Lv;
+    const int ntiles = (L.nx / J4_TC) * L.ny * L.nz;
+    const int grid = std::min(ntiles, ctx->num_sms);
+    const size_t smem = p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B);
+    auto fn = p->dim == 3 ? jacobian_mma4_kernel<3> : jacobian_mma4_kernel<2>;
+    LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
+    const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
+                              (uint64_t)Lv.n * B * 16};
+    const uint32_t boxC[5] = {2 * (uint32_t)B, 6, 1, 1, 2}, boxF[5] = {2 * (uint32_t)B, 4, 1, 1, 2};
+    const CUtensorMap mC = tma_map_8b((void*)fields, 5, dims, strd, boxC);
+    const CUtensorMap mF = tma_map_8b((void*)fields, 5, dims, strd, boxF);
+    launch(ctx, "jacobian", bytes, [&] {
+      fn<<<grid, J4_THREADS, smem, st>>>(mC, mF, L, kappa, stor, hd,
+                                         face_scale, n_src, n_rec, ns, dw + ns, J,
+                                         include_s ? J + s_off : nullptr, ldj, ntiles);
+    });
+  } else if (tensor_jac) {
+    const LevelView& L = Lv;
+    const int ntiles = ((L.nx + JW_TC - 1) / JW_TC) * L.ny * L.nz;
+    const int grid = std::min(ntiles, ctx->num_sms);
+    const size_t smem = p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B);
+    auto fn = p->dim == 3 ? jacobian_mma_kernel<3> : jacobian_mma_kernel<2>;
+    LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // 5-D maps over the cell-major fields: (item re/im, x, y, z, shift)
+    const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
+    const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
+                              (uint64_t)Lv.n * B * 16};
+    const uint32_t boxA[5] = {2 * (uint32_t)B, 4, 3, 1, 2}, boxB[5] = {2 * (uint32_t)B, 2, 1, 3, 2};
+    const CUtensorMap mA = tma_map_8b((void*)fields, 5, dims, strd, boxA);
+    const CUtensorMap mB = tma_map_8b((void*)fields, 5, dims, strd, boxB);
+    launch(ctx, "jacobian", bytes, [&] {
+      fn<<<grid, JW_THREADS, smem, st>>>(mA, mB, L, kappa, stor, hd,
+                                         face_scale, n_src, n_rec, ns, nullptr, dw + ns, J,
+                                         include_s ? J + s_off : nullptr, ldj, ntiles);
+    });
+  } else {
+    const int nsub_s = (n_src + SB - 1) / SB, nsub_r = (n_rec + RB - 1) / RB;
+  const int nsub_total = nsub_s * nsub_r;
+  LT_REQUIRE(nsub_total <= kT, "jacobian: too many source/receiver blocks for one CTA (n_src*n_rec too large)");
+  const int nf = 2 * p->dim + 1;
+  int TC = std::max(1, kT / nsub_total);
+  const LevelView& L = Lv;
+  TC = std::min(TC, L.nx);
+  auto smem_for = [&](int tc) {
+    return sizeof(double2) * (size_t)(nf - 1) * B * tc + sizeof(double) * nf * tc + sizeof(int64_t) * 2 * p->dim * tc;
+  };
+  while (TC > 1 && smem_for(TC) > 110 * 1024) TC /= 2;  // two CTAs per SM
+  LT_REQUIRE(nf * TC <= kT, "jacobian: tile too wide");
+  const size_t smem = smem_for(TC);
+  const int tiles_x = (L.nx + TC - 1) / TC;
+  const unsigned grid = (unsigned)(tiles_x * (int64_t)L.ny * L.nz);
+  auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
+  LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  launch(ctx, "jacobian", bytes, [&] {
+    fn<<<grid, kT, smem, st>>>(L, kappa, stor, hd, face_scale,
+                               fields, n_src, n_rec, ns, dw, dw + ns, TC,
+                               tiles_x, nsub_r, nsub_total, J, include_s ? J + s_off : nullptr, ldj);
+  });
+  }
+}
+
 void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double* jac_out, double* pred_out) {
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
@@ -1311,66 +1468,17 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
   std::vector<cd> nodes, weights;
   talbot_build(ex.n_quad, ex.times[t], ex.contour, nullptr, &nodes, nullptr, &weights);
 
-  PointSet src = make_points(p, ex.sources, n_src);
-  PointSet rec = make_points(p, ex.receivers, n_rec);
   const int B = n_src + n_rec;
-  // rhs: sources b_s, receivers -e_r  (jacobian.cpp:216, 227, solve_adjoint_fields cpp:49)
-  // sparse point weights of all items (sources +w, receivers -w), scattered on the device
-  std::vector<int64_t> pidx((size_t)B * 8, 0);
-  std::vector<double> pw((size_t)B * 8, 0.0);
-  std::vector<int> pcnt(B, 0);
-  for (int s = 0; s < n_src; ++s) {
-    pcnt[s] = src.cnt[s];
-    for (int q = 0; q < src.cnt[s]; ++q) { pidx[s * 8 + q] = src.idx[s * 8 + q]; pw[s * 8 + q] = src.w[s * 8 + q]; }
-  }
-  for (int r = 0; r < n_rec; ++r) {
-    pcnt[n_src + r] = rec.cnt[r];
-    for (int q = 0; q < rec.cnt[r]; ++q) {
-      pidx[(n_src + r) * 8 + q] = rec.idx[r * 8 + q];
-      pw[(n_src + r) * 8 + q] = -rec.w[r * 8 + q];
-    }
-  }
-  DeviceBuffer rhs(sizeof(double2) * (size_t)B * n, st);
-  {
-    DeviceBuffer didx(sizeof(int64_t) * pidx.size(), st), dwt(sizeof(double) * pw.size(), st), dcnt(sizeof(int) * B, st);
-    LT_CUDA(cudaMemcpyAsync(didx.get(), pidx.data(), sizeof(int64_t) * pidx.size(), cudaMemcpyHostToDevice, st));
-    LT_CUDA(cudaMemcpyAsync(dwt.get(), pw.data(), sizeof(double) * pw.size(), cudaMemcpyHostToDevice, st));
-    LT_CUDA(cudaMemcpyAsync(dcnt.get(), pcnt.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st));
-    LT_CUDA(cudaMemsetAsync(rhs.get(), 0, rhs.bytes(), st));
-    launch(ctx, "rhs", 0.0, [&] {
-      scatter_points<<<blocks_for((int64_t)B * 8, 128), 128, 0, st>>>(n, B, didx.as<int64_t>(), dwt.as<double>(),
-                                                                      dcnt.as<int>(), rhs.as<double2>());
-    });
-  }
-  std::vector<std::vector<cd>> shifts(B, nodes);
   OuterResult res;
-  {
-    TraceScope tr(ctx, "  solve_families", B);
-    solve_families(p, ex.solver, B, rhs.as<double2>(), shifts, res);
-  }
-  // forward failures first (jacobian.cpp:214-218), then adjoint
-  {
-    OuterResult* r = &res;
-    for (int b = 0; b < B; ++b) {
-      std::vector<int> bad;
-      for (int k = 0; k < ns; ++k)
-        if (!r->status[(size_t)b * ns + k].converged) bad.push_back(k);
-      if (!bad.empty()) {
-        g_last_unconverged = bad;
-        throw Error(LT_ERR_NOT_CONVERGED, std::string(b < n_src ? "forward solve" : "adjoint solve") + ": " +
-                                              std::to_string(bad.size()) + " of " + std::to_string(ns) +
-                                              " shifts unconverged after " + std::to_string(r->iterations[b]) + " iterations");
-      }
-    }
-  }
+  solve_slice_items(p, ex, nodes, 0, B, res);
+  const PointSet rec = make_points(p, ex.receivers, n_rec);
   // fields: phi_{s,k} = qhat_k U_s y_{s,k}; psi_{r,k} = U_r y_{r,k}
   std::vector<double2> scale((size_t)B * ns, make_double2(1.0, 0.0));
   for (int s = 0; s < n_src; ++s)
     for (int k = 0; k < ns; ++k) scale[(size_t)s * ns + k] = d2(ex.rates[s] / nodes[k]);
   // FD with <= 16 sources and <= 64 receivers: tensor-core Jacobian on cell-major fields (the
   // CUDA-core kernel otherwise)
-  const bool tensor_jac = p->kind != LT_GRID_P1_TRI && n_src <= JW_SMAX && n_rec <= JW_RMAX && 2 * B <= 256 &&
-                          (p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B)) <= 227 * 1024;
+  const bool tensor_jac = use_tensor_jacobian(p, n_src, n_rec);
   // tensor path: the quadrature weight w_k rides on the source fields (phi'_{s,k} = w_k phi_{s,k}),
   // which takes one complex product per A element out of the kernel's arrow transform
   if (tensor_jac)
@@ -1436,81 +1544,10 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
       jtmp.allocate(sizeof(double) * (size_t)n_src * n_rec * n_param, st);
       J = jtmp.as<double>();
     }
-    const double h = p->grid.h;
-    const double face_scale = p->dim == 3 ? h : 1.0;
-    const double hd = p->dim == 3 ? h * h * h : h * h;
-    const double bytes = (double)n * (16.0 * ns * B + 8.0 * n_src * n_rec * (ex.include_storativity ? 2 : 1));
-    // 4-cell tiles with 32-byte J stores where rows allow it (2-cell tiles otherwise)
-    const bool tile4 = tensor_jac && p->view(0).nx % J4_TC == 0 && n_param % 4 == 0 && n % 4 == 0 &&
-                       (reinterpret_cast<uintptr_t>(J) & 31) == 0 &&
-                       (p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B)) <= 227 * 1024;
-    if (tile4) {
-      LevelView L = p->view(0);
-      const int ntiles = (L.nx / J4_TC) * L.ny * L.nz;
-      const int grid = std::min(ntiles, ctx->num_sms);
-      const size_t smem = p->dim == 3 ? j4_smem<3>(B) : j4_smem<2>(B);
-      auto fn = p->dim == 3 ? jacobian_mma4_kernel<3> : jacobian_mma4_kernel<2>;
-      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
-      const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
-                                (uint64_t)n * B * 16};
-      const uint32_t boxC[5] = {2 * (uint32_t)B, 6, 1, 1, 2}, boxF[5] = {2 * (uint32_t)B, 4, 1, 1, 2};
-      const CUtensorMap mC = tma_map_8b(fields.get(), 5, dims, strd, boxC);
-      const CUtensorMap mF = tma_map_8b(fields.get(), 5, dims, strd, boxF);
-      launch(ctx, "jacobian", bytes, [&] {
-        fn<<<grid, J4_THREADS, smem, st>>>(mC, mF, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
-                                           face_scale, n_src, n_rec, ns, dw.as<double2>() + ns, J,
-                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles);
-      });
-      if (mem != LT_MEM_DEVICE)
-        LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
-    } else if (tensor_jac) {
-      LevelView L = p->view(0);
-      const int ntiles = ((L.nx + JW_TC - 1) / JW_TC) * L.ny * L.nz;
-      const int grid = std::min(ntiles, ctx->num_sms);
-      const size_t smem = p->dim == 3 ? jw_smem<3>(B) : jw_smem<2>(B);
-      auto fn = p->dim == 3 ? jacobian_mma_kernel<3> : jacobian_mma_kernel<2>;
-      LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      // 5-D maps over the cell-major fields: (item re/im, x, y, z, shift)
-      const uint64_t dims[5] = {2 * (uint64_t)B, (uint64_t)L.nx, (uint64_t)L.ny, (uint64_t)L.nz, (uint64_t)ns};
-      const uint64_t strd[4] = {(uint64_t)B * 16, (uint64_t)L.nx * B * 16, (uint64_t)L.nx * L.ny * B * 16,
-                                (uint64_t)n * B * 16};
-      const uint32_t boxA[5] = {2 * (uint32_t)B, 4, 3, 1, 2}, boxB[5] = {2 * (uint32_t)B, 2, 1, 3, 2};
-      const CUtensorMap mA = tma_map_8b(fields.get(), 5, dims, strd, boxA);
-      const CUtensorMap mB = tma_map_8b(fields.get(), 5, dims, strd, boxB);
-      launch(ctx, "jacobian", bytes, [&] {
-        fn<<<grid, JW_THREADS, smem, st>>>(mA, mB, L, p->kappa.as<double>(), p->storativity.as<double>(), hd,
-                                           face_scale, n_src, n_rec, ns, nullptr, dw.as<double2>() + ns, J,
-                                           ex.include_storativity ? J + n : nullptr, n_param, ntiles);
-      });
-      if (mem != LT_MEM_DEVICE)
-        LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
-    } else {
-    const int nsub_s = (n_src + SB - 1) / SB, nsub_r = (n_rec + RB - 1) / RB;
-    const int nsub_total = nsub_s * nsub_r;
-    LT_REQUIRE(nsub_total <= kT, "jacobian: too many source/receiver blocks for one CTA (n_src*n_rec too large)");
-    const int nf = 2 * p->dim + 1;
-    int TC = std::max(1, kT / nsub_total);
-    LevelView L = p->view(0);
-    TC = std::min(TC, L.nx);
-    auto smem_for = [&](int tc) {
-      return sizeof(double2) * (size_t)(nf - 1) * B * tc + sizeof(double) * nf * tc + sizeof(int64_t) * 2 * p->dim * tc;
-    };
-    while (TC > 1 && smem_for(TC) > 110 * 1024) TC /= 2;  // two CTAs per SM
-    LT_REQUIRE(nf * TC <= kT, "jacobian: tile too wide");
-    const size_t smem = smem_for(TC);
-    const int tiles_x = (L.nx + TC - 1) / TC;
-    const unsigned grid = (unsigned)(tiles_x * (int64_t)L.ny * L.nz);
-    auto fn = p->dim == 3 ? jacobian_kernel<3> : jacobian_kernel<2>;
-    LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch(ctx, "jacobian", bytes, [&] {
-      fn<<<grid, kT, smem, st>>>(L, p->kappa.as<double>(), p->storativity.as<double>(), hd, face_scale,
-                                 fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(), dw.as<double2>() + ns, TC,
-                                 tiles_x, nsub_r, nsub_total, J, ex.include_storativity ? J + n : nullptr, n_param);
-    });
+    fd_jacobian_kernels(p, p->view(0), p->kappa.as<double>(), p->storativity.as<double>(), fields.as<double2>(), n_src,
+                        n_rec, ns, dw.as<double2>(), tensor_jac, ex.include_storativity != 0, J, n_param, n);
     if (mem != LT_MEM_DEVICE)
       LT_CUDA(cudaMemcpyAsync(jac_out, J, sizeof(double) * (size_t)n_src * n_rec * n_param, cudaMemcpyDeviceToHost, st));
-    }
   }
   if (pred_out) {
     DeviceBuffer didx(sizeof(int64_t) * rec.idx.size(), st), dwt(sizeof(double) * rec.w.size(), st),
@@ -1525,6 +1562,211 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     });
     LT_CUDA(cudaMemcpyAsync(pred_out, dout.get(), sizeof(double) * (size_t)n_src * n_rec, cudaMemcpyDeviceToHost, st));
   }
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+
+// ---- the split build of one Jacobian time slice -----------------------
+// Items (sources, then receivers) are partitioned over ranks; each rank solves its items'
+// shifted families (split_solve), exports the rows of its bases that every z-slab (with a
+// one-plane halo) needs (split_export: the caller's all-to-all moves them, NCCL over NVLink),
+// and assembles the J columns of its own slab from every item's slab bases
+// (jacobian_assemble_slab).  J rows never need a reduction; each (s, r) pair's row is split by
+// columns only.
+namespace {
+
+// pred[s r_count + r] = 2 Re sum_k c_{s,k} sum_q wt_q sum_j Y[s,k,j] U_j[s][idx_q]
+__global__ void basis_predict_kernel(int64_t n, int n_src, int n_rec, int ns, const double2* const* __restrict__ cols,
+                                     const double2* __restrict__ Y, int ystride, const int* __restrict__ m_used,
+                                     const double2* __restrict__ c, const int64_t* __restrict__ idx,
+                                     const double* __restrict__ wt, const int* __restrict__ cnt, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_src * n_rec) return;
+  const int s = t / n_rec, r = t % n_rec;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int k = 0; k < ns; ++k) {
+    const int bk = s * ns + k;
+    double2 v = make_double2(0.0, 0.0);
+    for (int j = 0; j < m_used[bk]; ++j) {
+      double2 u = make_double2(0.0, 0.0);
+      for (int q = 0; q < cnt[r]; ++q) u = cadd(u, cscale(cols[j][(int64_t)s * n + idx[r * 8 + q]], wt[r * 8 + q]));
+      v = cfma(Y[(int64_t)bk * ystride + j], u, v);
+    }
+    acc = cfma(c[bk], v, acc);
+  }
+  out[t] = 2.0 * acc.x;
+}
+
+}  // namespace
+
+void split_solve(lt_split_s* sp) {
+  lt_pencil p = sp->p;
+  LT_REQUIRE(p->kind == LT_GRID_FD_CELL && !p->from_csr, "split build: FD grid pencils with parameter fields only");
+  const lt_experiment& ex = sp->ex;
+  LT_REQUIRE(ex.n_src >= 1 && ex.n_rec >= 1 && sp->t >= 0 && sp->t < ex.n_times, "split build: bad experiment / time");
+  LT_REQUIRE(ex.n_quad >= 4 && ex.n_quad % 2 == 0, "build_contour: n_quad must be even and at least 4");
+  talbot_build(ex.n_quad, ex.times[sp->t], ex.contour, nullptr, &sp->nodes, nullptr, &sp->weights);
+  solve_slice_items(p, ex, sp->nodes, sp->item0, sp->item1, sp->res);
+}
+
+void split_export(lt_split_s* sp, int plane0, int plane1, int m_pad, double2* dst, int mem) {
+  lt_pencil p = sp->p;
+  cudaStream_t st = p->ctx->stream;
+  const LevelView L = p->view(0);
+  const int nplanes = p->dim == 3 ? L.nz : L.ny;
+  const int64_t plane = p->dim == 3 ? (int64_t)L.nx * L.ny : L.nx;
+  LT_REQUIRE(0 <= plane0 && plane0 < plane1 && plane1 <= nplanes, "split export: bad plane range");
+  const int B = sp->item1 - sp->item0, ncols = (int)sp->res.U.size();
+  LT_REQUIRE(m_pad >= ncols, "split export: m_pad below this part's basis columns");
+  const int64_t cells = (int64_t)(plane1 - plane0) * plane;
+  const auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  for (int j = 0; j < m_pad; ++j) {
+    double2* d = dst + (int64_t)j * B * cells;
+    if (j < ncols) {
+      LT_CUDA(cudaMemcpy2DAsync(d, sizeof(double2) * cells, sp->res.U[j].as<double2>() + plane0 * plane,
+                                sizeof(double2) * p->n, sizeof(double2) * cells, B, kind, st));
+    } else if (mem == LT_MEM_DEVICE) {
+      LT_CUDA(cudaMemsetAsync(d, 0, sizeof(double2) * B * cells, st));
+    } else {
+      std::memset(d, 0, sizeof(double2) * B * cells);
+    }
+  }
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+void split_coefficients(lt_split_s* sp, double2* Y, int* m_used, int m_pad) {
+  cudaStream_t st = sp->p->ctx->stream;
+  const OuterResult& res = sp->res;
+  const int B = res.B, ns = res.n_shifts;
+  std::vector<double2> Yd((size_t)B * ns * res.maxit);
+  LT_CUDA(cudaMemcpyAsync(Yd.data(), res.Y.get(), sizeof(double2) * Yd.size(), cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+  for (int bk = 0; bk < B * ns; ++bk) {
+    const int mu = res.m_used[bk];
+    LT_REQUIRE(mu <= m_pad, "split coefficients: m_pad below this part's basis columns");
+    m_used[bk] = mu;
+    for (int j = 0; j < m_pad; ++j) Y[(size_t)bk * m_pad + j] = j < mu ? Yd[(size_t)bk * res.maxit + j] : make_double2(0, 0);
+  }
+}
+
+void split_predictions(lt_split_s* sp, double* out) {
+  lt_pencil p = sp->p;
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  const lt_experiment& ex = sp->ex;
+  const int s_end = std::min(sp->item1, ex.n_src);
+  const int n_loc = std::max(0, s_end - sp->item0);  // this part's sources: local items [0, n_loc)
+  if (n_loc == 0) return;
+  const OuterResult& res = sp->res;
+  const int ns = res.n_shifts;
+  std::vector<double2> c((size_t)n_loc * ns);
+  for (int s = 0; s < n_loc; ++s)
+    for (int k = 0; k < ns; ++k)
+      c[(size_t)s * ns + k] = d2(sp->weights[k] * (ex.rates[sp->item0 + s] / sp->nodes[k]));
+  const PointSet rec = make_points(p, ex.receivers, ex.n_rec);
+  std::vector<const double2*> cols(std::max<size_t>(res.U.size(), 1), nullptr);
+  for (size_t j = 0; j < res.U.size(); ++j) cols[j] = res.U[j].as<double2>();
+  DeviceBuffer dcols(sizeof(void*) * cols.size(), st), dmu(sizeof(int) * res.m_used.size(), st),
+      dc(sizeof(double2) * c.size(), st), didx(sizeof(int64_t) * rec.idx.size(), st),
+      dwt(sizeof(double) * rec.w.size(), st), dcnt(sizeof(int) * rec.cnt.size(), st),
+      dout(sizeof(double) * (size_t)n_loc * ex.n_rec, st);
+  LT_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(void*) * cols.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dmu.get(), res.m_used.data(), sizeof(int) * res.m_used.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dc.get(), c.data(), sizeof(double2) * c.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(didx.get(), rec.idx.data(), sizeof(int64_t) * rec.idx.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dwt.get(), rec.w.data(), sizeof(double) * rec.w.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dcnt.get(), rec.cnt.data(), sizeof(int) * rec.cnt.size(), cudaMemcpyHostToDevice, st));
+  launch(ctx, "predict", 0.0, [&] {
+    basis_predict_kernel<<<blocks_for((int64_t)n_loc * ex.n_rec, 128), 128, 0, st>>>(
+        p->n, n_loc, ex.n_rec, ns, dcols.as<const double2*>(), res.Y.as<double2>(), res.maxit, dmu.as<int>(),
+        dc.as<double2>(), didx.as<int64_t>(), dwt.as<double>(), dcnt.as<int>(), dout.as<double>());
+  });
+  LT_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * (size_t)n_loc * ex.n_rec, cudaMemcpyDeviceToHost, st));
+  LT_CUDA(cudaStreamSynchronize(st));
+}
+
+void jacobian_assemble_slab(lt_pencil p, const lt_experiment& ex, int t, int plane0, int plane1, int halo_lo,
+                            int halo_hi, const double2* U, int m, const double2* Y, const int* m_used, int mem,
+                            double* jac_out) {
+  lt_ctx ctx = p->ctx;
+  cudaStream_t st = ctx->stream;
+  LT_REQUIRE(p->kind == LT_GRID_FD_CELL && !p->from_csr, "split build: FD grid pencils with parameter fields only");
+  LT_REQUIRE(t >= 0 && t < ex.n_times && ex.n_quad >= 4 && ex.n_quad % 2 == 0, "split build: bad time / n_quad");
+  LevelView L = p->view(0);
+  const int nplanes = p->dim == 3 ? L.nz : L.ny;
+  const int64_t plane = p->dim == 3 ? (int64_t)L.nx * L.ny : L.nx;
+  LT_REQUIRE(0 <= plane0 && plane0 < plane1 && plane1 <= nplanes, "assemble slab: bad plane range");
+  LT_REQUIRE(halo_lo == (plane0 > 0 ? 1 : 0) && halo_hi == (plane1 < nplanes ? 1 : 0),
+             "assemble slab: one halo plane on each interior side");
+  LT_REQUIRE(m >= 1, "assemble slab: no basis columns");
+  const int n_src = ex.n_src, n_rec = ex.n_rec, B = n_src + n_rec, ns = ex.n_quad / 2;
+  const int ps = plane0 - halo_lo, V = plane1 + halo_hi - ps;
+  const int64_t n_view = (int64_t)V * plane, n_slab = (int64_t)(plane1 - plane0) * plane;
+  std::vector<cd> nodes, weights;
+  talbot_build(ex.n_quad, ex.times[t], ex.contour, nullptr, &nodes, nullptr, &weights);
+  // the slab's view of the fine level: planes [ps, ps + V)
+  LevelView Lv = L;
+  if (p->dim == 3) {
+    Lv.nz = V;
+    Lv.Tx += (int64_t)ps * L.ny * (L.nx + 1);
+    Lv.Ty += (int64_t)ps * (L.ny + 1) * L.nx;
+    Lv.Tz += (int64_t)ps * plane;
+  } else {
+    Lv.ny = V;
+    Lv.Tx += (int64_t)ps * (L.nx + 1);
+    Lv.Ty += (int64_t)ps * L.nx;
+  }
+  Lv.M += (int64_t)ps * plane;
+  Lv.n = n_view;
+  Lv.tiles_y = (Lv.ny + Lv.th - 1) / Lv.th;
+  Lv.ntiles = Lv.tiles_x * Lv.tiles_y * Lv.nz;
+  // the slab bases of all B items and their coefficients
+  DeviceBuffer ubuf;
+  const double2* Ud = U;
+  if (mem != LT_MEM_DEVICE) {
+    ubuf.allocate(sizeof(double2) * (size_t)m * B * n_view, st);
+    LT_CUDA(cudaMemcpyAsync(ubuf.get(), U, ubuf.bytes(), cudaMemcpyHostToDevice, st));
+    Ud = ubuf.as<double2>();
+  }
+  std::vector<const double2*> cols(m);
+  for (int j = 0; j < m; ++j) cols[j] = Ud + (int64_t)j * B * n_view;
+  DeviceBuffer dY(sizeof(double2) * (size_t)B * ns * m, st);
+  LT_CUDA(cudaMemcpyAsync(dY.get(), Y, dY.bytes(), cudaMemcpyHostToDevice, st));
+  std::vector<int> mu(m_used, m_used + (size_t)B * ns);
+  const bool tensor_jac = use_tensor_jacobian(p, n_src, n_rec);
+  std::vector<double2> scale((size_t)B * ns, make_double2(1.0, 0.0));
+  for (int s = 0; s < n_src; ++s)
+    for (int k = 0; k < ns; ++k) {
+      const cd f = ex.rates[s] / nodes[k];
+      scale[(size_t)s * ns + k] = d2(tensor_jac ? f * weights[k] : f);
+    }
+  DeviceBuffer dscale(sizeof(double2) * scale.size(), st);
+  LT_CUDA(cudaMemcpyAsync(dscale.get(), scale.data(), sizeof(double2) * scale.size(), cudaMemcpyHostToDevice, st));
+  DeviceBuffer fields(sizeof(double2) * (size_t)B * ns * n_view, st);
+  expand_raw(ctx, n_view, B, ns, cols, dY.as<double2>(), m, mu, dscale.as<double2>(), fields.as<double2>(), tensor_jac);
+  std::vector<double2> w(ns), wz(ns);
+  for (int k = 0; k < ns; ++k) {
+    w[k] = tensor_jac ? make_double2(1.0, 0.0) : d2(weights[k]);
+    const cd zf = ex.storativity_z_factor ? nodes[k] : cd(1.0, 0.0);
+    wz[k] = d2(tensor_jac ? zf : weights[k] * zf);
+  }
+  DeviceBuffer dw(sizeof(double2) * 2 * ns, st);
+  LT_CUDA(cudaMemcpyAsync(dw.get(), w.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dw.as<double2>() + ns, wz.data(), sizeof(double2) * ns, cudaMemcpyHostToDevice, st));
+  // J over the view (halo planes included), then the slab's columns of both blocks
+  const int pairs = n_src * n_rec;
+  const bool inc_s = ex.include_storativity != 0;
+  const int64_t ldv = inc_s ? 2 * n_view : n_view;
+  DeviceBuffer jv(sizeof(double) * (size_t)pairs * ldv, st);
+  fd_jacobian_kernels(p, Lv, p->kappa.as<double>() + (int64_t)ps * plane, p->storativity.as<double>() + (int64_t)ps * plane,
+                      fields.as<double2>(), n_src, n_rec, ns, dw.as<double2>(), tensor_jac, inc_s, jv.as<double>(), ldv,
+                      n_view);
+  const int64_t lds = inc_s ? 2 * n_slab : n_slab;
+  const auto kind = mem == LT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  for (int blk = 0; blk < (inc_s ? 2 : 1); ++blk)
+    LT_CUDA(cudaMemcpy2DAsync(jac_out + blk * n_slab, sizeof(double) * lds,
+                              jv.as<double>() + blk * n_view + (int64_t)halo_lo * plane, sizeof(double) * ldv,
+                              sizeof(double) * n_slab, pairs, kind, st));
   LT_CUDA(cudaStreamSynchronize(st));
 }
 

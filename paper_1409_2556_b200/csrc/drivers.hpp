@@ -7,6 +7,8 @@
 
 #include "laptomo_gpu.h"
 
+struct lt_split_s;
+
 namespace lt {
 
 extern thread_local std::vector<int> g_last_unconverged;
@@ -17,6 +19,15 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
              lt_time_diag* diag_out, double* shift_residuals);
 
 void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double* jac_out, double* pred_out);
+
+// split build of one time slice
+void split_solve(lt_split_s* sp);
+void split_export(lt_split_s* sp, int plane0, int plane1, int m_pad, double2* dst, int mem);
+void split_coefficients(lt_split_s* sp, double2* Y, int* m_used, int m_pad);
+void split_predictions(lt_split_s* sp, double* out);
+void jacobian_assemble_slab(lt_pencil p, const lt_experiment& ex, int t, int plane0, int plane1, int halo_lo,
+                            int halo_hi, const double2* U, int m, const double2* Y, const int* m_used, int mem,
+                            double* jac_out);
 
 void sample_field_grid(lt_ctx ctx, int dim, const int* shape, double h, double variance, const double* corr,
                        double mean, uint64_t seed, const double2* noise, int mem, double* out);

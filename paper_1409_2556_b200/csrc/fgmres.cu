@@ -964,21 +964,25 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
 }
 
 void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev, double2* x_out, bool cell_major) {
-  lt_ctx ctx = p->ctx;
-  cudaStream_t st = ctx->stream;
-  const int64_t n = p->n;
-  const int B = res.B, ns = res.n_shifts;
-  if (B == 0 || ns == 0) return;
   const int ncols = (int)res.U.size();
   std::vector<const double2*> cols(std::max(ncols, 1), nullptr);
   for (int j = 0; j < ncols; ++j) cols[j] = res.U[j].as<double2>();
+  expand_raw(p->ctx, p->n, res.B, res.n_shifts, cols, res.Y.as<double2>(), res.maxit, res.m_used, scale_dev, x_out,
+             cell_major);
+}
+
+void expand_raw(lt_ctx ctx, int64_t n, int B, int ns, const std::vector<const double2*>& cols, const double2* Y,
+                int ystride, const std::vector<int>& m_used, const double2* scale_dev, double2* x_out, bool cell_major) {
+  cudaStream_t st = ctx->stream;
+  if (B == 0 || ns == 0) return;
+  const int ncols = (int)cols.size();
   DeviceBuffer dcols(sizeof(void*) * cols.size(), st);
-  DeviceBuffer dmu(sizeof(int) * res.m_used.size(), st);
+  DeviceBuffer dmu(sizeof(int) * m_used.size(), st);
   LT_CUDA(cudaMemcpyAsync(dcols.get(), cols.data(), sizeof(void*) * cols.size(), cudaMemcpyHostToDevice, st));
-  LT_CUDA(cudaMemcpyAsync(dmu.get(), res.m_used.data(), sizeof(int) * res.m_used.size(), cudaMemcpyHostToDevice, st));
+  LT_CUDA(cudaMemcpyAsync(dmu.get(), m_used.data(), sizeof(int) * m_used.size(), cudaMemcpyHostToDevice, st));
   const int nblk = (int)blocks_for(n, kT);
   int mmax = 0;
-  for (int v : res.m_used) mmax = std::max(mmax, v);
+  for (int v : m_used) mmax = std::max(mmax, v);
   constexpr int kCT = 32;
   const size_t ys_bytes = sizeof(double2) * (size_t)ns * std::max(mmax, 1) * B;
   // cell-major v2 (coefficients staged in shared memory) up to 8 basis columns; the v1 kernel
@@ -986,7 +990,7 @@ void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_
   if (cell_major && mmax >= 1 && mmax <= 8 && mmax <= ncols && ys_bytes <= 110 * 1024) {
     DeviceBuffer ys(ys_bytes, st);
     const int ny = ns * mmax * B;
-    expand_coeffs<<<(unsigned)((ny + 255) / 256), 256, 0, st>>>(B, ns, res.maxit, mmax, res.Y.as<double2>(),
+    expand_coeffs<<<(unsigned)((ny + 255) / 256), 256, 0, st>>>(B, ns, ystride, mmax, Y,
                                                                  dmu.as<int>(), scale_dev, ys.as<double2>());
     auto fn = mmax <= 4 ? expand_cm2_kernel<4> : expand_cm2_kernel<8>;
     LT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ys_bytes));
@@ -1000,10 +1004,10 @@ void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_
   launch(ctx, "expand", (double)n * B * 16.0 * (ncols + ns), [&] {
     if (cell_major)
       expand_cm_kernel<<<dim3((unsigned)((n + 31) / 32), (unsigned)((B + 7) / 8)), 256, 0, st>>>(
-          n, B, ns, res.maxit, dcols.as<const double2*>(), res.Y.as<double2>(), dmu.as<int>(), scale_dev, x_out);
+          n, B, ns, ystride, dcols.as<const double2*>(), Y, dmu.as<int>(), scale_dev, x_out);
     else
-      expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, res.maxit, dcols.as<const double2*>(),
-                                                        res.Y.as<double2>(), dmu.as<int>(), scale_dev, x_out);
+      expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, ystride, dcols.as<const double2*>(),
+                                                        Y, dmu.as<int>(), scale_dev, x_out);
   });
   LT_CUDA(cudaStreamSynchronize(st));
 }

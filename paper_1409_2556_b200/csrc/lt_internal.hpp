@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -347,5 +348,20 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res);
 // cell_major: out[(k n + a) B + b] instead of out[(b ns + k) n + a]
 void expand_solutions(lt_pencil p, const OuterResult& res, const double2* scale_dev,
                       double2* x_out, bool cell_major = false);
+// the same from raw bases: cols[j] = column j (B items of n cells each, item stride n),
+// Y[(b ns + k) ystride + j] (device), m_used (host, B ns)
+void expand_raw(lt_ctx ctx, int64_t n, int B, int ns, const std::vector<const double2*>& cols, const double2* Y,
+                int ystride, const std::vector<int>& m_used, const double2* scale_dev, double2* x_out,
+                bool cell_major);
 
 }  // namespace lt
+
+// one rank's part of a split Jacobian time slice (drivers.cu)
+struct lt_split_s {
+  lt_pencil p = nullptr;
+  int t = 0, item0 = 0, item1 = 0;
+  std::vector<double> sources, receivers, rates, times;  // copies of the experiment's arrays
+  lt_experiment ex{};                                     // pointing into them
+  std::vector<std::complex<double>> nodes, weights;
+  lt::OuterResult res;
+};
