@@ -480,6 +480,26 @@ inline HeadSolution solve_forward_batch(const ShiftedPencil& pencil, const Forwa
   return detail::forward(pencil, problem, solver, 1);
 }
 
+/// crank_nicolson (forward.cpp:200-258): the head at each sample time, n x n_samples column-major.
+inline std::vector<double> crank_nicolson(const ShiftedPencil& pencil, const std::vector<double>& source, double rate,
+                                          const std::vector<double>& initial_head, double dt,
+                                          const std::vector<double>& sample_times, int* steps_out = nullptr) {
+  std::vector<double> out((size_t)pencil.rows() * sample_times.size());
+  detail::check(lt_crank_nicolson(pencil.handle(), source.data(), &rate, 1,
+                                  initial_head.empty() ? nullptr : initial_head.data(), dt,
+                                  sample_times.empty() ? nullptr : sample_times.data(), (int)sample_times.size(),
+                                  LT_MEM_HOST, out.data(), steps_out));
+  return out;
+}
+
+/// estimate_condition_1norm (condest.cpp:43-49) with the actions of K + z M (apply, adjoint,
+/// shift-and-invert solve and its adjoint).
+inline double estimate_condition_1norm(const ShiftedPencil& pencil, Complex z) {
+  double cond = 0.0;
+  detail::check(lt_pencil_condest(pencil.handle(), detail::c(z), nullptr, nullptr, &cond));
+  return cond;
+}
+
 // ---- Jacobian (jacobian.hpp:22-101) ---------------------------------------------------
 struct ThtExperiment {
   Grid grid;

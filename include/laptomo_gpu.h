@@ -282,6 +282,21 @@ lt_status lt_jacobian(lt_pencil p, const lt_experiment* exp, double* jac_out,
 /* ThtForwardModel::predict (jacobian.cpp:158-187): n_meas predictions. */
 lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_out);
 
+/* ---- time stepping and conditioning (forward.hpp:63-68, shifted_solver.hpp:141-149) ---- */
+/* crank_nicolson (forward.cpp:200-258): (M + dt/2 K) h_{n+1} = (M - dt/2 K) h_n + dt q b from
+ * h_0 = initial_head (NULL: zero) until the last sample time, for n_src problems in lockstep
+ * (sources n x n_src weights, rates n_src); samples_out[(s n_samples + i) n + a] = the head at
+ * sample_times[i] (linear interpolation between the two steps around it, as the reference).
+ * The step solve is the pencil's shift-and-invert at tau = 2/dt (the reference's LDLT of
+ * M + dt/2 K); steps_out may be NULL.  dt <= 0 or no sample times: LT_ERR_INVALID_ARGUMENT. */
+lt_status lt_crank_nicolson(lt_pencil p, const double* sources, const double* rates, int n_src,
+                            const double* initial_head, double dt, const double* sample_times,
+                            int n_samples, int mem, double* samples_out, int* steps_out);
+/* estimate_condition_1norm (condest.cpp:11-49) of A = K + z M: Hager 1-norm lower bounds of A
+ * (apply / apply_adjoint) and of A^{-1} (shift-and-invert solve / its adjoint) and their
+ * product (never above kappa_1(A)); any output may be NULL. */
+lt_status lt_pencil_condest(lt_pencil p, lt_complex z, double* norm_a, double* norm_inv, double* cond);
+
 /* ---- split build of one Jacobian time slice across ranks -------------
  * The rows of jacobian.cpp:205-246 are independent, and each needs phi_s and psi_r on the same
  * cells: one rank per GPU solves a contiguous range of the slice's items (sources, then

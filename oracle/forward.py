@@ -173,3 +173,48 @@ def solve_forward_batch(problem: ForwardProblem, solver: SolverConfig = SolverCo
         heads[:, it] = inverse_laplace_sum(contour, values)
         offset += contour.n_half()
     return HeadSolution(heads, [pooled_diag] * n_times)
+
+
+def crank_nicolson(stiffness, mass, source, rate: float, initial_head, dt: float, sample_times,
+                   return_steps: bool = False):
+    """forward.cpp:200-258: one factorisation of M + dt/2 K (SimplicialLDLT there, SuperLU
+    here) reused for every step; samples by linear interpolation between the two states
+    around each sample time."""
+    import scipy.sparse.linalg as spla
+    if not dt > 0.0:
+        raise ValueError("crank_nicolson: dt must be positive")
+    if len(sample_times) == 0:
+        raise ValueError("crank_nicolson: no sample times")
+    t_end = max(sample_times)
+    lhs = (mass + (0.5 * dt) * stiffness).tocsc()
+    solver = spla.splu(lhs)
+    rhs_op = (mass - (0.5 * dt) * stiffness).tocsr()
+    forcing = dt * rate * np.asarray(source, dtype=np.float64)
+    n = stiffness.shape[0]
+    head = np.zeros(n) if initial_head is None or len(initial_head) == 0 else np.asarray(initial_head, dtype=np.float64)
+    samples = np.zeros((n, len(sample_times)))
+    filled = [False] * len(sample_times)
+
+    def record(t_prev, head_prev, t_now, head_now):
+        for s, target in enumerate(sample_times):
+            if filled[s]:
+                continue
+            if target <= t_now + 1e-9 * dt:
+                if abs(target - t_now) <= 1e-9 * dt or t_now == t_prev:
+                    samples[:, s] = head_now
+                else:
+                    w = (target - t_prev) / (t_now - t_prev)
+                    samples[:, s] = (1.0 - w) * head_prev + w * head_now
+                filled[s] = True
+
+    record(0.0, head, 0.0, head)
+    steps = 0
+    t = 0.0
+    while t < t_end - 1e-9 * dt:
+        head_prev = head
+        head = solver.solve(rhs_op @ head + forcing)
+        t_prev = t
+        t += dt
+        steps += 1
+        record(t_prev, head_prev, t, head)
+    return (samples, steps) if return_steps else samples

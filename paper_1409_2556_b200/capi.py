@@ -131,6 +131,8 @@ SIGNATURES = {
     "lt_jacobian_slice": (I, [P, C.POINTER(LtExperiment), I, I, PD, PD]),
     "lt_jacobian": (I, [P, C.POINTER(LtExperiment), PD, PD]),
     "lt_predict": (I, [P, C.POINTER(LtExperiment), PD]),
+    "lt_crank_nicolson": (I, [P, PD, PD, I, PD, D, PD, I, I, PD, PI]),
+    "lt_pencil_condest": (I, [P, LtComplex, PD, PD, PD]),
     "lt_split_solve": (I, [P, C.POINTER(LtExperiment), I, I, I, C.POINTER(P)]),
     "lt_split_columns": (I, [P]),
     "lt_split_coefficients": (I, [P, I, PC, PI]),

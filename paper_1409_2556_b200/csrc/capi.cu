@@ -643,6 +643,24 @@ lt_status lt_predict(lt_pencil p, const lt_experiment* exp, double* predictions_
   });
 }
 
+lt_status lt_crank_nicolson(lt_pencil p, const double* sources, const double* rates, int n_src, const double* initial_head,
+                            double dt, const double* sample_times, int n_samples, int mem, double* samples_out,
+                            int* steps_out) {
+  return guard([&] {
+    check_pencil(p);
+    set_device(p->ctx);
+    lt::crank_nicolson(p, sources, rates, n_src, initial_head, dt, sample_times, n_samples, mem, samples_out, steps_out);
+  });
+}
+
+lt_status lt_pencil_condest(lt_pencil p, lt_complex z, double* norm_a, double* norm_inv, double* cond) {
+  return guard([&] {
+    check_pencil(p);
+    set_device(p->ctx);
+    lt::condition_estimate(p, lt::to_d2(z), norm_a, norm_inv, cond);
+  });
+}
+
 lt_status lt_split_solve(lt_pencil p, const lt_experiment* exp, int time_index, int item0, int item1, lt_split* out) {
   return guard([&] {
     check_pencil(p);

@@ -20,6 +20,11 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
 
 void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double* jac_out, double* pred_out);
 
+// timestep.cu
+void crank_nicolson(lt_pencil p, const double* sources, const double* rates, int n_src, const double* initial_head,
+                    double dt, const double* sample_times, int n_samples, int mem, double* out, int* steps_out);
+void condition_estimate(lt_pencil p, double2 z, double* norm_a, double* norm_inv, double* cond);
+
 // split build of one time slice
 void split_solve(lt_split_s* sp);
 void split_export(lt_split_s* sp, int plane0, int plane1, int m_pad, double2* dst, int mem);

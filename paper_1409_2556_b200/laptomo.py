@@ -705,6 +705,44 @@ def solve_adjoint_fields(pencil: ShiftedPencil, receiver, contour: TalbotContour
     return res.solutions
 
 
+def crank_nicolson(pencil: ShiftedPencil, source, rate: float, initial_head, dt: float, sample_times,
+                   return_steps: bool = False):
+    """crank_nicolson (forward.cpp:200-258) on the device: n x n_samples heads.  `source` may be
+    (n,) or (n_src, n) with `rate` a scalar or n_src rates (lockstep problems: then
+    (n_src, n, n_samples))."""
+    n = pencil.rows()
+    src = np.ascontiguousarray(np.asarray(source, dtype=np.float64).reshape(-1, n))
+    ns = src.shape[0]
+    rates = np.ascontiguousarray(np.broadcast_to(np.asarray(rate, dtype=np.float64), (ns,)).copy())
+    times = np.ascontiguousarray(np.asarray(list(sample_times), dtype=np.float64))
+    ih = None
+    if initial_head is not None and len(initial_head) > 0:
+        ih = np.ascontiguousarray(np.broadcast_to(np.asarray(initial_head, dtype=np.float64).reshape(-1, n), (ns, n)).copy())
+    out = np.zeros((ns, max(times.size, 1), n))
+    steps = C.c_int()
+    check(lib().lt_crank_nicolson(pencil.handle, dptr(src), dptr(rates), ns, dptr(ih) if ih is not None else None,
+                                  float(dt), dptr(times) if times.size else None, int(times.size), capi.LT_MEM_HOST,
+                                  dptr(out), C.byref(steps)))
+    samples = np.ascontiguousarray(np.transpose(out, (0, 2, 1)))
+    samples = samples[0] if np.asarray(source).ndim == 1 else samples
+    return (samples, steps.value) if return_steps else samples
+
+
+def estimate_condition_1norm(pencil: ShiftedPencil, z) -> float:
+    """estimate_condition_1norm (condest.cpp:43-49) of K + z M on the device (the actions are the
+    pencil's apply / adjoint and its shift-and-invert solve / adjoint)."""
+    na, ni, cond = C.c_double(), C.c_double(), C.c_double()
+    check(lib().lt_pencil_condest(pencil.handle, lc(z), C.byref(na), C.byref(ni), C.byref(cond)))
+    return float(cond.value)
+
+
+def estimate_norms_1(pencil: ShiftedPencil, z):
+    """(||K + zM||_1 estimate, ||(K + zM)^-1||_1 estimate)."""
+    na, ni, cond = C.c_double(), C.c_double(), C.c_double()
+    check(lib().lt_pencil_condest(pencil.handle, lc(z), C.byref(na), C.byref(ni), C.byref(cond)))
+    return float(na.value), float(ni.value)
+
+
 # ---- Jacobian ----------------------------------------------------------------------------
 @dataclass
 class ThtExperiment:
