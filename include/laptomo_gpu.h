@@ -297,6 +297,59 @@ lt_status lt_crank_nicolson(lt_pencil p, const double* sources, const double* ra
  * product (never above kappa_1(A)); any output may be NULL. */
 lt_status lt_pencil_condest(lt_pencil p, lt_complex z, double* norm_a, double* norm_inv, double* cond);
 
+/* ---- Gauss-Newton step of the geostatistical inversion (inversion.hpp:17-91) ----------
+ * InversionProblem: y (n_y), r_diag (n_y, > 0), drift X (n_s x p, column-major like Eigen) and
+ * the prior Q, either dense (prior != NULL: n_s x n_s, the reference's matrix; jittered
+ * Cholesky for the prior term) or, prior == NULL, a stationary exponential covariance
+ * variance[b] exp(-|(dx/l0, dy/l1, dz/l2)|) between the cells of `grid` for each of n_blocks
+ * parameter blocks (s = [block 0 cells, block 1 cells]: log kappa then log S), applied exactly by
+ * FFT (Q J^T) and inverted by CG for the prior term.  The forward handles are
+ * callbacks (InversionProblem::predict / jacobian_and_predict, inversion.hpp:25-26): s and h
+ * are host arrays, J_out a DEVICE buffer of n_y x n_s doubles (row-major, rows in y's order),
+ * e.g. filled by lt_jacobian_slice with LT_MEM_DEVICE; a nonzero return is raised as that
+ * lt_status.                                                                             */
+typedef int (*lt_predict_fn)(void* user, const double* s, double* h_out);
+typedef int (*lt_jacobian_fn)(void* user, const double* s, double* J_out_device, double* h_out);
+typedef struct {
+  int n_y, n_s, p;
+  const double* y;
+  const double* r_diag;
+  const double* drift;
+  const double* prior;
+  lt_grid grid;
+  int n_blocks;
+  double variance[2];
+  double corr[2][3];
+  lt_predict_fn predict;
+  lt_jacobian_fn jacobian_and_predict;
+  void* user;
+} lt_gn_problem;
+
+typedef struct { /* GnOptions (inversion.hpp:29-34) */
+  int max_gn;       /* 15 */
+  double rtol;      /* 1e-3 */
+  int damping;      /* 1 */
+  int max_halvings; /* 5 */
+} lt_gn_options;
+
+typedef struct { /* GnIterate scalars (inversion.hpp:36-47) */
+  double objective, misfit, prior, step_norm, alpha, saddle_residual, drift_violation;
+} lt_gn_stats;
+
+void lt_gn_default_options(lt_gn_options* out);
+/* GaussNewtonSolver::step (inversion.cpp:78-148): s_out (n_s), beta_out (p), xi_out (n_y or NULL). */
+lt_status lt_gn_step(lt_ctx ctx, const lt_gn_problem* problem, const double* s, const double* beta,
+                     const lt_gn_options* options, double* s_out, double* beta_out, double* xi_out,
+                     lt_gn_stats* stats);
+/* GaussNewtonSolver::invert (inversion.cpp:150-186): returns the number of steps taken in
+ * *steps_out; history (max_gn entries) may be NULL; reason is the stop_reason (NUL-terminated). */
+lt_status lt_gn_invert(lt_ctx ctx, const lt_gn_problem* problem, const double* s0, const double* beta0,
+                       const lt_gn_options* options, double* s_hat, double* beta_hat, lt_gn_stats* history,
+                       int* steps_out, int* converged, char* reason, int reason_capacity);
+/* GaussNewtonSolver::objective = misfit(predict(s)) + prior_term(s, beta) (inversion.cpp:58-76). */
+lt_status lt_gn_objective(lt_ctx ctx, const lt_gn_problem* problem, const double* s, const double* beta,
+                          double* objective, double* misfit, double* prior);
+
 /* ---- split build of one Jacobian time slice across ranks -------------
  * The rows of jacobian.cpp:205-246 are independent, and each needs phi_s and psi_r on the same
  * cells: one rank per GPU solves a contiguous range of the slice's items (sources, then

@@ -63,6 +63,26 @@ class LtSparse(C.Structure):
                 ("index_bytes", C.c_int)]
 
 
+PREDICT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+JACOBIAN_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_double))
+
+
+class LtGnProblem(C.Structure):
+    _fields_ = [("n_y", C.c_int), ("n_s", C.c_int), ("p", C.c_int), ("y", C.POINTER(C.c_double)),
+                ("r_diag", C.POINTER(C.c_double)), ("drift", C.POINTER(C.c_double)), ("prior", C.POINTER(C.c_double)),
+                ("grid", LtGrid), ("n_blocks", C.c_int), ("variance", C.c_double * 2), ("corr", (C.c_double * 3) * 2),
+                ("predict", PREDICT_FN), ("jacobian_and_predict", JACOBIAN_FN), ("user", C.c_void_p)]
+
+
+class LtGnOptions(C.Structure):
+    _fields_ = [("max_gn", C.c_int), ("rtol", C.c_double), ("damping", C.c_int), ("max_halvings", C.c_int)]
+
+
+class LtGnStats(C.Structure):
+    _fields_ = [("objective", C.c_double), ("misfit", C.c_double), ("prior", C.c_double), ("step_norm", C.c_double),
+                ("alpha", C.c_double), ("saddle_residual", C.c_double), ("drift_violation", C.c_double)]
+
+
 class LtTimeDiag(C.Structure):
     _fields_ = [("iterations", C.c_int), ("all_converged", C.c_int)]
 
@@ -133,6 +153,11 @@ SIGNATURES = {
     "lt_predict": (I, [P, C.POINTER(LtExperiment), PD]),
     "lt_crank_nicolson": (I, [P, PD, PD, I, PD, D, PD, I, I, PD, PI]),
     "lt_pencil_condest": (I, [P, LtComplex, PD, PD, PD]),
+    "lt_gn_default_options": (None, [C.POINTER(LtGnOptions)]),
+    "lt_gn_step": (I, [P, C.POINTER(LtGnProblem), PD, PD, C.POINTER(LtGnOptions), PD, PD, PD, C.POINTER(LtGnStats)]),
+    "lt_gn_invert": (I, [P, C.POINTER(LtGnProblem), PD, PD, C.POINTER(LtGnOptions), PD, PD, C.POINTER(LtGnStats), PI, PI,
+                         C.c_char_p, I]),
+    "lt_gn_objective": (I, [P, C.POINTER(LtGnProblem), PD, PD, PD, PD, PD]),
     "lt_split_solve": (I, [P, C.POINTER(LtExperiment), I, I, I, C.POINTER(P)]),
     "lt_split_columns": (I, [P]),
     "lt_split_coefficients": (I, [P, I, PC, PI]),

@@ -661,6 +661,45 @@ lt_status lt_pencil_condest(lt_pencil p, lt_complex z, double* norm_a, double* n
   });
 }
 
+void lt_gn_default_options(lt_gn_options* out) {
+  if (out) *out = lt_gn_options{15, 1e-3, 1, 5};
+}
+
+lt_status lt_gn_step(lt_ctx ctx, const lt_gn_problem* problem, const double* s, const double* beta,
+                     const lt_gn_options* options, double* s_out, double* beta_out, double* xi_out, lt_gn_stats* stats) {
+  return guard([&] {
+    LT_REQUIRE(ctx && problem && s && s_out && (problem->p == 0 || (beta && beta_out)), "gauss_newton_step: null argument");
+    set_device(ctx);
+    lt_gn_options o;
+    if (options) o = *options; else lt_gn_default_options(&o);
+    lt::gn_step(ctx, *problem, s, beta, o, s_out, beta_out, xi_out, stats);
+  });
+}
+
+lt_status lt_gn_invert(lt_ctx ctx, const lt_gn_problem* problem, const double* s0, const double* beta0,
+                       const lt_gn_options* options, double* s_hat, double* beta_hat, lt_gn_stats* history, int* steps_out,
+                       int* converged, char* reason, int reason_capacity) {
+  return guard([&] {
+    LT_REQUIRE(ctx && problem && s0 && s_hat && (problem->p == 0 || (beta0 && beta_hat)), "invert: null argument");
+    set_device(ctx);
+    lt_gn_options o;
+    if (options) o = *options; else lt_gn_default_options(&o);
+    const int k = lt::gn_invert(ctx, *problem, s0, beta0, o, s_hat, beta_hat, history, o.max_gn, converged, reason,
+                                reason_capacity);
+    if (steps_out) *steps_out = k;
+  });
+}
+
+lt_status lt_gn_objective(lt_ctx ctx, const lt_gn_problem* problem, const double* s, const double* beta,
+                          double* objective, double* misfit, double* prior) {
+  return guard([&] {
+    LT_REQUIRE(ctx && problem && s && (problem->p == 0 || beta), "objective: null argument");
+    set_device(ctx);
+    const double o = lt::gn_objective(ctx, *problem, s, beta, misfit, prior);
+    if (objective) *objective = o;
+  });
+}
+
 lt_status lt_split_solve(lt_pencil p, const lt_experiment* exp, int time_index, int item0, int item1, lt_split* out) {
   return guard([&] {
     check_pencil(p);

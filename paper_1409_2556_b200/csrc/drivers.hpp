@@ -25,6 +25,15 @@ void crank_nicolson(lt_pencil p, const double* sources, const double* rates, int
                     double dt, const double* sample_times, int n_samples, int mem, double* out, int* steps_out);
 void condition_estimate(lt_pencil p, double2 z, double* norm_a, double* norm_inv, double* cond);
 
+// gn.cu
+void gn_step(lt_ctx ctx, const lt_gn_problem& pb, const double* s, const double* beta, const lt_gn_options& opt,
+             double* s_out, double* beta_out, double* xi_out, lt_gn_stats* stats);
+int gn_invert(lt_ctx ctx, const lt_gn_problem& pb, const double* s0, const double* beta0, const lt_gn_options& opt,
+              double* s_hat, double* beta_hat, lt_gn_stats* history, int history_cap, int* converged, char* reason,
+              int reason_cap);
+double gn_objective(lt_ctx ctx, const lt_gn_problem& pb, const double* s, const double* beta, double* misfit,
+                    double* prior);
+
 // split build of one time slice
 void split_solve(lt_split_s* sp);
 void split_export(lt_split_s* sp, int plane0, int plane1, int m_pad, double2* dst, int mem);
