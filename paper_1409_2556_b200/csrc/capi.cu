@@ -102,20 +102,20 @@ __global__ void conj_kernel(const double2* in, double2* out, int64_t n) {
 }
 
 // A shift-and-invert solve (the reference's exact LU) that ended above the inner solve's
-// stagnation floor (1e4 x its tolerance) fails with LT_ERR_NOT_CONVERGED; lt_last_unconverged
+// stagnation floor (kInnerFloor x its tolerance) fails with LT_ERR_NOT_CONVERGED; lt_last_unconverged
 // lists the offending right-hand sides (or shifts).
 void check_inner(lt_pencil p, const std::vector<double>& rel, int shift = -1) {
   std::vector<int> bad;
   double worst = 0.0;
   for (size_t b = 0; b < rel.size(); ++b)
-    if (!(rel[b] <= 1e4 * p->inner_tol)) {
+    if (!(rel[b] <= kInnerFloor * p->inner_tol)) {
       bad.push_back(shift >= 0 ? shift : (int)b);
       worst = std::max(worst, rel[b]);
     }
   if (bad.empty()) return;
   lt::g_last_unconverged = bad;
   throw lt::Error(LT_ERR_NOT_CONVERGED, "shift-and-invert solve: relative residual " + std::to_string(worst) +
-                                            " above " + std::to_string(1e4 * p->inner_tol) + " after " +
+                                            " above " + std::to_string(kInnerFloor * p->inner_tol) + " after " +
                                             std::to_string(p->inner_maxit) + " iterations");
 }
 
@@ -544,7 +544,7 @@ lt_status lt_solve_shifted_direct(lt_pencil p, const lt_complex* b, int n_rhs, c
       lt::inner_solve(p, n_rhs, t.data(), bin.ptr, n, xo.ptr + (size_t)k * n, (int64_t)n * n_shifts, nullptr,
                       rel.data());
       for (double r : rel)
-        if (!(r <= 1e4 * p->inner_tol)) {
+        if (!(r <= kInnerFloor * p->inner_tol)) {
           if (bad.empty() || bad.back() != k) bad.push_back(k);
           worst = std::max(worst, r);
         }

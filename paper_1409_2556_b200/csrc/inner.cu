@@ -2455,7 +2455,7 @@ __device__ __forceinline__ double block_max(double v) {
 }
 
 // Per iteration, after ||r||^2: converged at ||r|| <= tol ||v||; stagnated at the rounding
-// floor (within 1e4 of the tolerance and no halving of the residual in 6 iterations; far from
+// floor (within kInnerFloor of the tolerance and no halving of the residual in 6 iterations; far from
 // the floor COCG's residual is non-monotone on the indefinite pencils Re tau < 0 gives, so
 // plateaus there are not stagnation).  An item stopping here still owes its deferred u += alpha p
 // (pending).  The count of items still iterating and the worst remaining ratio to the tolerance
@@ -2474,7 +2474,7 @@ __global__ void cocg_control_kernel(int B, int* __restrict__ done, const double*
     bool stop = r <= lim;
     if (!stop) {
       if (r < 0.25 * best[b]) { best[b] = r; stall[b] = 0; }
-      else if (r <= 1e8 * lim && ++stall[b] >= 6) stop = true;
+      else if (r <= kInnerFloor * kInnerFloor * lim && ++stall[b] >= 6) stop = true;
     }
     if (stop) { done[b] = 1; pending[b] = 1; }
     else { ++cnt; worst = fmax(worst, r / lim); }
@@ -2831,10 +2831,8 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
 }
 
-}  // namespace
-
-void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us,
-                 const int* active, double* rel_out) {
+void inner_solve_mg(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u,
+                    int64_t us, const int* active, double* rel_out) {
   // Chunk so that the Krylov + multigrid workspace stays bounded.
   const int64_t n = p->n;
   const double avail = available_device_bytes(p->ctx);
@@ -2849,6 +2847,73 @@ void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v,
     if (p->dim == 3) inner_chunk<3>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us, act, rel);
     else inner_chunk<2>(p, bc, taus_host + b0, v + b0 * vs, vs, u + b0 * us, us, act, rel);
   }
+}
+
+}  // namespace
+
+void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs, double2* u, int64_t us,
+                 const int* active, double* rel_out) {
+  // Items whose shift is known to need the exact banded solve (2-D pencils, strongly indefinite
+  // shifts) take it directly; the others run MG-COCG, and an item that does not reach the
+  // stagnation floor (kInnerFloor x the inner tolerance) is redone by the banded solve when the pencil
+  // allows it (band.cu) -- else the preconditioner has failed (FactorizationError).
+  std::vector<int> act(B, 1);
+  if (active) {
+    LT_CUDA(cudaMemcpyAsync(act.data(), active, sizeof(int) * B, cudaMemcpyDeviceToHost, p->ctx->stream));
+    LT_CUDA(cudaStreamSynchronize(p->ctx->stream));
+  }
+  auto is_band = [&](double2 t) {
+    for (const double2& b : p->band_taus)
+      if (b.x == t.x && b.y == t.y) return true;
+    return false;
+  };
+  std::vector<int> band(B, 0), mg(B, 0);
+  int n_band = 0, n_mg = 0;
+  for (int b = 0; b < B; ++b) {
+    if (!act[b]) continue;
+    if (is_band(taus_host[b])) { band[b] = 1; ++n_band; }
+    else { mg[b] = 1; ++n_mg; }
+  }
+  std::vector<double> rel(B, 0.0);
+  if (n_mg) {
+    DeviceBuffer dmask;
+    const int* mask = active;
+    if (n_band) {
+      dmask.allocate(sizeof(int) * B, p->ctx->stream);
+      LT_CUDA(cudaMemcpyAsync(dmask.get(), mg.data(), sizeof(int) * B, cudaMemcpyHostToDevice, p->ctx->stream));
+      mask = dmask.as<int>();
+    }
+    inner_solve_mg(p, B, taus_host, v, vs, u, us, mask, rel.data());
+    for (int b = 0; b < B; ++b) {
+      if (!mg[b] || rel[b] <= kInnerFloor * p->inner_tol) continue;
+      if (!band_feasible(p)) {
+        if (rel_out) continue;  // the caller reports it
+        throw Error(LT_ERR_PRECONDITIONER, "shift-and-invert solve: the multigrid-preconditioned inner solve did not "
+                                           "converge (relative residual " + std::to_string(rel[b]) + ")");
+      }
+      if (!is_band(taus_host[b])) p->band_taus.push_back(taus_host[b]);
+      band[b] = 1;
+      ++n_band;
+    }
+  }
+  if (n_band) {
+    for (int b = 0; b < B; ++b) {
+      if (!band[b]) continue;
+      const BandFactor& f = pencil_band_factor(p, taus_host[b]);
+      // every item of this shift in one launch (one warp each)
+      int b1 = b;
+      while (b1 + 1 < B && band[b1 + 1] && taus_host[b1 + 1].x == taus_host[b].x && taus_host[b1 + 1].y == taus_host[b].y)
+        ++b1;
+      band_solve(p, f, b1 - b + 1, v + b * vs, vs, u + b * us, us);
+      for (int q = b; q <= b1; ++q) {
+        rel[q] = 0.0;  // exact LU, like the reference's factorisation
+        band[q] = 0;
+      }
+      b = b1;
+    }
+  }
+  if (rel_out)
+    for (int b = 0; b < B; ++b) rel_out[b] = rel[b];
 }
 
 }  // namespace lt

@@ -92,6 +92,11 @@ struct PendingEvent {
 // kFlagRing slots in mapped pinned memory written by the control kernel, each slot paired with
 // an event; the host reads slot it - kFlagLag while iteration it is still queued.
 constexpr int kFlagRing = 4, kFlagLag = 1;
+// The inner shift-and-invert solve is accepted at a relative residual of kInnerFloor x its
+// tolerance (1e-11 by default): converged at the tolerance, or stagnated at the rounding floor
+// within this margin.  Anything above would break the outer method's Arnoldi relation
+// (K + tau_j M) u_j = v_j at the 1e-10 level of the shifts' own tolerance.
+constexpr double kInnerFloor = 10.0;
 struct FlagSlot {
   double worst;  // max over the items still iterating of ||r||^2 / (tol^2 ||v||^2)
   int active;    // items still iterating
@@ -252,6 +257,15 @@ struct CoarseFactor {
   DeviceBuffer inverse32;  // A^{-1} n_c x n_c complex64, row-major (V-cycle coarsest solve)
 };
 
+// Exact banded LU of K + tau M for 2-D pencils (band.cu), LAPACK zgbtrf layout
+struct BandFactor {
+  double2 tau;
+  int64_t n = 0;
+  int kl = 0, ku = 0, ldab = 0;
+  DeviceBuffer ab;    // ldab x n complex128
+  DeviceBuffer ipiv;  // n pivots + info
+};
+
 // Per-solve FGMRES basis kept for keep_basis queries.
 struct KeptBasis {
   int n_rhs = 0;
@@ -270,6 +284,8 @@ struct lt_pencil_s {
   int64_t n = 0;
   std::vector<std::unique_ptr<lt::Level>> levels;
   std::vector<std::unique_ptr<lt::CoarseFactor>> factors;  // keyed by exact tau
+  std::vector<std::unique_ptr<lt::BandFactor>> band_factors;  // exact banded LU, keyed by exact tau
+  std::vector<double2> band_taus;  // shifts whose inner solve needs the banded direct solve
   lt::DeviceBuffer kappa;         // per cell (fine), for Jacobian
   lt::DeviceBuffer storativity;   // per cell (fine)
   bool from_csr = false;          // built by lt_pencil_create_csr: no parameter fields
@@ -315,6 +331,11 @@ double available_device_bytes(lt_ctx ctx);
 // (recursive COCG residual).
 void inner_solve(lt_pencil p, int B, const double2* taus_host, const double2* v, int64_t vs,
                  double2* u, int64_t us, const int* active = nullptr, double* rel_out = nullptr);
+
+// band.cu: the exact banded shift-and-invert of 2-D pencils
+bool band_feasible(const lt_pencil_s* p);
+const BandFactor& pencil_band_factor(lt_pencil p, double2 tau);
+void band_solve(lt_pencil p, const BandFactor& f, int B, const double2* v, int64_t vs, double2* u, int64_t us);
 
 // fgmres.cu
 struct OuterProblem {

@@ -116,7 +116,7 @@ unsigned grid_for(int64_t n, lt_ctx ctx) { return (unsigned)std::min<int64_t>(bl
 
 void check_inner_cn(lt_pencil p, const std::vector<double>& rel) {
   for (double r : rel)
-    if (!(r <= 1e4 * p->inner_tol))
+    if (!(r <= kInnerFloor * p->inner_tol))
       throw Error(LT_ERR_PRECONDITIONER, "crank_nicolson: the shift-and-invert solve of M + dt/2 K did not converge "
                                          "(relative residual " + std::to_string(r) + ")");
 }
@@ -227,7 +227,7 @@ void condition_estimate(lt_pencil p, double2 z, double* norm_a, double* norm_inv
     std::vector<double> rel(1);
     const double2 tau = adjoint ? make_double2(z.x, -z.y) : z;
     inner_solve(p, 1, &tau, in, n, outv, n, nullptr, rel.data());
-    if (!(rel[0] <= 1e4 * p->inner_tol))
+    if (!(rel[0] <= kInnerFloor * p->inner_tol))
       throw Error(LT_ERR_PRECONDITIONER, "estimate_condition_1norm: shift-and-invert solve failed to converge");
   };
   auto l1 = [&](const double2* v) {

@@ -182,13 +182,47 @@ def test_not_converged_paths():
     with pytest.raises(capi.ConvergenceError) as e:
         L.solve_forward(p, prob, L.SolverConfig(maxit=1))
     assert e.value.unconverged_shifts == ref.unconverged()
-    # an inner shift-and-invert solve that cannot reach its floor: LT_ERR_NOT_CONVERGED
+    # a 2-D pencil whose multigrid inner solve cannot reach its floor falls back to the exact
+    # banded LU (band.cu): the solve is exact
     p.set_inner_tolerance(1e-12, 1)
+    u = p.factorization(sched.taus[0]).solve(np.stack([b, 2 * b]))
+    ref = spla.splu((ops.stiffness + sched.taus[0] * ops.mass).tocsc()).solve(b)
+    assert rel(u[0], ref) <= 1e-12 and rel(u[1], 2 * ref) <= 1e-12
+    # a 3-D pencil has no banded fallback: LT_ERR_NOT_CONVERGED with the right-hand sides
+    cfg3, lk3, ls3, grid3, ops3 = fd_case(4, (12, 10, 8))
+    p3 = L.ShiftedPencil(L.Grid(tuple(cfg3.shape), cfg3.h), lk3, ls3)
+    b3 = ofd.point_weights(grid3, (0.5, 0.4, 0.3)).astype(np.complex128)
+    p3.set_inner_tolerance(1e-12, 1)
     with pytest.raises(capi.ConvergenceError) as e:
-        p.factorization(sched.taus[0]).solve(np.stack([b, 2 * b]))
+        p3.factorization(sched.taus[0]).solve(np.stack([b3, 2 * b3]))
     assert e.value.unconverged_shifts == [0, 1]
     with pytest.raises(capi.ConvergenceError):
-        L.solve_shifted_direct(p, b, shifts[:2])
+        L.solve_shifted_direct(p3, b3, shifts[:2])
+    # ... and inside FGMRES-Sh the failed preconditioner is a FactorizationError
+    with pytest.raises(capi.FactorizationError):
+        L.solve_shifted_flexible(p3, b3, shifts, gs)
+
+
+@pytest.mark.parametrize("mesh_n", [41, 101])
+def test_banded_exact_shift_and_invert_for_indefinite_2d_shifts(mesh_n):
+    """Strongly indefinite shifts (the paper's t = 1 min on the 100 m square, Re tau = -0.83)
+    defeat the multigrid V-cycle; 2-D pencils take the exact banded LU instead (band.cu), cached
+    by tau, identical to the reference's sparse LU (factorization.cpp:14-33)."""
+    rng = np.random.default_rng(mesh_n)
+    mesh = fem.build_mesh(mesh_n, 100.0)
+    lk = np.log(1e-4) + 1.3 * rng.standard_normal(mesh.n_elements())
+    ls = np.full(mesh.n_elements(), np.log(1e-5))
+    ops = fem.assemble(mesh, np.exp(lk), np.exp(ls))
+    p = L.ShiftedPencil(L.build_mesh(mesh_n, 100.0), lk, ls)
+    tau = -0.8312938858819381 + 0.5401183169684252j
+    v = rng.standard_normal((3, ops.n_free())) + 1j * rng.standard_normal((3, ops.n_free()))
+    A = (ops.stiffness + tau * ops.mass).tocsc()
+    lu = spla.splu(A, permc_spec="COLAMD")
+    u = p.factorization(tau).solve(v)
+    for r in range(3):
+        assert rel(u[r], lu.solve(v[r])) <= 1e-10
+    ua = p.factorization(tau).solve_adjoint(v[0])
+    assert rel(ua, spla.splu((ops.stiffness + np.conj(tau) * ops.mass).tocsc()).solve(v[0])) <= 1e-10
 
 
 def test_pooled_forty_times_over_256_shifts_per_item():
