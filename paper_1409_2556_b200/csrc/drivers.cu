@@ -311,9 +311,24 @@ __device__ __forceinline__ void tma5(void* dst, const CUtensorMap* m, int c0, in
 }
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+#ifdef LT_JAC_DFMA
+  // A/B build only (scripts/jac_ab.py): the same m8n8k4 product on the DFMA pipe.  Lane (g, q)
+  // holds A[g][q], B[q][g] and C[g][2q .. 2q+1]; it gathers A[g][0..3] and B[0..3][2q .. 2q+1]
+  // from the owning lanes.
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const double ak = __shfl_sync(0xffffffff, a, g * 4 + k);
+    const double b0 = __shfl_sync(0xffffffff, b, (2 * q) * 4 + k);
+    const double b1 = __shfl_sync(0xffffffff, b, (2 * q + 1) * 4 + k);
+    c[0] = fma(ak, b0, c[0]);
+    c[1] = fma(ak, b1, c[1]);
+  }
+#else
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
+#endif
 }
 __device__ __forceinline__ uint32_t jw_s(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -30,7 +30,7 @@ u = f.solve(v)
 ctx.set_profiling(False)
 prof = ctx.profile()
 tot = sum(x[0] for x in prof.values())
-its = prof.get("cocg_apply", (0, 0, 0))[1]
+its = prof.get("cocg_apply:operator", (0, 0, 0))[1]
 print(f"lib={os.environ.get('LT_LIB', 'default')} config={index} B={B} iterations={its} "
       f"kernel_ms={tot:.1f} per_item_iter_us={tot * 1e3 / max(its, 1) / B:.1f}")
 for k, (ms, cnt, by) in sorted(prof.items(), key=lambda kv: -kv[1][0]):
