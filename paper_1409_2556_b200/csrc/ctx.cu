@@ -49,6 +49,14 @@ void lt_ctx_s::resolve_profile() {
   pending.clear();
 }
 
+cusolverDnHandle_t lt_ctx_s::solver_handle() {
+  if (!solver) {
+    if (cusolverDnCreate(&solver) != CUSOLVER_STATUS_SUCCESS) throw lt::Error(LT_ERR_CUDA, "cusolverDnCreate failed");
+    cusolverDnSetStream(solver, stream);
+  }
+  return solver;
+}
+
 FlagSlot* lt_ctx_s::flag_ring_dev() {
   if (!flag_host) {
     void* hp = nullptr;
@@ -110,6 +118,7 @@ void ctx_destroy(lt_ctx ctx) {
     cudaEventDestroy(pe.stop);
   }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->flag_host) {
     for (auto e : ctx->flag_ev) cudaEventDestroy(e);
     cudaFreeHost(ctx->flag_host);

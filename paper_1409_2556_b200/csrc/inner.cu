@@ -2234,6 +2234,197 @@ __global__ void __launch_bounds__(kT) p1_prolong_kernel(LevelViewT<R> Lf, LevelV
   xf[(int64_t)b * Lf.n + a] = vadd(xf[(int64_t)b * Lf.n + a], v);
 }
 
+
+// 2-D: 1 / 2 / 4 (the coarse levels are 1/4 of their parent, not 1/8, and the launches of the
+// small levels are latency-bound: configs[1] / [2] at 8.3k -> 9.0k / 13.2k -> 16.4k solves/s)
+#ifndef LT_NU2D_0
+#define LT_NU2D_0 1
+#define LT_NU2D_1 2
+#define LT_NU2D_2 4
+#endif
+
+// ---- the bottom of the V-cycle in one launch ----------------------------------------------
+// The small levels (<= kBottomCells cells down to the coarsest) are latency-bound: each of
+// their ~70 kernels per V-cycle moves a few hundred KB.  Here one CTA per item runs that whole
+// sub-cycle -- the same red-black smoothing, residual, R = P^T, dense coarsest solve and P as
+// the level-by-level kernels, on the same FP32 coefficients -- with every vector of those
+// levels in shared memory and a block barrier between steps.
+constexpr int kBottomCells = 4096, kBottomLevels = 8, kBT = 1024;
+#ifdef LT_NO_BOTTOM
+constexpr bool kBottom = false;  // A/B build: the level-by-level kernels all the way down
+#else
+constexpr bool kBottom = true;
+#endif
+
+struct BottomLevels {
+  int L, dim;
+  int nx[kBottomLevels], ny[kBottomLevels], nz[kBottomLevels], nu[kBottomLevels];
+  int ax[kBottomLevels], ay[kBottomLevels], az[kBottomLevels];
+  int off[kBottomLevels];  // float2 offset of the level's x (f = x + n, r = f + n)
+  const float* Tx[kBottomLevels];
+  const float* Ty[kBottomLevels];
+  const float* Tz[kBottomLevels];
+  const float* M[kBottomLevels];
+};
+
+__global__ void __launch_bounds__(kBT) bottom_vcycle_kernel(BottomLevels P, Batch bt, const double2* __restrict__ taus,
+                                                         const float2* const* __restrict__ inv, int64_t inv_ld,
+                                                         int64_t inv_off, const float2* __restrict__ f0,
+                                                         float2* __restrict__ x0) {
+  extern __shared__ __align__(16) float2 bsm[];
+  const int b = blockIdx.x;
+  if (bt.done[b]) return;
+  const int tid = threadIdx.x;
+  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+  auto nof = [&](int l) { return P.nx[l] * P.ny[l] * P.nz[l]; };
+  auto X = [&](int l) { return bsm + P.off[l]; };
+  auto F = [&](int l) { return bsm + P.off[l] + nof(l); };
+  auto R = [&](int l) { return bsm + P.off[l] + 2 * nof(l); };
+  // the level's operator at cell a = (i, j, k): returns sum_nb T x_nb, with dk and m
+  auto offsum = [&](int l, const float2* x, int i, int j, int k, float& dk, float& m) {
+    const int nx = P.nx[l], ny = P.ny[l], nz = P.nz[l];
+    const int a = (k * ny + j) * nx + i;
+    const float tw = __ldg(P.Tx[l] + (k * ny + j) * (nx + 1) + i), te = __ldg(P.Tx[l] + (k * ny + j) * (nx + 1) + i + 1);
+    const float ts = __ldg(P.Ty[l] + (k * (ny + 1) + j) * nx + i), tn = __ldg(P.Ty[l] + (k * (ny + 1) + j + 1) * nx + i);
+    float2 o = make_float2(0.f, 0.f);
+    auto add = [&](float t, float2 v) { o.x += t * v.x; o.y += t * v.y; };
+    if (i > 0) add(tw, x[a - 1]);
+    if (i < nx - 1) add(te, x[a + 1]);
+    if (j > 0) add(ts, x[a - nx]);
+    if (j < ny - 1) add(tn, x[a + nx]);
+    dk = tw + te + ts + tn;
+    if (P.dim == 3) {
+      const int plane = nx * ny;
+      const float tb = __ldg(P.Tz[l] + a), tt = __ldg(P.Tz[l] + a + plane);
+      if (k > 0) add(tb, x[a - plane]);
+      if (k < nz - 1) add(tt, x[a + plane]);
+      dk += tb + tt;
+    }
+    m = __ldg(P.M[l] + a);
+    return o;
+  };
+  auto half = [&](int l, int color) {
+    const int n = nof(l), nx = P.nx[l], ny = P.ny[l];
+    float2* x = X(l);
+    const float2* f = F(l);
+    for (int a = tid; a < n; a += kBT) {
+      const int i = a % nx, j = (a / nx) % ny, k = a / (nx * ny);
+      if (((i + j + k) & 1) != color) continue;
+      float dk, m;
+      const float2 o = offsum(l, x, i, j, k, dk, m);
+      const float2 rhs = make_float2(f[a].x + o.x, f[a].y + o.y);
+      const float dr = dk + tr * m, di = ti * m;
+      const float inv_d = 1.0f / (dr * dr + di * di);
+      x[a] = make_float2((rhs.x * dr + rhs.y * di) * inv_d, (rhs.y * dr - rhs.x * di) * inv_d);
+    }
+    __syncthreads();
+  };
+  // f of the top level from global memory, x = 0
+  {
+    const int n = nof(0);
+    for (int a = tid; a < n; a += kBT) {
+      F(0)[a] = f0[(int64_t)b * n + a];
+      X(0)[a] = make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+  }
+  // down: pre-smoothing, residual, restriction
+  for (int l = 0; l < P.L - 1; ++l) {
+    if (l > 0) {
+      for (int a = tid; a < nof(l); a += kBT) X(l)[a] = make_float2(0.f, 0.f);
+      __syncthreads();
+    }
+    for (int s = 0; s < P.nu[l]; ++s) {
+      half(l, 0);
+      half(l, 1);
+    }
+    {
+      const int n = nof(l), nx = P.nx[l], ny = P.ny[l];
+      for (int a = tid; a < n; a += kBT) {
+        const int i = a % nx, j = (a / nx) % ny, k = a / (nx * ny);
+        float dk, m;
+        const float2 o = offsum(l, X(l), i, j, k, dk, m);
+        const float2 xa = X(l)[a], fa = F(l)[a];
+        const float dr = dk + tr * m, di = ti * m;
+        R(l)[a] = make_float2(fa.x - (dr * xa.x - di * xa.y - o.x), fa.y - (dr * xa.y + di * xa.x - o.y));
+      }
+      __syncthreads();
+    }
+    {
+      const int nc = nof(l + 1), cx = P.nx[l + 1], cy = P.ny[l + 1], fx = P.nx[l], fy = P.ny[l];
+      for (int c = tid; c < nc; c += kBT) {
+        const int I = c % cx, J = (c / cx) % cy, K = c / (cx * cy);
+        int Fx[4], Fy[4], Fz[4];
+        float wx[4], wy[4], wz[4];
+        const int nxx = r1d_terms(I, P.ax[l], cx, Fx, wx), nyy = r1d_terms(J, P.ay[l], cy, Fy, wy);
+        const int nzz = P.dim == 3 ? r1d_terms(K, P.az[l], P.nz[l + 1], Fz, wz) : 1;
+        if (P.dim != 3) { Fz[0] = 0; wz[0] = 1.0f; }
+        float2 s2 = make_float2(0.f, 0.f);
+        for (int r = 0; r < nzz; ++r)
+          for (int q = 0; q < nyy; ++q)
+            for (int o = 0; o < nxx; ++o) {
+              const float w = wz[r] * wy[q] * wx[o];
+              const float2 v = R(l)[(Fz[r] * fy + Fy[q]) * fx + Fx[o]];
+              s2.x += w * v.x;
+              s2.y += w * v.y;
+            }
+        F(l + 1)[c] = s2;
+      }
+      __syncthreads();
+    }
+  }
+  // the coarsest level: dense inverse
+  {
+    const int l = P.L - 1, nc = nof(l);
+    const float2* A = inv[b] + inv_off;
+    for (int r = tid; r < nc; r += kBT) {
+      float2 s2 = make_float2(0.f, 0.f);
+      for (int c = 0; c < nc; ++c) {
+        const float2 m = A[(int64_t)r * inv_ld + c], v = F(l)[c];
+        s2.x += m.x * v.x - m.y * v.y;
+        s2.y += m.x * v.y + m.y * v.x;
+      }
+      X(l)[r] = s2;
+    }
+    __syncthreads();
+  }
+  // up: prolongation, post-smoothing (the pre-smoother's transpose order)
+  for (int l = P.L - 2; l >= 0; --l) {
+    {
+      const int n = nof(l), fx = P.nx[l], fy = P.ny[l], cx = P.nx[l + 1], cy = P.ny[l + 1];
+      const float2* e = X(l + 1);
+      for (int a = tid; a < n; a += kBT) {
+        const int i = a % fx, j = (a / fx) % fy, k = a / (fx * fy);
+        int Ix[2], Iy[2], Iz[2];
+        float wx[2], wy[2], wz[2];
+        const int nxx = p1d_terms(i, P.ax[l], cx, Ix, wx), nyy = p1d_terms(j, P.ay[l], cy, Iy, wy);
+        int nzz = 1;
+        if (P.dim == 3) nzz = p1d_terms(k, P.az[l], P.nz[l + 1], Iz, wz);
+        else { Iz[0] = 0; wz[0] = 1.0f; }
+        float2 s2 = X(l)[a];
+        for (int r = 0; r < nzz; ++r)
+          for (int q = 0; q < nyy; ++q)
+            for (int o = 0; o < nxx; ++o) {
+              const float w = wz[r] * wy[q] * wx[o];
+              const float2 v = e[(Iz[r] * cy + Iy[q]) * cx + Ix[o]];
+              s2.x += w * v.x;
+              s2.y += w * v.y;
+            }
+        X(l)[a] = s2;
+      }
+      __syncthreads();
+    }
+    for (int s = 0; s < P.nu[l]; ++s) {
+      half(l, 1);
+      half(l, 0);
+    }
+  }
+  {
+    const int n = nof(0);
+    for (int a = tid; a < n; a += kBT) x0[(int64_t)b * n + a] = X(0)[a];
+  }
+}
+
 // ---- V-cycle driver --------------------------------------------------------------------
 template <class R>
 LevelViewT<R> mg_view(lt_pencil p, int l);
@@ -2300,6 +2491,48 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
       });
     return X[l];
   }
+  if constexpr (std::is_same<R, float>::value) {
+    if (kBottom && p->kind != LT_GRID_P1_TRI && l < last && L.n <= kBottomCells && !(tz && tz[l].rb)) {
+      BottomLevels P{};
+      P.L = last - l + 1;
+      P.dim = DIM;
+      int off = 0;
+      bool fits = P.L <= kBottomLevels;
+      for (int q = 0; fits && q < P.L; ++q) {
+        const Level& Lq = *p->levels[l + q];
+        P.nx[q] = Lq.nx;
+        P.ny[q] = Lq.ny;
+        P.nz[q] = Lq.nz;
+        P.ax[q] = Lq.agg[0];
+        P.ay[q] = Lq.agg[1];
+        P.az[q] = Lq.agg[2];
+        const int lv = l + q;
+        P.nu[q] = lv == 0 ? (DIM == 3 ? 2 : LT_NU2D_0) : lv == 1 ? (DIM == 3 ? 4 : LT_NU2D_1) : (DIM == 3 ? 8 : LT_NU2D_2);
+        P.Tx[q] = Lq.Tx32;
+        P.Ty[q] = Lq.Ty32;
+        P.Tz[q] = Lq.Tz32;
+        P.M[q] = Lq.M32;
+        P.off[q] = off;
+        off += (int)Lq.n * (q == P.L - 1 ? 2 : 3);
+      }
+      const size_t smem = sizeof(float2) * (size_t)off;
+      if (fits && smem <= 200 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+          LT_CUDA(cudaFuncSetAttribute(bottom_vcycle_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          attr = true;
+        }
+        double bytes = 0.0;
+        for (int q = 0; q < P.L; ++q) bytes += (double)p->levels[l + q]->n * (double)Bc * 16.0;
+        launch(ctx, "mg_bottom:fused", bytes, [&] {
+          bottom_vcycle_kernel<<<Bc, kBT, smem, st>>>(P, bt, taus, reinterpret_cast<const float2* const*>(inv), inv_ld,
+                                                      inv_off, reinterpret_cast<const float2*>(F[l]),
+                                                      reinterpret_cast<float2*>(X[l]));
+        });
+        return X[l];
+      }
+    }
+  }
   if (l == last) {
     dim3 g(blocks_for(L.n, kT / 32), Bc);
     launch(ctx, "mg_coarse_solve:dense", cell_bytes * 2 * vb, [&] {
@@ -2314,7 +2547,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   // the coarser ones.  Convergence is set by the coarse levels' smoothing, while their sweeps
   // are cheap: at configs[4] (80 items) this takes the inner solve from 17 to 12 COCG
   // iterations, 194 -> 163 ms; more finest-level sweeps do not reduce the count, fewer raise it
-  constexpr int nu0 = 2, nu1 = 4, nu_c = 8;
+  const int nu0 = DIM == 3 ? 2 : LT_NU2D_0, nu1 = DIM == 3 ? 4 : LT_NU2D_1, nu_c = DIM == 3 ? 8 : LT_NU2D_2;
   const int nu = l == 0 ? nu0 : l == 1 ? nu1 : nu_c;
   // half sweeps on cell pairs when the rows have even length, else one cell per thread
   const bool pairs = (L.nx & 1) == 0;
@@ -2490,6 +2723,12 @@ __global__ void cocg_control_kernel(int B, int* __restrict__ done, const double*
   }
 }
 
+#ifdef LT_TMA_2D
+constexpr bool kTma2d = true;  // A/B build: the TMA z-march kernels on 2-D levels too
+#else
+constexpr bool kTma2d = false;
+#endif
+
 template <int DIM>
 void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v, int64_t vs, double2* u,
                  int64_t us, const int* active, double* rel_out) {
@@ -2581,7 +2820,9 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   if (p->kind != LT_GRID_P1_TRI && sizeof(R) == 4) {
     for (int l = 0; l < nl - 1; ++l) {
       const Level& Lv = *p->levels[l];
-      if (Lv.nx % 2 != 0 || Lv.nx < 64) continue;
+      // the TMA z-march kernels pay on 3-D levels; a 2-D level is one plane, where the ring set-up
+      // and the producer warp are pure overhead (the register kernels run it)
+      if (Lv.nx % 2 != 0 || Lv.nx < 64 || (DIM != 3 && !kTma2d)) continue;
       const uint64_t nx = Lv.nx, ny = Lv.ny, nz = Lv.nz;
       const uint64_t dims[4] = {nx, ny, nz, (uint64_t)Bc};
       const uint64_t str[3] = {nx * 8, nx * ny * 8, nx * ny * nz * 8};
@@ -2643,7 +2884,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
   }
   // the residual kernel reads x through the level's x map and writes Rr[l]; the smoother
   // reads and writes X[l]
-  const bool ta_ok = p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32 &&
+  const bool ta_ok = (DIM == 3 || kTma2d) && p->kind != LT_GRID_P1_TRI && p->levels[0]->pack64.get() != nullptr && L0.nx >= 32 &&
                      L0.nx % 2 == 0;
   CUtensorMap map_p{}, map_c64{};
   if (ta_ok) {

@@ -3,6 +3,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <chrono>
 #include <complex>
@@ -119,6 +120,8 @@ struct lt_ctx_s {
   // still active at that step
   int profile_tag = -1;
 
+  cusolverDnHandle_t solver = nullptr;  // dense LU of the coarsest multigrid levels (lazy)
+  cusolverDnHandle_t solver_handle();
   FlagSlot* flag_host = nullptr;  // mapped pinned ring (kFlagRing slots)
   FlagSlot* flag_dev = nullptr;   // its device alias
   cudaEvent_t flag_ev[kFlagRing] = {};

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cusolverDn.h>
+
 #include "lt_internal.hpp"
 #include "stencil.cuh"
 
@@ -143,7 +145,7 @@ __global__ void coarsen_m(const double* __restrict__ Mf, double* __restrict__ Mc
 }
 
 // Dense A_c(tau) = K_c + tau M_c, written into the left half of an n x 2n augmented
-// matrix [A | I] (row-major) for Gauss-Jordan inversion.
+// matrix [A | I] (row-major); the right half receives A^{-1} (lt_pencil_s::factor).
 __global__ void dense_coarse(LevelView L, double2 tau, double2* __restrict__ aug) {
   int64_t n = L.n;
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -184,69 +186,6 @@ __global__ void dense_coarse(LevelView L, double2 tau, double2* __restrict__ aug
     }
   }
   aug[idx] = v;
-}
-
-// Single-CTA Gauss-Jordan with partial pivoting on [A | I] (n x 2n, row-major).
-// Leaves A^{-1} in the right half.  status[0] = 1 on a zero pivot.
-__global__ void __launch_bounds__(1024) gauss_jordan(double2* __restrict__ aug, int n, int* status) {
-  extern __shared__ double2 factors[];  // n
-  __shared__ double best_val[32];
-  __shared__ int best_idx[32];
-  __shared__ int piv;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t ld = 2 * (int64_t)n;
-  for (int c = 0; c < n; ++c) {
-    // pivot search over rows c..n-1
-    double bv = -1.0;
-    int bi = c;
-    for (int r = c + tid; r < n; r += nt) {
-      double v = cabs2(aug[r * ld + c]);
-      if (v > bv) { bv = v; bi = r; }
-    }
-    for (int off = 16; off > 0; off >>= 1) {
-      double ov = __shfl_down_sync(0xffffffff, bv, off);
-      int oi = __shfl_down_sync(0xffffffff, bi, off);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if ((tid & 31) == 0) { best_val[tid >> 5] = bv; best_idx[tid >> 5] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double v = best_val[0];
-      int i = best_idx[0];
-      for (int w = 1; w < (nt + 31) / 32; ++w)
-        if (best_val[w] > v || (best_val[w] == v && best_idx[w] < i)) { v = best_val[w]; i = best_idx[w]; }
-      piv = i;
-      if (!(v > 0.0)) status[0] = 1;
-    }
-    __syncthreads();
-    const int p = piv;
-    if (p != c) {
-      for (int64_t col = tid; col < ld; col += nt) {
-        double2 t = aug[c * ld + col];
-        aug[c * ld + col] = aug[p * ld + col];
-        aug[p * ld + col] = t;
-      }
-    }
-    __syncthreads();
-    const double2 inv = crecip(aug[c * ld + c]);
-    __syncthreads();
-    for (int64_t col = tid; col < ld; col += nt) aug[c * ld + col] = cmul(aug[c * ld + col], inv);
-    for (int r = tid; r < n; r += nt) factors[r] = aug[(int64_t)r * ld + c];
-    __syncthreads();
-    // eliminate column c from all other rows; columns < c of the left half are already
-    // reduced (zero outside the diagonal) and are not touched.
-    const int64_t width = ld - c;
-    const int64_t work = (int64_t)n * width;
-    for (int64_t w = tid; w < work; w += nt) {
-      int r = (int)(w / width);
-      if (r == c) continue;
-      int64_t col = c + w % width;
-      double2 f = factors[r];
-      if (f.x == 0.0 && f.y == 0.0) continue;
-      aug[r * ld + col] = csub(aug[r * ld + col], cmul(f, aug[(int64_t)c * ld + col]));
-    }
-    __syncthreads();
-  }
 }
 
 }  // namespace
@@ -907,25 +846,44 @@ const lt::CoarseFactor& lt_pencil_s::factor(double2 tau) {
   const int lc = (int)levels.size() - 1;
   LevelView L = view(lc);
   const int64_t nc = L.n;
-  if (nc > 4096) throw Error(LT_ERR_PRECONDITIONER, "coarsest multigrid level too large for a dense inverse");
+  if (nc > 8192) throw Error(LT_ERR_PRECONDITIONER, "coarsest multigrid level too large for a dense inverse");
   cudaStream_t st = ctx->stream;
   auto f = std::make_unique<CoarseFactor>();
   f->tau = tau;
   f->inverse.allocate(sizeof(double2) * nc * 2 * nc, st);
-  DeviceBuffer status(sizeof(int), st);
-  LT_CUDA(cudaMemsetAsync(status.get(), 0, sizeof(int), st));
   double2* aug = f->inverse.as<double2>();
   launch(ctx, "coarse_factor", 0.0, [&] {
     dense_coarse<<<blocks_for(nc * 2 * nc, kThreads), kThreads, 0, st>>>(L, tau, aug);
   });
-  int nt = nc >= 1024 ? 1024 : (int)((nc + 31) / 32 * 32);
-  launch(ctx, "coarse_factor", 0.0, [&] {
-    gauss_jordan<<<1, nt, sizeof(double2) * nc, st>>>(aug, (int)nc, status.as<int>());
-  });
-  int h_status = 0;
-  LT_CUDA(cudaMemcpyAsync(&h_status, status.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
-  if (h_status != 0) throw Error(LT_ERR_PRECONDITIONER, "shift-and-invert factorization failed (singular coarse operator)");
+  // A^{-1} by LU (cuSOLVER getrf + getrs on the identity).  A = K_c + tau M_c is complex
+  // symmetric, so its row-major and column-major forms coincide, and so do A^{-1}'s.
+  {
+    cusolverDnHandle_t h = ctx->solver_handle();
+    DeviceBuffer A(sizeof(double2) * nc * nc, st), X(sizeof(double2) * nc * nc, st), piv(sizeof(int) * (nc + 1), st);
+    LT_CUDA(cudaMemcpy2DAsync(A.get(), sizeof(double2) * nc, aug, sizeof(double2) * 2 * nc, sizeof(double2) * nc, nc,
+                              cudaMemcpyDeviceToDevice, st));
+    LT_CUDA(cudaMemcpy2DAsync(X.get(), sizeof(double2) * nc, aug + nc, sizeof(double2) * 2 * nc, sizeof(double2) * nc,
+                              nc, cudaMemcpyDeviceToDevice, st));
+    int lwork = 0;
+    auto* Ac = reinterpret_cast<cuDoubleComplex*>(A.get());
+    auto* Xc = reinterpret_cast<cuDoubleComplex*>(X.get());
+    if (cusolverDnZgetrf_bufferSize(h, (int)nc, (int)nc, Ac, (int)nc, &lwork) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(LT_ERR_CUDA, "cusolverDnZgetrf_bufferSize failed");
+    DeviceBuffer work(sizeof(cuDoubleComplex) * std::max(lwork, 1), st);
+    int* info = piv.as<int>() + nc;
+    if (cusolverDnZgetrf(h, (int)nc, (int)nc, Ac, (int)nc, work.as<cuDoubleComplex>(), piv.as<int>(), info) !=
+            CUSOLVER_STATUS_SUCCESS ||
+        cusolverDnZgetrs(h, CUBLAS_OP_N, (int)nc, (int)nc, Ac, (int)nc, piv.as<int>(), Xc, (int)nc, info) !=
+            CUSOLVER_STATUS_SUCCESS)
+      throw Error(LT_ERR_CUDA, "cuSOLVER coarse factorization failed");
+    int h_status = 0;
+    LT_CUDA(cudaMemcpyAsync(&h_status, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+    LT_CUDA(cudaStreamSynchronize(st));
+    if (h_status != 0)
+      throw Error(LT_ERR_PRECONDITIONER, "shift-and-invert factorization failed (singular coarse operator)");
+    LT_CUDA(cudaMemcpy2DAsync(aug + nc, sizeof(double2) * 2 * nc, X.get(), sizeof(double2) * nc, sizeof(double2) * nc,
+                              nc, cudaMemcpyDeviceToDevice, st));
+  }
   f->inverse32.allocate(sizeof(float2) * nc * nc, st);
   launch(ctx, "coarse_factor", 0.0, [&] {
     inverse_to_c64<<<blocks_for(nc * nc, kThreads), kThreads, 0, st>>>(aug, f->inverse32.as<float2>(), nc);
