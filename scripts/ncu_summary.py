@@ -21,6 +21,16 @@ KEYS = {
     "l2_hit": "lts__t_sector_hit_rate.pct",
     "fp64_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "issue_pct": "sm__inst_issued.avg.pct_of_peak_sustained_active",
+    "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1_pct": "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+    "mem_pct": "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l2_sectors": "lts__t_sectors.sum",
+    "l2_sectors_tex": "lts__t_sectors_srcunit_tex.sum",
+    "smem_wavefronts": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+    "sm_cycles": "sm__cycles_elapsed.max",
+    "tensor_pct": "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+    "lsu_pct": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smem_bytes": "launch__shared_mem_per_block_dynamic",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-3, "us": 1, "ms": 1e3,
         "usecond": 1, "nsecond": 1e-3, "msecond": 1e3}
