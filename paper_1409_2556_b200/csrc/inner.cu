@@ -1380,7 +1380,7 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c
 // once per slot the coefficients of both colours over rows y0 .. y0+RB_H, positions
 // m0 .. m0+35.
 #ifndef RB_DEPTH
-#define RB_DEPTH 5
+#define RB_DEPTH (RB_BF16 ? 7 : 5)
 #endif
 #ifndef RB_MINB
 #define RB_MINB 2
@@ -1388,7 +1388,17 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* m, int c
 #ifndef RB_NI
 #define RB_NI 2  // items per CTA of the colour-split half sweeps
 #endif
-constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + 4, RB_D = RB_DEPTH;
+// coefficient rows of the slot: RB_P + 1 positions, padded to a 16-byte multiple
+constexpr int RB_P = 32, RB_H = 8, RB_XP = RB_P + 4, RB_CP = RB_P + (RB_BF16 ? 8 : 4), RB_D = RB_DEPTH;
+__device__ __forceinline__ float rb_coef(float v) { return v; }
+__device__ __forceinline__ float rb_coef(unsigned short v) { return __uint_as_float((uint32_t)v << 16); }  // bf16 bits
+// persistent launches of the colour-split half sweeps (RB_PERSIST=0: one CTA per work item).
+// Measured at configs[4], 80 items: half sweeps 128^3 38.8 -> 38.3 ms, 64^3 13.3 -> 12.4 ms per
+// inner solve; the residual (one item per CTA) is faster with one CTA per work item (8.2 vs
+// 9.6 ms) and stays that way.
+#ifndef RB_PERSIST
+#define RB_PERSIST 1
+#endif
 template <int MODE, int NI>
 struct RbSlot {
   static constexpr int NX = MODE == 0 ? 1 : 2;  // colours of x in the slot
@@ -1396,7 +1406,7 @@ struct RbSlot {
   static constexpr uint32_t XBA = (XB + 127) / 128 * 128;
   // f per item: both colours when NI == 1 (residual, or a sweep forming f^T x), else its own
   static constexpr uint32_t FB = sizeof(float2) * RB_P * (NI == 1 ? 2 : 1) * RB_H;
-  static constexpr uint32_t CB = sizeof(float) * RB_CP * 2 * 4 * (RB_H + 1);
+  static constexpr uint32_t CB = sizeof(rb_coef_t) * RB_CP * 2 * 4 * (RB_H + 1);
   static constexpr uint32_t OFF_F = XBA * NI;
   static constexpr uint32_t OFF_C = OFF_F + FB * NI;
   static constexpr uint32_t SLOT = (OFF_C + CB + 127) / 128 * 128;
@@ -1410,6 +1420,11 @@ struct RbSlot {
 #define RB_ZC_SMALL 16
 #endif
 __host__ __device__ __forceinline__ int rb_zc(int nz) { return nz >= 128 ? ZM_ZC : RB_ZC_SMALL; }
+
+// CTAs of a persistent launch: RB_MINB per SM
+inline unsigned rb_persist_grid(lt_ctx ctx) {
+  return RB_PERSIST ? (unsigned)(ctx->num_sms * RB_MINB) : 0xffffffffu;
+}
 
 template <class VW>
 inline int rb_blocks(const VW& L) {
@@ -1444,28 +1459,19 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
                                                        const __grid_constant__ CUtensorMap mf,
                                                        const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                        const double2* __restrict__ taus, float2* __restrict__ out,
-                                                       int color, int zero_init, double2* __restrict__ dot, int nblk) {
+                                                       int color, int zero_init, double2* __restrict__ dot, int nblk,
+                                                       int zc) {
   using S = RbSlot<MODE, NI>;
   extern __shared__ __align__(128) unsigned char rb_smem[];
   __shared__ __align__(8) uint64_t full[S::D], empty[S::D];
+  // Work items w = block * ngroups + item group, taken grid-strided: a persistent launch (fewer
+  // CTAs than work items; never with dot) keeps its plane ring running across work items, so
+  // the next item's first planes are in flight while the last planes of this one are computed.
   const int ngroups = (bt.B + NI - 1) / NI;
-  const int grp = (int)(blockIdx.x % ngroups), cb = (int)(blockIdx.x / ngroups);
-  bool live[NI];
-  int nlive = 0;
-#pragma unroll
-  for (int t = 0; t < NI; ++t) {
-    const int b = grp * NI + t;
-    live[t] = b < bt.B && !bt.done[b];
-    nlive += live[t];
-  }
-  if (nlive == 0) return;
+  const int nwork = nblk * ngroups;
   const int nh = L.nx >> 1;
   const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
   const int ntile = tiles_x * tiles_y;
-  const int tile = cb % ntile, chunk = cb / ntile;
-  const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
-  const int zc = rb_zc(L.nz);
-  const int k0 = chunk * zc, k1 = min(L.nz, k0 + zc);
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
   const bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
   if (tid == 0) {
@@ -1480,139 +1486,175 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   double2 acc[NI];
 #pragma unroll
   for (int t = 0; t < NI; ++t) acc[t] = make_double2(0.0, 0.0);
-  if (wy == kT / 32) {  // producer warp
-    if (lane == 0) {
-      const bool ldx = MODE == 1 || !zero_init;
-      const uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
-      uint32_t bytes_xf = 0;
-#pragma unroll
-      for (int t = 0; t < NI; ++t)
-        if (live[t]) bytes_xf += (ldx ? S::XB : 0u);
-      int q = 0, use = 0;
-      for (int p = k0 - 1; p <= k1; ++p) {
-        if (use > 0) mbar_wait(&empty[q], (uint32_t)((use - 1) & 1));
-        unsigned char* sp = rb_smem + (size_t)q * S::SLOT;
-        const bool lf = p >= k0 && p < k1, lc = p >= k0;
-        uint32_t bytes = bytes_xf + (lc ? S::CB : 0u);
-        if (lf)
-#pragma unroll
-          for (int t = 0; t < NI; ++t) bytes += live[t] ? fb : 0u;
-        mbar_arrive_tx(&full[q], bytes);
-#pragma unroll
-        for (int t = 0; t < NI; ++t) {
-          if (!live[t]) continue;
-          const int b = grp * NI + t;
-          if (ldx) tma_load5(sp + t * S::XBA, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[q]);
-          if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, &full[q]);
-        }
-        if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[q]);
-        if (++q == S::D) { q = 0; ++use; }
-      }
-    }
-  } else {
-    const int m = m0 + lane, j = y0 + wy;
-    const bool in = m < nh && j < L.ny;
-    float tr[NI], ti[NI];
+  bool worked = false;
+  int qn = 0;        // ring position of the next plane (the same sequence in producer and consumers)
+  uint32_t un = 0;   // its use count (producer) / phase parity (consumers)
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const int grp = w % ngroups, cb = w / ngroups;
+    bool live[NI];
+    int nlive = 0;
 #pragma unroll
     for (int t = 0; t < NI; ++t) {
-      const int b = min(grp * NI + t, bt.B - 1);
-      tr[t] = (float)taus[b].x;
-      ti[t] = (float)taus[b].y;
+      const int b = grp * NI + t;
+      live[t] = b < bt.B && !bt.done[b];
+      nlive += live[t];
     }
-    const int nf = fboth ? 2 : 1;
-    // ring: planes k - 1, k, k + 1 in slots qm, q0, qu; qu's phase parity pu
-    int qm = 0, q0 = 1, qu = 2;
-    uint32_t pu = 0;
-    mbar_wait_u32(full0 + 8 * qm, 0);
-    mbar_wait_u32(full0 + 8 * q0, 0);
-    const int r = wy + 1, xq = lane + 2;
-    for (int k = k0; k < k1; ++k) {
-      mbar_wait_u32(full0 + 8 * qu, pu);
-      const unsigned char* sm = rb_smem + (size_t)qm * S::SLOT;
-      const unsigned char* s0 = rb_smem + (size_t)q0 * S::SLOT;
-      const unsigned char* su = rb_smem + (size_t)qu * S::SLOT;
-      // x[item t][row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
-      auto X = [](const unsigned char* sl, int t, int rr, int h, int q) {
-        return reinterpret_cast<const float2*>(sl + t * S::XBA)[(rr * S::NX + h) * RB_XP + q];
-      };
-      auto F = [&](int t, int h) {
-        return reinterpret_cast<const float2*>(s0 + S::OFF_F + t * S::FB)[(wy * nf + h) * RB_P + lane];
-      };
-      // coefficient comp of colour h at [row rc = j - y0][position qc = pos - m0]
-      auto C = [](const unsigned char* sl, int rc, int comp, int h, int qc) {
-        return reinterpret_cast<const float*>(sl + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc];
-      };
-      if (in) {
-        const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
-        // the colour-c cell at (row j, position m) is i = 2m + s; its coefficients (E, N, T from
-        // the other colour's W, S of row j + 1, B of plane k + 1)
-        auto coef = [&](int c, float& tw, float& te, float& ts, float& tn, float& tb, float& tt, float& mm) {
-          const int sft = (j + k + c) & 1;
-          tw = C(s0, wy, 0, c, lane);
-          ts = C(s0, wy, 1, c, lane);
-          tb = C(s0, wy, 2, c, lane);
-          mm = C(s0, wy, 3, c, lane);
-          te = C(s0, wy, 0, c ^ 1, lane + sft);
-          tn = C(s0, wy + 1, 1, c ^ 1, lane);
-          tt = C(su, wy, 2, c ^ 1, lane);
-          return sft;
-        };
-        // sum of T x over the six other-colour neighbours (xh: their colour in the slot)
-        auto offsum = [&](int t, int xh, int sft, float tw, float te, float ts, float tn, float tb, float tt) {
-          const float2 w = X(s0, t, r, xh, xq - 1 + sft), e = X(s0, t, r, xh, xq + sft);
-          const float2 so = X(s0, t, r - 1, xh, xq), no = X(s0, t, r + 1, xh, xq);
-          const float2 dn = X(sm, t, r, xh, xq), up = X(su, t, r, xh, xq);
-          return make_float2(tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x,
-                             tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y);
-        };
-        if (MODE == 0) {
-          float tw, te, ts, tn, tb, tt, mm;
-          const int sft = coef(color, tw, te, ts, tn, tb, tt, mm);
-          const float dk = tw + te + ts + tn + tb + tt;
+    if (nlive == 0) continue;
+    worked = true;
+    const int tile = cb % ntile, chunk = cb / ntile;
+    const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
+    const int k0 = chunk * zc, k1 = min(L.nz, k0 + zc);
+    if (wy == kT / 32) {  // producer warp
+      if (lane == 0) {
+        const bool ldx = MODE == 1 || !zero_init;
+        const uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
+        uint32_t bytes_xf = 0;
 #pragma unroll
-          for (int t = 0; t < NI; ++t) {
-            if (!live[t]) continue;
-            const float2 fcol = F(t, fboth ? color : 0);
-            float2 o = fcol;
-            if (!zero_init) {
-              const float2 os = offsum(t, 0, sft, tw, te, ts, tn, tb, tt);
-              o.x += os.x;
-              o.y += os.y;
+        for (int t = 0; t < NI; ++t)
+          if (live[t]) bytes_xf += (ldx ? S::XB : 0u);
+        for (int p = k0 - 1; p <= k1; ++p) {
+          if (un > 0) mbar_wait(&empty[qn], (un - 1) & 1u);
+          unsigned char* sp = rb_smem + (size_t)qn * S::SLOT;
+          const bool lf = p >= k0 && p < k1, lc = p >= k0;
+          uint32_t bytes = bytes_xf + (lc ? S::CB : 0u);
+          if (lf)
+#pragma unroll
+            for (int t = 0; t < NI; ++t) bytes += live[t] ? fb : 0u;
+          if (bytes == 0) {
+            // nothing to load (plane k0 - 1 of a sweep from zero): complete the phase by hand
+            mbar_arrive(&full[qn]);
+          } else {
+            mbar_arrive_tx(&full[qn], bytes);
+#pragma unroll
+            for (int t = 0; t < NI; ++t) {
+              if (!live[t]) continue;
+              const int b = grp * NI + t;
+              if (ldx) tma_load5(sp + t * S::XBA, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[qn]);
+              if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, &full[qn]);
             }
-            const float dr = dk + tr[t] * mm, di = ti[t] * mm;
-            const float inv = __frcp_rn(dr * dr + di * di);
-            const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
-            const int b = grp * NI + t;
-            out[(int64_t)b * L.n + row + (int64_t)color * nh + m] = xn;
-            if (dot) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
+            if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[qn]);
           }
-        } else {
+          if (++qn == S::D) { qn = 0; ++un; }
+        }
+      }
+    } else {
+      const int m = m0 + lane, j = y0 + wy;
+      const bool in = m < nh && j < L.ny;
+      float tr[NI], ti[NI];
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+      for (int t = 0; t < NI; ++t) {
+        const int b = min(grp * NI + t, bt.B - 1);
+        tr[t] = (float)taus[b].x;
+        ti[t] = (float)taus[b].y;
+      }
+      const int nf = fboth ? 2 : 1;
+      // ring: planes k - 1, k, k + 1 in slots qm, q0, qu; qu's phase parity pu
+      int qm = qn;
+      mbar_wait_u32(full0 + 8 * qn, un);
+      if (++qn == S::D) { qn = 0; un ^= 1u; }
+      int q0 = qn;
+      mbar_wait_u32(full0 + 8 * qn, un);
+      if (++qn == S::D) { qn = 0; un ^= 1u; }
+      int qu = qn;
+      uint32_t pu = un;
+      const int r = wy + 1, xq = lane + 2;
+      for (int k = k0; k < k1; ++k) {
+        mbar_wait_u32(full0 + 8 * qu, pu);
+        const unsigned char* sm = rb_smem + (size_t)qm * S::SLOT;
+        const unsigned char* s0 = rb_smem + (size_t)q0 * S::SLOT;
+        const unsigned char* su = rb_smem + (size_t)qu * S::SLOT;
+        // x[item t][row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
+        auto X = [](const unsigned char* sl, int t, int rr, int h, int q) {
+          return reinterpret_cast<const float2*>(sl + t * S::XBA)[(rr * S::NX + h) * RB_XP + q];
+        };
+        auto F = [&](int t, int h) {
+          return reinterpret_cast<const float2*>(s0 + S::OFF_F + t * S::FB)[(wy * nf + h) * RB_P + lane];
+        };
+        // coefficient comp of colour h at [row rc = j - y0][position qc = pos - m0]
+        auto C = [](const unsigned char* sl, int rc, int comp, int h, int qc) {
+          return rb_coef(reinterpret_cast<const rb_coef_t*>(sl + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc]);
+        };
+        if (in) {
+          const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
+          // the colour-c cell at (row j, position m) is i = 2m + s; its coefficients (E, N, T from
+          // the other colour's W, S of row j + 1, B of plane k + 1)
+          auto coef = [&](int c, float& tw, float& te, float& ts, float& tn, float& tb, float& tt, float& mm) {
+            const int sft = (j + k + c) & 1;
+            tw = C(s0, wy, 0, c, lane);
+            ts = C(s0, wy, 1, c, lane);
+            tb = C(s0, wy, 2, c, lane);
+            mm = C(s0, wy, 3, c, lane);
+            te = C(s0, wy, 0, c ^ 1, lane + sft);
+            tn = C(s0, wy + 1, 1, c ^ 1, lane);
+            tt = C(su, wy, 2, c ^ 1, lane);
+            return sft;
+          };
+          // sum of T x over the six other-colour neighbours (xh: their colour in the slot)
+          auto offsum = [&](int t, int xh, int sft, float tw, float te, float ts, float tn, float tb, float tt) {
+            const float2 w = X(s0, t, r, xh, xq - 1 + sft), e = X(s0, t, r, xh, xq + sft);
+            const float2 so = X(s0, t, r - 1, xh, xq), no = X(s0, t, r + 1, xh, xq);
+            const float2 dn = X(sm, t, r, xh, xq), up = X(su, t, r, xh, xq);
+            return make_float2(tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x,
+                               tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y);
+          };
+          if (MODE == 0) {
             float tw, te, ts, tn, tb, tt, mm;
-            const int sft = coef(c, tw, te, ts, tn, tb, tt, mm);
+            const int sft = coef(color, tw, te, ts, tn, tb, tt, mm);
             const float dk = tw + te + ts + tn + tb + tt;
 #pragma unroll
             for (int t = 0; t < NI; ++t) {
               if (!live[t]) continue;
-              const float2 os = offsum(t, c ^ 1, sft, tw, te, ts, tn, tb, tt);
-              const float2 xa = X(s0, t, r, c, xq), f = F(t, c);
+              const float2 fcol = F(t, fboth ? color : 0);
+              float2 o = fcol;
+              if (!zero_init) {
+                const float2 os = offsum(t, 0, sft, tw, te, ts, tn, tb, tt);
+                o.x += os.x;
+                o.y += os.y;
+              }
               const float dr = dk + tr[t] * mm, di = ti[t] * mm;
+              const float inv = __frcp_rn(dr * dr + di * di);
+              const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
               const int b = grp * NI + t;
-              out[(int64_t)b * L.n + row + (int64_t)c * nh + m] =
-                  make_float2(f.x - (dr * xa.x - di * xa.y - os.x), f.y - (dr * xa.y + di * xa.x - os.y));
+              out[(int64_t)b * L.n + row + (int64_t)color * nh + m] = xn;
+              if (dot) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float tw, te, ts, tn, tb, tt, mm;
+              const int sft = coef(c, tw, te, ts, tn, tb, tt, mm);
+              const float dk = tw + te + ts + tn + tb + tt;
+#pragma unroll
+              for (int t = 0; t < NI; ++t) {
+                if (!live[t]) continue;
+                const float2 os = offsum(t, c ^ 1, sft, tw, te, ts, tn, tb, tt);
+                const float2 xa = X(s0, t, r, c, xq), f = F(t, c);
+                const float dr = dk + tr[t] * mm, di = ti[t] * mm;
+                const int b = grp * NI + t;
+                out[(int64_t)b * L.n + row + (int64_t)c * nh + m] =
+                    make_float2(f.x - (dr * xa.x - di * xa.y - os.x), f.y - (dr * xa.y + di * xa.x - os.y));
+              }
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // this warp is done with plane k - 1
+        qm = q0;
+        q0 = qu;
+        if (++qu == S::D) { qu = 0; pu ^= 1u; }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // this warp is done with plane k - 1
-      qm = q0;
-      q0 = qu;
-      if (++qu == S::D) { qu = 0; pu ^= 1u; }
+      // planes k1 - 1 and k1 go back to the producer as well; the next work item starts at qu
+      if (lane == 0) {
+        mbar_arrive_u32(empty0 + 8 * qm);
+        mbar_arrive_u32(empty0 + 8 * q0);
+      }
+      qn = qu;
+      un = pu;
     }
   }
-  if (MODE == 0 && dot) {
+  if (MODE == 0 && dot && worked) {
+    // with dot the launch has one CTA per work item
+    const int grp = (int)blockIdx.x % ngroups, cb = (int)blockIdx.x / ngroups;
 #pragma unroll
     for (int t = 0; t < NI; ++t) {
       const double2 v = block_sum(acc[t]);
@@ -2565,8 +2607,9 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
     launch(ctx, kSmooth[ln], hb + coef, [&] {
       if (rbk)
-        mg_rb_kernel<0, RB_NI><<<rgrid2, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus,
-                                                                   (float2*)X[l], color, zero_init, dot, rb_blocks(L));
+        mg_rb_kernel<0, RB_NI><<<dot ? rgrid2 : std::min(rgrid2, rb_persist_grid(ctx)), kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
+            tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, (float2*)X[l], color, zero_init, dot, rb_blocks(L),
+            rb_zc(L.nz));
       else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
@@ -2585,8 +2628,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   }
   launch(ctx, kResid[ln], cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
-      mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus,
-                                                               (float2*)Rr[l], 0, 0, nullptr, 0);
+      mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(
+          tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus, (float2*)Rr[l], 0, 0, nullptr, rb_blocks(L), rb_zc(L.nz));
     else if (tma)
       mg_tma_kernel<1><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
                                                  nullptr, 0);
@@ -2843,13 +2886,14 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
         const uint32_t bf1[5] = {RB_P, 1, RB_H, 1, 1}, bf2[5] = {RB_P, 2, RB_H, 1, 1};
         const uint64_t P = (uint64_t)Lv.rb_P;
         const uint64_t kd[5] = {P, 2, 4, ny + 1, nz + 1};
-        const uint64_t ks[4] = {P * 4, 2 * P * 4, 8 * P * 4, 8 * P * 4 * (ny + 1)};
+        const uint64_t cw = sizeof(rb_coef_t);
+        const uint64_t ks[4] = {P * cw, 2 * P * cw, 8 * P * cw, 8 * P * cw * (ny + 1)};
         const uint32_t kb[5] = {RB_CP, 2, 4, RB_H + 1, 1};
         tzm[l].rx0 = tma_map_8b(X[l], 5, vd, vs, bx0);
         tzm[l].rx1 = tma_map_8b(X[l], 5, vd, vs, bx1);
         tzm[l].rf1 = tma_map_8b(F[l], 5, vd, vs, bf1);
         tzm[l].rf2 = tma_map_8b(F[l], 5, vd, vs, bf2);
-        tzm[l].rc = tma_map_4b(Lv.packrb.get(), 5, kd, ks, kb);
+        tzm[l].rc = RB_BF16 ? tma_map_2b(Lv.packrb.get(), 5, kd, ks, kb) : tma_map_4b(Lv.packrb.get(), 5, kd, ks, kb);
         tzm[l].rb = true;
         const uint32_t brt[5] = {RT_P, 2, RT_R, 1, 1};
         tzm[l].rt = tma_map_8b(Rr[l], 5, vd, vs, brt);

@@ -196,6 +196,21 @@ class TraceScope {
 //   Ty[(k*(ny+1) + j)*nx + i]  face between rows j-1 and j
 //   Tz[(k*ny + j)*nx + i]      face between planes k-1 and k  (k in [0, nz])
 //   M[a]                       diagonal mass (S h^d, summed on coarse levels)
+// Storage type of Level::packrb.  bfloat16 (default): the colour-split V-cycle is then the exact
+// V-cycle of the operator A' whose faces and masses are the bf16 roundings of A's -- every
+// face term of K and every mass is perturbed by a relative 2^-9 at most, so A' is spectrally
+// equivalent to A within (1 +- 0.002) and as good a COCG preconditioner as the FP32 one
+// (same iteration counts), symmetric as before -- while the coefficient tiles, half of what
+// a half sweep's CTA pulls from L2, shrink to half: a 7-deep plane ring fits where 5 did.
+#ifndef RB_BF16
+#define RB_BF16 1
+#endif
+#if RB_BF16
+typedef unsigned short rb_coef_t;
+#else
+typedef float rb_coef_t;
+#endif
+
 struct Level {
   int nx = 1, ny = 1, nz = 1;
   int64_t n = 0;
@@ -224,10 +239,10 @@ struct Level {
   // records) for the natural-layout TMA kernels, pack64 (FP64, finest level, planar
   // [k][j][comp][i] with rows of nx + 2) for the COCG operator
   DeviceBuffer pack32, pack64;
-  // FD levels with nx % 4 == 0 and nx >= 64: the same FP32 coefficients in the colour-split
-  // layout of the red-black TMA kernels (inner.cu), [k][j][comp W,S,B,M][colour][pos] with
-  // pos = i / 2, colour = (i + j + k) & 1, rb_P >= nx / 2 + 1 positions per colour (padded
-  // to a multiple of 4)
+  // FD levels with nx % 4 == 0 and nx >= 64: the coefficients in the colour-split layout of
+  // the red-black TMA kernels (inner.cu), [k][j][comp W,S,B,M][colour][pos] with pos = i / 2,
+  // colour = (i + j + k) & 1, rb_P >= nx / 2 + 1 positions per colour (padded to a multiple
+  // of 8), stored as rb_coef_t
   DeviceBuffer packrb;
   int rb_P = 0;
   int agg[3] = {1, 1, 1};  // aggregation to the next coarser level (FD)
@@ -324,6 +339,8 @@ CUtensorMap tma_map_8b(const void* base, int rank, const uint64_t* dims, const u
 // the same over 4-byte (FP32) elements.  Every box must start 16-byte aligned in its
 // innermost dimension: an unaligned start faults ("illegal instruction") on B200.
 CUtensorMap tma_map_4b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box);
+CUtensorMap tma_map_2b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                        const uint32_t* box);
 
 // device bytes a solve may still take: free + the pool's reserved-but-unused memory (ctx.cu)

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstring>
 
+#include <cuda_bf16.h>
 #include <cusolverDn.h>
 
 #include "lt_internal.hpp"
@@ -374,10 +375,17 @@ __global__ void pack_planar64_kernel(const double* __restrict__ Tx, const double
   out[(row + 3) * P + i] = (ci && cj && ck) ? M[((int64_t)k * ny + j) * nx + i] : 0.0;
 }
 
-// The FP32 coefficients in the colour-split layout (Level::packrb)
+// The coefficients in the colour-split layout (Level::packrb), rounded to rb_coef_t
+__device__ __forceinline__ rb_coef_t to_rb_coef(double v) {
+#if RB_BF16
+  return __bfloat16_as_ushort(__float2bfloat16_rn((float)v));
+#else
+  return (float)v;
+#endif
+}
 __global__ void pack_rb_kernel(const double* __restrict__ Tx, const double* __restrict__ Ty,
                                const double* __restrict__ Tz, const double* __restrict__ M, int nx, int ny, int nz,
-                               int P, float* __restrict__ out) {
+                               int P, rb_coef_t* __restrict__ out) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t cnt = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
   if (t >= cnt) return;
@@ -391,7 +399,7 @@ __global__ void pack_rb_kernel(const double* __restrict__ Tx, const double* __re
                        (ci && cj && ck) ? M[((int64_t)k * ny + j) * nx + i] : 0.0};
   const int h = (i + j + k) & 1, pos = i >> 1;
   const int64_t row = (int64_t)k * (ny + 1) + j;
-  for (int c = 0; c < 4; ++c) out[((row * 4 + c) * 2 + h) * P + pos] = (float)v[c];
+  for (int c = 0; c < 4; ++c) out[((row * 4 + c) * 2 + h) * P + pos] = to_rb_coef(v[c]);
 }
 
 static void make_fp32_copies(lt_pencil p) {
@@ -573,13 +581,13 @@ static void build_hierarchy_fd(lt_pencil p) {
                                                                                Lv.nz, Lv.pack32.as<float4>());
     });
     if (p->kind != LT_GRID_P1_TRI && Lv.nx % 4 == 0 && Lv.nx >= 64 && Lv.Tz) {
-      Lv.rb_P = ((Lv.nx / 2 + 1) + 3) / 4 * 4;
-      const size_t rb = sizeof(float) * (size_t)(Lv.nz + 1) * (Lv.ny + 1) * 8 * Lv.rb_P;
+      Lv.rb_P = ((Lv.nx / 2 + 1) + 7) / 8 * 8;
+      const size_t rb = sizeof(rb_coef_t) * (size_t)(Lv.nz + 1) * (Lv.ny + 1) * 8 * Lv.rb_P;
       Lv.packrb.allocate(rb, st);
       LT_CUDA(cudaMemsetAsync(Lv.packrb.get(), 0, rb, st));
       launch(ctx, "assemble", 48.0 * cnt, [&] {
         pack_rb_kernel<<<blocks_for(cnt, kThreads), kThreads, 0, st>>>(Lv.Tx, Lv.Ty, Lv.Tz, Lv.M, Lv.nx, Lv.ny, Lv.nz,
-                                                                       Lv.rb_P, Lv.packrb.as<float>());
+                                                                       Lv.rb_P, Lv.packrb.as<rb_coef_t>());
       });
     }
     if (l == 0 && Lv.nx % 2 == 0) {

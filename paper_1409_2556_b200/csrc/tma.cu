@@ -55,4 +55,9 @@ CUtensorMap tma_map_4b(const void* base, int rank, const uint64_t* dims, const u
   return tma_map(base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_DATA_TYPE_FLOAT32);
 }
 
+CUtensorMap tma_map_2b(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                       const uint32_t* box) {
+  return tma_map(base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16);
+}
+
 }  // namespace lt
