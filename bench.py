@@ -468,7 +468,7 @@ def main():
                        for k, v in sorted(classes.items(), key=lambda kv: -kv[1][0])}
     traffic_all = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.config == 4:  # the ncu captures are of configs[4] launches
         try:
             traffic_all = json.load(open(tpath))
         except Exception:
@@ -491,7 +491,11 @@ def main():
         roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic_all.get(dname), "peak_kind": peak_kind,
                     "algorithmic_bytes_per_launch": dbytes / dcnt if dcnt else None,
-                    "avg_launch_us": dms / dcnt * 1e3 if dcnt else None}
+                    "avg_launch_us": dms / dcnt * 1e3 if dcnt else None,
+                    "traffic_how": "dram__bytes_read.sum + dram__bytes_write.sum of one launch with every item of "
+                                   "the batch active (ncu --set full, profiles/traffic.json via scripts/make_traffic.py); "
+                                   "algorithmic_bytes_per_launch averages over the launches of the run, where items "
+                                   "that have converged are skipped"}
     # the dominant HBM-bound kernel and the time-weighted HBM fraction over every HBM-bound kernel
     hbm = {k: v for k, v in prof.items() if kernel_class(k) in HBM_CLASSES and v[2] > 0 and v[0] > 0}
     hname, (hms, hcnt, hbytes) = max(hbm.items(), key=lambda kv: kv[1][0]) if hbm else ("none", (0.0, 1, 0.0))

@@ -1409,7 +1409,10 @@ struct RbSlot {
   static constexpr uint32_t CB = sizeof(rb_coef_t) * RB_CP * 2 * 4 * (RB_H + 1);
   static constexpr uint32_t OFF_F = XBA * NI;
   static constexpr uint32_t OFF_C = OFF_F + FB * NI;
-  static constexpr uint32_t SLOT = (OFF_C + CB + 127) / 128 * 128;
+  // the slot's own full / empty mbarriers sit behind its data, so one slot address reaches
+  // the data and both barriers with immediate offsets
+  static constexpr uint32_t OFF_FULL = (OFF_C + CB + 15) / 16 * 16, OFF_EMPTY = OFF_FULL + 8;
+  static constexpr uint32_t SLOT = (OFF_EMPTY + 8 + 127) / 128 * 128;
   static constexpr int D = NI >= 4 ? 4 : RB_D;  // ring depth (4 items: 4 deep, 2 CTAs per SM)
   static constexpr size_t SMEM = (size_t)SLOT * D;
 };
@@ -1448,24 +1451,28 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-// MODE 0: red-black half sweep of `color`, in place on the colour's half of x (zero_init: x = 0
-// on entry, so no x is read; dot: also the partials of f^T x over the colour's cells, written
-// to dot[((item * 2 + color) * nblk + block] -- the last black and the last red sweep of the
-// post-smoother together form f^T x).  MODE 1: r = f - A x on both colours.  mx / mf: 5-D maps {pos, colour, y, z, item}
-// of x and f with the slot's boxes, mc: {pos, colour, comp, y, z} of Level::packrb.  Blocks:
-// rb_blocks(L) per group of NI consecutive items (item group fastest).
-template <int MODE, int NI>
+// MODE 0: red-black half sweep of `color`, in place on the colour's half of x (ZI: x = 0 on
+// entry, so no x is read; DOT: also the partials of f^T x over the colour's cells, written to
+// dot[((item * 2 + color) * nblk + block] -- the last black and the last red sweep of the
+// post-smoother together form f^T x; one CTA per work item then).  MODE 1: r = f - A x on both
+// colours.  mx / mf: 5-D maps {pos, colour, y, z, item} of x and f with the slot's boxes, mc:
+// {pos, colour, comp, y, z} of Level::packrb.  Work items: rb_blocks(L) per group of NI
+// consecutive items (item group fastest), zc planes each.
+//
+// The consumer loop is written for instruction count (ncu: the previous version issued 231
+// warp instructions per plane, 2.9x its loads and arithmetic, at 64-68% issue utilisation):
+// every shared-memory operand is one of six per-plane base registers plus an immediate, the
+// store pointers advance by a plane, and ZI / DOT are compile time.
+template <int MODE, int NI, bool ZI, bool DOT>
 __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_constant__ CUtensorMap mx,
                                                        const __grid_constant__ CUtensorMap mf,
                                                        const __grid_constant__ CUtensorMap mc, TzDims L, Batch bt,
                                                        const double2* __restrict__ taus, float2* __restrict__ out,
-                                                       int color, int zero_init, double2* __restrict__ dot, int nblk,
-                                                       int zc) {
+                                                       int color, double2* __restrict__ dot, int nblk, int zc) {
   using S = RbSlot<MODE, NI>;
   extern __shared__ __align__(128) unsigned char rb_smem[];
-  __shared__ __align__(8) uint64_t full[S::D], empty[S::D];
   // Work items w = block * ngroups + item group, taken grid-strided: a persistent launch (fewer
-  // CTAs than work items; never with dot) keeps its plane ring running across work items, so
+  // CTAs than work items; never with DOT) keeps its plane ring running across work items, so
   // the next item's first planes are in flight while the last planes of this one are computed.
   const int ngroups = (bt.B + NI - 1) / NI;
   const int nwork = nblk * ngroups;
@@ -1473,22 +1480,23 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   const int tiles_x = (nh + RB_P - 1) / RB_P, tiles_y = (L.ny + RB_H - 1) / RB_H;
   const int ntile = tiles_x * tiles_y;
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
-  const bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
+  constexpr bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
+  constexpr int nf = fboth ? 2 : 1;
+  const uint32_t ring0 = smem_u32(rb_smem), ring1 = ring0 + (uint32_t)(S::D * S::SLOT);
   if (tid == 0) {
     for (int q = 0; q < S::D; ++q) {
-      mbar_init(&full[q], 1);
-      mbar_init(&empty[q], kT / 32);
+      mbar_init(reinterpret_cast<uint64_t*>(rb_smem + (size_t)q * S::SLOT + S::OFF_FULL), 1);
+      mbar_init(reinterpret_cast<uint64_t*>(rb_smem + (size_t)q * S::SLOT + S::OFF_EMPTY), kT / 32);
     }
     mbar_init_fence();
   }
   __syncthreads();
-  const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
   double2 acc[NI];
 #pragma unroll
   for (int t = 0; t < NI; ++t) acc[t] = make_double2(0.0, 0.0);
   bool worked = false;
-  int qn = 0;        // ring position of the next plane (the same sequence in producer and consumers)
-  uint32_t un = 0;   // its use count (producer) / phase parity (consumers)
+  uint32_t an = ring0;  // slot of the next plane (the same sequence in producer and consumers)
+  uint32_t un = 0;      // its use count (producer) / phase parity (consumers)
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const int grp = w % ngroups, cb = w / ngroups;
     bool live[NI];
@@ -1506,154 +1514,143 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
     const int k0 = chunk * zc, k1 = min(L.nz, k0 + zc);
     if (wy == kT / 32) {  // producer warp
       if (lane == 0) {
-        const bool ldx = MODE == 1 || !zero_init;
-        const uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
-        uint32_t bytes_xf = 0;
-#pragma unroll
-        for (int t = 0; t < NI; ++t)
-          if (live[t]) bytes_xf += (ldx ? S::XB : 0u);
+        constexpr bool ldx = MODE == 1 || !ZI;
+        constexpr uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
+        const uint32_t bytes_xf = ldx ? (uint32_t)nlive * S::XB : 0u;
         for (int p = k0 - 1; p <= k1; ++p) {
-          if (un > 0) mbar_wait(&empty[qn], (un - 1) & 1u);
-          unsigned char* sp = rb_smem + (size_t)qn * S::SLOT;
+          unsigned char* sp = rb_smem + (an - ring0);
+          uint64_t* fullb = reinterpret_cast<uint64_t*>(sp + S::OFF_FULL);
+          if (un > 0) mbar_wait(reinterpret_cast<uint64_t*>(sp + S::OFF_EMPTY), (un - 1) & 1u);
           const bool lf = p >= k0 && p < k1, lc = p >= k0;
-          uint32_t bytes = bytes_xf + (lc ? S::CB : 0u);
-          if (lf)
+          const uint32_t bytes = bytes_xf + (lc ? S::CB : 0u) + (lf ? (uint32_t)nlive * fb : 0u);
+          mbar_arrive_tx(fullb, bytes);  // 0 bytes (plane k0 - 1 of a sweep from zero) completes the phase
 #pragma unroll
-            for (int t = 0; t < NI; ++t) bytes += live[t] ? fb : 0u;
-          if (bytes == 0) {
-            // nothing to load (plane k0 - 1 of a sweep from zero): complete the phase by hand
-            mbar_arrive(&full[qn]);
-          } else {
-            mbar_arrive_tx(&full[qn], bytes);
-#pragma unroll
-            for (int t = 0; t < NI; ++t) {
-              if (!live[t]) continue;
-              const int b = grp * NI + t;
-              if (ldx) tma_load5(sp + t * S::XBA, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, &full[qn]);
-              if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, &full[qn]);
-            }
-            if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, &full[qn]);
+          for (int t = 0; t < NI; ++t) {
+            if (!live[t]) continue;
+            const int b = grp * NI + t;
+            if (ldx) tma_load5(sp + t * S::XBA, &mx, m0 - 2, MODE == 0 ? color ^ 1 : 0, y0 - 1, p, b, fullb);
+            if (lf) tma_load5(sp + S::OFF_F + t * S::FB, &mf, m0, fboth ? 0 : color, y0, p, b, fullb);
           }
-          if (++qn == S::D) { qn = 0; ++un; }
+          if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, fullb);
+          an += S::SLOT;
+          if (an == ring1) { an = ring0; ++un; }
         }
       }
     } else {
       const int m = m0 + lane, j = y0 + wy;
       const bool in = m < nh && j < L.ny;
       float tr[NI], ti[NI];
+      float2* op[NI];  // this thread's output cell of plane k, colour 0's half of the row
 #pragma unroll
       for (int t = 0; t < NI; ++t) {
         const int b = min(grp * NI + t, bt.B - 1);
         tr[t] = (float)taus[b].x;
         ti[t] = (float)taus[b].y;
+        op[t] = out + (int64_t)b * L.n + ((int64_t)k0 * L.ny + j) * L.nx + m;
       }
-      const int nf = fboth ? 2 : 1;
-      // ring: planes k - 1, k, k + 1 in slots qm, q0, qu; qu's phase parity pu
-      int qm = qn;
-      mbar_wait_u32(full0 + 8 * qn, un);
-      if (++qn == S::D) { qn = 0; un ^= 1u; }
-      int q0 = qn;
-      mbar_wait_u32(full0 + 8 * qn, un);
-      if (++qn == S::D) { qn = 0; un ^= 1u; }
-      int qu = qn;
-      uint32_t pu = un;
-      const int r = wy + 1, xq = lane + 2;
+      const int64_t plane = (int64_t)L.nx * L.ny;
+      // ring: planes k - 1, k, k + 1 in slots am, a0, au; au's phase parity pu
+      uint32_t am = an;
+      mbar_wait_u32(an + S::OFF_FULL, un);
+      an += S::SLOT;
+      if (an == ring1) { an = ring0; un ^= 1u; }
+      uint32_t a0 = an;
+      mbar_wait_u32(an + S::OFF_FULL, un);
+      an += S::SLOT;
+      if (an == ring1) { an = ring0; un ^= 1u; }
+      uint32_t au = an, pu = un;
+      // byte offsets of this thread's operands inside a slot
+      constexpr uint32_t XROW = sizeof(float2) * RB_XP * S::NX, XCOL = sizeof(float2) * RB_XP;
+      constexpr uint32_t CW = sizeof(rb_coef_t), CROW = CW * RB_CP * 8, CCOMP = CW * RB_CP * 2, CCOL = CW * RB_CP;
+      const uint32_t xoff = (uint32_t)(wy + 1) * XROW + (uint32_t)(lane + 2) * 8u;
+      const uint32_t foff = S::OFF_F + ((uint32_t)(wy * nf) * RB_P + lane) * 8u;
+      const uint32_t coff = S::OFF_C + (uint32_t)wy * CROW + (uint32_t)lane * CW;
+      const unsigned char* base = rb_smem - ring0;  // slot address (shared window) -> pointer
+      auto LX = [](const unsigned char* p, uint32_t off) { return *reinterpret_cast<const float2*>(p + off); };
+      auto LC = [](const unsigned char* p, uint32_t off) {
+        return rb_coef(*reinterpret_cast<const rb_coef_t*>(p + off));
+      };
+      int sft0 = (j + k0) & 1;  // (j + k) & 1, toggled per plane
+      const bool all = nlive == NI;
       for (int k = k0; k < k1; ++k) {
-        mbar_wait_u32(full0 + 8 * qu, pu);
-        const unsigned char* sm = rb_smem + (size_t)qm * S::SLOT;
-        const unsigned char* s0 = rb_smem + (size_t)q0 * S::SLOT;
-        const unsigned char* su = rb_smem + (size_t)qu * S::SLOT;
-        // x[item t][row r = j - y0 + 1][colour h of the slot][position q = pos - m0 + 2]
-        auto X = [](const unsigned char* sl, int t, int rr, int h, int q) {
-          return reinterpret_cast<const float2*>(sl + t * S::XBA)[(rr * S::NX + h) * RB_XP + q];
-        };
-        auto F = [&](int t, int h) {
-          return reinterpret_cast<const float2*>(s0 + S::OFF_F + t * S::FB)[(wy * nf + h) * RB_P + lane];
-        };
-        // coefficient comp of colour h at [row rc = j - y0][position qc = pos - m0]
-        auto C = [](const unsigned char* sl, int rc, int comp, int h, int qc) {
-          return rb_coef(reinterpret_cast<const rb_coef_t*>(sl + S::OFF_C)[((rc * 4 + comp) * 2 + h) * RB_CP + qc]);
-        };
+        mbar_wait_u32(au + S::OFF_FULL, pu);
         if (in) {
-          const int64_t row = ((int64_t)k * L.ny + j) * L.nx;
-          // the colour-c cell at (row j, position m) is i = 2m + s; its coefficients (E, N, T from
-          // the other colour's W, S of row j + 1, B of plane k + 1)
-          auto coef = [&](int c, float& tw, float& te, float& ts, float& tn, float& tb, float& tt, float& mm) {
-            const int sft = (j + k + c) & 1;
-            tw = C(s0, wy, 0, c, lane);
-            ts = C(s0, wy, 1, c, lane);
-            tb = C(s0, wy, 2, c, lane);
-            mm = C(s0, wy, 3, c, lane);
-            te = C(s0, wy, 0, c ^ 1, lane + sft);
-            tn = C(s0, wy + 1, 1, c ^ 1, lane);
-            tt = C(su, wy, 2, c ^ 1, lane);
-            return sft;
-          };
-          // sum of T x over the six other-colour neighbours (xh: their colour in the slot)
-          auto offsum = [&](int t, int xh, int sft, float tw, float te, float ts, float tn, float tb, float tt) {
-            const float2 w = X(s0, t, r, xh, xq - 1 + sft), e = X(s0, t, r, xh, xq + sft);
-            const float2 so = X(s0, t, r - 1, xh, xq), no = X(s0, t, r + 1, xh, xq);
-            const float2 dn = X(sm, t, r, xh, xq), up = X(su, t, r, xh, xq);
-            return make_float2(tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x,
-                               tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y);
-          };
-          if (MODE == 0) {
-            float tw, te, ts, tn, tb, tt, mm;
-            const int sft = coef(color, tw, te, ts, tn, tb, tt, mm);
+          const unsigned char* xm = base + am + xoff;
+          const unsigned char* x0 = base + a0 + xoff;
+          const unsigned char* xu = base + au + xoff;
+          const unsigned char* f0 = base + a0 + foff;
+          const unsigned char* c0 = base + a0 + coff;
+          const unsigned char* cu = base + au + coff;
+          // colour c: the cell at (row j, position m) is i = 2m + sft; coefficients W, S, B, M of
+          // its own colour, E = the other colour's W at position m + sft, N = its S of row j + 1,
+          // T = its B of plane k + 1; the six neighbours are of the other colour (xh: that
+          // colour's index in the slot)
+          auto sweep = [&](const int c, const int xh, auto&& emit) {
+            const int sft = sft0 ^ c;
+            const uint32_t own = (uint32_t)c * CCOL, oth = (uint32_t)(c ^ 1) * CCOL;
+            const float tw = LC(c0, own), ts = LC(c0, own + CCOMP), tb = LC(c0, own + 2 * CCOMP);
+            const float mm = LC(c0, own + 3 * CCOMP);
+            const float te = LC(c0, oth + (uint32_t)sft * CW), tn = LC(c0, oth + CROW + CCOMP);
+            const float tt = LC(cu, oth + 2 * CCOMP);
             const float dk = tw + te + ts + tn + tb + tt;
+            const uint32_t xc = (uint32_t)xh * XCOL, xs = xc + (uint32_t)sft * 8u;
 #pragma unroll
             for (int t = 0; t < NI; ++t) {
-              if (!live[t]) continue;
-              const float2 fcol = F(t, fboth ? color : 0);
-              float2 o = fcol;
-              if (!zero_init) {
-                const float2 os = offsum(t, 0, sft, tw, te, ts, tn, tb, tt);
-                o.x += os.x;
-                o.y += os.y;
+              if (!all && !live[t]) continue;
+              float2 os = make_float2(0.f, 0.f);
+              if (MODE == 1 || !ZI) {
+                const uint32_t it = (uint32_t)t * S::XBA;
+                const float2 w = LX(x0, it + xs - 8u), e = LX(x0, it + xs);
+                const float2 so = LX(x0, it + xc - XROW), no = LX(x0, it + xc + XROW);
+                const float2 dn = LX(xm, it + xc), up = LX(xu, it + xc);
+                os = make_float2(tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x,
+                                 tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y);
               }
               const float dr = dk + tr[t] * mm, di = ti[t] * mm;
+              emit(t, c, os, dr, di);
+            }
+          };
+          if (MODE == 0) {
+            sweep(color, 0, [&](int t, int c, float2 os, float dr, float di) {
+              const float2 fcol = LX(f0, (uint32_t)t * S::FB + (fboth ? (uint32_t)c * RB_P * 8u : 0u));
+              const float2 o = make_float2(fcol.x + os.x, fcol.y + os.y);
               const float inv = __frcp_rn(dr * dr + di * di);
               const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
-              const int b = grp * NI + t;
-              out[(int64_t)b * L.n + row + (int64_t)color * nh + m] = xn;
-              if (dot) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
-            }
+              op[t][(int64_t)c * nh] = xn;
+              if (DOT) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
+            });
           } else {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float tw, te, ts, tn, tb, tt, mm;
-              const int sft = coef(c, tw, te, ts, tn, tb, tt, mm);
-              const float dk = tw + te + ts + tn + tb + tt;
-#pragma unroll
-              for (int t = 0; t < NI; ++t) {
-                if (!live[t]) continue;
-                const float2 os = offsum(t, c ^ 1, sft, tw, te, ts, tn, tb, tt);
-                const float2 xa = X(s0, t, r, c, xq), f = F(t, c);
-                const float dr = dk + tr[t] * mm, di = ti[t] * mm;
-                const int b = grp * NI + t;
-                out[(int64_t)b * L.n + row + (int64_t)c * nh + m] =
+            for (int c = 0; c < 2; ++c)
+              sweep(c, c ^ 1, [&](int t, int cc, float2 os, float dr, float di) {
+                const float2 xa = LX(x0, (uint32_t)t * S::XBA + (uint32_t)cc * XCOL);
+                const float2 f = LX(f0, (uint32_t)t * S::FB + (uint32_t)cc * RB_P * 8u);
+                op[t][(int64_t)cc * nh] =
                     make_float2(f.x - (dr * xa.x - di * xa.y - os.x), f.y - (dr * xa.y + di * xa.x - os.y));
-              }
-            }
+              });
           }
         }
+#pragma unroll
+        for (int t = 0; t < NI; ++t) op[t] += plane;
+        sft0 ^= 1;
         __syncwarp();
-        if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);  // this warp is done with plane k - 1
-        qm = q0;
-        q0 = qu;
-        if (++qu == S::D) { qu = 0; pu ^= 1u; }
+        if (lane == 0) mbar_arrive_u32(am + S::OFF_EMPTY);  // this warp is done with plane k - 1
+        am = a0;
+        a0 = au;
+        au += S::SLOT;
+        if (au == ring1) { au = ring0; pu ^= 1u; }
       }
-      // planes k1 - 1 and k1 go back to the producer as well; the next work item starts at qu
+      // planes k1 - 1 and k1 go back to the producer as well; the next work item starts at au
       if (lane == 0) {
-        mbar_arrive_u32(empty0 + 8 * qm);
-        mbar_arrive_u32(empty0 + 8 * q0);
+        mbar_arrive_u32(am + S::OFF_EMPTY);
+        mbar_arrive_u32(a0 + S::OFF_EMPTY);
       }
-      qn = qu;
+      an = au;
       un = pu;
     }
   }
-  if (MODE == 0 && dot && worked) {
-    // with dot the launch has one CTA per work item
+  if (MODE == 0 && DOT && worked) {
+    // with DOT the launch has one CTA per work item
     const int grp = (int)blockIdx.x % ngroups, cb = (int)blockIdx.x / ngroups;
 #pragma unroll
     for (int t = 0; t < NI; ++t) {
@@ -2606,10 +2603,20 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     // Colour-split: a half sweep moves half of f and of x twice (1.5 c per cell, 1 from zero)
     const double hb = rbk ? cell_bytes * (zero_init ? 1.0 : 1.5) * vb : cell_bytes * (zero_init ? 2 : 3) * vb;
     launch(ctx, kSmooth[ln], hb + coef, [&] {
-      if (rbk)
-        mg_rb_kernel<0, RB_NI><<<dot ? rgrid2 : std::min(rgrid2, rb_persist_grid(ctx)), kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
-            tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, (float2*)X[l], color, zero_init, dot, rb_blocks(L),
-            rb_zc(L.nz));
+      if (rbk) {
+        const unsigned pg = std::min(rgrid2, rb_persist_grid(ctx));
+        const int nb = rb_blocks(L), zc = rb_zc(L.nz);
+        float2* xo = (float2*)X[l];
+        if (dot)
+          mg_rb_kernel<0, RB_NI, false, true><<<rgrid2, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
+              tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, xo, color, dot, nb, zc);
+        else if (zero_init)
+          mg_rb_kernel<0, RB_NI, true, false><<<pg, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
+              tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, xo, color, nullptr, nb, zc);
+        else
+          mg_rb_kernel<0, RB_NI, false, false><<<pg, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
+              tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, xo, color, nullptr, nb, zc);
+      }
       else if (tma)
         mg_tma_kernel<0><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)X[l], color,
                                                    zero_init, dot, tz_blocks(L));
@@ -2628,8 +2635,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   }
   launch(ctx, kResid[ln], cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
-      mg_rb_kernel<1, 1><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(
-          tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus, (float2*)Rr[l], 0, 0, nullptr, rb_blocks(L), rb_zc(L.nz));
+      mg_rb_kernel<1, 1, false, false><<<rgrid, kTP, RbSlot<1, 1>::SMEM, st>>>(
+          tz[l].rx1, tz[l].rf2, tz[l].rc, tdims, bt, taus, (float2*)Rr[l], 0, nullptr, rb_blocks(L), rb_zc(L.nz));
     else if (tma)
       mg_tma_kernel<1><<<tgrid, kTP, TZ_SMEM, st>>>(tz[l].x, tz[l].f, tz[l].c, tdims, bt, taus, (float2*)Rr[l], 0, 0,
                                                  nullptr, 0);
@@ -2848,9 +2855,13 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(mg_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TZ_SMEM));
       LT_CUDA(cudaFuncSetAttribute(apply_tma2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TA2_SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<0, RB_NI>::SMEM));
-      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0, RB_NI>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<0, RB_NI, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)RbSlot<0, RB_NI>::SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM));
       LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
