@@ -18,9 +18,12 @@
 #include <vector>
 
 #include "lt_internal.hpp"
+#include <cooperative_groups.h>
+
 #include "stencil.cuh"
 
 namespace lt {
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -2464,6 +2467,103 @@ __global__ void __launch_bounds__(kBT) bottom_vcycle_kernel(BottomLevels P, Batc
   }
 }
 
+// ---- all sweeps of a mid level in one launch: one thread-block cluster per item -----------
+// The levels between the colour-split ones and the fused bottom (32^3 at configs[4], 32 x 32 x 16
+// at configs[3]) are L2-resident and their half sweeps issue-bound: a 32^3 half sweep of 80 items
+// took 24 us as its own launch, 8 + 8 sweeps = 32 launches per V-cycle.  Here a cluster of CL CTAs
+// owns one item: CTA r keeps planes [r slab, (r + 1) slab) of x in its shared memory for the
+// whole pre- or post-smoothing, reads the two planes next to its slab from its neighbours'
+// shared memory (DSMEM) and separates half sweeps by a cluster barrier -- a half sweep of one
+// colour reads only the other colour, which no CTA writes between two barriers, so one barrier
+// per half sweep is enough and no halo copies are kept.  f and the FP32 coefficients come
+// from global memory (L2) as before; x is read once (or starts at zero) and written once.
+// Thread = one cell pair (2 ip, 2 ip + 1) of a row, marching the slab's planes: exactly one cell
+// of the pair has the sweep's colour on every plane.  Same arithmetic as the pair kernel
+// (diag_solve_r on f + sum T x_nb).
+#ifndef LT_MID_CLUSTER
+#define LT_MID_CLUSTER 1
+#endif
+constexpr bool kMidCluster = LT_MID_CLUSTER != 0;
+constexpr int kMT = 256;  // three CTAs per SM (<= 85 registers): 111 four-CTA clusters resident
+#ifndef LT_MID_SMEM_KB
+#define LT_MID_SMEM_KB 32
+#endif
+constexpr size_t kMidSmem = LT_MID_SMEM_KB * 1024;  // x slab per CTA (32^3: clusters of 8; 64 KB / clusters of 4 measured 5.9 vs 5.1 ms per inner solve)
+struct MidLevel {
+  int nx, ny, nz, slab;
+  const float* Tx;
+  const float* Ty;
+  const float* Tz;
+  const float* M;
+};
+
+__global__ void __launch_bounds__(kMT, 3) mid_sweeps_kernel(MidLevel P, Batch bt, const double2* __restrict__ taus,
+                                                        const float2* __restrict__ f, float2* __restrict__ x,
+                                                        int first_color, int n_half, int zero_init) {
+  extern __shared__ __align__(16) float2 msm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int b = (int)blockIdx.x / CL;
+  if (bt.done[b]) return;  // the same for every CTA of the cluster
+  const int tid = threadIdx.x;
+  const int nx = P.nx, ny = P.ny, plane = nx * ny, hx = nx >> 1, pairs = hx * ny;
+  const int kb = rank * P.slab, nloc = P.slab * plane;
+  const int64_t n = (int64_t)plane * P.nz;
+  const float2* fb = f + (int64_t)b * n + (int64_t)kb * plane;
+  float2* xb = x + (int64_t)b * n + (int64_t)kb * plane;
+  for (int a = tid; a < nloc; a += kMT) msm[a] = zero_init ? make_float2(0.f, 0.f) : xb[a];
+  // the neighbours' slabs: the plane below is the last plane of rank - 1, the plane above the
+  // first plane of rank + 1 (the domain boundary is the Dirichlet ghost: no neighbour term)
+  const float2* below = rank > 0 ? cl.map_shared_rank(msm, rank - 1) + (P.slab - 1) * plane : nullptr;
+  const float2* above = rank < CL - 1 ? cl.map_shared_rank(msm, rank + 1) : nullptr;
+  const float tr = (float)taus[b].x, ti = (float)taus[b].y;
+  cl.sync();
+  for (int h = 0; h < n_half; ++h) {
+    const int color = first_color ^ (h & 1);
+    for (int p = tid; p < pairs; p += kMT) {
+      const int j = p / hx, ip = p - j * hx;
+      const float* Txr = P.Tx + ((int64_t)kb * ny + j) * (nx + 1) + 2 * ip;
+      const float* Tyr = P.Ty + ((int64_t)kb * (ny + 1) + j) * nx + 2 * ip;
+      const int c0 = j * nx + 2 * ip;  // the pair's first cell within a plane
+      const float* Tzr = P.Tz + (int64_t)kb * plane + c0;
+      const float* Mr = P.M + (int64_t)kb * plane + c0;
+      const int sx = ny * (nx + 1), sy = (ny + 1) * nx;  // plane strides of Tx, Ty
+#pragma unroll 8
+      for (int kl = 0; kl < P.slab; ++kl) {
+        const int o = (j + kb + kl + color) & 1;  // which cell of the pair has the colour
+        const int i = 2 * ip + o, a = kl * plane + c0 + o;
+        const float tw = __ldg(Txr + kl * sx + o), te = __ldg(Txr + kl * sx + o + 1);
+        const float ts = __ldg(Tyr + kl * sy + o), tn = __ldg(Tyr + kl * sy + nx + o);
+        const float tb = __ldg(Tzr + kl * plane + o), tt = __ldg(Tzr + (kl + 1) * plane + o);
+        const float mm = __ldg(Mr + kl * plane + o);
+        const float2 fv = fb[a];
+        float2 acc = fv;
+        auto add = [&](float t, float2 v) { acc.x += t * v.x; acc.y += t * v.y; };
+        if (i > 0) add(tw, msm[a - 1]);
+        if (i < nx - 1) add(te, msm[a + 1]);
+        if (j > 0) add(ts, msm[a - nx]);
+        if (j < ny - 1) add(tn, msm[a + nx]);
+        if (kl > 0) add(tb, msm[a - plane]);
+        else if (below) add(tb, below[c0 + o]);
+        if (kl < P.slab - 1) add(tt, msm[a + plane]);
+        else if (above) add(tt, above[c0 + o]);
+        msm[a] = diag_solve_r<float, float2>(tw + te + ts + tn + tb + tt, mm, tr, ti, acc);
+      }
+    }
+    cl.sync();
+  }
+  for (int a = tid; a < nloc; a += kMT) xb[a] = msm[a];
+}
+
+// cluster size for a level, 0 when the cluster kernel does not apply
+template <class VW>
+inline int mid_cluster(const VW& L) {
+  if (L.dim != 3 || (L.nx & 1) || !L.Tz) return 0;
+  for (int cl = 1; cl <= 8; cl *= 2)
+    if (L.nz % cl == 0 && (size_t)(L.n / cl) * sizeof(float2) <= kMidSmem) return cl;
+  return 0;
+}
+
 // ---- V-cycle driver --------------------------------------------------------------------
 template <class R>
 LevelViewT<R> mg_view(lt_pencil p, int l);
@@ -2626,12 +2726,45 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
         rbhalf_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, bt, taus, F[l], X[l], color, zero_init);
     });
   };
+  // mid levels (not colour-split, small enough for a cluster's shared memory): all half sweeps
+  // of the pre- / post-smoothing in one cluster launch
+  int mid_cl = 0;
+  if constexpr (std::is_same<R, float>::value && DIM == 3) {
+    if (kMidCluster && l > 0 && !rbk && !tma && pairs && p->kind != LT_GRID_P1_TRI) mid_cl = mid_cluster(L);
+  }
+  auto mid = [&](int first_color, int zero_init) {
+    if constexpr (std::is_same<R, float>::value) {
+      // x read (unless from zero) and written once, f once per sweep of its colour
+      const double mb = cell_bytes * vb * ((zero_init ? 1.0 : 2.0) + nu) + coef;
+      launch(ctx, kSmooth[ln], mb, [&] {
+        const MidLevel M{L.nx, L.ny, L.nz, L.nz / mid_cl, L.Tx, L.Ty, L.Tz, L.M};
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)(Bc * mid_cl));
+        cfg.blockDim = dim3(kMT);
+        cfg.dynamicSmemBytes = sizeof(float2) * (size_t)(L.n / mid_cl);
+        cfg.stream = st;
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = (unsigned)mid_cl;
+        at.val.clusterDim.y = 1;
+        at.val.clusterDim.z = 1;
+        cfg.attrs = &at;
+        cfg.numAttrs = 1;
+        LT_CUDA(cudaLaunchKernelEx(&cfg, mid_sweeps_kernel, M, bt, taus, (const float2*)F[l], (float2*)X[l],
+                                   first_color, 2 * nu, zero_init));
+      });
+    }
+  };
   // pre-smoothing: red half sweep from zero (f read, x written), then black, red, ...
-  half(0, 1, nullptr);
-  half(1, 0, nullptr);
-  for (int s = 1; s < nu; ++s) {
-    half(0, 0, nullptr);
+  if (mid_cl) {
+    mid(0, 1);
+  } else {
+    half(0, 1, nullptr);
     half(1, 0, nullptr);
+    for (int s = 1; s < nu; ++s) {
+      half(0, 0, nullptr);
+      half(1, 0, nullptr);
+    }
   }
   launch(ctx, kResid[ln], cell_bytes * 3 * vb + coef, [&] {
     if (rbk)
@@ -2688,7 +2821,8 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
     }
     prolong_zm_kernel<R><<<zgrid, kT, 0, st>>>(L, Lc, lev.agg[0], lev.agg[1], lev.agg[2], bt, ec, X[l]);
   });
-  for (int s = 0; s < nu; ++s) {
+  if (mid_cl) mid(1, 0);
+  for (int s = 0; s < (mid_cl ? 0 : nu); ++s) {
     // the last half sweeps also form the partial sums of f^T x when asked (and possible):
     // colour-split, each of the last black and red sweeps over its own colour; else the last
     // (red) sweep over both
@@ -2864,6 +2998,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
       LT_CUDA(cudaFuncSetAttribute(mg_rb_kernel<1, 1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)RbSlot<1, 1>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(restrict_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM));
+      LT_CUDA(cudaFuncSetAttribute(mid_sweeps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMidSmem));
       LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)PtGeom<true>::SMEM));
       LT_CUDA(cudaFuncSetAttribute(prolong_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
