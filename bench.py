@@ -409,10 +409,14 @@ def main():
     sampler = ClockSampler(local)
     if not os.environ.get("LT_BENCH_NOSMI"):
         sampler.start()
+    ctx.reset_profile()
     launches0 = ctx.launch_count()
     ms = timed(False)
     launches = ctx.launch_count() - launches0
     clocks = sampler.stop()
+    # host gaps of the production pass: wall time from the return of a stream synchronisation
+    # (stream empty) to the next kernel launch, accumulated by the library
+    gap = ctx.profile().get("host_gap", (0.0, 0, 0.0))
     # ---- 2. kernel profile: the same steps, CUDA events on 1 in 8 launches per kernel ----
     ctx.reset_profile()
     ctx.set_profile_sampling(PROFILE_EVERY)
@@ -420,6 +424,7 @@ def main():
     ms_prof = timed(False)
     ctx.set_profiling(False)
     prof = ctx.profile()
+    prof.pop("host_gap", None)
     # ---- 3. end-to-end through the public API with host inputs ----
     ms_e2e = timed(True)
     # ---- the full Jacobian's host copy (one time slice, chunked through pinned staging) ----
@@ -537,6 +542,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
+        "host_gap": {"ms_per_step": gap[0] / args.steps, "gaps_per_step": gap[1] / args.steps,
+                     "how": "wall time between the return of a stream synchronisation and the next kernel launch "
+                            "(the GPU is idle at least that long), production pass"},
         "clocks": clocks,
     }
     if jac:

@@ -5,6 +5,7 @@
 // every later use is stream-ordered after every earlier one.  Misses go to the stream-ordered
 // pool (cudaMallocAsync); an out-of-memory returns every cached block to the pool (in stream
 // order) and retries once.
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -42,7 +43,13 @@ size_t round_size(size_t bytes) {
 }
 
 // return cached blocks (all streams, or one) to the pool; caller holds the lock
+std::atomic<uint64_t>& driver_epoch() {
+  static std::atomic<uint64_t> e{0};
+  return e;
+}
+
 void drain_locked(Cache& c, const cudaStream_t* only) {
+  driver_epoch().fetch_add(1, std::memory_order_relaxed);
   for (auto it = c.free_blocks.begin(); it != c.free_blocks.end();) {
     if (only && it->first.s != *only) {
       ++it;
@@ -58,6 +65,8 @@ void drain_locked(Cache& c, const cudaStream_t* only) {
 
 }  // namespace
 
+uint64_t cache_driver_epoch() { return driver_epoch().load(std::memory_order_relaxed); }
+
 void* cache_alloc(size_t bytes, cudaStream_t s) {
   const size_t rb = round_size(bytes);
   Cache& c = cache();
@@ -72,6 +81,7 @@ void* cache_alloc(size_t bytes, cudaStream_t s) {
     }
   }
   void* p = nullptr;
+  driver_epoch().fetch_add(1, std::memory_order_relaxed);  // the driver's free-memory figure changes
   cudaError_t e = cudaMallocAsync(&p, rb, s);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();

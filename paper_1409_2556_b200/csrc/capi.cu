@@ -198,6 +198,8 @@ lt_status lt_ctx_reset_profile(lt_ctx ctx) {
     ctx->profile.clear();
     ctx->class_counter.clear();
     ctx->launches = 0;
+    ctx->gap_ms = 0.0;
+    ctx->gap_count = 0;
   });
 }
 
@@ -216,6 +218,13 @@ int lt_ctx_profile(lt_ctx ctx, int capacity, char* name_buf, double* total_ms, i
   } catch (const lt::Error& e) {
     g_err = e.what();
     return -1;
+  }
+  // the host gaps after stream synchronisations, as a pseudo entry
+  if (ctx->gap_count > 0) {
+    auto& e = ctx->profile["host_gap"];
+    e.ms = ctx->gap_ms;
+    e.launches = ctx->gap_count;
+    e.bytes = 0.0;
   }
   // with 1-in-N sampling, scale the timed launches of a class to all its launches
   std::map<std::string, int64_t> total;

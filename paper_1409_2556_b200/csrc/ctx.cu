@@ -76,6 +76,13 @@ double available_device_bytes(lt_ctx ctx) {
   // device free memory + what the stream-ordered pool holds reserved but unused + the block
   // cache: freed buffers stay reserved, so cudaMemGetInfo alone would shrink chunk sizes (and
   // the batching efficiency) as a run goes on; a request the cache cannot serve drains it
+  // cudaMemGetInfo costs ~1 ms on a 180 GB device and this runs before every inner solve with
+  // the stream drained: the driver-side figure is cached until this library's allocator next
+  // goes to the driver, an outer solve starts (ctx->mem_probe_valid reset) or 2 s pass
+  const auto now = std::chrono::steady_clock::now();
+  if (ctx->mem_probe_valid && ctx->mem_probe_epoch == cache_driver_epoch() &&
+      std::chrono::duration<double>(now - ctx->mem_probe_t).count() < 2.0)
+    return ctx->mem_probe + (double)cache_cached_bytes();
   size_t free_b = 0, total_b = 0;
   LT_CUDA(cudaMemGetInfo(&free_b, &total_b));
   cudaMemPool_t pool;
@@ -85,7 +92,11 @@ double available_device_bytes(lt_ctx ctx) {
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
   }
   cudaGetLastError();
-  return (double)free_b + (double)(reserved > used ? reserved - used : 0) + (double)cache_cached_bytes();
+  ctx->mem_probe = (double)free_b + (double)(reserved > used ? reserved - used : 0);
+  ctx->mem_probe_epoch = cache_driver_epoch();
+  ctx->mem_probe_t = now;
+  ctx->mem_probe_valid = true;
+  return ctx->mem_probe + (double)cache_cached_bytes();
 }
 
 lt_ctx ctx_create(int device) {

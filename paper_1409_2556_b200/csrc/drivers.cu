@@ -1127,7 +1127,7 @@ void recombine(lt_pencil p, const OuterResult& res, const std::vector<double2>& 
     recombine_kernel<<<blocks_for(n, kT) * B, kT, 0, st>>>(n, B, mc, dcols.as<const double2*>(), dc.as<double2>(),
                                                             ddst.as<int64_t>(), heads_dev);
   });
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
 }
 
 }  // namespace
@@ -1165,7 +1165,7 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
     ih_h.resize((size_t)n * n_src);
     LT_CUDA(cudaMemcpyAsync(ih_h.data(), ih_dev.get(), sizeof(double) * n * n_src, cudaMemcpyDeviceToHost, st));
   }
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
   for (int s = 0; s < n_src && initial_head; ++s) {
     double mx = 0.0;
     for (int64_t a = 0; a < n; ++a) mx = std::max(mx, std::fabs(ih_h[(size_t)s * n + a]));
@@ -1276,7 +1276,7 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
         }
         if (anyp) recombine(p, res, c, mc, dst, heads_dev.as<double>());
       }
-      LT_CUDA(cudaStreamSynchronize(st));
+      stream_sync(ctx);
     }
   }
   if (heads_out) {
@@ -1298,14 +1298,14 @@ void forward(lt_pencil p, const double* sources, const double* rates, int n_src,
     });
     std::vector<double> g((size_t)Bh * n_rec);
     LT_CUDA(cudaMemcpyAsync(g.data(), dout.get(), sizeof(double) * g.size(), cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
     // reorder (s, t, r) -> (s, r, t)  (ThtExperiment::measurement_index, jacobian.hpp:37-41)
     for (int s = 0; s < n_src; ++s)
       for (int t = 0; t < n_times; ++t)
         for (int r = 0; r < n_rec; ++r)
           drawdown_out[((size_t)s * n_rec + r) * n_times + t] = g[((size_t)s * n_times + t) * n_rec + r];
   }
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
   if (diag_out)
     for (int t = 0; t < n_times; ++t) diag_out[t] = diags[t];
 }
@@ -1577,7 +1577,7 @@ void jacobian_slice(lt_pencil p, const lt_experiment& ex, int t, int mem, double
     });
     LT_CUDA(cudaMemcpyAsync(pred_out, dout.get(), sizeof(double) * (size_t)n_src * n_rec, cudaMemcpyDeviceToHost, st));
   }
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
 }
 
 
@@ -1646,7 +1646,7 @@ void split_export(lt_split_s* sp, int plane0, int plane1, int m_pad, double2* ds
       std::memset(d, 0, sizeof(double2) * B * cells);
     }
   }
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(p->ctx);
 }
 
 void split_coefficients(lt_split_s* sp, double2* Y, int* m_used, int m_pad) {
@@ -1655,7 +1655,7 @@ void split_coefficients(lt_split_s* sp, double2* Y, int* m_used, int m_pad) {
   const int B = res.B, ns = res.n_shifts;
   std::vector<double2> Yd((size_t)B * ns * res.maxit);
   LT_CUDA(cudaMemcpyAsync(Yd.data(), res.Y.get(), sizeof(double2) * Yd.size(), cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(sp->p->ctx);
   for (int bk = 0; bk < B * ns; ++bk) {
     const int mu = res.m_used[bk];
     LT_REQUIRE(mu <= m_pad, "split coefficients: m_pad below this part's basis columns");
@@ -1697,7 +1697,7 @@ void split_predictions(lt_split_s* sp, double* out) {
         dc.as<double2>(), didx.as<int64_t>(), dwt.as<double>(), dcnt.as<int>(), dout.as<double>());
   });
   LT_CUDA(cudaMemcpyAsync(out, dout.get(), sizeof(double) * (size_t)n_loc * ex.n_rec, cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
 }
 
 void jacobian_assemble_slab(lt_pencil p, const lt_experiment& ex, int t, int plane0, int plane1, int halo_lo,
@@ -1782,7 +1782,7 @@ void jacobian_assemble_slab(lt_pencil p, const lt_experiment& ex, int t, int pla
     LT_CUDA(cudaMemcpy2DAsync(jac_out + blk * n_slab, sizeof(double) * lds,
                               jv.as<double>() + blk * n_view + (int64_t)halo_lo * plane, sizeof(double) * ldv,
                               sizeof(double) * n_slab, pairs, kind, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
 }
 
 }  // namespace lt

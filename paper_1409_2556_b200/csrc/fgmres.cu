@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(256) expand_cm2_kernel(int64_t n, int B, int n
 }  // namespace
 
 void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
+  p->ctx->mem_probe_valid = false;  // re-read the device's free memory once per outer solve
   lt_ctx ctx = p->ctx;
   cudaStream_t st = ctx->stream;
   const int B = prob.B, ns = prob.n_shifts;
@@ -783,7 +784,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
   int* d_iterations = dIter.as<int>();
   std::vector<int> h_active(B, 0);
   LT_CUDA(cudaMemcpyAsync(h_active.data(), active, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
   std::vector<double2> taus_j(B);
   DeviceBuffer gather_v, gather_u, gather_idx;
   for (int j = 0; j < maxit; ++j) {
@@ -872,7 +873,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
       outer_control<<<1, 256, 0, st>>>(S, m, d_iterations);
     });
     LT_CUDA(cudaMemcpyAsync(h_active.data(), active, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
   }
   std::vector<double> h_beta(B);
   std::vector<int> h_brk(B, 0), h_unconv(B, 0);
@@ -880,7 +881,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
   LT_CUDA(cudaMemcpyAsync(res.iterations.data(), d_iterations, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
   LT_CUDA(cudaMemcpyAsync(h_unconv.data(), n_unconv, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
   LT_CUDA(cudaMemcpyAsync(h_brk.data(), brk, sizeof(int) * B, cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
   int m_global = 0;
   for (int b = 0; b < B; ++b) m_global = std::max(m_global, res.iterations[b]);
   res.cap = maxit;
@@ -921,7 +922,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
   LT_CUDA(cudaMemcpyAsync(h_true.data(), true_res, sizeof(double) * n_bs, cudaMemcpyDeviceToHost, st));
   if (prob.record_history)
     LT_CUDA(cudaMemcpyAsync(res.history.data(), dHist.get(), sizeof(double) * n_bs * maxit, cudaMemcpyDeviceToHost, st));
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
   for (size_t t = 0; t < n_bs; ++t) {
     res.status[t] = lt_shift_status{h_conv[t], h_iter[t], h_est[t], h_true[t]};
     res.m_used[t] = h_mu[t];
@@ -941,7 +942,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
     kb.taus.assign(B, {});
     std::vector<double2> hH((size_t)B * maxit * (maxit + 1));
     LT_CUDA(cudaMemcpyAsync(hH.data(), dH.get(), sizeof(double2) * hH.size(), cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
     for (int b = 0; b < B; ++b) {
       const int m = res.iterations[b];
       kb.V[b].assign((size_t)n * (m + 1), make_double2(0, 0));
@@ -959,7 +960,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
         for (int i = 0; i <= m; ++i) kb.H[b][(size_t)jj * (m + 1) + i] = hH[((size_t)b * maxit + jj) * (maxit + 1) + i];
       kb.taus[b].assign(prob.tau_table[b].begin(), prob.tau_table[b].begin() + m);
     }
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
   }
 }
 
@@ -998,7 +999,7 @@ void expand_raw(lt_ctx ctx, int64_t n, int B, int ns, const std::vector<const do
       fn<<<(unsigned)((n + kCT - 1) / kCT), 256, ys_bytes, st>>>(n, B, ns, mmax, kCT, dcols.as<const double2*>(),
                                                                   ys.as<double2>(), x_out);
     });
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
     return;
   }
   launch(ctx, "expand", (double)n * B * 16.0 * (ncols + ns), [&] {
@@ -1009,7 +1010,7 @@ void expand_raw(lt_ctx ctx, int64_t n, int B, int ns, const std::vector<const do
       expand_kernel<<<(unsigned)nblk * B, kT, 0, st>>>(n, B, ns, ystride, dcols.as<const double2*>(),
                                                         Y, dmu.as<int>(), scale_dev, x_out);
   });
-  LT_CUDA(cudaStreamSynchronize(st));
+  stream_sync(ctx);
 }
 
 }  // namespace lt

@@ -3233,7 +3233,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     // charge every tagged launch of this chunk for the items active at its step
     std::vector<int> cnt(issued + 1, Bc);
     LT_CUDA(cudaMemcpyAsync(cnt.data(), d_counts, sizeof(int) * (size_t)(issued + 1), cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
     for (size_t e = pend0; e < ctx->pending.size(); ++e) {
       auto& pe = ctx->pending[e];
       if (pe.tag >= 0 && pe.tag < (int)cnt.size()) pe.bytes *= (double)cnt[pe.tag] / Bc;
@@ -3251,7 +3251,7 @@ void inner_chunk(lt_pencil p, int Bc, const double2* taus_host, const double2* v
     std::vector<int> done(Bc);
     LT_CUDA(cudaMemcpyAsync(rr.data(), d_rr, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
     LT_CUDA(cudaMemcpyAsync(bb.data(), d_bb, sizeof(double) * Bc, cudaMemcpyDeviceToHost, st));
-    LT_CUDA(cudaStreamSynchronize(st));
+    stream_sync(ctx);
     for (int b = 0; b < Bc; ++b) {
       const double rel = bb[b] > 0.0 ? std::sqrt(rr[b] / bb[b]) : 0.0;
       if (rel_out) rel_out[b] = rel;

@@ -29,7 +29,8 @@ namespace lt {
 void* cache_alloc(size_t bytes, cudaStream_t s);
 void cache_free(void* p, size_t bytes, cudaStream_t s);
 void cache_release_stream(cudaStream_t s);  // return a stream's cached blocks to the pool
-size_t cache_cached_bytes();                // bytes held in free lists
+size_t cache_cached_bytes();
+uint64_t cache_driver_epoch();                // bytes held in free lists
 
 // ---- stream-ordered device buffer -------------------------------------------------------
 class DeviceBuffer {
@@ -119,6 +120,17 @@ struct lt_ctx_s {
   // (written for every item of the batch) are scaled once the loop knows how many items were
   // still active at that step
   int profile_tag = -1;
+  // host gap accounting: wall time from the return of a stream synchronisation (the stream is
+  // empty) to the next kernel launch -- the GPU is idle for at least that long
+  bool drained = false;
+  std::chrono::steady_clock::time_point drain_t{};
+  double gap_ms = 0.0;
+  // cached driver-side free memory (available_device_bytes)
+  bool mem_probe_valid = false;
+  double mem_probe = 0.0;
+  uint64_t mem_probe_epoch = 0;
+  std::chrono::steady_clock::time_point mem_probe_t{};
+  int64_t gap_count = 0;
 
   cusolverDnHandle_t solver = nullptr;  // dense LU of the coarsest multigrid levels (lazy)
   cusolverDnHandle_t solver_handle();
@@ -141,9 +153,19 @@ inline bool debug_sync() {
   return on;
 }
 // Launch a kernel (callable issuing exactly one launch on ctx->stream) with accounting.
+inline void stream_sync(lt_ctx ctx) {
+  LT_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->drain_t = std::chrono::steady_clock::now();
+  ctx->drained = true;
+}
 template <class F>
 inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f) {
   ctx->launches++;
+  if (ctx->drained) {
+    ctx->gap_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ctx->drain_t).count();
+    ctx->gap_count++;
+    ctx->drained = false;
+  }
   if (ctx->profiling && (ctx->class_counter[name]++ % ctx->sample_every) == 0) {
     cudaEvent_t a = ctx->take_event(), b = ctx->take_event();
     cudaEventRecord(a, ctx->stream);
