@@ -1457,7 +1457,7 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
 // MODE 0: red-black half sweep of `color`, in place on the colour's half of x (ZI: x = 0 on
 // entry, so no x is read; DOT: also the partials of f^T x over the colour's cells, written to
 // dot[((item * 2 + color) * nblk + block] -- the last black and the last red sweep of the
-// post-smoother together form f^T x; one CTA per work item then).  MODE 1: r = f - A x on both
+// post-smoother together form f^T x).  MODE 1: r = f - A x on both
 // colours.  mx / mf: 5-D maps {pos, colour, y, z, item} of x and f with the slot's boxes, mc:
 // {pos, colour, comp, y, z} of Level::packrb.  Work items: rb_blocks(L) per group of NI
 // consecutive items (item group fastest), zc planes each.
@@ -1475,7 +1475,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   using S = RbSlot<MODE, NI>;
   extern __shared__ __align__(128) unsigned char rb_smem[];
   // Work items w = block * ngroups + item group, taken grid-strided: a persistent launch (fewer
-  // CTAs than work items; never with DOT) keeps its plane ring running across work items, so
+  // CTAs than work items) keeps its plane ring running across work items, so
   // the next item's first planes are in flight while the last planes of this one are computed.
   const int ngroups = (bt.B + NI - 1) / NI;
   const int nwork = nblk * ngroups;
@@ -1497,7 +1497,8 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   double2 acc[NI];
 #pragma unroll
   for (int t = 0; t < NI; ++t) acc[t] = make_double2(0.0, 0.0);
-  bool worked = false;
+  __shared__ double2 dsh[2][NI][kT / 32];  // DOT: per-warp partials of a work item
+  int par = 0;
   uint32_t an = ring0;  // slot of the next plane (the same sequence in producer and consumers)
   uint32_t un = 0;      // its use count (producer) / phase parity (consumers)
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
@@ -1511,7 +1512,6 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
       nlive += live[t];
     }
     if (nlive == 0) continue;
-    worked = true;
     const int tile = cb % ntile, chunk = cb / ntile;
     const int m0 = (tile % tiles_x) * RB_P, y0 = (tile / tiles_x) * RB_H;
     const int k0 = chunk * zc, k1 = min(L.nz, k0 + zc);
@@ -1650,17 +1650,30 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
       }
       an = au;
       un = pu;
-    }
-  }
-  if (MODE == 0 && DOT && worked) {
-    // with DOT the launch has one CTA per work item
-    const int grp = (int)blockIdx.x % ngroups, cb = (int)blockIdx.x / ngroups;
+      if (MODE == 0 && DOT) {
+        // this work item's partial of f^T x: the consumer warps alone reduce through shared
+        // memory (named barrier 1; the producer warp never joins), in a fixed order.  The
+        // scratch is double-buffered by work item, so one barrier per item is enough: a warp
+        // writes buffer `par` again only after passing the barrier of the item in between,
+        // which warp 0 reaches after reading it.
 #pragma unroll
-    for (int t = 0; t < NI; ++t) {
-      const double2 v = block_sum(acc[t]);
-      const int b = grp * NI + t;
-      if (threadIdx.x == 0 && b < bt.B) dot[((int64_t)b * 2 + color) * nblk + cb] = v;
-      __syncthreads();  // block_sum's shared scratch is reused by the next item
+        for (int t = 0; t < NI; ++t) {
+          const double2 v = warp_sum(acc[t]);
+          if (lane == 0) dsh[par][t][wy] = v;
+          acc[t] = make_double2(0.0, 0.0);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kT) : "memory");
+        if (wy == 0) {
+#pragma unroll
+          for (int t = 0; t < NI; ++t) {
+            double2 v = lane < kT / 32 ? dsh[par][t][lane] : make_double2(0.0, 0.0);
+            v = warp_sum(v);
+            const int b = grp * NI + t;
+            if (lane == 0 && b < bt.B) dot[((int64_t)b * 2 + color) * nblk + cb] = v;
+          }
+        }
+        par ^= 1;
+      }
     }
   }
 }
@@ -2708,7 +2721,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
         const int nb = rb_blocks(L), zc = rb_zc(L.nz);
         float2* xo = (float2*)X[l];
         if (dot)
-          mg_rb_kernel<0, RB_NI, false, true><<<rgrid2, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
+          mg_rb_kernel<0, RB_NI, false, true><<<pg, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(
               tz[l].rx0, tz[l].rf1, tz[l].rc, tdims, bt, taus, xo, color, dot, nb, zc);
         else if (zero_init)
           mg_rb_kernel<0, RB_NI, true, false><<<pg, kTP, RbSlot<0, RB_NI>::SMEM, st>>>(

@@ -29,6 +29,7 @@ ctx.set_profiling(True)
 u = f.solve(v)
 ctx.set_profiling(False)
 prof = ctx.profile()
+prof.pop("host_gap", None)
 tot = sum(x[0] for x in prof.values())
 its = prof.get("cocg_apply:operator", (0, 0, 0))[1]
 print(f"lib={os.environ.get('LT_LIB', 'default')} config={index} B={B} iterations={its} "
