@@ -454,6 +454,134 @@ __global__ void __launch_bounds__(kT, 2) verify_residual(LevelView L, State S, i
   }  // window
 }
 
+// The same true residuals for the first outer iterations (m <= 4 Krylov columns: every
+// BASELINE config converges in 2-4), FD pencils.  K u_j and M u_j of all columns stay in
+// registers and the shifts are walked one after the other with a single accumulator, so a
+// thread holds 4 m + 16 doubles instead of the 32 + 16 of the general kernel (which ncu shows
+// latency-bound at 25% occupancy, FP64 pipe 20% busy: 128 registers, one shared-memory
+// read-modify-write per shift and plane) and the per-shift norms live in registers.
+// A formulation on the FP64 tensor cores (one m8n8k4 per 8 cells, column and 4 shifts; lane =
+// one real of K u / M u) was built and measured 1.5x SLOWER at these small m: with 8 cells per
+// warp instruction the per-cell set-up (coefficients, offsets, right-hand side) costs 4x more
+// instructions than the products it feeds.
+template <int DIM, int MC>
+__global__ void __launch_bounds__(kT, MC <= 1 ? 3 : 2) verify_residual_small(LevelView L, State S, const double2* __restrict__ rhs,
+                                                               const double2* const* __restrict__ Ucols,
+                                                               double* __restrict__ part) {
+  constexpr int KC = 16, NW = kT / 32;
+  __shared__ int flagged[256];
+  __shared__ int nflag;
+  __shared__ double2 ysm[MC][KC], yzsm[MC][KC];
+  __shared__ double nsm[NW][KC];
+  LT_ITEM_BLOCK(S.B, b, cb);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tpp = L.tiles_x * L.tiles_y;
+  const int tile = (int)(cb % tpp), zc = (int)(cb / tpp);
+  const int kz0 = DIM == 3 ? zc * VR_Z : 0, kz1 = DIM == 3 ? min(L.nz, kz0 + VR_Z) : 1;
+  int i, jj, kk;
+  int64_t a0;
+  const bool in = tile_cell(L, tile, i, jj, kk, a0);
+  const int64_t plane = (int64_t)L.nx * L.ny;
+  const double2* ub[MC];
+#pragma unroll
+  for (int j = 0; j < MC; ++j) ub[j] = Ucols[j] + b * L.n;
+  for (int base = 0; base < S.ns; base += 256) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int cnt = 0;
+      for (int k = base; k < S.ns && k < base + 256; ++k)
+        if (S.flag[b * S.ns + k]) flagged[cnt++] = k;
+      nflag = cnt;
+    }
+    __syncthreads();
+    if (nflag == 0) continue;  // uniform
+    for (int c0 = 0; c0 < nflag; c0 += KC) {
+      const int nc = min(KC, nflag - c0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < KC * MC; e += blockDim.x) {
+        const int j = e / KC, q = e % KC;
+        double2 y = make_double2(0.0, 0.0), yz = y;
+        if (q < nc) {
+          const int t = b * S.ns + flagged[c0 + q];
+          y = S.Y[(int64_t)t * S.maxit + j];
+          yz = cmul(y, S.shifts[t]);
+        }
+        ysm[j][q] = y;
+        yzsm[j][q] = yz;
+      }
+      __syncthreads();
+      double nrm[KC];
+#pragma unroll
+      for (int q = 0; q < KC; ++q) nrm[q] = 0.0;
+      if (in) {
+        for (int k = kz0; k < kz1; ++k) {
+          const int64_t a = a0 + k * plane;
+          const double2 bv = rhs[b * L.n + a];
+          const double mval = __ldg(L.M + a);
+          double2 Ku[MC], Mu[MC];
+#pragma unroll
+          for (int j = 0; j < MC; ++j) {
+            double2 off;
+            double dk;
+            gather<DIM>(L, ub[j], a, i, jj, k, off, dk);
+            const double2 ua = ub[j][a];
+            Ku[j] = csub(cscale(ua, dk), off);
+            Mu[j] = cscale(ua, mval);
+          }
+#pragma unroll
+          for (int q = 0; q < KC; ++q) {
+            if (q < nc) {
+              double2 r = bv;
+#pragma unroll
+              for (int j = 0; j < MC; ++j) {
+                const double2 y = ysm[j][q], yz = yzsm[j][q];
+                r.x -= y.x * Ku[j].x - y.y * Ku[j].y + yz.x * Mu[j].x - yz.y * Mu[j].y;
+                r.y -= y.x * Ku[j].y + y.y * Ku[j].x + yz.x * Mu[j].y + yz.y * Mu[j].x;
+              }
+              nrm[q] += r.x * r.x + r.y * r.y;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        const double v = warp_sum_d(nrm[q]);
+        if (lane == 0) nsm[w][q] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x < nc) {
+        double t = 0.0;
+        for (int v = 0; v < NW; ++v) t += nsm[v][threadIdx.x];
+        part[((int64_t)b * S.ns + flagged[c0 + threadIdx.x]) * S.nblk_tile + cb] = t;
+      }
+    }
+  }  // window
+}
+
+// verify_residual: the small-m kernel when it applies (FD, m <= 4)
+#ifndef LT_VERIFY_SMALL
+#define LT_VERIFY_SMALL 1
+#endif
+template <int DIM>
+static void launch_verify_dim(const LevelView& L0, const State& S, int m, const double2* rhs,
+                              const double2* const* Ucols, double* part, unsigned grid, cudaStream_t st) {
+  if (LT_VERIFY_SMALL && !L0.Mx && m <= 4) {
+    switch (m) {
+      case 1: verify_residual_small<DIM, 1><<<grid, kT, 0, st>>>(L0, S, rhs, Ucols, part); return;
+      case 2: verify_residual_small<DIM, 2><<<grid, kT, 0, st>>>(L0, S, rhs, Ucols, part); return;
+      case 3: verify_residual_small<DIM, 3><<<grid, kT, 0, st>>>(L0, S, rhs, Ucols, part); return;
+      default: verify_residual_small<DIM, 4><<<grid, kT, 0, st>>>(L0, S, rhs, Ucols, part); return;
+    }
+  }
+  verify_residual<DIM><<<grid, kT, 0, st>>>(L0, S, m, rhs, Ucols, part);
+}
+static void launch_verify(lt_pencil p, const LevelView& L0, const State& S, int m, const double2* rhs,
+                          const double2* const* Ucols, double* part, int B, cudaStream_t st) {
+  const unsigned grid = (unsigned)S.nblk_tile * (unsigned)B;
+  if (p->dim == 3) launch_verify_dim<3>(L0, S, m, rhs, Ucols, part, grid, st);
+  else launch_verify_dim<2>(L0, S, m, rhs, Ucols, part, grid, st);
+}
+
 // per (item, shift) flagged: true_rel; freeze or back off.  best_effort: record only.
 __global__ void __launch_bounds__(kT) verify_finalize(State S, int m, const double* __restrict__ part, int best_effort) {
   __shared__ double sh[32];
@@ -863,10 +991,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
     launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 0); });
     partials.ensure(sizeof(double) * n_bs * std::max(nblk, S.nblk_tile), st);
     launch(ctx, "fgmres_verify:verify_residual", nba * (16.0 * (m + 1)) + n * 8.0 * (p->dim + 1), [&] {
-      if (p->dim == 3)
-        verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
-      else
-        verify_residual<2><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+      launch_verify(p, L0, S, m, prob.b, dUcols, partials.as<double>(), B, st);
     });
     launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 0); });
     launch(ctx, "fgmres_small", 0.0, [&] {
@@ -903,10 +1028,7 @@ void outer_solve(lt_pencil p, const OuterProblem& prob, OuterResult& res) {
       launch(ctx, "fgmres_small", 0.0, [&] { small_solve<<<blocks_for(n_bs, 128), 128, 0, st>>>(S, m, 1); });
       // restrict flags to the items of this m
       launch(ctx, "fgmres_verify:verify_residual", 0.0, [&] {
-        if (p->dim == 3)
-          verify_residual<3><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
-        else
-          verify_residual<2><<<(unsigned)S.nblk_tile * B, kT, 0, st>>>(L0, S, m, prob.b, dUcols, partials.as<double>());
+        launch_verify(p, L0, S, m, prob.b, dUcols, partials.as<double>(), B, st);
       });
       launch(ctx, "fgmres_small", 0.0, [&] { verify_finalize<<<(unsigned)n_bs, kT, 0, st>>>(S, m, partials.as<double>(), 1); });
     }
