@@ -37,6 +37,7 @@ RULES = [
     ("axpy_norm_kernel", "cocg_vec:axpy_norm"),
     ("copy_norm_kernel", "cocg_vec:copy_norm"),
     ("bottom_vcycle_kernel", "mg_bottom:fused"),
+    ("mid_sweeps_kernel", "mg_smooth_coarse:l2"),
     ("rbpair_zm_kernel", "mg_smooth_coarse:l2"),
     ("residual_pair_zm_kernel", "mg_residual:l2"),
     ("jacobian_mma4_kernel", "jacobian"),
