@@ -2000,18 +2000,26 @@ __global__ void __launch_bounds__(kTA, 2) apply_tma2_kernel(const __grid_constan
     const int64_t plane = (int64_t)L.nx * L.ny;
     double2* qb0 = q + (int64_t)b0 * L.n;
     double2* qb1 = q + (int64_t)(b0 + 1) * L.n;
-    int qm = 0, q0 = 1, qu = 2;
+    // The consumers hold two slots (planes k, k + 1): the value below comes from a register (the
+    // centre of the previous step), so a plane's slot goes back to the producer as soon as its
+    // own step is done and D - 2 = 3 planes are in flight instead of 2.
+    auto X = [](const unsigned char* sl, int it, int yy, int xx) {
+      return reinterpret_cast<const double2*>(sl + it * TA2_XBA)[yy * TA_XW + xx];
+    };
+    int q0 = 1, qu = 2;
     uint32_t pu = 0;
-    mbar_wait_u32(full0 + 8 * qm, 0);
+    mbar_wait_u32(full0, 0);
+    double2 below[2];
+#pragma unroll
+    for (int it = 0; it < 2; ++it)
+      below[it] = (it == 0 || has1) ? X(ta_smem, it, wy + 1, lane + 1) : make_double2(0.0, 0.0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_u32(empty0);  // plane k0 - 1 is in registers
     mbar_wait_u32(full0 + 8 * q0, 0);
     for (int k = k0; k < k1; ++k) {
       mbar_wait_u32(full0 + 8 * qu, pu);
-      const unsigned char* sm = ta_smem + (size_t)qm * TA2_SLOT;
       const unsigned char* s0 = ta_smem + (size_t)q0 * TA2_SLOT;
       const unsigned char* sp = ta_smem + (size_t)qu * TA2_SLOT;
-      auto X = [](const unsigned char* sl, int it, int yy, int xx) {
-        return reinterpret_cast<const double2*>(sl + it * TA2_XBA)[yy * TA_XW + xx];
-      };
       auto C = [](const unsigned char* sl, int comp, int yy, int xx) {
         return reinterpret_cast<const double*>(sl + TA2_OFF_C)[(yy * 4 + comp) * TA_CW + xx];
       };
@@ -2032,7 +2040,7 @@ __global__ void __launch_bounds__(kTA, 2) apply_tma2_kernel(const __grid_constan
         if (lane == 31) e = X(s0, it, wy + 1, TA_XW - 1);
         if (in) {
           const double2 so = X(s0, it, wy, lane + 1), no = X(s0, it, wy + 2, lane + 1);
-          const double2 dn = X(sm, it, wy + 1, lane + 1), up = X(sp, it, wy + 1, lane + 1);
+          const double2 dn = below[it], up = X(sp, it, wy + 1, lane + 1);
           const double ox = tw * w.x + te * e.x + ts * so.x + tn * no.x + tb * dn.x + tt * up.x;
           const double oy = tw * w.y + te * e.y + ts * so.y + tn * no.y + tb * dn.y + tt * up.y;
           const double2 tau = it == 0 ? tau0 : tau1;
@@ -2047,10 +2055,10 @@ __global__ void __launch_bounds__(kTA, 2) apply_tma2_kernel(const __grid_constan
             acc1 = cfma(pc, qa, acc1);
           }
         }
+        below[it] = pc;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty0 + 8 * qm);
-      qm = q0;
+      if (lane == 0) mbar_arrive_u32(empty0 + 8 * q0);  // plane k is done: its centre stays in `below`
       q0 = qu;
       if (++qu == TA2_D) { qu = 0; pu ^= 1u; }
     }
