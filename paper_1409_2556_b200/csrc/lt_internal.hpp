@@ -162,9 +162,12 @@ template <class F>
 inline void launch(lt_ctx ctx, const char* name, double algorithmic_bytes, F&& f) {
   ctx->launches++;
   if (ctx->drained) {
-    ctx->gap_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ctx->drain_t).count();
+    const double gap = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ctx->drain_t).count();
+    ctx->gap_ms += gap;
     ctx->gap_count++;
     ctx->drained = false;
+    static const bool gap_trace = std::getenv("LT_GAPTRACE") != nullptr;  // diagnostics: name the long gaps
+    if (gap_trace && gap > 0.3) std::fprintf(stderr, "[lt] host gap %8.3f ms before %s\n", gap, name);
   }
   if (ctx->profiling && (ctx->class_counter[name]++ % ctx->sample_every) == 0) {
     cudaEvent_t a = ctx->take_event(), b = ctx->take_event();
