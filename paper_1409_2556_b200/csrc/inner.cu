@@ -1450,6 +1450,13 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+// 1 / x by MUFU alone (1 ulp-class; __frcp_rn adds a range check and a slow path per call).  The
+// half sweep's diagonal inverse only has to be the same in the pre- and the post-smoother.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -1485,7 +1492,8 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   const int tid = threadIdx.x, lane = tid & 31, wy = tid >> 5;
   constexpr bool fboth = NI == 1 && MODE == 1;  // f of both colours in the slot (residual)
   constexpr int nf = fboth ? 2 : 1;
-  const uint32_t ring0 = smem_u32(rb_smem), ring1 = ring0 + (uint32_t)(S::D * S::SLOT);
+  const uint32_t ring0 = smem_u32(rb_smem);
+  constexpr uint32_t RING = (uint32_t)(S::D * S::SLOT);
   if (tid == 0) {
     for (int q = 0; q < S::D; ++q) {
       mbar_init(reinterpret_cast<uint64_t*>(rb_smem + (size_t)q * S::SLOT + S::OFF_FULL), 1);
@@ -1499,7 +1507,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
   for (int t = 0; t < NI; ++t) acc[t] = make_double2(0.0, 0.0);
   __shared__ double2 dsh[2][NI][kT / 32];  // DOT: per-warp partials of a work item
   int par = 0;
-  uint32_t an = ring0;  // slot of the next plane (the same sequence in producer and consumers)
+  uint32_t an = 0;      // slot (byte offset in the ring) of the next plane: the same sequence in producer and consumers
   uint32_t un = 0;      // its use count (producer) / phase parity (consumers)
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const int grp = w % ngroups, cb = w / ngroups;
@@ -1521,7 +1529,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
         constexpr uint32_t fb = fboth || NI > 1 ? S::FB : S::FB / 2;
         const uint32_t bytes_xf = ldx ? (uint32_t)nlive * S::XB : 0u;
         for (int p = k0 - 1; p <= k1; ++p) {
-          unsigned char* sp = rb_smem + (an - ring0);
+          unsigned char* sp = rb_smem + an;
           uint64_t* fullb = reinterpret_cast<uint64_t*>(sp + S::OFF_FULL);
           if (un > 0) mbar_wait(reinterpret_cast<uint64_t*>(sp + S::OFF_EMPTY), (un - 1) & 1u);
           const bool lf = p >= k0 && p < k1, lc = p >= k0;
@@ -1536,7 +1544,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
           }
           if (lc) tma_load5(sp + S::OFF_C, &mc, m0, 0, 0, y0, p, fullb);
           an += S::SLOT;
-          if (an == ring1) { an = ring0; ++un; }
+          if (an == RING) { an = 0; ++un; }
         }
       }
     } else {
@@ -1549,18 +1557,18 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
         const int b = min(grp * NI + t, bt.B - 1);
         tr[t] = (float)taus[b].x;
         ti[t] = (float)taus[b].y;
-        op[t] = out + (int64_t)b * L.n + ((int64_t)k0 * L.ny + j) * L.nx + m;
+        op[t] = out + (int64_t)b * L.n + ((int64_t)k0 * L.ny + j) * L.nx + m + (MODE == 0 ? (int64_t)color * nh : 0);
       }
       const int64_t plane = (int64_t)L.nx * L.ny;
       // ring: planes k - 1, k, k + 1 in slots am, a0, au; au's phase parity pu
       uint32_t am = an;
-      mbar_wait_u32(an + S::OFF_FULL, un);
+      mbar_wait_u32(ring0 + an + S::OFF_FULL, un);
       an += S::SLOT;
-      if (an == ring1) { an = ring0; un ^= 1u; }
+      if (an == RING) { an = 0; un ^= 1u; }
       uint32_t a0 = an;
-      mbar_wait_u32(an + S::OFF_FULL, un);
+      mbar_wait_u32(ring0 + an + S::OFF_FULL, un);
       an += S::SLOT;
-      if (an == ring1) { an = ring0; un ^= 1u; }
+      if (an == RING) { an = 0; un ^= 1u; }
       uint32_t au = an, pu = un;
       // byte offsets of this thread's operands inside a slot
       constexpr uint32_t XROW = sizeof(float2) * RB_XP * S::NX, XCOL = sizeof(float2) * RB_XP;
@@ -1568,22 +1576,24 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
       const uint32_t xoff = (uint32_t)(wy + 1) * XROW + (uint32_t)(lane + 2) * 8u;
       const uint32_t foff = S::OFF_F + ((uint32_t)(wy * nf) * RB_P + lane) * 8u;
       const uint32_t coff = S::OFF_C + (uint32_t)wy * CROW + (uint32_t)lane * CW;
-      const unsigned char* base = rb_smem - ring0;  // slot address (shared window) -> pointer
+      const unsigned char* base = rb_smem;  // + slot offset + operand offset: plain shared-memory addressing
       auto LX = [](const unsigned char* p, uint32_t off) { return *reinterpret_cast<const float2*>(p + off); };
       auto LC = [](const unsigned char* p, uint32_t off) {
         return rb_coef(*reinterpret_cast<const rb_coef_t*>(p + off));
       };
       int sft0 = (j + k0) & 1;  // (j + k) & 1, toggled per plane
-      const bool all = nlive == NI;
+      // the plane loop, compiled twice: every item of the group live (no per-item branches), or not
+      auto planes = [&](auto allc) {
+      constexpr bool all = decltype(allc)::value;
       for (int k = k0; k < k1; ++k) {
-        mbar_wait_u32(au + S::OFF_FULL, pu);
+        mbar_wait_u32(ring0 + au + S::OFF_FULL, pu);
         if (in) {
-          const unsigned char* xm = base + am + xoff;
-          const unsigned char* x0 = base + a0 + xoff;
-          const unsigned char* xu = base + au + xoff;
-          const unsigned char* f0 = base + a0 + foff;
-          const unsigned char* c0 = base + a0 + coff;
-          const unsigned char* cu = base + au + coff;
+          const unsigned char* xm = base + (am + xoff);
+          const unsigned char* x0 = base + (a0 + xoff);
+          const unsigned char* xu = base + (au + xoff);
+          const unsigned char* f0 = base + (a0 + foff);
+          const unsigned char* c0 = base + (a0 + coff);
+          const unsigned char* cu = base + (au + coff);
           // colour c: the cell at (row j, position m) is i = 2m + sft; coefficients W, S, B, M of
           // its own colour, E = the other colour's W at position m + sft, N = its S of row j + 1,
           // T = its B of plane k + 1; the six neighbours are of the other colour (xh: that
@@ -1617,9 +1627,9 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
             sweep(color, 0, [&](int t, int c, float2 os, float dr, float di) {
               const float2 fcol = LX(f0, (uint32_t)t * S::FB + (fboth ? (uint32_t)c * RB_P * 8u : 0u));
               const float2 o = make_float2(fcol.x + os.x, fcol.y + os.y);
-              const float inv = __frcp_rn(dr * dr + di * di);
+              const float inv = rcp_approx(dr * dr + di * di);
               const float2 xn = make_float2((o.x * dr + o.y * di) * inv, (o.y * dr - o.x * di) * inv);
-              op[t][(int64_t)c * nh] = xn;
+              op[t][0] = xn;
               if (DOT) acc[t] = cfma(make_double2(fcol.x, fcol.y), make_double2(xn.x, xn.y), acc[t]);
             });
           } else {
@@ -1628,7 +1638,7 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
               sweep(c, c ^ 1, [&](int t, int cc, float2 os, float dr, float di) {
                 const float2 xa = LX(x0, (uint32_t)t * S::XBA + (uint32_t)cc * XCOL);
                 const float2 f = LX(f0, (uint32_t)t * S::FB + (uint32_t)cc * RB_P * 8u);
-                op[t][(int64_t)cc * nh] =
+                op[t][cc ? nh : 0] =
                     make_float2(f.x - (dr * xa.x - di * xa.y - os.x), f.y - (dr * xa.y + di * xa.x - os.y));
               });
           }
@@ -1637,16 +1647,19 @@ __global__ void __launch_bounds__(kTP, RB_MINB) mg_rb_kernel(const __grid_consta
         for (int t = 0; t < NI; ++t) op[t] += plane;
         sft0 ^= 1;
         __syncwarp();
-        if (lane == 0) mbar_arrive_u32(am + S::OFF_EMPTY);  // this warp is done with plane k - 1
+        if (lane == 0) mbar_arrive_u32(ring0 + am + S::OFF_EMPTY);  // this warp is done with plane k - 1
         am = a0;
         a0 = au;
         au += S::SLOT;
-        if (au == ring1) { au = ring0; pu ^= 1u; }
+        if (au == RING) { au = 0; pu ^= 1u; }
       }
+      };
+      if (nlive == NI) planes(std::true_type{});
+      else planes(std::false_type{});
       // planes k1 - 1 and k1 go back to the producer as well; the next work item starts at au
       if (lane == 0) {
-        mbar_arrive_u32(am + S::OFF_EMPTY);
-        mbar_arrive_u32(a0 + S::OFF_EMPTY);
+        mbar_arrive_u32(ring0 + am + S::OFF_EMPTY);
+        mbar_arrive_u32(ring0 + a0 + S::OFF_EMPTY);
       }
       an = au;
       un = pu;
