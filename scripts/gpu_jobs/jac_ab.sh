@@ -1,6 +1,7 @@
-# Jacobian DMMA vs DFMA (same m8n8k4 formulation) A/B at configs[4], plus ncu of each
-timeout 600 python scripts/jac_ab.py
-LT_LIB=paper_1409_2556_b200/_lib/liblaptomo_gpu_dfma.so timeout 900 python scripts/jac_ab.py
-timeout 900 ncu --set full --clock-control none -k regex:jacobian_mma4 -c 1 -o gpurun_out/r2_jac_dmma -f python scripts/jac_ab.py > gpurun_out/r2_jac_dmma.log 2>&1
-LT_LIB=paper_1409_2556_b200/_lib/liblaptomo_gpu_dfma.so timeout 1200 ncu --set full --clock-control none -k regex:jacobian_mma4 -c 1 -o gpurun_out/r2_jac_dfma -f python scripts/jac_ab.py > gpurun_out/r2_jac_dfma.log 2>&1
-ls -la gpurun_out/r2_jac_*
+# A/B of the Jacobian kernel builds present in _lib (default first), then the Jacobian parity tests
+for L in "" $(ls paper_1409_2556_b200/_lib/liblaptomo_gpu_*.so 2>/dev/null); do
+  if [ -z "$L" ]; then unset LT_LIB; else export LT_LIB=$PWD/$L; fi
+  timeout 600 python scripts/jac_ab.py 2>&1 | tail -1
+done
+unset LT_LIB
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_gpu_fullsize.py tests/test_gpu_split.py -q -x 2>&1 | tail -3
