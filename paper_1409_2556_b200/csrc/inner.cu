@@ -2313,6 +2313,16 @@ __global__ void __launch_bounds__(kT) p1_prolong_kernel(LevelViewT<R> Lf, LevelV
 
 // 2-D: 1 / 2 / 4 (the coarse levels are 1/4 of their parent, not 1/8, and the launches of the
 // small levels are latency-bound: configs[1] / [2] at 8.3k -> 9.0k / 13.2k -> 16.4k solves/s)
+// red-black sweeps per pre- / post-smoothing on the finest, the next and the coarser 3-D levels
+#ifndef LT_NU3D_0
+#define LT_NU3D_0 2
+#endif
+#ifndef LT_NU3D_1
+#define LT_NU3D_1 4
+#endif
+#ifndef LT_NU3D_2
+#define LT_NU3D_2 8
+#endif
 #ifndef LT_NU2D_0
 #define LT_NU2D_0 1
 #define LT_NU2D_1 2
@@ -2680,7 +2690,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
         P.ay[q] = Lq.agg[1];
         P.az[q] = Lq.agg[2];
         const int lv = l + q;
-        P.nu[q] = lv == 0 ? (DIM == 3 ? 2 : LT_NU2D_0) : lv == 1 ? (DIM == 3 ? 4 : LT_NU2D_1) : (DIM == 3 ? 8 : LT_NU2D_2);
+        P.nu[q] = lv == 0 ? (DIM == 3 ? LT_NU3D_0 : LT_NU2D_0) : lv == 1 ? (DIM == 3 ? LT_NU3D_1 : LT_NU2D_1) : (DIM == 3 ? LT_NU3D_2 : LT_NU2D_2);
         P.Tx[q] = Lq.Tx32;
         P.Ty[q] = Lq.Ty32;
         P.Tz[q] = Lq.Tz32;
@@ -2720,7 +2730,7 @@ const typename CT<R>::V* vcycle(lt_pencil p, int l, int Bc, const Batch& bt, con
   // the coarser ones.  Convergence is set by the coarse levels' smoothing, while their sweeps
   // are cheap: at configs[4] (80 items) this takes the inner solve from 17 to 12 COCG
   // iterations, 194 -> 163 ms; more finest-level sweeps do not reduce the count, fewer raise it
-  const int nu0 = DIM == 3 ? 2 : LT_NU2D_0, nu1 = DIM == 3 ? 4 : LT_NU2D_1, nu_c = DIM == 3 ? 8 : LT_NU2D_2;
+  const int nu0 = DIM == 3 ? LT_NU3D_0 : LT_NU2D_0, nu1 = DIM == 3 ? LT_NU3D_1 : LT_NU2D_1, nu_c = DIM == 3 ? LT_NU3D_2 : LT_NU2D_2;
   const int nu = l == 0 ? nu0 : l == 1 ? nu1 : nu_c;
   // half sweeps on cell pairs when the rows have even length, else one cell per thread
   const bool pairs = (L.nx & 1) == 0;
