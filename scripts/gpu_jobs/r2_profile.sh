@@ -15,7 +15,7 @@ python scripts/launch_shares.py $REP/launches.csv $OUT/${TAG}_launch_shares.json
 gzip -c $REP/launches.csv > $OUT/${TAG}_launches.csv.gz
 NOWARM=1 timeout 300 python scripts/perf_inner.py 4 80 > $OUT/${TAG}_inner_plain.log 2>&1 &&
 NOWARM=1 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"${KIN:-mg_rb_kernel|rbpair_zm|residual_pair|apply_tma2|prolong|restrict|bottom_vcycle|pupdate|axpy_norm}" \
+  -k regex:"${KIN:-mg_rb_kernel|mid_sweeps|rbpair_zm|residual_pair|apply_tma2|prolong|restrict|bottom_vcycle|pupdate|axpy_norm}" \
   --launch-skip ${SKIN:-130} -c ${CIN:-70} -o $REP/full_inner -f python scripts/perf_inner.py 4 80 \
   > $OUT/${TAG}_ncu_inner.log 2>&1 || echo "inner capture failed"
 tail -3 $OUT/${TAG}_inner_plain.log
